@@ -1,0 +1,274 @@
+// glibc-2.39-faithful double-precision log1p / sin / cos, host+device.
+//
+// Why: the reference draws normals in `boxmuller_block` (sobench/_kernels.py:178-190)
+// with numba's math.log1p/sin/cos, which call the host glibc.  On FMA+AVX2 hosts
+// glibc dispatches (IFUNC) to variants compiled with -mfma, so a bit-exact port
+// must reproduce both the algorithm (sysdeps/ieee754/dbl-64/s_log1p.c, s_sin.c)
+// and exactly where GCC contracted a*b+c into one FMA.  The FMA placement below
+// was read off the disassembly of libm.so.6 (glibc 2.39-0ubuntu8.5):
+//   __log1p_fma @0x7aff0, __sin_fma @0x7b2d0, __cos_fma @0x7bad0.
+// Every fused operation is an explicit fma(); everything else must be compiled
+// WITHOUT contraction (gcc -ffp-contract=off, nvcc -fmad=false), so the same
+// source is bit-identical on the CPU test harness and on sm_100a.
+//
+// Domain: log1p over all finite x > -1 (plus the x <= -1 specials);
+// sin/cos over |x| < 105414350 (glibc's reduce_sincos range).  Box-Muller only
+// ever evaluates sin/cos on [0, 2*pi).  Larger |x| (glibc __branred) returns NaN.
+#pragma once
+#include <stdint.h>
+#include <math.h>
+#include <string.h>
+
+#if defined(__CUDACC__)
+#define SIMOPT_HD __host__ __device__ __forceinline__
+#else
+#define SIMOPT_HD static inline
+#endif
+
+SIMOPT_HD uint64_t gm_bits(double x) {
+#if defined(__CUDA_ARCH__)
+  return (uint64_t)__double_as_longlong(x);
+#else
+  uint64_t u; memcpy(&u, &x, 8); return u;
+#endif
+}
+SIMOPT_HD double gm_from_bits(uint64_t u) {
+#if defined(__CUDA_ARCH__)
+  return __longlong_as_double((long long)u);
+#else
+  double x; memcpy(&x, &u, 8); return x;
+#endif
+}
+SIMOPT_HD int32_t gm_hi(double x) { return (int32_t)(gm_bits(x) >> 32); }
+SIMOPT_HD uint32_t gm_lo(double x) { return (uint32_t)gm_bits(x); }
+SIMOPT_HD double gm_set_hi(double x, int32_t hi) {
+  return gm_from_bits(((uint64_t)(uint32_t)hi << 32) | (gm_bits(x) & 0xffffffffULL));
+}
+SIMOPT_HD double gm_fma(double a, double b, double c) { return fma(a, b, c); }
+SIMOPT_HD double gm_abs(double x) { return gm_from_bits(gm_bits(x) & 0x7fffffffffffffffULL); }
+SIMOPT_HD double gm_copysign(double x, double s) {
+  return gm_from_bits((gm_bits(x) & 0x7fffffffffffffffULL) | (gm_bits(s) & 0x8000000000000000ULL));
+}
+
+// ---------------------------------------------------------------------------
+// log1p  (fdlibm algorithm as shipped in glibc s_log1p.c, FMA variant)
+// ---------------------------------------------------------------------------
+#define GM_LN2_HI 0x1.62e42fee00000p-1
+#define GM_LN2_LO 0x1.a39ef35793c76p-33
+#define GM_LP1 0x1.5555555555593p-1
+#define GM_LP2 0x1.999999997fa04p-2
+#define GM_LP3 0x1.2492494229359p-2
+#define GM_LP4 0x1.c71c51d8e78afp-3
+#define GM_LP5 0x1.7466496cb03dep-3
+#define GM_LP6 0x1.39a09d078c69fp-3
+#define GM_LP7 0x1.2f112df3e5244p-3
+
+SIMOPT_HD double glibc_log1p(double x) {
+  const int32_t hx = gm_hi(x);
+  const int32_t ax = hx & 0x7fffffff;
+  double f, c = 0.0, u;
+  int32_t k, hu;
+  if (hx < 0x3FDA827A) {                    // x < 0.41422
+    if (ax >= 0x3ff00000) {                 // x <= -1.0
+      if (x == -1.0) return -INFINITY;
+      return NAN;
+    }
+    if (ax < 0x3e200000) {                  // |x| < 2**-29
+      if (ax < 0x3c900000) return x;        // |x| < 2**-54
+      return gm_fma(-(x * x), 0.5, x);      // x - x*x*0.5  (7b2c0)
+    }
+    // asm 7b02e: k=0 iff (uint32)(hx + 0x402d413c) > 0x402d413c
+    if ((uint32_t)hx + 0x402d413cu > 0x402d413cu) {
+      k = 0; f = x; hu = 1;
+      goto poly;
+    }
+  } else if (hx >= 0x7ff00000) {
+    return x + x;
+  }
+  // k != 0 branch
+  if (hx < 0x43400000) {
+    u = 1.0 + x;
+    hu = gm_hi(u);
+    k = (hu >> 20) - 1023;
+    c = (k > 0) ? 1.0 - (u - x) : x - (u - 1.0);
+    c = c / u;
+  } else {
+    u = x;
+    hu = gm_hi(u);
+    k = (hu >> 20) - 1023;
+    c = 0.0;
+  }
+  hu &= 0x000fffff;
+  if (hu < 0x6a09e) {
+    u = gm_set_hi(u, hu | 0x3ff00000);
+  } else {
+    k += 1;
+    u = gm_set_hi(u, hu | 0x3fe00000);
+    hu = (0x00100000 - hu) >> 2;
+  }
+  f = u - 1.0;
+poly: {
+    const double hfsq = (f * 0.5) * f;
+    if (hu == 0) {                          // |f| < 2**-20
+      if (f == 0.0) {
+        if (k == 0) return 0.0;
+        const double kd = (double)k;
+        c = gm_fma(kd, GM_LN2_LO, c);
+        return gm_fma(kd, GM_LN2_HI, c);
+      }
+      const double R = gm_fma(-f, 0x1.5555555555555p-1, 1.0) * hfsq;
+      if (k == 0) return f - R;
+      const double kd = (double)k;
+      return gm_fma(kd, GM_LN2_HI, -((R - gm_fma(kd, GM_LN2_LO, c)) - f));
+    }
+    const double s = f / (f + 2.0);
+    const double z = s * s;
+    const double R2 = gm_fma(z, GM_LP3, GM_LP2);
+    const double R3 = gm_fma(z, GM_LP5, GM_LP4);
+    const double R4 = gm_fma(z, GM_LP7, GM_LP6);
+    const double z2 = z * z;
+    const double z4 = z2 * z2;
+    const double z6 = z2 * z4;
+    double R = gm_fma(z, GM_LP1, z2 * R2);
+    R = gm_fma(z4, R3, R);
+    R = gm_fma(z6, R4, R);
+    const double shr = s * (R + hfsq);
+    if (k == 0) return f - (hfsq - shr);
+    const double kd = (double)k;
+    const double t = (hfsq - (gm_fma(kd, GM_LN2_LO, c) + shr)) - f;
+    return gm_fma(kd, GM_LN2_HI, -t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sin / cos  (IBM accurate library as refactored in glibc s_sin.c, FMA variant)
+// `tab` points at the 440 doubles of __sincostab (global, constant or shared).
+// ---------------------------------------------------------------------------
+#define GM_SN3 -0x1.5555555555515p-3
+#define GM_SN5 0x1.11110e829872fp-7
+#define GM_CS2 0x1.0000000000000p-1
+#define GM_CS4 -0x1.5555555555535p-5
+#define GM_CS6 0x1.6c16bedd9e239p-10
+#define GM_S1 -0x1.5555555555555p-3
+#define GM_S2 0x1.1111111110ecep-7
+#define GM_S3 -0x1.a01a019db08b8p-13
+#define GM_S4 0x1.71de27b9a7ed9p-19
+#define GM_S5 -0x1.addffc2fcdf59p-26
+#define GM_BIG 0x1.8p45
+#define GM_HP0 0x1.921fb54442d18p0
+#define GM_HP1 0x1.1a62633145c07p-54
+#define GM_MP1 0x1.921fb58000000p0
+#define GM_MP2 -0x1.dde973c000000p-27
+#define GM_PP3 -0x1.cb3b398000000p-55
+#define GM_PP4 -0x1.d747f23e32ed7p-83
+#define GM_HPINV 0x1.45f306dc9c883p-1
+#define GM_TOINT 0x1.8p52
+
+// TAYLOR_SIN(xx, a, da) (asm 7b950 / 7c0d0)
+SIMOPT_HD double gm_taylor_sin(double a, double da) {
+  const double xx = a * a;
+  double p = gm_fma(GM_S5, xx, GM_S4);
+  p = gm_fma(p, xx, GM_S3);
+  p = gm_fma(p, xx, GM_S2);
+  p = gm_fma(p, xx, GM_S1);
+  const double t = gm_fma(xx, gm_fma(p, a, -(0.5 * da)), da);
+  return a + t;
+}
+
+// do_sin(x, dx) (asm 7b35d..7b43d, 7b9ba..)
+SIMOPT_HD double gm_do_sin(double x, double dx, const double* tab) {
+  const double xold = x;
+  if (gm_abs(x) < 0.126) return gm_taylor_sin(x, dx);
+  if (x <= 0) dx = -dx;
+  const double ux = GM_BIG + gm_abs(x);
+  x = gm_abs(x) - (ux - GM_BIG);
+  const int k = (int)(gm_lo(ux) << 2);
+  const double xx = x * x;
+  const double s = x + gm_fma(x * xx, gm_fma(xx, GM_SN5, GM_SN3), dx);
+  const double c = gm_fma(x, dx, xx * gm_fma(xx, gm_fma(xx, GM_CS6, GM_CS4), GM_CS2));
+  const double sn = tab[k], ssn = tab[k + 1], cs = tab[k + 2], ccs = tab[k + 3];
+  double cor = gm_fma(s, ccs, ssn);
+  cor = gm_fma(-c, sn, cor);
+  cor = gm_fma(s, cs, cor);
+  return gm_copysign(sn + cor, xold);
+}
+
+// do_cos(x, dx) (asm 7b5e0.., 7b780.., 7bb36..)
+SIMOPT_HD double gm_do_cos(double x, double dx, const double* tab) {
+  if (x < 0) dx = -dx;
+  const double ux = GM_BIG + gm_abs(x);
+  x = (gm_abs(x) - (ux - GM_BIG)) + dx;
+  const int k = (int)(gm_lo(ux) << 2);
+  const double xx = x * x;
+  const double s = gm_fma(x * xx, gm_fma(xx, GM_SN5, GM_SN3), x);
+  const double c = xx * gm_fma(xx, gm_fma(xx, GM_CS6, GM_CS4), GM_CS2);
+  const double sn = tab[k], ssn = tab[k + 1], cs = tab[k + 2], ccs = tab[k + 3];
+  double cor = gm_fma(-s, ssn, ccs);
+  cor = gm_fma(-c, cs, cor);
+  cor = gm_fma(-s, sn, cor);
+  return cs + cor;
+}
+
+// reduce_sincos (asm 7b476.., 7bd53..)
+SIMOPT_HD int gm_reduce_sincos(double x, double* a, double* da) {
+  const double t = gm_fma(x, GM_HPINV, GM_TOINT);
+  const double xn = t - GM_TOINT;
+  const int n = (int)(gm_lo(t) & 3u);
+  const double y = gm_fma(-xn, GM_MP2, gm_fma(-xn, GM_MP1, x));
+  const double t2 = gm_fma(-xn, GM_PP3, y);
+  double db = gm_fma(-xn, GM_PP3, y - t2);
+  const double b = gm_fma(-xn, GM_PP4, t2);
+  db = db + gm_fma(-xn, GM_PP4, t2 - b);
+  *a = b;
+  *da = db;
+  return n;
+}
+
+SIMOPT_HD double gm_do_sincos(double a, double da, int n, const double* tab) {
+  const double r = (n & 1) ? gm_do_cos(a, da, tab) : gm_do_sin(a, da, tab);
+  return (n & 2) ? -r : r;
+}
+
+SIMOPT_HD double glibc_sin(double x, const double* tab) {
+  const int32_t k = gm_hi(x) & 0x7fffffff;
+  if (k < 0x3e500000) return x;                       // |x| < 2^-26
+  if (k < 0x3feb6000) return gm_do_sin(x, 0.0, tab);  // |x| < 0.855469
+  if (k < 0x400368fd) {                               // |x| < 2.426265
+    const double t = GM_HP0 - gm_abs(x);
+    return gm_copysign(gm_do_cos(t, GM_HP1, tab), x);
+  }
+  if (k < 0x419921FB) {                               // |x| < 105414350
+    double a, da;
+    const int n = gm_reduce_sincos(x, &a, &da);
+    return gm_do_sincos(a, da, n, tab);
+  }
+  return NAN;  // outside the ported domain (glibc: __branred / x/x)
+}
+
+SIMOPT_HD double glibc_cos(double x, const double* tab) {
+  const int32_t k = gm_hi(x) & 0x7fffffff;
+  if (k < 0x3e400000) return 1.0;                     // |x| < 2^-27
+  if (k < 0x3feb6000) return gm_do_cos(x, 0.0, tab);
+  if (k < 0x400368fd) {
+    const double y = GM_HP0 - gm_abs(x);
+    const double a = y + GM_HP1;
+    const double da = (y - a) + GM_HP1;
+    return gm_do_sin(a, da, tab);
+  }
+  if (k < 0x419921FB) {
+    double a, da;
+    const int n = gm_reduce_sincos(x, &a, &da);
+    return gm_do_sincos(a, da, n + 1, tab);
+  }
+  return NAN;
+}
+
+// Box-Muller pair exactly as boxmuller_block (sobench/_kernels.py:184-190):
+//   r = sqrt(-2.0 * log1p(-u1)); th = TAU * u2; (r*cos(th), r*sin(th))
+#define GM_TAU 6.283185307179586
+SIMOPT_HD void glibc_boxmuller(double u1, double u2, const double* tab, double* z0, double* z1) {
+  const double r = sqrt(-2.0 * glibc_log1p(-u1));
+  const double th = GM_TAU * u2;
+  *z0 = r * glibc_cos(th, tab);
+  *z1 = r * glibc_sin(th, tab);
+}

@@ -1,0 +1,70 @@
+// Philox4x64-10 (Random123; numpy.random.Philox), host+device.
+//
+// The reference's RngStream (sobench/sampling.py:51-80) keys numpy's Philox
+// with key=(seed, stream_id) and a 256-bit counter whose two low words hold the
+// stream's 128-bit block counter.  numpy pre-increments the counter before every
+// block, so block b of a stream at counter c is Philox(ctr = c + b + 1, key)
+// (carry propagating through all four words).  uniform01 (sampling.py:87-102)
+// turns word w into (w >> 11) * 2^-53.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define PHX_HD __host__ __device__ __forceinline__
+#else
+#define PHX_HD static inline
+#endif
+
+#define PHILOX_M0 0xD2E7470EE14C6C93ULL
+#define PHILOX_M1 0xCA5A826395121157ULL
+#define PHILOX_W0 0x9E3779B97F4A7C15ULL
+#define PHILOX_W1 0xBB67AE8584CAA73BULL
+
+PHX_HD void phx_mulhilo(uint64_t a, uint64_t b, uint64_t* hi, uint64_t* lo) {
+#if defined(__CUDA_ARCH__)
+  *lo = a * b;
+  *hi = __umul64hi(a, b);
+#else
+  const unsigned __int128 p = (unsigned __int128)a * b;
+  *lo = (uint64_t)p;
+  *hi = (uint64_t)(p >> 64);
+#endif
+}
+
+typedef struct phx4 { uint64_t v[4]; } phx4;
+
+PHX_HD phx4 philox4x64_10(phx4 c, uint64_t k0, uint64_t k1) {
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+  for (int r = 0; r < 10; ++r) {
+    uint64_t hi0, lo0, hi1, lo1;
+    phx_mulhilo(PHILOX_M0, c.v[0], &hi0, &lo0);
+    phx_mulhilo(PHILOX_M1, c.v[2], &hi1, &lo1);
+    phx4 o;
+    o.v[0] = hi1 ^ c.v[1] ^ k0;
+    o.v[1] = lo1;
+    o.v[2] = hi0 ^ c.v[3] ^ k1;
+    o.v[3] = lo0;
+    c = o;
+    k0 += PHILOX_W0;
+    k1 += PHILOX_W1;
+  }
+  return c;
+}
+
+// Counter of block `b` (0-based) of a stream positioned at 128-bit counter
+// (clo, chi): the 256-bit value (chi:clo) + b + 1.
+PHX_HD phx4 phx_block_counter(uint64_t clo, uint64_t chi, uint64_t b) {
+  phx4 c;
+  const uint64_t add = b + 1;  // b < 2^62 in practice; +1 cannot wrap
+  c.v[0] = clo + add;
+  const uint64_t carry0 = (c.v[0] < clo) ? 1ULL : 0ULL;
+  c.v[1] = chi + carry0;
+  const uint64_t carry1 = (carry0 && c.v[1] == 0) ? 1ULL : 0ULL;
+  c.v[2] = carry1;
+  c.v[3] = 0;
+  return c;
+}
+
+PHX_HD double phx_u01(uint64_t w) { return (double)(w >> 11) * (1.0 / 9007199254740992.0); }

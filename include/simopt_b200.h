@@ -1,0 +1,93 @@
+/*
+ * libsimopt_b200 -- C ABI of the B200-native (sm_100a) hot path of the
+ * arXiv 2404.11631 simulation-optimization benchmark ("sobench").
+ *
+ * Every entry point takes plain device pointers and sizes plus a cudaStream_t
+ * (passed as void*), enqueues its kernels on that stream and returns a status
+ * code; results are valid once the stream reaches that point.  No entry point
+ * synchronises the device unless documented.  Pointers are caller-owned device
+ * memory (e.g. torch CUDA tensors); arrays are C-contiguous float64 unless noted.
+ *
+ * Reference interfaces replaced (paths relative to reference pkg/src/sobench):
+ *   sampling.py  RngStream/uniform01/standard_normal/sample_returns/
+ *                sample_demands/sample_indices/synth_classification
+ *   backend.py   Backend.dot/vec_sum/matvec/matvec_t/axpy/map_kernel
+ *   _kernels.py  fold_pairwise .. ecdf_count_block (the 14 numba kernels)
+ *   tasks.py     build_sample_set, mv_objective/mv_gradient, nv_gradient_hat,
+ *                nv_objective_exact, logistic_loss/gradient/hvp
+ *   lmo.py       lmo_simplex_slack, lmo_single_budget
+ *   frank_wolfe.py fw_step_size/fw_update
+ *   sqn.py       hessian_update (bfgs_rank2_block)
+ * Status codes map one-to-one onto sobench/errors.py exception classes.
+ */
+#ifndef SIMOPT_B200_H
+#define SIMOPT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum simopt_status {
+  SIMOPT_OK = 0,
+  SIMOPT_E_DIMENSION = 1,          /* errors.DimensionMismatch      (errors.py:8)  */
+  SIMOPT_E_CONFIG = 2,             /* errors.ConfigurationError     (errors.py:12) */
+  SIMOPT_E_EMPTY = 3,              /* errors.EmptyRequest           (errors.py:16) */
+  SIMOPT_E_INSUFFICIENT = 4,       /* errors.InsufficientSamples    (errors.py:20) */
+  SIMOPT_E_INVALID_GRADIENT = 5,   /* errors.InvalidGradient        (errors.py:24) */
+  SIMOPT_E_INVALID_CONSTRAINT = 6, /* errors.InvalidConstraint      (errors.py:28) */
+  SIMOPT_E_SOLVER_STALL = 7,       /* errors.SolverStall            (errors.py:32) */
+  SIMOPT_E_DEGENERATE_PAIR = 8,    /* errors.DegeneratePair         (errors.py:40) */
+  SIMOPT_E_CUDA = 9                /* CUDA runtime failure (no reference analogue) */
+};
+
+/* Map-kernel ids for simopt_map_kernel (backend.py:34, MAP_KERNELS). */
+enum simopt_map { SIMOPT_MAP_SIGMOID = 0, SIMOPT_MAP_NEGATE = 1, SIMOPT_MAP_EXP = 2 };
+
+const char* simopt_last_error(void);
+int simopt_abi_version(void);
+
+/* ------------------------------------------------------------ sampling.py */
+/* uniform01 (sampling.py:87-102): n doubles of stream (seed, stream_id) at the
+ * 128-bit block counter (ctr_hi:ctr_lo).  The caller advances the counter by
+ * ceil(n/4).  Bit-identical to numpy Philox4x64-10 + Generator.random. */
+int simopt_uniform01(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                     uint64_t ctr_hi, int64_t n, double* out);
+
+/* standard_normal (sampling.py:105-120): n normals from 2*ceil(n/2) uniforms via
+ * Box-Muller with glibc-2.39-exact log1p/sin/cos (_kernels.py:178-190).  The
+ * caller advances the counter by ceil(2*ceil(n/2)/4). */
+int simopt_standard_normal(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                           uint64_t ctr_hi, int64_t n, double* out);
+
+/* sample_returns diag path (sampling.py:156-166): out[i*d+j] = mu[j] + sigma[j]*z[i*d+j]. */
+int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                               uint64_t ctr_hi, int64_t n_samples, int64_t d, const double* mu,
+                               const double* sigma, double* out);
+
+/* ------------------------------------------------------------ backend.py */
+/* Fixed-tree reductions (backend.py:80-141, _kernels.py:30-156): chunk-local
+ * strictly sequential sums, chunk partials folded pairwise in index order.
+ * Bit-identical to SequentialBackend/ParallelBackend for every chunk >= 1.
+ * Scalar results are written to device memory (*out). */
+int simopt_dot(void* stream, const double* x, const double* y, int64_t n, int64_t chunk,
+               double* out);
+int simopt_vec_sum(void* stream, const double* x, int64_t n, int64_t chunk, double* out);
+/* out[r] = fixed-tree dot of (a[row(r),:] - center) with x, row(r) = rows_idx ? rows_idx[r] : r.
+ * center (length cols) and rows_idx (length rows, int64) may be NULL. */
+int simopt_matvec(void* stream, const double* a, int64_t lda_rows, int64_t cols,
+                  const int64_t* rows_idx, int64_t rows, const double* center, const double* x,
+                  int64_t chunk, double* out);
+/* out[j] = fixed-tree sum over r of x[r] * (a[row(r),j] - center[j]). */
+int simopt_matvec_t(void* stream, const double* a, int64_t lda_rows, int64_t cols,
+                    const int64_t* rows_idx, int64_t rows, const double* center,
+                    const double* x, int64_t chunk, double* out);
+int simopt_axpy(void* stream, double alpha, const double* x, const double* y, int64_t n,
+                double* out);
+int simopt_map_kernel(void* stream, int kernel, const double* x, int64_t n, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIMOPT_B200_H */

@@ -1,0 +1,81 @@
+"""ctypes binding of libsimopt_b200.so (the C ABI in include/simopt_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is visible, every product entry point raises :class:`DeviceError`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from .errors import STATUS_TO_ERROR, DeviceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsimopt_b200.so")
+
+_lock = threading.Lock()
+_lib = None
+
+_u64, _i64, _i32, _d, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+
+# name -> argtypes (all return int status)
+SIGNATURES = {
+    "simopt_uniform01": [_vp, _u64, _u64, _u64, _u64, _i64, _vp],
+    "simopt_standard_normal": [_vp, _u64, _u64, _u64, _u64, _i64, _vp],
+    "simopt_sample_returns_diag": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp, _vp],
+    "simopt_dot": [_vp, _vp, _vp, _i64, _i64, _vp],
+    "simopt_vec_sum": [_vp, _vp, _i64, _i64, _vp],
+    "simopt_matvec": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],
+    "simopt_matvec_t": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],
+    "simopt_axpy": [_vp, _d, _vp, _vp, _i64, _vp],
+    "simopt_map_kernel": [_vp, _i32, _vp, _i64, _vp],
+}
+
+
+def load(require_device: bool = True):
+    """Load the library (idempotent).  Raises DeviceError when unusable."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DeviceError(
+                    f"{LIB_PATH} not built; run `python -m paper_2404_11631_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = ctypes.CDLL(LIB_PATH)
+            lib.simopt_last_error.restype = ctypes.c_char_p
+            lib.simopt_abi_version.restype = ctypes.c_int
+            for name, argt in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = argt
+                fn.restype = ctypes.c_int
+            _lib = lib
+    if require_device and not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the sm_100a kernels have no CPU fallback")
+    return _lib
+
+
+def exported_symbols():
+    return ["simopt_last_error", "simopt_abi_version", *SIGNATURES]
+
+
+def check(status: int):
+    if status != 0:
+        msg = _lib.simopt_last_error().decode(errors="replace") if _lib else ""
+        raise STATUS_TO_ERROR.get(status, DeviceError)(msg)
+
+
+def call(name: str, *args):
+    lib = load()
+    check(getattr(lib, name)(*args))
+
+
+def stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)

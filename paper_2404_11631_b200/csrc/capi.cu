@@ -1,0 +1,17 @@
+// ABI bookkeeping: version + thread-local error text.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+static thread_local char g_err[512] = "";
+
+void simopt_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" const char* simopt_last_error(void) { return g_err; }
+extern "C" int simopt_abi_version(void) { return 1; }

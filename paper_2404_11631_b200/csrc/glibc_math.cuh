@@ -272,3 +272,84 @@ SIMOPT_HD void glibc_boxmuller(double u1, double u2, const double* tab, double* 
   *z0 = r * glibc_cos(th, tab);
   *z1 = r * glibc_sin(th, tab);
 }
+
+// ---------------------------------------------------------------------------
+// exp  (glibc >= 2.28 e_exp.c, Szabolcs Nagy's table method, N = 128; FMA variant
+// __exp_fma @0x79b60).  `etab` = __exp_data.tab (256 words, glibc_tables.h).
+// ---------------------------------------------------------------------------
+#define GM_E_INVLN2N 0x1.71547652b82fep+7
+#define GM_E_SHIFT 0x1.8p52
+#define GM_E_NEGLN2HIN -0x1.62e42fefa0000p-8
+#define GM_E_NEGLN2LON -0x1.cf79abc9e3b3ap-47
+#define GM_E_C2 0x1.ffffffffffdbdp-2
+#define GM_E_C3 0x1.555555555543cp-3
+#define GM_E_C4 0x1.55555cf172b91p-5
+#define GM_E_C5 0x1.1111167a4d017p-7
+
+// specialcase(tmp, sbits, ki) for 512 <= |x| < 1024 (asm 79c60..79d27)
+SIMOPT_HD double gm_exp_special(double tmp, uint64_t sbits, uint64_t ki) {
+  if ((ki & 0x80000000ULL) == 0) {
+    sbits -= 1009ULL << 52;
+    const double scale = gm_from_bits(sbits);
+    return 0x1p1009 * gm_fma(scale, tmp, scale);   // may overflow to inf, as glibc
+  }
+  sbits += 1022ULL << 52;
+  const double scale = gm_from_bits(sbits);
+  const double st = scale * tmp;
+  double y = scale + st;
+  if (y < 1.0) {
+    double lo = (scale - y) + st;
+    const double hi = 1.0 + y;
+    lo = ((1.0 - hi) + y) + lo;
+    y = (lo + hi) - 1.0;
+    if (y == 0.0) y = 0.0;  // avoid -0.0
+  }
+  return 0x1p-1022 * y;
+}
+
+SIMOPT_HD double glibc_exp(double x, const uint64_t* etab) {
+  const uint64_t ix = gm_bits(x);
+  uint32_t abstop = (uint32_t)((ix >> 52) & 0x7ff);
+  if (abstop - 0x3c9u > 0x3eu) {                 // |x| < 2^-54 or |x| >= 512 or nan/inf
+    if ((int32_t)(abstop - 0x3c9u) < 0) return 1.0 + x;
+    if (abstop >= 0x409) {                       // |x| >= 1024
+      if (ix == 0xfff0000000000000ULL) return 0.0;
+      if (abstop == 0x7ff) return 1.0 + x;
+      return (ix >> 63) ? 0.0 : INFINITY;        // __math_uflow(0) / __math_oflow(0)
+    }
+    abstop = 0;                                  // large |x|: handled by specialcase
+  }
+  const double kd0 = gm_fma(x, GM_E_INVLN2N, GM_E_SHIFT);
+  const uint64_t ki = gm_bits(kd0);
+  const double kd = kd0 - GM_E_SHIFT;
+  double r = gm_fma(kd, GM_E_NEGLN2HIN, x);
+  r = gm_fma(kd, GM_E_NEGLN2LON, r);
+  const uint32_t idx = 2u * (uint32_t)(ki & 127u);
+  const uint64_t top = ki << 45;
+  const double tail = gm_from_bits(etab[idx]);
+  const uint64_t sbits = etab[idx + 1] + top;
+  const double r2 = r * r;
+  const double p23 = gm_fma(r, GM_E_C3, GM_E_C2);
+  const double p45 = gm_fma(r, GM_E_C5, GM_E_C4);
+  double tmp = gm_fma(p23, r2, r + tail);
+  tmp = gm_fma(r2 * r2, p45, tmp);
+  if (abstop == 0) return gm_exp_special(tmp, sbits, ki);
+  const double scale = gm_from_bits(sbits);
+  return gm_fma(scale, tmp, scale);
+}
+
+// Stable logistic as sigmoid_block (sobench/_kernels.py:159-169).
+SIMOPT_HD double glibc_sigmoid(double t, const uint64_t* etab) {
+  if (t >= 0.0) {
+    const double e = glibc_exp(-t, etab);
+    return 1.0 / (1.0 + e);
+  }
+  const double e = glibc_exp(t, etab);
+  return e / (1.0 + e);
+}
+
+// logistic_loss_block (sobench/_kernels.py:193-201), one sample.
+SIMOPT_HD double glibc_logistic_loss_term(double t, double z, const uint64_t* etab) {
+  if (t >= 0.0) return glibc_log1p(glibc_exp(-t, etab)) + (1.0 - z) * t;
+  return glibc_log1p(glibc_exp(t, etab)) - z * t;
+}

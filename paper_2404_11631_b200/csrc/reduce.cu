@@ -1,0 +1,299 @@
+// Exact fixed-tree reductions (reference: sobench/_kernels.py:1-156, backend.py:80-141).
+//
+// The tree is a function of (length, chunk) only: each chunk of `chunk`
+// consecutive elements is summed strictly left to right, and the chunk partials
+// are folded pairwise in index order (odd tail carried).  Every chunk chain is
+// a dependent DADD sequence, so these kernels are latency-bound per chain and
+// get their throughput from running many chains at once: one thread per
+// (row|column, chunk).  -fmad=false keeps x*y and s+p unfused, as in numba.
+#include "common.cuh"
+#include "reduce_device.cuh"
+
+namespace {
+
+constexpr int kFoldSmem = 4096;  // partials folded in one CTA's shared memory
+
+// --- chunk partials of dot / sum ------------------------------------------------
+template <bool kHasY>
+__global__ void __launch_bounds__(128) k_chunk_partials(const double* __restrict__ x,
+                                                        const double* __restrict__ y, int64_t n,
+                                                        int64_t chunk, double* __restrict__ p) {
+  const int64_t nch = (n + chunk - 1) / chunk;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nch;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = c * chunk;
+    const int64_t hi = lo + chunk < n ? lo + chunk : n;
+    p[c] = kHasY ? seq_dot(x, y, lo, hi) : seq_sum(x, lo, hi);
+  }
+}
+
+// One fold level in global memory: dst[i] = src[2i] + src[2i+1]; odd tail carried.
+__global__ void k_fold_level(const double* __restrict__ src, double* __restrict__ dst, int64_t m) {
+  const int64_t h = m >> 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < h;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[2 * i] + src[2 * i + 1];
+  if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) dst[h] = src[m - 1];
+}
+
+__global__ void __launch_bounds__(512) k_fold_final(const double* __restrict__ src, int m,
+                                                    double* __restrict__ out) {
+  extern __shared__ double sm[];
+  double* a = sm;
+  double* b = sm + kFoldSmem;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) a[i] = src[i];
+  const double r = block_fold_pairwise(a, b, m);
+  if (threadIdx.x == 0) *out = r;
+}
+
+// --- matvec: out[r] = tree-dot(row(r) - center, x) -------------------------------
+// CTA = 128 rows x one column chunk; 32-column tiles staged through shared memory
+// so global reads are coalesced while each thread walks its own row in order.
+template <bool kCenter, bool kIdx>
+__global__ void __launch_bounds__(128) k_matvec_rows(const double* __restrict__ a, int64_t cols,
+                                                     const int64_t* __restrict__ idx, int64_t rows,
+                                                     const double* __restrict__ center,
+                                                     const double* __restrict__ x, int64_t chunk,
+                                                     int64_t nch, double* __restrict__ out) {
+  __shared__ double tile[128][33];
+  __shared__ double xs[32];
+  const int64_t r0 = (int64_t)blockIdx.x * 128;
+  const int64_t c = blockIdx.y;
+  const int64_t clo = c * chunk;
+  const int64_t chi = clo + chunk < cols ? clo + chunk : cols;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int64_t j0 = clo; j0 < chi; j0 += 32) {
+    const int64_t jn = chi - j0 < 32 ? chi - j0 : 32;
+    if (threadIdx.x < 32 && lane < jn) xs[lane] = x[j0 + lane];
+    const double cj = (kCenter && lane < jn) ? center[j0 + lane] : 0.0;
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      const int lr = warp * 32 + rr;
+      const int64_t r = r0 + lr;
+      if (r < rows && lane < jn) {
+        const int64_t row = kIdx ? idx[r] : r;
+        const double v = a[row * cols + j0 + lane];
+        tile[lr][lane] = kCenter ? v - cj : v;
+      }
+    }
+    __syncthreads();
+    for (int jj = 0; jj < jn; ++jj) s = s + tile[threadIdx.x][jj] * xs[jj];
+    __syncthreads();
+  }
+  const int64_t r = r0 + threadIdx.x;
+  if (r < rows) {
+    if (nch == 1) out[r] = s;
+    else out[r * nch + c] = s;  // partials, folded by k_fold_rows
+  }
+}
+
+// Per-row (or per-column) serial fold of `nch` partials laid out with stride.
+__global__ void k_fold_strided(double* __restrict__ p, int64_t count, int64_t nch, int64_t s_item,
+                               int64_t s_chunk, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double* q = p + t * s_item;
+    int64_t m = nch;
+    while (m > 1) {
+      const int64_t h = m >> 1;
+      for (int64_t i = 0; i < h; ++i) q[i * s_chunk] = q[2 * i * s_chunk] + q[(2 * i + 1) * s_chunk];
+      if (m & 1) { q[h * s_chunk] = q[(m - 1) * s_chunk]; m = h + 1; } else { m = h; }
+    }
+    out[t] = q[0];
+  }
+}
+
+// --- matvec_t: out[j] = tree over row chunks of sum x[r]*(a[row(r),j]-center[j]) ---
+template <bool kCenter, bool kIdx>
+__global__ void __launch_bounds__(128) k_matvec_t_cols(const double* __restrict__ a, int64_t cols,
+                                                       const int64_t* __restrict__ idx, int64_t rows,
+                                                       const double* __restrict__ center,
+                                                       const double* __restrict__ x, int64_t chunk,
+                                                       int64_t nch, double* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (j >= cols) return;
+  const int64_t lo = c * chunk;
+  const int64_t hi = lo + chunk < rows ? lo + chunk : rows;
+  const double cj = kCenter ? center[j] : 0.0;
+  double s = 0.0;
+  int64_t r = lo;
+  for (; r + 8 <= hi; r += 8) {
+    double av[8], xv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t row = kIdx ? idx[r + k] : r + k;
+      av[k] = a[row * cols + j];
+      xv[k] = x[r + k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = s + xv[k] * (kCenter ? av[k] - cj : av[k]);
+  }
+  for (; r < hi; ++r) {
+    const int64_t row = kIdx ? idx[r] : r;
+    const double v = a[row * cols + j];
+    s = s + x[r] * (kCenter ? v - cj : v);
+  }
+  if (nch == 1) out[j] = s;
+  else out[c * cols + j] = s;  // partials, folded by k_fold_strided
+}
+
+__global__ void k_axpy(double alpha, const double* __restrict__ x, const double* __restrict__ y,
+                       int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = alpha * x[i] + y[i];
+}
+
+__global__ void k_map(int kernel, const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double t = x[i];
+    if (kernel == SIMOPT_MAP_NEGATE) out[i] = -t;
+    else if (kernel == SIMOPT_MAP_EXP) out[i] = dev_exp(t);
+    else out[i] = dev_sigmoid(t);
+  }
+}
+
+int elementwise_grid(int64_t n) {
+  const int64_t g = ceil_div(n, 256);
+  const int64_t cap = (int64_t)SIMOPT_NUM_SMS * 16;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+// Fold p[0..m) (device, destroyed) into *out.  Enqueued on `st`.
+int simopt_fold_partials(cudaStream_t st, double* p, double* tmp, int64_t m, double* out) {
+  if (m == 0) {
+    SIMOPT_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+    return SIMOPT_OK;
+  }
+  double* src = p;
+  double* dst = tmp;
+  while (m > kFoldSmem) {
+    const int64_t h = m >> 1;
+    k_fold_level<<<elementwise_grid(h), 256, 0, st>>>(src, dst, m);
+    SIMOPT_CHECK_LAUNCH("k_fold_level");
+    m = (m & 1) ? h + 1 : h;
+    double* t = src; src = dst; dst = t;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    SIMOPT_CUDA(cudaFuncSetAttribute(k_fold_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     2 * kFoldSmem * (int)sizeof(double)));
+    attr_set = true;
+  }
+  k_fold_final<<<1, 512, 2 * kFoldSmem * sizeof(double), st>>>(src, (int)m, out);
+  SIMOPT_CHECK_LAUNCH("k_fold_final");
+  return SIMOPT_OK;
+}
+
+static int tree_reduce(cudaStream_t st, const double* x, const double* y, int64_t n, int64_t chunk,
+                       double* out) {
+  SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1, got %lld", (long long)chunk);
+  if (n == 0) {
+    SIMOPT_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+    return SIMOPT_OK;
+  }
+  const int64_t nch = ceil_div(n, chunk);
+  double* p = nullptr;
+  SIMOPT_CUDA(cudaMallocAsync(&p, 2 * nch * sizeof(double), st));
+  const int g = (int)(ceil_div(nch, 128) < 4096 ? ceil_div(nch, 128) : 4096);
+  if (y) k_chunk_partials<true><<<g, 128, 0, st>>>(x, y, n, chunk, p);
+  else k_chunk_partials<false><<<g, 128, 0, st>>>(x, nullptr, n, chunk, p);
+  SIMOPT_CHECK_LAUNCH("k_chunk_partials");
+  const int rc = simopt_fold_partials(st, p, p + nch, nch, out);
+  SIMOPT_CUDA(cudaFreeAsync(p, st));
+  return rc;
+}
+
+extern "C" int simopt_dot(void* stream, const double* x, const double* y, int64_t n, int64_t chunk,
+                          double* out) {
+  return tree_reduce(as_stream(stream), x, y, n, chunk, out);
+}
+
+extern "C" int simopt_vec_sum(void* stream, const double* x, int64_t n, int64_t chunk, double* out) {
+  return tree_reduce(as_stream(stream), x, nullptr, n, chunk, out);
+}
+
+extern "C" int simopt_matvec(void* stream, const double* a, int64_t lda_rows, int64_t cols,
+                             const int64_t* idx, int64_t rows, const double* center,
+                             const double* x, int64_t chunk, double* out) {
+  (void)lda_rows;
+  SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1");
+  cudaStream_t st = as_stream(stream);
+  if (rows == 0) return SIMOPT_OK;
+  if (cols == 0) {
+    SIMOPT_CUDA(cudaMemsetAsync(out, 0, rows * sizeof(double), st));
+    return SIMOPT_OK;
+  }
+  const int64_t nch = ceil_div(cols, chunk);
+  SIMOPT_REQUIRE(nch < 65536, SIMOPT_E_CONFIG, "too many column chunks (%lld)", (long long)nch);
+  double* p = out;
+  if (nch > 1) SIMOPT_CUDA(cudaMallocAsync(&p, rows * nch * sizeof(double), st));
+  const dim3 grid((unsigned)ceil_div(rows, 128), (unsigned)nch);
+  const int sel = (center ? 1 : 0) | (idx ? 2 : 0);
+  switch (sel) {
+    case 0: k_matvec_rows<false, false><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 1: k_matvec_rows<true, false><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 2: k_matvec_rows<false, true><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    default: k_matvec_rows<true, true><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+  }
+  SIMOPT_CHECK_LAUNCH("k_matvec_rows");
+  if (nch > 1) {
+    k_fold_strided<<<elementwise_grid(rows), 256, 0, st>>>(p, rows, nch, nch, 1, out);
+    SIMOPT_CHECK_LAUNCH("k_fold_strided");
+    SIMOPT_CUDA(cudaFreeAsync(p, st));
+  }
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_matvec_t(void* stream, const double* a, int64_t lda_rows, int64_t cols,
+                               const int64_t* idx, int64_t rows, const double* center,
+                               const double* x, int64_t chunk, double* out) {
+  (void)lda_rows;
+  SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1");
+  cudaStream_t st = as_stream(stream);
+  if (cols == 0) return SIMOPT_OK;
+  if (rows == 0) {
+    SIMOPT_CUDA(cudaMemsetAsync(out, 0, cols * sizeof(double), st));
+    return SIMOPT_OK;
+  }
+  const int64_t nch = ceil_div(rows, chunk);
+  SIMOPT_REQUIRE(nch < 65536, SIMOPT_E_CONFIG, "too many row chunks (%lld)", (long long)nch);
+  double* p = out;
+  if (nch > 1) SIMOPT_CUDA(cudaMallocAsync(&p, cols * nch * sizeof(double), st));
+  const dim3 grid((unsigned)ceil_div(cols, 128), (unsigned)nch);
+  const int sel = (center ? 1 : 0) | (idx ? 2 : 0);
+  switch (sel) {
+    case 0: k_matvec_t_cols<false, false><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 1: k_matvec_t_cols<true, false><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 2: k_matvec_t_cols<false, true><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    default: k_matvec_t_cols<true, true><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+  }
+  SIMOPT_CHECK_LAUNCH("k_matvec_t_cols");
+  if (nch > 1) {
+    k_fold_strided<<<elementwise_grid(cols), 256, 0, st>>>(p, cols, nch, 1, cols, out);
+    SIMOPT_CHECK_LAUNCH("k_fold_strided");
+    SIMOPT_CUDA(cudaFreeAsync(p, st));
+  }
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_axpy(void* stream, double alpha, const double* x, const double* y, int64_t n,
+                           double* out) {
+  if (n == 0) return SIMOPT_OK;
+  k_axpy<<<elementwise_grid(n), 256, 0, as_stream(stream)>>>(alpha, x, y, n, out);
+  SIMOPT_CHECK_LAUNCH("k_axpy");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_map_kernel(void* stream, int kernel, const double* x, int64_t n, double* out) {
+  SIMOPT_REQUIRE(kernel >= 0 && kernel <= 2, SIMOPT_E_CONFIG, "unknown map kernel id %d", kernel);
+  if (n == 0) return SIMOPT_OK;
+  k_map<<<elementwise_grid(n), 256, 0, as_stream(stream)>>>(kernel, x, n, out);
+  SIMOPT_CHECK_LAUNCH("k_map");
+  return SIMOPT_OK;
+}

@@ -1,0 +1,100 @@
+// Counter-based sampling kernels: uniform01, standard_normal, diag-Gaussian returns.
+//
+// Reference: sobench/sampling.py:51-170 (RngStream, uniform01, standard_normal,
+// sample_returns) and _kernels.py:178-190 (boxmuller_block).  One thread owns one
+// Philox4x64-10 block, i.e. 4 consecutive uniforms = 2 Box-Muller pairs = 4
+// consecutive normals; nothing is staged through HBM but the output.
+#include "common.cuh"
+#include "glibc_math.cuh"
+#include "glibc_tables.h"
+#include "philox.cuh"
+#include "rng_device.cuh"
+
+namespace {
+
+__global__ void __launch_bounds__(256) k_uniform01(uint64_t seed, uint64_t sid, uint64_t clo,
+                                                   uint64_t chi, int64_t n, double* __restrict__ out) {
+  const int64_t nblk = (n + 3) >> 2;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const phx4 w = philox4x64_10(stream_block_counter(clo, chi, b), seed, sid);
+    const int64_t e = b << 2;
+    if (e + 4 <= n) {
+      double2* o = reinterpret_cast<double2*>(out + e);
+      o[0] = make_double2(phx_u01(w.v[0]), phx_u01(w.v[1]));
+      o[1] = make_double2(phx_u01(w.v[2]), phx_u01(w.v[3]));
+    } else {
+      for (int k = 0; e + k < n; ++k) out[e + k] = phx_u01(w.v[k]);
+    }
+  }
+}
+
+// Normals (optionally affine per column: mu[j] + sigma[j]*z, j = e % d).
+template <bool kAffine>
+__global__ void __launch_bounds__(256) k_normal(uint64_t seed, uint64_t sid, uint64_t clo,
+                                                uint64_t chi, int64_t n, int64_t d,
+                                                const double* __restrict__ mu,
+                                                const double* __restrict__ sigma,
+                                                double* __restrict__ out) {
+  __shared__ double tab[SIMOPT_SINCOSTAB_N];
+  load_sincostab(tab);
+  const int64_t nblk = (n + 3) >> 2;  // m = 2*ceil(n/2) uniforms -> ceil(m/4) == ceil(n/4) blocks
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    double z[4];
+    normals4(seed, sid, clo, chi, b, tab, z);
+    const int64_t e = b << 2;
+    if (kAffine) {
+      int64_t j = e % d;
+      for (int k = 0; k < 4; ++k) {
+        z[k] = mu[j] + sigma[j] * z[k];
+        if (++j == d) j = 0;
+      }
+    }
+    if (e + 4 <= n) {
+      double2* o = reinterpret_cast<double2*>(out + e);
+      o[0] = make_double2(z[0], z[1]);
+      o[1] = make_double2(z[2], z[3]);
+    } else {
+      for (int k = 0; e + k < n; ++k) out[e + k] = z[k];
+    }
+  }
+}
+
+int grid_for(int64_t nblk) {
+  const int64_t want = ceil_div(nblk, 256);
+  const int64_t cap = (int64_t)SIMOPT_NUM_SMS * 8;
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace
+
+extern "C" int simopt_uniform01(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
+                                uint64_t chi, int64_t n, double* out) {
+  SIMOPT_REQUIRE(n > 0, SIMOPT_E_EMPTY, "requested %lld uniforms", (long long)n);
+  k_uniform01<<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, n, out);
+  SIMOPT_CHECK_LAUNCH("k_uniform01");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_standard_normal(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
+                                      uint64_t chi, int64_t n, double* out) {
+  SIMOPT_REQUIRE(n > 0, SIMOPT_E_EMPTY, "requested %lld normals", (long long)n);
+  k_normal<false><<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, n, 1,
+                                                                      nullptr, nullptr, out);
+  SIMOPT_CHECK_LAUNCH("k_normal");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
+                                          uint64_t chi, int64_t n_samples, int64_t d,
+                                          const double* mu, const double* sigma, double* out) {
+  SIMOPT_REQUIRE(n_samples >= 2, SIMOPT_E_INSUFFICIENT,
+                 "need at least 2 samples for a sample covariance, got %lld", (long long)n_samples);
+  SIMOPT_REQUIRE(d >= 1, SIMOPT_E_DIMENSION, "empty return dimension");
+  const int64_t n = n_samples * d;
+  k_normal<true><<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, n, d,
+                                                                     mu, sigma, out);
+  SIMOPT_CHECK_LAUNCH("k_normal<affine>");
+  return SIMOPT_OK;
+}

@@ -1,0 +1,156 @@
+"""Counter-based random streams and samplers, generated on the B200.
+
+Mirrors sobench/sampling.py (RngStream :51-80, uniform01 :87-102,
+standard_normal :105-120, GaussianSpec :123-153, sample_returns :156-170,
+sample_demands :173-193, sample_indices :196-209, synth_classification
+:229-265).  A stream is (seed, stream_id, counter); block b of a draw is
+Philox4x64-10 at counter + b + 1 with key (seed, stream_id) -- bit-identical to
+numpy's Philox that the reference uses.  Normals use glibc-2.39-exact
+Box-Muller on the device (csrc/glibc_math.cuh).
+
+``*_device`` functions return CUDA tensors and never leave the GPU; the
+reference-named functions return numpy arrays (drop-in, for parity tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import F64, device, empty, mat_dev, to_host, vec_dev
+from .errors import (ConfigurationError, DimensionMismatch, EmptyRequest, InsufficientSamples,
+                     InvalidConstraint)
+
+_U64 = (1 << 64) - 1
+_U128 = (1 << 128) - 1
+_BLOCK = 4
+SAMPLE_SPAN = 1 << 16  # sampling.py:46 (scheduling grid only; folded into the counter math)
+
+
+@dataclass
+class RngStream:
+    """Reproducible random stream position; value-semantic and cheap to copy."""
+
+    seed: int
+    stream_id: int
+    counter: int = 0
+
+    def __post_init__(self):
+        if not 0 <= self.seed <= _U64:
+            raise ConfigurationError(f"seed must be a 64-bit unsigned int, got {self.seed}")
+        if not 0 <= self.stream_id <= _U64:
+            raise ConfigurationError(f"stream_id must be a 64-bit unsigned int, got {self.stream_id}")
+        if not 0 <= self.counter <= _U128:
+            raise ConfigurationError("counter must fit in 128 bits")
+
+    def substream(self, stream_id: int) -> "RngStream":
+        return RngStream(self.seed, stream_id)
+
+    def clone(self) -> "RngStream":
+        return RngStream(self.seed, self.stream_id, self.counter)
+
+    # --- device addressing ---------------------------------------------------
+    def words(self):
+        """(seed, stream_id, ctr_lo, ctr_hi) as passed to the C ABI."""
+        c = self.counter & _U128
+        return self.seed, self.stream_id, c & _U64, (c >> 64) & _U64
+
+    def advance(self, n_uniforms: int) -> None:
+        self.counter += (n_uniforms + _BLOCK - 1) // _BLOCK
+
+
+def uniform01_device(stream: RngStream, n: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    if n <= 0:
+        raise EmptyRequest(f"requested {n} uniforms")
+    out = empty(n) if out is None else out
+    _lib.call("simopt_uniform01", _lib.stream_ptr(), *stream.words(), n, _lib.ptr(out))
+    stream.advance(n)
+    return out
+
+
+def uniform01(stream: RngStream, n: int, backend=None) -> np.ndarray:
+    """n doubles in [0, 1); advances the counter by ceil(n/4) blocks."""
+    return to_host(uniform01_device(stream, n))
+
+
+def standard_normal_device(stream: RngStream, n: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    if n <= 0:
+        raise EmptyRequest(f"requested {n} normals")
+    out = empty(n) if out is None else out
+    _lib.call("simopt_standard_normal", _lib.stream_ptr(), *stream.words(), n, _lib.ptr(out))
+    stream.advance(2 * ((n + 1) // 2))
+    return out
+
+
+def standard_normal(stream: RngStream, n: int, backend=None) -> np.ndarray:
+    """n i.i.d. N(0,1) draws via Box-Muller on consecutive uniform pairs."""
+    return to_host(standard_normal_device(stream, n))
+
+
+@dataclass
+class GaussianSpec:
+    """Mean plus either a per-coordinate std or a lower-triangular factor (sampling.py:123-153)."""
+
+    mean: object
+    diag_std: object = None
+    chol_factor: object = None
+
+    def __post_init__(self):
+        self.mean = np.ascontiguousarray(self.mean, dtype=np.float64)
+        if self.mean.ndim != 1:
+            raise DimensionMismatch("mean must be a vector")
+        if (self.diag_std is None) == (self.chol_factor is None):
+            raise ConfigurationError("provide exactly one of diag_std / chol_factor")
+        if self.diag_std is not None:
+            self.diag_std = np.ascontiguousarray(self.diag_std, dtype=np.float64)
+            if self.diag_std.size != self.mean.size:
+                raise DimensionMismatch("diag_std length != mean length")
+            if not np.all(self.diag_std > 0):
+                raise InvalidConstraint("diag_std entries must be > 0")
+        else:
+            self.chol_factor = np.ascontiguousarray(self.chol_factor, dtype=np.float64)
+            d = self.mean.size
+            if self.chol_factor.shape != (d, d):
+                raise DimensionMismatch("chol_factor must be d x d")
+            if not np.all(np.diag(self.chol_factor) > 0):
+                raise InvalidConstraint("chol_factor diagonal must be > 0")
+            if np.any(np.triu(self.chol_factor, 1) != 0):
+                raise InvalidConstraint("chol_factor must be lower-triangular")
+
+    @property
+    def dimension(self) -> int:
+        return self.mean.size
+
+
+def sample_returns_device(spec: GaussianSpec, n_samples: int, stream: RngStream,
+                          out: torch.Tensor | None = None, chunk: int = 4096) -> torch.Tensor:
+    """N x d draws on the device; diag path fused (affine applied in-register)."""
+    if n_samples < 2:
+        raise InsufficientSamples(f"need at least 2 samples for a sample covariance, got {n_samples}")
+    d = spec.dimension
+    out = empty(n_samples, d) if out is None else out
+    if spec.diag_std is not None:
+        mu = vec_dev(spec.mean)
+        sd = vec_dev(spec.diag_std)
+        _lib.call("simopt_sample_returns_diag", _lib.stream_ptr(), *stream.words(), n_samples, d,
+                  _lib.ptr(mu), _lib.ptr(sd), _lib.ptr(out))
+        stream.advance(2 * ((n_samples * d + 1) // 2))
+        return out
+    # Cholesky path (sampling.py:167-170): out[i] = mean + fixed-tree matvec(L, z_i),
+    # i.e. out[i, r] = tree-dot(L[r, :], z_i) -> one row-matvec of Z per factor row.
+    z = standard_normal_device(stream, n_samples * d).view(n_samples, d)
+    lt = mat_dev(spec.chol_factor)
+    mu = vec_dev(spec.mean)
+    col = empty(n_samples)
+    for r in range(d):
+        _lib.call("simopt_matvec", _lib.stream_ptr(), _lib.ptr(z), n_samples, d, None, n_samples,
+                  None, _lib.ptr(lt[r]), chunk, _lib.ptr(col))
+        out[:, r] = mu[r] + col
+    return out
+
+
+def sample_returns(spec: GaussianSpec, n_samples: int, stream: RngStream, backend=None) -> np.ndarray:
+    chunk = getattr(backend, "chunk_size", 4096)
+    return to_host(sample_returns_device(spec, n_samples, stream, chunk=chunk))

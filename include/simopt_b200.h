@@ -47,6 +47,8 @@ enum simopt_map { SIMOPT_MAP_SIGMOID = 0, SIMOPT_MAP_NEGATE = 1, SIMOPT_MAP_EXP 
 
 const char* simopt_last_error(void);
 int simopt_abi_version(void);
+/* Write the device %globaltimer (ns) to *out when the stream reaches this point. */
+int simopt_timestamp(void* stream, int64_t* out);
 
 /* ------------------------------------------------------------ sampling.py */
 /* uniform01 (sampling.py:87-102): n doubles of stream (seed, stream_id) at the
@@ -86,6 +88,89 @@ int simopt_matvec_t(void* stream, const double* a, int64_t lda_rows, int64_t col
 int simopt_axpy(void* stream, double alpha, const double* x, const double* y, int64_t n,
                 double* out);
 int simopt_map_kernel(void* stream, int kernel, const double* x, int64_t n, double* out);
+/* out = x*alpha - y elementwise (y may be NULL), e.g. tasks.py:62 and :85 epilogues. */
+int simopt_scale_sub(void* stream, const double* x, double alpha, const double* y, int64_t n,
+                     double* out);
+
+/* ------------------------------------------------------------ lmo.py */
+/* lmo_simplex_slack (lmo.py:56-65) and lmo_single_budget (lmo.py:68-89):
+ * s_out = vertex (one-hot or zero).  A NaN in g ORs SIMOPT_E_INVALID_GRADIENT
+ * into *status (device int, caller-zeroed) instead of failing synchronously.
+ * Positivity of c is the caller's precondition (checked once per instance). */
+int simopt_lmo_simplex_slack(void* stream, const double* g, int64_t n, double* s_out, int* status);
+int simopt_lmo_single_budget(void* stream, const double* g, const double* c, double budget,
+                             int64_t n, double* s_out, int* status);
+
+/* *out = min(x) (NaN-propagating): feasibility all(w >= -tol) (tasks.py:289-290, :327-328). */
+int simopt_min_value(void* stream, const double* x, int64_t n, double* out);
+
+/* ------------------------------------------------------------ newsvendor */
+/* Epoch layout sizes: demands d*S f64,
+ * bucket starts d*nseg*1024 u16, nseg = ceil(S/4096). */
+int simopt_nv_layout(int64_t d, int64_t S, int64_t* nseg, int64_t* dem_elems, int64_t* off_elems);
+
+/* sample_demands (sampling.py:173-193) fused with the partition the gradient
+ * needs: draws D[j,s] = mu_j + sigma_j*z[j*S+s] (z = standard_normal(d*S) of the
+ * stream at the given counter) are written bucket-partitioned per 4096-draw
+ * segment.  Caller advances the counter by ceil(2*ceil(d*S/2)/4).  kappa[d] is
+ * filled.  Rows sorted by the reference contain exactly the same multiset. */
+int simopt_nv_resample(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                       uint64_t ctr_hi, int64_t d, int64_t S, const double* mu,
+                       const double* sigma, double* kappa, double* dem, uint16_t* off);
+
+/* ECDF counts #{D[j,:] <= x_j} (ecdf_count_block, _kernels.py:245-259). */
+int simopt_nv_counts(void* stream, const double* dem, const uint16_t* off, const double* kappa,
+                     const double* mu, int64_t d, int64_t S, const double* x, int64_t* counts);
+
+/* ecdf_count_block on reference-format rows (each row sorted ascending). */
+int simopt_ecdf_count_sorted(void* stream, const double* samples, int64_t rows, int64_t s,
+                             const double* x, int64_t* counts);
+/* nv_gradient_hat epilogue (tasks.py:158-160): g = (k - v) + ((h + v) * (counts / S)). */
+int simopt_nv_grad_from_counts(void* stream, const int64_t* counts, int64_t S, const double* k,
+                               const double* h, const double* v, int64_t d, double* g);
+
+/* Device-resident FW state for one newsvendor run. */
+typedef struct NvState {
+  int64_t jstar;          /* LMO vertex index of the last gradient            */
+  double sval;            /* vertex value C/c_j* if g_j* < 0 else 0            */
+  unsigned blocks_done;   /* last-block-done counter (kept 0 between launches) */
+  unsigned pad;
+} NvState;
+
+#define NV_FLAG_NAN_GRADIENT 1 /* InvalidGradient at this step's LMO (lmo.py:78-79) */
+#define NV_FLAG_NEGATIVE 2     /* iterate < -FEAS_TOL after this step (tasks.py:328) */
+
+/* One fused FW kernel (frank_wolfe.py:106-117 for NewsvendorProblem):
+ *  do_update: x <- (gamma*((-1*x) + s)) + x with the vertex in *state, objective
+ *             terms (newsvendor_cost_block) into terms[], flags[step] |= NEGATIVE;
+ *  do_grad:   g = nv_gradient_hat(x) (tasks.py:141-160), LMO argmin of
+ *             g*(budget/c) (lmo.py:68-89) into *state, flags[grad_step] |= NAN. */
+typedef struct NvIterArgs {
+  int64_t d, S, nseg;
+  const double* dem;
+  const uint16_t* off;
+  const double* kappa;
+  const double *mu, *sigma, *k, *h, *v, *c;
+  double budget;
+  const double* x_in; /* iterate before this step                               */
+  double* x;          /* iterate after this step (== x_in when do_update == 0)  */
+  double* g;
+  double* terms;
+  double gamma;
+  int do_update, do_grad;
+  int64_t step, grad_step;
+  int* flags;
+  NvState* state;
+  double* part_v;
+  int64_t* part_i;
+  int64_t part_capacity;
+} NvIterArgs;
+int simopt_nv_iter(void* stream, const NvIterArgs* args);
+
+/* newsvendor_cost_block (_kernels.py:210-223): out[j] = expected cost of product j. */
+int simopt_nv_cost_terms(void* stream, const double* x, const double* mu, const double* sigma,
+                         const double* unit, const double* hold, const double* sell, int64_t d,
+                         double* out);
 
 #ifdef __cplusplus
 }

@@ -32,6 +32,18 @@ SIGNATURES = {
     "simopt_matvec_t": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],
     "simopt_axpy": [_vp, _d, _vp, _vp, _i64, _vp],
     "simopt_map_kernel": [_vp, _i32, _vp, _i64, _vp],
+    "simopt_timestamp": [_vp, _vp],
+    "simopt_scale_sub": [_vp, _vp, _d, _vp, _i64, _vp],
+    "simopt_min_value": [_vp, _vp, _i64, _vp],
+    "simopt_lmo_simplex_slack": [_vp, _vp, _i64, _vp, _vp],
+    "simopt_lmo_single_budget": [_vp, _vp, _vp, _d, _i64, _vp, _vp],
+    "simopt_nv_layout": [_i64, _i64, _vp, _vp, _vp],
+    "simopt_nv_resample": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
+    "simopt_nv_counts": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp],
+    "simopt_nv_iter": [_vp, _vp],
+    "simopt_ecdf_count_sorted": [_vp, _vp, _i64, _i64, _vp, _vp],
+    "simopt_nv_grad_from_counts": [_vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp],
+    "simopt_nv_cost_terms": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
 }
 
 

@@ -14,16 +14,35 @@ namespace {
 constexpr int kFoldSmem = 4096;  // partials folded in one CTA's shared memory
 
 // --- chunk partials of dot / sum ------------------------------------------------
+// One warp per chunk: lanes load 32 consecutive elements (coalesced) and form the
+// products; lane 0 adds them in index order (one dependent DADD chain per chunk),
+// with the next 32 elements already in flight.
 template <bool kHasY>
-__global__ void __launch_bounds__(128) k_chunk_partials(const double* __restrict__ x,
+__global__ void __launch_bounds__(256) k_chunk_partials(const double* __restrict__ x,
                                                         const double* __restrict__ y, int64_t n,
                                                         int64_t chunk, double* __restrict__ p) {
   const int64_t nch = (n + chunk - 1) / chunk;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nch;
-       c += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t c = blockIdx.x * wpb + (threadIdx.x >> 5); c < nch; c += (int64_t)gridDim.x * wpb) {
     const int64_t lo = c * chunk;
     const int64_t hi = lo + chunk < n ? lo + chunk : n;
-    p[c] = kHasY ? seq_dot(x, y, lo, hi) : seq_sum(x, lo, hi);
+    double s = 0.0;
+    int64_t i = lo + lane;
+    double cur = 0.0;
+    if (i < hi) cur = kHasY ? x[i] * y[i] : x[i];
+    for (int64_t base = lo; base < hi; base += 32) {
+      const int64_t inext = base + 32 + lane;
+      double nxt = 0.0;
+      if (inext < hi) nxt = kHasY ? x[inext] * y[inext] : x[inext];
+      const int cnt = (int)(hi - base < 32 ? hi - base : 32);
+      for (int k = 0; k < cnt; ++k) {
+        const double v = __shfl_sync(0xffffffffu, cur, k);
+        s = s + v;
+      }
+      cur = nxt;
+    }
+    if (lane == 0) p[c] = s;
   }
 }
 
@@ -200,9 +219,9 @@ static int tree_reduce(cudaStream_t st, const double* x, const double* y, int64_
   const int64_t nch = ceil_div(n, chunk);
   double* p = nullptr;
   SIMOPT_CUDA(cudaMallocAsync(&p, 2 * nch * sizeof(double), st));
-  const int g = (int)(ceil_div(nch, 128) < 4096 ? ceil_div(nch, 128) : 4096);
-  if (y) k_chunk_partials<true><<<g, 128, 0, st>>>(x, y, n, chunk, p);
-  else k_chunk_partials<false><<<g, 128, 0, st>>>(x, nullptr, n, chunk, p);
+  const int g = (int)(ceil_div(nch, 8) < 8 * SIMOPT_NUM_SMS ? ceil_div(nch, 8) : 8 * SIMOPT_NUM_SMS);
+  if (y) k_chunk_partials<true><<<g, 256, 0, st>>>(x, y, n, chunk, p);
+  else k_chunk_partials<false><<<g, 256, 0, st>>>(x, nullptr, n, chunk, p);
   SIMOPT_CHECK_LAUNCH("k_chunk_partials");
   const int rc = simopt_fold_partials(st, p, p + nch, nch, out);
   SIMOPT_CUDA(cudaFreeAsync(p, st));
@@ -295,5 +314,26 @@ extern "C" int simopt_map_kernel(void* stream, int kernel, const double* x, int6
   if (n == 0) return SIMOPT_OK;
   k_map<<<elementwise_grid(n), 256, 0, as_stream(stream)>>>(kernel, x, n, out);
   SIMOPT_CHECK_LAUNCH("k_map");
+  return SIMOPT_OK;
+}
+
+namespace {
+// out = x * alpha - y (y may be NULL): the epilogues `col_sums * (1.0 / n)`
+// (tasks.py:62) and `gq * (1.0 / (N - 1)) - mean` (tasks.py:85), unfused.
+__global__ void k_scale_sub(const double* __restrict__ x, double alpha, const double* __restrict__ y,
+                            int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double t = x[i] * alpha;
+    out[i] = y ? t - y[i] : t;
+  }
+}
+}  // namespace
+
+extern "C" int simopt_scale_sub(void* stream, const double* x, double alpha, const double* y,
+                                int64_t n, double* out) {
+  if (n == 0) return SIMOPT_OK;
+  k_scale_sub<<<elementwise_grid(n), 256, 0, as_stream(stream)>>>(x, alpha, y, n, out);
+  SIMOPT_CHECK_LAUNCH("k_scale_sub");
   return SIMOPT_OK;
 }

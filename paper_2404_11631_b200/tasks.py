@@ -1,0 +1,538 @@
+"""The three problem definitions on the device (mirror of sobench/tasks.py).
+
+Problem adapters implement the reference's duck-typed FW protocol
+(``dimension/resample/gradient/lmo/check_feasible/objective``, frank_wolfe.py:91-121)
+so the reference's own ``fw_run`` can drive them, and additionally
+``fw_run_device``, the B200 path: the whole run is enqueued on one CUDA
+stream and its trace is read back once per epoch.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import F64, empty, is_tensor, like_input, mat_dev, to_dev, to_host, vec_dev
+from .errors import (ConfigurationError, DimensionMismatch, InsufficientSamples, InvalidConstraint,
+                     InvalidGradient, RunAborted)
+from .frank_wolfe import fw_step_size
+from .lmo import SimplexSlackSet, lmo_simplex_slack, lmo_single_budget
+from .records import TraceBuilder
+from .sampling import GaussianSpec, RngStream
+
+FEAS_TOL = 1e-10  # tasks.py:27
+
+
+# ---------------------------------------------------------------------------
+# ctypes mirror of NvIterArgs / NvState (include/simopt_b200.h)
+class NvIterArgs(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int64), ("S", ctypes.c_int64), ("nseg", ctypes.c_int64),
+        ("dem", ctypes.c_void_p), ("off", ctypes.c_void_p), ("kappa", ctypes.c_void_p),
+        ("mu", ctypes.c_void_p), ("sigma", ctypes.c_void_p), ("k", ctypes.c_void_p),
+        ("h", ctypes.c_void_p), ("v", ctypes.c_void_p), ("c", ctypes.c_void_p),
+        ("budget", ctypes.c_double),
+        ("x_in", ctypes.c_void_p), ("x", ctypes.c_void_p), ("g", ctypes.c_void_p), ("terms", ctypes.c_void_p),
+        ("gamma", ctypes.c_double),
+        ("do_update", ctypes.c_int), ("do_grad", ctypes.c_int),
+        ("step", ctypes.c_int64), ("grad_step", ctypes.c_int64),
+        ("flags", ctypes.c_void_p), ("state", ctypes.c_void_p),
+        ("part_v", ctypes.c_void_p), ("part_i", ctypes.c_void_p),
+        ("part_capacity", ctypes.c_int64),
+    ]
+
+
+NV_FLAG_NAN_GRADIENT = 1
+NV_FLAG_NEGATIVE = 2
+_NV_PART_CAPACITY = 4 * 148
+
+
+# ---------------------------------------------------------------------------
+# Task 2: multi-product newsvendor
+@dataclass
+class NewsvendorTask:
+    """Per-product costs, Gaussian demand and the single budget (tasks.py:93-138).
+
+    Only the single-budget form is supported (the multi-resource ``polytope``
+    form needs the dense simplex LMO, out of scope -- see lmo.py).
+    """
+
+    unit_cost: object
+    holding_cost: object
+    selling_value: object
+    demand_mean: object
+    demand_std: object
+    budget_costs: object = None
+    budget: float | None = None
+    polytope: object = None
+
+    def __post_init__(self):
+        conv = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+        self.unit_cost = conv(self.unit_cost)
+        self.holding_cost = conv(self.holding_cost)
+        self.selling_value = conv(self.selling_value)
+        self.demand_mean = conv(self.demand_mean)
+        self.demand_std = conv(self.demand_std)
+        n = self.unit_cost.size
+        for v in (self.holding_cost, self.selling_value, self.demand_mean, self.demand_std):
+            if v.size != n:
+                raise DimensionMismatch("newsvendor parameter vectors must share one length")
+        if not np.all(self.selling_value + self.holding_cost > 0):
+            raise InvalidConstraint("need v + h > 0 per product (convex per-product cost)")
+        if not np.all(self.unit_cost - self.selling_value < 0):
+            raise InvalidConstraint("need k - v < 0 per product (nondegenerate stocking)")
+        if not np.all(self.demand_std > 0):
+            raise InvalidConstraint("demand std must be > 0")
+        has_budget = self.budget_costs is not None and self.budget is not None
+        if has_budget == (self.polytope is not None):
+            raise ConfigurationError("set exactly one of (budget_costs, budget) or polytope")
+        if self.polytope is not None:
+            raise ConfigurationError("multi-resource polytope LMO (lmo_general) is not provided "
+                                     "by the cuda package")
+        self.budget_costs = conv(self.budget_costs)
+        if self.budget_costs.size != n:
+            raise DimensionMismatch("budget cost length mismatch")
+        if not np.all(self.budget_costs > 0) or not self.budget > 0:
+            raise InvalidConstraint("budget data must be strictly positive")
+        self.budget = float(self.budget)
+
+    @property
+    def dimension(self) -> int:
+        return self.unit_cost.size
+
+
+class _NvDevice:
+    """Device copies of a NewsvendorTask plus the epoch's demand layout."""
+
+    def __init__(self, task: NewsvendorTask):
+        self.d = task.dimension
+        self.mu = to_dev(task.demand_mean)
+        self.sigma = to_dev(task.demand_std)
+        self.k = to_dev(task.unit_cost)
+        self.h = to_dev(task.holding_cost)
+        self.v = to_dev(task.selling_value)
+        self.c = to_dev(task.budget_costs)
+        self.budget = task.budget
+        self.kappa = empty(self.d)
+        self.S = None
+        self.dem = None
+        self.off = None
+        self.nseg = 0
+
+    def ensure_layout(self, S: int):
+        if S == self.S:
+            return
+        ns, de, oe = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.call("simopt_nv_layout", self.d, S, ctypes.byref(ns), ctypes.byref(de), ctypes.byref(oe))
+        self.dem = None
+        self.off = None
+        torch.cuda.empty_cache()
+        self.dem = torch.empty(de.value, dtype=F64, device="cuda")
+        self.off = torch.empty(oe.value, dtype=torch.int16, device="cuda")
+        self.nseg = ns.value
+        self.S = S
+
+    def resample(self, stream: RngStream, S: int):
+        if S < 1:
+            raise InsufficientSamples("need at least one demand sample per product")
+        self.ensure_layout(S)
+        _lib.call("simopt_nv_resample", _lib.stream_ptr(), *stream.words(), self.d, S,
+                  _lib.ptr(self.mu), _lib.ptr(self.sigma), _lib.ptr(self.kappa),
+                  _lib.ptr(self.dem), _lib.ptr(self.off))
+        stream.advance(2 * ((self.d * S + 1) // 2))
+
+    def counts(self, x: torch.Tensor) -> torch.Tensor:
+        out = torch.empty(self.d, dtype=torch.int64, device="cuda")
+        _lib.call("simopt_nv_counts", _lib.stream_ptr(), _lib.ptr(self.dem), _lib.ptr(self.off),
+                  _lib.ptr(self.kappa), _lib.ptr(self.mu), self.d, self.S, _lib.ptr(x), _lib.ptr(out))
+        return out
+
+
+class NewsvendorProblem:
+    """Newsvendor wired for FW: sampled gradient, exact recorded objective (tasks.py:293-334)."""
+
+    name = "newsvendor"
+
+    def __init__(self, task: NewsvendorTask, backend):
+        self.task = task
+        self.backend = backend
+        self.dev = _NvDevice(task)
+        self._stream = None
+
+    @property
+    def dimension(self) -> int:
+        return self.task.dimension
+
+    # ---- duck-typed protocol (host arrays in/out, for the reference fw_run) ----
+    def resample(self, stream: RngStream, n_samples: int) -> None:
+        self.dev.resample(stream, n_samples)
+
+    def gradient(self, x):
+        xd = vec_dev(x)
+        cnt = self.dev.counts(xd)
+        g = empty(self.dev.d)
+        _lib.call("simopt_nv_grad_from_counts", _lib.stream_ptr(), _lib.ptr(cnt), self.dev.S,
+                  _lib.ptr(self.dev.k), _lib.ptr(self.dev.h), _lib.ptr(self.dev.v), self.dev.d,
+                  _lib.ptr(g))
+        return like_input(x, g)
+
+    def lmo(self, g):
+        return lmo_single_budget(g, self.dev.c if is_tensor(g) else self.task.budget_costs,
+                                 self.task.budget)
+
+    def check_feasible(self, x) -> bool:
+        xd = vec_dev(x)
+        if bool((xd < -FEAS_TOL).any()):
+            return False
+        spent = self.backend.dot(self.dev.c, xd)
+        return float(spent) <= self.task.budget * (1.0 + FEAS_TOL)
+
+    def objective(self, x) -> float:
+        return nv_objective_exact(x, self.task, self.backend)
+
+    # ---- B200 path ---------------------------------------------------------------
+    def fw_run_device(self, config, backend, *, task_label, size, rep):
+        return _nv_fw_run_device(self, config, backend, task_label, size, rep)
+
+
+def _nv_fw_run_device(prob: NewsvendorProblem, config, backend, label, size, rep):
+    """Device-resident frank_wolfe.fw_run for the newsvendor (frank_wolfe.py:91-121).
+
+    Per step t (epoch k, inner m): one fused kernel updates x with the previous
+    LMO vertex, writes objective terms, computes the next ECDF gradient and its
+    LMO argmin; two exact-tree reductions record dot(c, x) and the objective.
+    Iterates live in a ring of 2M+1 buffers so a failure detected at the epoch
+    check still has the reference's final_iterate at hand.
+    """
+    dev = prob.dev
+    d, M, K = dev.d, config.inner_iters, config.epochs
+    T = K * M
+    H = 2 * M + 1
+    xs = torch.zeros(H, d, dtype=F64, device="cuda")
+    g = empty(d)
+    terms = empty(d)
+    flags = torch.zeros(T + 1, dtype=torch.int32, device="cuda")
+    spent = empty(T)
+    objs = empty(T)
+    stamps = torch.zeros(T + 1, dtype=torch.int64, device="cuda")
+    state = torch.zeros(4, dtype=torch.int64, device="cuda")  # NvState (32 bytes)
+    part_v = empty(_NV_PART_CAPACITY)
+    part_i = torch.empty(_NV_PART_CAPACITY, dtype=torch.int64, device="cuda")
+    sp = _lib.stream_ptr()
+    chunk = backend.chunk_size
+    a = NvIterArgs()
+    a.d, a.mu, a.sigma = d, dev.mu.data_ptr(), dev.sigma.data_ptr()
+    a.k, a.h, a.v, a.c = dev.k.data_ptr(), dev.h.data_ptr(), dev.v.data_ptr(), dev.c.data_ptr()
+    a.budget = dev.budget
+    a.g, a.terms, a.flags, a.state = g.data_ptr(), terms.data_ptr(), flags.data_ptr(), state.data_ptr()
+    a.part_v, a.part_i, a.part_capacity = part_v.data_ptr(), part_i.data_ptr(), _NV_PART_CAPACITY
+    lib = _lib.load()
+    trace = TraceBuilder()
+    host = {}
+
+    def check_epoch(k_done):
+        """Validate steps of epoch k_done (host sync on that epoch only)."""
+        lo, hi = k_done * M, (k_done + 1) * M
+        fl = to_host(flags[lo:hi + 1])
+        sp_ = to_host(spent[lo:hi])
+        ob = to_host(objs[lo:hi])
+        ts = to_host(stamps[lo:hi])
+        t0 = host.setdefault("t0", int(stamps[T].item()))
+        for i in range(M):
+            t = lo + i
+            if fl[i] & NV_FLAG_NAN_GRADIENT:
+                return t, InvalidGradient("gradient contains NaN"), xs[t % H]
+            if (fl[i] & NV_FLAG_NEGATIVE) or not sp_[i] <= dev.budget * (1.0 + FEAS_TOL):
+                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), xs[(t + 1) % H]
+            trace.append(t + 1, float(ob[i]), int(ts[i]) - t0)
+        return None
+
+    def abort(t, exc, it):
+        partial = trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(it))
+        raise RunAborted(f"frank-wolfe run failed at step {len(trace) + 1}: {exc}", partial) from exc
+
+    _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[T:])))
+    events = []
+    for k in range(K):
+        dev.resample(config.stream, config.epoch_sample_size(k))
+        a.S, a.nseg, a.dem, a.off, a.kappa = dev.S, dev.nseg, dev.dem.data_ptr(), dev.off.data_ptr(), dev.kappa.data_ptr()
+        t0 = k * M
+        # gradient + LMO at the epoch's first iterate
+        a.x_in = a.x = xs[t0 % H].data_ptr()
+        a.do_update, a.do_grad, a.step, a.grad_step, a.gamma = 0, 1, t0, t0, 0.0
+        _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
+        for m in range(M):
+            t = t0 + m
+            # x_{t+1} = update(x_t) in its own ring slot, then gradient at x_{t+1}
+            xin, xout = xs[t % H], xs[(t + 1) % H]
+            a.x_in, a.x = xin.data_ptr(), xout.data_ptr()
+            a.gamma = fw_step_size(k, M, m)
+            a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), t, t + 1
+            _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
+            _lib.check(lib.simopt_dot(sp, _lib.ptr(dev.c), _lib.ptr(xout), d, chunk, _lib.ptr(spent[t:])))
+            _lib.check(lib.simopt_vec_sum(sp, _lib.ptr(terms), d, chunk, _lib.ptr(objs[t:])))
+            _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[t:])))
+        ev = torch.cuda.Event()
+        ev.record()
+        events.append(ev)
+        if k >= 1:  # validate the previous epoch while this one runs
+            events[k - 1].synchronize()
+            bad = check_epoch(k - 1)
+            if bad:
+                abort(*bad)
+    events[-1].synchronize()
+    bad = check_epoch(K - 1)
+    if bad:
+        abort(*bad)
+    return trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(xs[T % H]))
+
+
+def nv_gradient_hat(x, demands, task: NewsvendorTask, backend):
+    """k - v + (h+v) * empirical CDF at x (tasks.py:141-160) on reference-format sorted rows."""
+    dem = mat_dev(demands)
+    xd = vec_dev(x)
+    if dem.shape[0] != xd.numel():
+        raise DimensionMismatch("demand rows != product count")
+    if dem.shape[1] == 0:
+        raise InsufficientSamples("empty demand sample array")
+    cnt = torch.empty(xd.numel(), dtype=torch.int64, device="cuda")
+    _lib.call("simopt_ecdf_count_sorted", _lib.stream_ptr(), _lib.ptr(dem), dem.shape[0],
+              dem.shape[1], _lib.ptr(xd), _lib.ptr(cnt))
+    k, h, v = (to_dev(a) for a in (task.unit_cost, task.holding_cost, task.selling_value))
+    g = empty(xd.numel())
+    _lib.call("simopt_nv_grad_from_counts", _lib.stream_ptr(), _lib.ptr(cnt), dem.shape[1],
+              _lib.ptr(k), _lib.ptr(h), _lib.ptr(v), xd.numel(), _lib.ptr(g))
+    return like_input(x, g)
+
+
+def nv_objective_exact(x, task: NewsvendorTask, backend) -> float:
+    """Expected cost under Gaussian demand, fixed-tree sum (tasks.py:174-188)."""
+    xd = vec_dev(x)
+    if xd.numel() != task.dimension:
+        raise DimensionMismatch("stock vector length != product count")
+    terms = nv_cost_terms_device(xd, task)
+    return backend.vec_sum(terms) if is_tensor(x) else float(backend.vec_sum_device(terms).item())
+
+
+def nv_cost_terms_device(xd, task: NewsvendorTask):
+    out = empty(xd.numel())
+    dev = [to_dev(a) for a in (task.demand_mean, task.demand_std, task.unit_cost,
+                               task.holding_cost, task.selling_value)]
+    _lib.call("simopt_nv_cost_terms", _lib.stream_ptr(), _lib.ptr(xd), *(_lib.ptr(t) for t in dev),
+              xd.numel(), _lib.ptr(out))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Task 1: mean-variance portfolio
+@dataclass
+class MeanVarTask:
+    """Return distribution for the mean-variance objective (tasks.py:33-41)."""
+
+    spec: GaussianSpec
+
+    @property
+    def dimension(self) -> int:
+        return self.spec.dimension
+
+
+class MeanVarSampleSet:
+    """One epoch's draws X (N x d, device), their column mean, and N (tasks.py:44-53).
+
+    The centered matrix Xc = X - mean is never stored: every kernel subtracts
+    the mean on the fly, which is the same IEEE subtraction numpy performs
+    when materialising it (tasks.py:63).  ``centered`` materialises on demand.
+    """
+
+    def __init__(self, samples: torch.Tensor, mean: torch.Tensor):
+        self.samples = samples
+        self.mean = mean
+        self.count = samples.shape[0]
+
+    @property
+    def centered(self) -> torch.Tensor:
+        return self.samples - self.mean[None, :]
+
+
+def build_sample_set(samples, backend) -> MeanVarSampleSet:
+    """colsum = tree matvec_t(X, 1); mean = colsum * (1/n) (tasks.py:56-64)."""
+    x = mat_dev(samples)
+    n = x.shape[0]
+    if n < 2:
+        raise InsufficientSamples("sample covariance needs at least 2 rows")
+    ones = torch.ones(n, dtype=F64, device="cuda")
+    col = backend.matvec_t_device(x, ones)
+    mean = empty(x.shape[1])
+    _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(col), 1.0 / n, None, col.numel(),
+              _lib.ptr(mean))
+    return MeanVarSampleSet(x, mean)
+
+
+def mv_objective(w, ss: MeanVarSampleSet, backend) -> float:
+    """0.5/(N-1) * |Xc w|^2 - w.mean (tasks.py:67-75)."""
+    wd = vec_dev(w)
+    if wd.numel() != ss.mean.numel():
+        raise DimensionMismatch("weight length != asset count")
+    q = backend.matvec_device(ss.samples, wd, center=ss.mean)
+    quad = float(backend.dot_device(q, q).item())
+    lin = float(backend.dot_device(wd, ss.mean).item())
+    return 0.5 * quad / (ss.count - 1) - lin
+
+
+def mv_gradient(w, ss: MeanVarSampleSet, backend):
+    """(1/(N-1)) Xc^T (Xc w) - mean (tasks.py:78-85)."""
+    wd = vec_dev(w)
+    if wd.numel() != ss.mean.numel():
+        raise DimensionMismatch("weight length != asset count")
+    q = backend.matvec_device(ss.samples, wd, center=ss.mean)
+    gq = backend.matvec_t_device(ss.samples, q, center=ss.mean)
+    g = empty(gq.numel())
+    _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(gq), 1.0 / (ss.count - 1),
+              _lib.ptr(ss.mean), gq.numel(), _lib.ptr(g))
+    return like_input(w, g)
+
+
+class MeanVarProblem:
+    """Mean-variance task wired for the FW engine (tasks.py:261-290)."""
+
+    name = "meanvar"
+
+    def __init__(self, task: MeanVarTask, backend):
+        self.task = task
+        self.backend = backend
+        self.constraint = SimplexSlackSet(task.dimension)
+        self.sample_set: MeanVarSampleSet | None = None
+        self._x = None
+
+    @property
+    def dimension(self) -> int:
+        return self.task.dimension
+
+    def resample(self, stream: RngStream, n_samples: int) -> None:
+        from .sampling import sample_returns_device
+        d = self.dimension
+        if self._x is None or self._x.shape[0] != n_samples:
+            self._x = None
+            self._x = empty(n_samples, d)
+        x = sample_returns_device(self.task.spec, n_samples, stream, out=self._x,
+                                  chunk=self.backend.chunk_size)
+        self.sample_set = build_sample_set(x, self.backend)
+
+    def objective(self, w) -> float:
+        return mv_objective(w, self.sample_set, self.backend)
+
+    def gradient(self, w):
+        return mv_gradient(w, self.sample_set, self.backend)
+
+    def lmo(self, g):
+        return lmo_simplex_slack(g)
+
+    def check_feasible(self, w) -> bool:
+        wh = to_host(w) if is_tensor(w) else np.asarray(w)
+        return bool(np.all(wh >= -FEAS_TOL) and np.sum(wh) <= 1.0 + FEAS_TOL)
+
+    def fw_run_device(self, config, backend, *, task_label, size, rep):
+        return _mv_fw_run_device(self, config, backend, task_label, size, rep)
+
+
+def _mv_fw_run_device(prob: MeanVarProblem, config, backend, label, size, rep):
+    """Device-resident fw_run for the mean-variance task (frank_wolfe.py:91-121).
+
+    q = Xc w_{t+1} computed for the objective of step t is reused as the first
+    half of gradient(w_{t+1}) inside an epoch (same kernel, same bits).
+    Feasibility: min(w) and an exact-tree sum (the reference uses numpy's
+    pairwise np.sum, tasks.py:290; both are within 1e-15 of the exact sum, far
+    inside the 1e-10 tolerance of that boolean test).
+    """
+    d, M, K = prob.dimension, config.inner_iters, config.epochs
+    T = K * M
+    H = 2 * M + 1
+    ws = torch.zeros(H, d, dtype=F64, device="cuda")
+    g = empty(d)
+    s = empty(d)
+    dirn = empty(d)
+    status = torch.zeros(T + 1, dtype=torch.int32, device="cuda")
+    wmin = empty(T)
+    wsum = empty(T)
+    quad = empty(T)
+    lin = empty(T)
+    stamps = torch.zeros(T + 1, dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    sp = _lib.stream_ptr()
+    chunk = backend.chunk_size
+    trace = TraceBuilder()
+    host = {}
+    q = None
+    gq = None
+
+    def check_epoch(k_done):
+        lo, hi = k_done * M, (k_done + 1) * M
+        st = to_host(status[lo:hi])
+        mn, sm = to_host(wmin[lo:hi]), to_host(wsum[lo:hi])
+        qd, ln = to_host(quad[lo:hi]), to_host(lin[lo:hi])
+        ts = to_host(stamps[lo:hi])
+        t0 = host.setdefault("t0", int(stamps[T].item()))
+        n_eff = host[("N", k_done)]
+        for i in range(M):
+            t = lo + i
+            if st[i] != 0:
+                return t, InvalidGradient("gradient contains NaN"), ws[t % H]
+            if not (mn[i] >= -FEAS_TOL and sm[i] <= 1.0 + FEAS_TOL):
+                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), ws[(t + 1) % H]
+            f = 0.5 * float(qd[i]) / (n_eff - 1) - float(ln[i])  # tasks.py:75
+            trace.append(t + 1, f, int(ts[i]) - t0)
+        return None
+
+    def abort(t, exc, it):
+        partial = trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(it))
+        raise RunAborted(f"frank-wolfe run failed at step {len(trace) + 1}: {exc}", partial) from exc
+
+    _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[T:])))
+    events = []
+    for k in range(K):
+        n_k = config.epoch_sample_size(k)
+        host[("N", k)] = n_k
+        prob.resample(config.stream, n_k)
+        ss = prob.sample_set
+        x, mean = ss.samples, ss.mean
+        if q is None or q.numel() != n_k:
+            q = empty(n_k)
+        gq = empty(d) if gq is None else gq
+        inv = 1.0 / (n_k - 1)
+        for m in range(M):
+            t = k * M + m
+            w_in, w_out = ws[t % H], ws[(t + 1) % H]
+            if m == 0:  # first gradient of the epoch: q = Xc w_t
+                _lib.check(lib.simopt_matvec(sp, _lib.ptr(x), n_k, d, None, n_k, _lib.ptr(mean),
+                                             _lib.ptr(w_in), chunk, _lib.ptr(q)))
+            _lib.check(lib.simopt_matvec_t(sp, _lib.ptr(x), n_k, d, None, n_k, _lib.ptr(mean),
+                                           _lib.ptr(q), chunk, _lib.ptr(gq)))
+            _lib.check(lib.simopt_scale_sub(sp, _lib.ptr(gq), inv, _lib.ptr(mean), d, _lib.ptr(g)))
+            _lib.check(lib.simopt_lmo_simplex_slack(sp, _lib.ptr(g), d, _lib.ptr(s), _lib.ptr(status[t:])))
+            gamma = fw_step_size(k, M, m)
+            _lib.check(lib.simopt_axpy(sp, -1.0, _lib.ptr(w_in), _lib.ptr(s), d, _lib.ptr(dirn)))
+            _lib.check(lib.simopt_axpy(sp, gamma, _lib.ptr(dirn), _lib.ptr(w_in), d, _lib.ptr(w_out)))
+            _lib.check(lib.simopt_min_value(sp, _lib.ptr(w_out), d, _lib.ptr(wmin[t:])))
+            _lib.check(lib.simopt_vec_sum(sp, _lib.ptr(w_out), d, chunk, _lib.ptr(wsum[t:])))
+            # objective(w_{t+1}); q is reused by the next gradient of this epoch
+            _lib.check(lib.simopt_matvec(sp, _lib.ptr(x), n_k, d, None, n_k, _lib.ptr(mean),
+                                         _lib.ptr(w_out), chunk, _lib.ptr(q)))
+            _lib.check(lib.simopt_dot(sp, _lib.ptr(q), _lib.ptr(q), n_k, chunk, _lib.ptr(quad[t:])))
+            _lib.check(lib.simopt_dot(sp, _lib.ptr(w_out), _lib.ptr(mean), d, chunk, _lib.ptr(lin[t:])))
+            _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[t:])))
+        ev = torch.cuda.Event()
+        ev.record()
+        events.append(ev)
+        if k >= 1:
+            events[k - 1].synchronize()
+            bad = check_epoch(k - 1)
+            if bad:
+                abort(*bad)
+    events[-1].synchronize()
+    bad = check_epoch(K - 1)
+    if bad:
+        abort(*bad)
+    return trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(ws[T % H]))

@@ -76,6 +76,10 @@ int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t stream_id, 
 int simopt_dot(void* stream, const double* x, const double* y, int64_t n, int64_t chunk,
                double* out);
 int simopt_vec_sum(void* stream, const double* x, int64_t n, int64_t chunk, double* out);
+/* Two independent fixed-tree reductions in one launch: out_k = dot(x_k, y_k) (y_k != NULL)
+ * or vec_sum(x_k) (y_k == NULL). */
+int simopt_tree_sums2(void* stream, const double* x0, const double* y0, int64_t n0, double* out0,
+                      const double* x1, const double* y1, int64_t n1, double* out1, int64_t chunk);
 /* out[r] = fixed-tree dot of (a[row(r),:] - center) with x, row(r) = rows_idx ? rows_idx[r] : r.
  * center (length cols) and rows_idx (length rows, int64) may be NULL. */
 int simopt_matvec(void* stream, const double* a, int64_t lda_rows, int64_t cols,

@@ -28,6 +28,7 @@ SIGNATURES = {
     "simopt_sample_returns_diag": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp, _vp],
     "simopt_dot": [_vp, _vp, _vp, _i64, _i64, _vp],
     "simopt_vec_sum": [_vp, _vp, _i64, _i64, _vp],
+    "simopt_tree_sums2": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64],
     "simopt_matvec": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],
     "simopt_matvec_t": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],
     "simopt_axpy": [_vp, _d, _vp, _vp, _i64, _vp],

@@ -18,6 +18,9 @@
 #include <stdint.h>
 #include <math.h>
 #include <string.h>
+#if !defined(__cplusplus)
+#include <stdbool.h>
+#endif
 
 #if defined(__CUDACC__)
 #define SIMOPT_HD __host__ __device__ __forceinline__
@@ -352,4 +355,137 @@ SIMOPT_HD double glibc_sigmoid(double t, const uint64_t* etab) {
 SIMOPT_HD double glibc_logistic_loss_term(double t, double z, const uint64_t* etab) {
   if (t >= 0.0) return glibc_log1p(glibc_exp(-t, etab)) + (1.0 - z) * t;
   return glibc_log1p(glibc_exp(t, etab)) - z * t;
+}
+
+// ---------------------------------------------------------------------------
+// Divergence-free Box-Muller for the device: the same glibc arithmetic as
+// glibc_boxmuller(), restructured so that every lane of a warp executes one
+// instruction stream.  sin and cos of theta in [0, 2pi) always need exactly one
+// do_sin-type and one do_cos-type evaluation (glibc s_sin.c, per region):
+//   theta < 0.855469 : sin = do_sin(x,0)          cos = do_cos(x,0)
+//   theta < 2.426265 : sin = do_cos(y,hp1)        cos = do_sin(y+hp1, (y-a)+hp1),  y = hp0-x
+//   otherwise        : (a,da,n) = reduce_sincos(x); sin/cos pick do_sin/do_cos(a,da) by n
+// Region arguments are selected, both evaluations run unconditionally, and the
+// Taylor branch of do_sin (|a| < 0.126) is evaluated and selected.  log1p's two
+// prologues (k = 0 / k != 0) are likewise both computed and selected.
+// Bit-identity with glibc_boxmuller() is checked on the CPU (tools/) and on the GPU.
+// ---------------------------------------------------------------------------
+SIMOPT_HD double gm_do_sin_nb(double x, double dx, const double* tab) {
+  const double xold = x;
+  const double ax = gm_abs(x);
+  const double tay = gm_taylor_sin(x, dx);
+  const double dxs = (x <= 0) ? -dx : dx;
+  const double ux = GM_BIG + ax;
+  const double xr = ax - (ux - GM_BIG);
+  const int k = (int)(gm_lo(ux) << 2);
+  const double xx = xr * xr;
+  const double s = xr + gm_fma(xr * xx, gm_fma(xx, GM_SN5, GM_SN3), dxs);
+  const double c = gm_fma(xr, dxs, xx * gm_fma(xx, gm_fma(xx, GM_CS6, GM_CS4), GM_CS2));
+  const double sn = tab[k], ssn = tab[k + 1], cs = tab[k + 2], ccs = tab[k + 3];
+  double cor = gm_fma(s, ccs, ssn);
+  cor = gm_fma(-c, sn, cor);
+  cor = gm_fma(s, cs, cor);
+  const double big = gm_copysign(sn + cor, xold);
+  return (ax < 0.126) ? tay : big;
+}
+
+SIMOPT_HD void glibc_sincos_pos(double x, const double* tab, double* sin_out, double* cos_out) {
+  // x >= 0, x < 105414350 (Box-Muller theta)
+  const int32_t kx = gm_hi(x) & 0x7fffffff;
+  const bool r2 = kx < 0x3feb6000;
+  const bool r3 = !r2 && kx < 0x400368fd;
+  // region 3 arguments
+  const double y = GM_HP0 - x;
+  const double a3 = y + GM_HP1;
+  const double da3 = (y - a3) + GM_HP1;
+  // region 4 arguments
+  double a4, da4;
+  const int n = gm_reduce_sincos(x, &a4, &da4);
+  const double as = r2 ? x : (r3 ? a3 : a4);
+  const double das = r2 ? 0.0 : (r3 ? da3 : da4);
+  const double ac = r2 ? x : (r3 ? y : a4);
+  const double dac = r2 ? 0.0 : (r3 ? GM_HP1 : da4);
+  const double S = gm_do_sin_nb(as, das, tab);
+  const double C = gm_do_cos(ac, dac, tab);
+  double sv, cv;
+  if (r2) {
+    sv = S;
+    cv = C;
+  } else if (r3) {
+    sv = gm_copysign(C, x);
+    cv = S;
+  } else {
+    const double s4 = (n & 1) ? C : S;
+    sv = (n & 2) ? -s4 : s4;
+    const int m = n + 1;
+    const double c4 = (m & 1) ? C : S;
+    cv = (m & 2) ? -c4 : c4;
+  }
+  if (kx < 0x3e500000) sv = x;
+  if (kx < 0x3e400000) cv = 1.0;
+  *sin_out = sv;
+  *cos_out = cv;
+}
+
+// log1p for x in (-1, 0] (Box-Muller's -u1) with both prologues computed.
+SIMOPT_HD double glibc_log1p_neg(double x) {
+  const int32_t hx = gm_hi(x);
+  const int32_t ax = hx & 0x7fffffff;
+  if (ax < 0x3e200000) {                   // |x| < 2**-29 (rare)
+    if (ax < 0x3c900000) return x;
+    return gm_fma(-(x * x), 0.5, x);
+  }
+  const bool k0 = (uint32_t)hx + 0x402d413cu > 0x402d413cu;
+  // k != 0 prologue (x <= -0.2929): u = 1 + x in (0, 0.71]; k <= 0 so c = x - (u - 1)
+  double u = 1.0 + x;
+  int32_t hu = gm_hi(u);
+  int32_t k = (hu >> 20) - 1023;
+  double c = (x - (u - 1.0)) / u;
+  hu &= 0x000fffff;
+  if (hu < 0x6a09e) {
+    u = gm_set_hi(u, hu | 0x3ff00000);
+  } else {
+    k += 1;
+    u = gm_set_hi(u, hu | 0x3fe00000);
+    hu = (0x00100000 - hu) >> 2;
+  }
+  double f = u - 1.0;
+  if (k0) { k = 0; f = x; hu = 1; c = 0.0; }
+  const double hfsq = (f * 0.5) * f;
+  if (hu == 0) {                           // |f| < 2**-20 (rare)
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      const double kd = (double)k;
+      return gm_fma(kd, GM_LN2_HI, gm_fma(kd, GM_LN2_LO, c));
+    }
+    const double R = gm_fma(-f, 0x1.5555555555555p-1, 1.0) * hfsq;
+    if (k == 0) return f - R;
+    const double kd = (double)k;
+    return gm_fma(kd, GM_LN2_HI, -((R - gm_fma(kd, GM_LN2_LO, c)) - f));
+  }
+  const double s = f / (f + 2.0);
+  const double z = s * s;
+  const double R2 = gm_fma(z, GM_LP3, GM_LP2);
+  const double R3 = gm_fma(z, GM_LP5, GM_LP4);
+  const double R4 = gm_fma(z, GM_LP7, GM_LP6);
+  const double z2 = z * z;
+  const double z4 = z2 * z2;
+  const double z6 = z2 * z4;
+  double R = gm_fma(z, GM_LP1, z2 * R2);
+  R = gm_fma(z4, R3, R);
+  R = gm_fma(z6, R4, R);
+  const double shr = s * (R + hfsq);
+  const double kd = (double)k;
+  const double tk = (hfsq - (gm_fma(kd, GM_LN2_LO, c) + shr)) - f;
+  return k0 ? f - (hfsq - shr) : gm_fma(kd, GM_LN2_HI, -tk);
+}
+
+SIMOPT_HD void glibc_boxmuller_fast(double u1, double u2, const double* tab, double* z0,
+                                    double* z1) {
+  const double r = sqrt(-2.0 * glibc_log1p_neg(-u1));
+  const double th = GM_TAU * u2;
+  double sv, cv;
+  glibc_sincos_pos(th, tab, &sv, &cv);
+  *z0 = r * cv;
+  *z1 = r * sv;
 }

@@ -14,35 +14,102 @@ namespace {
 constexpr int kFoldSmem = 4096;  // partials folded in one CTA's shared memory
 
 // --- chunk partials of dot / sum ------------------------------------------------
-// One warp per chunk: lanes load 32 consecutive elements (coalesced) and form the
-// products; lane 0 adds them in index order (one dependent DADD chain per chunk),
-// with the next 32 elements already in flight.
-template <bool kHasY>
-__global__ void __launch_bounds__(256) k_chunk_partials(const double* __restrict__ x,
-                                                        const double* __restrict__ y, int64_t n,
-                                                        int64_t chunk, double* __restrict__ p) {
-  const int64_t nch = (n + chunk - 1) / chunk;
+// One warp per chunk.  The warp stages 256-element tiles through shared memory
+// (coalesced loads, products formed by all lanes, next tile already in flight)
+// and lane 0 adds the tile in index order: a single dependent DADD chain per
+// chunk, fed from shared memory so the chain runs at DADD latency.
+constexpr int kTile = 256;
+constexpr int kPartialWarps = 4;
+
+struct TreeJob {
+  const double* x;
+  const double* y;  // NULL: plain sum
+  int64_t n;
+  double* out;      // root (device scalar)
+};
+struct TreeJobs {
+  TreeJob job[4];
+  int njobs;
+  int64_t chunk;
+  int64_t first_chunk[5];  // prefix of chunk counts
+};
+
+__device__ __forceinline__ double warp_chunk_sum(const double* __restrict__ x,
+                                                 const double* __restrict__ y, int64_t lo,
+                                                 int64_t hi, double* buf) {
   const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t c = blockIdx.x * wpb + (threadIdx.x >> 5); c < nch; c += (int64_t)gridDim.x * wpb) {
-    const int64_t lo = c * chunk;
-    const int64_t hi = lo + chunk < n ? lo + chunk : n;
-    double s = 0.0;
-    int64_t i = lo + lane;
-    double cur = 0.0;
-    if (i < hi) cur = kHasY ? x[i] * y[i] : x[i];
-    for (int64_t base = lo; base < hi; base += 32) {
-      const int64_t inext = base + 32 + lane;
-      double nxt = 0.0;
-      if (inext < hi) nxt = kHasY ? x[inext] * y[inext] : x[inext];
-      const int cnt = (int)(hi - base < 32 ? hi - base : 32);
-      for (int k = 0; k < cnt; ++k) {
-        const double v = __shfl_sync(0xffffffffu, cur, k);
-        s = s + v;
-      }
-      cur = nxt;
+  double r[kTile / 32];
+  auto load = [&](int64_t base) {
+#pragma unroll
+    for (int t = 0; t < kTile / 32; ++t) {
+      const int64_t i = base + lane + 32 * t;
+      r[t] = (i < hi) ? (y ? x[i] * y[i] : x[i]) : 0.0;
     }
-    if (lane == 0) p[c] = s;
+  };
+  double s = 0.0;
+  load(lo);
+  int parity = 0;
+  for (int64_t base = lo; base < hi; base += kTile) {
+    double* b = buf + parity * kTile;
+#pragma unroll
+    for (int t = 0; t < kTile / 32; ++t) b[lane + 32 * t] = r[t];
+    __syncwarp();
+    if (base + kTile < hi) load(base + kTile);
+    if (lane == 0) {
+      const int cnt = (int)(hi - base < kTile ? hi - base : kTile);
+      int i = 0;
+      for (; i + 8 <= cnt; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = b[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = s + v[k];
+      }
+      for (; i < cnt; ++i) s = s + b[i];
+    }
+    parity ^= 1;
+  }
+  __syncwarp();
+  return s;
+}
+
+__global__ void __launch_bounds__(kPartialWarps * 32)
+    k_tree_jobs(TreeJobs jobs, double* __restrict__ partials, unsigned* __restrict__ counters) {
+  __shared__ double buf[kPartialWarps][2 * kTile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = jobs.first_chunk[jobs.njobs];
+  for (int64_t g = (int64_t)blockIdx.x * kPartialWarps + warp; g < total;
+       g += (int64_t)gridDim.x * kPartialWarps) {
+    int jb = 0;
+    while (g >= jobs.first_chunk[jb + 1]) ++jb;
+    const TreeJob J = jobs.job[jb];
+    const int64_t c = g - jobs.first_chunk[jb];
+    const int64_t nch = jobs.first_chunk[jb + 1] - jobs.first_chunk[jb];
+    const int64_t lo = c * jobs.chunk;
+    const int64_t hi = lo + jobs.chunk < J.n ? lo + jobs.chunk : J.n;
+    const double s = warp_chunk_sum(J.x, J.y, lo, hi, buf[warp]);
+    double* p = partials + jobs.first_chunk[jb];
+    if (lane == 0) {
+      p[c] = s;
+      if (nch <= 64) {  // the warp finishing a small job folds it (otherwise host folds)
+        __threadfence();
+        const unsigned prev = atomicAdd(&counters[jb], 1u);
+        if (prev == nch - 1) {
+          __threadfence();
+          volatile double* vp = p;
+          double q[64];
+          for (int i = 0; i < nch; ++i) q[i] = vp[i];
+          int m = (int)nch;
+          while (m > 1) {
+            const int h = m >> 1;
+            for (int i = 0; i < h; ++i) q[i] = q[2 * i] + q[2 * i + 1];
+            if (m & 1) { q[h] = q[m - 1]; m = h + 1; } else { m = h; }
+          }
+          *J.out = q[0];
+          counters[jb] = 0;
+        }
+      }
+    }
   }
 }
 
@@ -209,23 +276,56 @@ int simopt_fold_partials(cudaStream_t st, double* p, double* tmp, int64_t m, dou
   return SIMOPT_OK;
 }
 
+// Enqueue up to 4 independent fixed-tree reductions in one launch.
+static int tree_jobs(cudaStream_t st, TreeJob* js, int nj, int64_t chunk) {
+  SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1, got %lld", (long long)chunk);
+  TreeJobs J{};
+  J.chunk = chunk;
+  int k = 0;
+  for (int i = 0; i < nj; ++i) {
+    if (js[i].n == 0) {
+      SIMOPT_CUDA(cudaMemsetAsync(js[i].out, 0, sizeof(double), st));
+      continue;
+    }
+    J.job[k++] = js[i];
+  }
+  if (k == 0) return SIMOPT_OK;
+  J.njobs = k;
+  J.first_chunk[0] = 0;
+  for (int i = 0; i < k; ++i) J.first_chunk[i + 1] = J.first_chunk[i] + ceil_div(J.job[i].n, chunk);
+  const int64_t total = J.first_chunk[k];
+  unsigned char* ws = nullptr;
+  SIMOPT_CUDA(cudaMallocAsync(&ws, 2 * total * sizeof(double) + 64, st));
+  double* partials = reinterpret_cast<double*>(ws);
+  unsigned* counters = reinterpret_cast<unsigned*>(ws + 2 * total * sizeof(double));
+  SIMOPT_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned), st));
+  const int64_t g = ceil_div(total, kPartialWarps);
+  const int grid = (int)(g < 16 * SIMOPT_NUM_SMS ? g : 16 * SIMOPT_NUM_SMS);
+  k_tree_jobs<<<grid, kPartialWarps * 32, 0, st>>>(J, partials, counters);
+  SIMOPT_CHECK_LAUNCH("k_tree_jobs");
+  for (int i = 0; i < k; ++i) {
+    const int64_t nch = J.first_chunk[i + 1] - J.first_chunk[i];
+    if (nch > 64) {
+      const int rc = simopt_fold_partials(st, partials + J.first_chunk[i], partials + total + J.first_chunk[i],
+                                          nch, J.job[i].out);
+      if (rc) return rc;
+    }
+  }
+  SIMOPT_CUDA(cudaFreeAsync(ws, st));
+  return SIMOPT_OK;
+}
+
 static int tree_reduce(cudaStream_t st, const double* x, const double* y, int64_t n, int64_t chunk,
                        double* out) {
-  SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1, got %lld", (long long)chunk);
-  if (n == 0) {
-    SIMOPT_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
-    return SIMOPT_OK;
-  }
-  const int64_t nch = ceil_div(n, chunk);
-  double* p = nullptr;
-  SIMOPT_CUDA(cudaMallocAsync(&p, 2 * nch * sizeof(double), st));
-  const int g = (int)(ceil_div(nch, 8) < 8 * SIMOPT_NUM_SMS ? ceil_div(nch, 8) : 8 * SIMOPT_NUM_SMS);
-  if (y) k_chunk_partials<true><<<g, 256, 0, st>>>(x, y, n, chunk, p);
-  else k_chunk_partials<false><<<g, 256, 0, st>>>(x, nullptr, n, chunk, p);
-  SIMOPT_CHECK_LAUNCH("k_chunk_partials");
-  const int rc = simopt_fold_partials(st, p, p + nch, nch, out);
-  SIMOPT_CUDA(cudaFreeAsync(p, st));
-  return rc;
+  TreeJob j{x, y, n, out};
+  return tree_jobs(st, &j, 1, chunk);
+}
+
+extern "C" int simopt_tree_sums2(void* stream, const double* x0, const double* y0, int64_t n0,
+                                 double* out0, const double* x1, const double* y1, int64_t n1,
+                                 double* out1, int64_t chunk) {
+  TreeJob j[2] = {{x0, y0, n0, out0}, {x1, y1, n1, out1}};
+  return tree_jobs(as_stream(stream), j, 2, chunk);
 }
 
 extern "C" int simopt_dot(void* stream, const double* x, const double* y, int64_t n, int64_t chunk,

@@ -26,6 +26,6 @@ __device__ __forceinline__ void load_sincostab(double* tab) {
 __device__ __forceinline__ void normals4(uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi,
                                          uint64_t b, const double* tab, double z[4]) {
   const phx4 w = philox4x64_10(stream_block_counter(clo, chi, b), seed, sid);
-  glibc_boxmuller(phx_u01(w.v[0]), phx_u01(w.v[1]), tab, &z[0], &z[1]);
-  glibc_boxmuller(phx_u01(w.v[2]), phx_u01(w.v[3]), tab, &z[2], &z[3]);
+  glibc_boxmuller_fast(phx_u01(w.v[0]), phx_u01(w.v[1]), tab, &z[0], &z[1]);
+  glibc_boxmuller_fast(phx_u01(w.v[2]), phx_u01(w.v[3]), tab, &z[2], &z[3]);
 }

@@ -198,96 +198,126 @@ class NewsvendorProblem:
         return _nv_fw_run_device(self, config, backend, task_label, size, rep)
 
 
-def _nv_fw_run_device(prob: NewsvendorProblem, config, backend, label, size, rep):
-    """Device-resident frank_wolfe.fw_run for the newsvendor (frank_wolfe.py:91-121).
+class NvFwEngine:
+    """Device-resident Frank-Wolfe loop for one newsvendor run (frank_wolfe.py:91-121).
 
     Per step t (epoch k, inner m): one fused kernel updates x with the previous
     LMO vertex, writes objective terms, computes the next ECDF gradient and its
-    LMO argmin; two exact-tree reductions record dot(c, x) and the objective.
-    Iterates live in a ring of 2M+1 buffers so a failure detected at the epoch
-    check still has the reference's final_iterate at hand.
+    LMO argmin; one launch records dot(c, x) and the objective with the exact
+    tree.  Iterates live in a ring of 2M+1 buffers so a failure found at an
+    epoch check still has the reference's final_iterate at hand.
     """
-    dev = prob.dev
-    d, M, K = dev.d, config.inner_iters, config.epochs
-    T = K * M
-    H = 2 * M + 1
-    xs = torch.zeros(H, d, dtype=F64, device="cuda")
-    g = empty(d)
-    terms = empty(d)
-    flags = torch.zeros(T + 1, dtype=torch.int32, device="cuda")
-    spent = empty(T)
-    objs = empty(T)
-    stamps = torch.zeros(T + 1, dtype=torch.int64, device="cuda")
-    state = torch.zeros(4, dtype=torch.int64, device="cuda")  # NvState (32 bytes)
-    part_v = empty(_NV_PART_CAPACITY)
-    part_i = torch.empty(_NV_PART_CAPACITY, dtype=torch.int64, device="cuda")
-    sp = _lib.stream_ptr()
-    chunk = backend.chunk_size
-    a = NvIterArgs()
-    a.d, a.mu, a.sigma = d, dev.mu.data_ptr(), dev.sigma.data_ptr()
-    a.k, a.h, a.v, a.c = dev.k.data_ptr(), dev.h.data_ptr(), dev.v.data_ptr(), dev.c.data_ptr()
-    a.budget = dev.budget
-    a.g, a.terms, a.flags, a.state = g.data_ptr(), terms.data_ptr(), flags.data_ptr(), state.data_ptr()
-    a.part_v, a.part_i, a.part_capacity = part_v.data_ptr(), part_i.data_ptr(), _NV_PART_CAPACITY
-    lib = _lib.load()
-    trace = TraceBuilder()
-    host = {}
 
-    def check_epoch(k_done):
-        """Validate steps of epoch k_done (host sync on that epoch only)."""
-        lo, hi = k_done * M, (k_done + 1) * M
-        fl = to_host(flags[lo:hi + 1])
-        sp_ = to_host(spent[lo:hi])
-        ob = to_host(objs[lo:hi])
-        ts = to_host(stamps[lo:hi])
-        t0 = host.setdefault("t0", int(stamps[T].item()))
+    def __init__(self, prob: "NewsvendorProblem", inner_iters: int, epochs: int, chunk: int):
+        dev = prob.dev
+        self.prob, self.dev = prob, dev
+        self.M, self.K, self.chunk = inner_iters, epochs, chunk
+        d, M = dev.d, inner_iters
+        T = epochs * M
+        self.T, self.H = T, 2 * M + 1
+        self.xs = torch.zeros(self.H, d, dtype=F64, device="cuda")
+        self.g = empty(d)
+        self.terms = empty(d)
+        self.flags = torch.zeros(T + 1, dtype=torch.int32, device="cuda")
+        self.spent = empty(T)
+        self.objs = empty(T)
+        self.stamps = torch.zeros(T + 1, dtype=torch.int64, device="cuda")
+        self.state = torch.zeros(4, dtype=torch.int64, device="cuda")  # NvState (32 bytes)
+        self.part_v = empty(_NV_PART_CAPACITY)
+        self.part_i = torch.empty(_NV_PART_CAPACITY, dtype=torch.int64, device="cuda")
+        a = NvIterArgs()
+        a.d, a.mu, a.sigma = d, dev.mu.data_ptr(), dev.sigma.data_ptr()
+        a.k, a.h, a.v, a.c = dev.k.data_ptr(), dev.h.data_ptr(), dev.v.data_ptr(), dev.c.data_ptr()
+        a.budget = dev.budget
+        a.g, a.terms = self.g.data_ptr(), self.terms.data_ptr()
+        a.flags, a.state = self.flags.data_ptr(), self.state.data_ptr()
+        a.part_v, a.part_i, a.part_capacity = (self.part_v.data_ptr(), self.part_i.data_ptr(),
+                                               _NV_PART_CAPACITY)
+        self.args = a
+        self.lib = _lib.load()
+        self.t0 = None
+        self.resample_events = []
+
+    def start(self):
+        _lib.check(self.lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(self.stamps[self.T:])))
+
+    def enqueue_epoch(self, k: int, stream: RngStream, n_samples: int, time_resample: bool = False):
+        dev, a, lib, M, H = self.dev, self.args, self.lib, self.M, self.H
+        sp = _lib.stream_ptr()
+        if time_resample:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        dev.resample(stream, n_samples)
+        if time_resample:
+            e1.record()
+            self.resample_events.append((e0, e1))
+        a.S, a.nseg = dev.S, dev.nseg
+        a.dem, a.off, a.kappa = dev.dem.data_ptr(), dev.off.data_ptr(), dev.kappa.data_ptr()
+        t0 = k * M
+        a.x_in = a.x = self.xs[t0 % H].data_ptr()  # gradient + LMO at the epoch's first iterate
+        a.do_update, a.do_grad, a.step, a.grad_step, a.gamma = 0, 1, t0, t0, 0.0
+        _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
+        for m in range(M):
+            t = t0 + m
+            xin, xout = self.xs[t % H], self.xs[(t + 1) % H]
+            a.x_in, a.x = xin.data_ptr(), xout.data_ptr()
+            a.gamma = fw_step_size(k, M, m)
+            a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), t, t + 1
+            _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
+            # dot(c, x_{t+1}) for check_feasible and the objective's vec_sum, one launch
+            _lib.check(lib.simopt_tree_sums2(sp, _lib.ptr(dev.c), _lib.ptr(xout), dev.d,
+                                             _lib.ptr(self.spent[t:]), _lib.ptr(self.terms), None,
+                                             dev.d, _lib.ptr(self.objs[t:]), self.chunk))
+            _lib.check(lib.simopt_timestamp(sp, _lib.ptr(self.stamps[t:])))
+
+    def check_epoch(self, k: int, trace: TraceBuilder):
+        """Append epoch k's rows to `trace`; return (t, exc, iterate) at the first failure."""
+        M, H = self.M, self.H
+        lo, hi = k * M, (k + 1) * M
+        fl = to_host(self.flags[lo:hi + 1])
+        sp_ = to_host(self.spent[lo:hi])
+        ob = to_host(self.objs[lo:hi])
+        ts = to_host(self.stamps[lo:hi])
+        if self.t0 is None:
+            self.t0 = int(self.stamps[self.T].item())
         for i in range(M):
             t = lo + i
             if fl[i] & NV_FLAG_NAN_GRADIENT:
-                return t, InvalidGradient("gradient contains NaN"), xs[t % H]
-            if (fl[i] & NV_FLAG_NEGATIVE) or not sp_[i] <= dev.budget * (1.0 + FEAS_TOL):
-                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), xs[(t + 1) % H]
-            trace.append(t + 1, float(ob[i]), int(ts[i]) - t0)
+                return t, InvalidGradient("gradient contains NaN"), self.xs[t % H]
+            if (fl[i] & NV_FLAG_NEGATIVE) or not sp_[i] <= self.dev.budget * (1.0 + FEAS_TOL):
+                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), self.xs[(t + 1) % H]
+            trace.append(t + 1, float(ob[i]), int(ts[i]) - self.t0)
         return None
+
+    def iterate(self, t: int) -> torch.Tensor:
+        return self.xs[t % self.H]
+
+
+def _nv_fw_run_device(prob: "NewsvendorProblem", config, backend, label, size, rep):
+    eng = NvFwEngine(prob, config.inner_iters, config.epochs, backend.chunk_size)
+    trace = TraceBuilder()
 
     def abort(t, exc, it):
         partial = trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(it))
         raise RunAborted(f"frank-wolfe run failed at step {len(trace) + 1}: {exc}", partial) from exc
 
-    _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[T:])))
+    eng.start()
     events = []
-    for k in range(K):
-        dev.resample(config.stream, config.epoch_sample_size(k))
-        a.S, a.nseg, a.dem, a.off, a.kappa = dev.S, dev.nseg, dev.dem.data_ptr(), dev.off.data_ptr(), dev.kappa.data_ptr()
-        t0 = k * M
-        # gradient + LMO at the epoch's first iterate
-        a.x_in = a.x = xs[t0 % H].data_ptr()
-        a.do_update, a.do_grad, a.step, a.grad_step, a.gamma = 0, 1, t0, t0, 0.0
-        _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
-        for m in range(M):
-            t = t0 + m
-            # x_{t+1} = update(x_t) in its own ring slot, then gradient at x_{t+1}
-            xin, xout = xs[t % H], xs[(t + 1) % H]
-            a.x_in, a.x = xin.data_ptr(), xout.data_ptr()
-            a.gamma = fw_step_size(k, M, m)
-            a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), t, t + 1
-            _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
-            _lib.check(lib.simopt_dot(sp, _lib.ptr(dev.c), _lib.ptr(xout), d, chunk, _lib.ptr(spent[t:])))
-            _lib.check(lib.simopt_vec_sum(sp, _lib.ptr(terms), d, chunk, _lib.ptr(objs[t:])))
-            _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[t:])))
+    for k in range(config.epochs):
+        eng.enqueue_epoch(k, config.stream, config.epoch_sample_size(k))
         ev = torch.cuda.Event()
         ev.record()
         events.append(ev)
         if k >= 1:  # validate the previous epoch while this one runs
             events[k - 1].synchronize()
-            bad = check_epoch(k - 1)
+            bad = eng.check_epoch(k - 1, trace)
             if bad:
                 abort(*bad)
     events[-1].synchronize()
-    bad = check_epoch(K - 1)
+    bad = eng.check_epoch(config.epochs - 1, trace)
     if bad:
         abort(*bad)
-    return trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(xs[T % H]))
+    return trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(eng.iterate(eng.T)))
 
 
 def nv_gradient_hat(x, demands, task: NewsvendorTask, backend):
@@ -516,12 +546,12 @@ def _mv_fw_run_device(prob: MeanVarProblem, config, backend, label, size, rep):
             _lib.check(lib.simopt_axpy(sp, -1.0, _lib.ptr(w_in), _lib.ptr(s), d, _lib.ptr(dirn)))
             _lib.check(lib.simopt_axpy(sp, gamma, _lib.ptr(dirn), _lib.ptr(w_in), d, _lib.ptr(w_out)))
             _lib.check(lib.simopt_min_value(sp, _lib.ptr(w_out), d, _lib.ptr(wmin[t:])))
-            _lib.check(lib.simopt_vec_sum(sp, _lib.ptr(w_out), d, chunk, _lib.ptr(wsum[t:])))
             # objective(w_{t+1}); q is reused by the next gradient of this epoch
             _lib.check(lib.simopt_matvec(sp, _lib.ptr(x), n_k, d, None, n_k, _lib.ptr(mean),
                                          _lib.ptr(w_out), chunk, _lib.ptr(q)))
-            _lib.check(lib.simopt_dot(sp, _lib.ptr(q), _lib.ptr(q), n_k, chunk, _lib.ptr(quad[t:])))
-            _lib.check(lib.simopt_dot(sp, _lib.ptr(w_out), _lib.ptr(mean), d, chunk, _lib.ptr(lin[t:])))
+            _lib.check(lib.simopt_tree_sums2(sp, _lib.ptr(q), _lib.ptr(q), n_k, _lib.ptr(quad[t:]),
+                                             _lib.ptr(w_out), _lib.ptr(mean), d, _lib.ptr(lin[t:]), chunk))
+            _lib.check(lib.simopt_vec_sum(sp, _lib.ptr(w_out), d, chunk, _lib.ptr(wsum[t:])))
             _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[t:])))
         ev = torch.cuda.Event()
         ev.record()

@@ -109,14 +109,16 @@ int simopt_lmo_single_budget(void* stream, const double* g, const double* c, dou
 int simopt_min_value(void* stream, const double* x, int64_t n, double* out);
 
 /* ------------------------------------------------------------ newsvendor */
+/* Segment length and buckets per segment of the partitioned demand layout. */
+int simopt_nv_geometry(int64_t* seg, int64_t* buckets);
 /* Epoch layout sizes: demands d*S f64,
- * bucket starts d*nseg*1024 u16, nseg = ceil(S/4096). */
+ * bucket starts d*nseg*buckets u16, nseg = ceil(S/seg). */
 int simopt_nv_layout(int64_t d, int64_t S, int64_t* nseg, int64_t* dem_elems, int64_t* off_elems);
 
 /* sample_demands (sampling.py:173-193) fused with the partition the gradient
  * needs: draws D[j,s] = mu_j + sigma_j*z[j*S+s] (z = standard_normal(d*S) of the
- * stream at the given counter) are written bucket-partitioned per 4096-draw
- * segment.  Caller advances the counter by ceil(2*ceil(d*S/2)/4).  kappa[d] is
+ * stream at the given counter) are written bucket-partitioned per
+ * segment (simopt_nv_geometry).  Caller advances the counter by ceil(2*ceil(d*S/2)/4).  kappa[d] is
  * filled.  Rows sorted by the reference contain exactly the same multiset. */
 int simopt_nv_resample(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
                        uint64_t ctr_hi, int64_t d, int64_t S, const double* mu,

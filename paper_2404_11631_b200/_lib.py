@@ -39,6 +39,7 @@ SIGNATURES = {
     "simopt_lmo_simplex_slack": [_vp, _vp, _i64, _vp, _vp],
     "simopt_lmo_single_budget": [_vp, _vp, _vp, _d, _i64, _vp, _vp],
     "simopt_nv_layout": [_i64, _i64, _vp, _vp, _vp],
+    "simopt_nv_geometry": [_vp, _vp],
     "simopt_nv_resample": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
     "simopt_nv_counts": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp],
     "simopt_nv_iter": [_vp, _vp],

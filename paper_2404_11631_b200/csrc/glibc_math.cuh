@@ -53,18 +53,170 @@ SIMOPT_HD double gm_copysign(double x, double s) {
   return gm_from_bits((gm_bits(x) & 0x7fffffffffffffffULL) | (gm_bits(s) & 0x8000000000000000ULL));
 }
 
+#define GM_LN2_HI_V 0x1.62e42fee00000p-1
+#define GM_LN2_LO_V 0x1.a39ef35793c76p-33
+#define GM_LP1_V 0x1.5555555555593p-1
+#define GM_LP2_V 0x1.999999997fa04p-2
+#define GM_LP3_V 0x1.2492494229359p-2
+#define GM_LP4_V 0x1.c71c51d8e78afp-3
+#define GM_LP5_V 0x1.7466496cb03dep-3
+#define GM_LP6_V 0x1.39a09d078c69fp-3
+#define GM_LP7_V 0x1.2f112df3e5244p-3
+#define GM_SN3_V -0x1.5555555555515p-3
+#define GM_SN5_V 0x1.11110e829872fp-7
+#define GM_CS2_V 0x1.0000000000000p-1
+#define GM_CS4_V -0x1.5555555555535p-5
+#define GM_CS6_V 0x1.6c16bedd9e239p-10
+#define GM_S1_V -0x1.5555555555555p-3
+#define GM_S2_V 0x1.1111111110ecep-7
+#define GM_S3_V -0x1.a01a019db08b8p-13
+#define GM_S4_V 0x1.71de27b9a7ed9p-19
+#define GM_S5_V -0x1.addffc2fcdf59p-26
+#define GM_BIG_V 0x1.8p45
+#define GM_HP0_V 0x1.921fb54442d18p0
+#define GM_HP1_V 0x1.1a62633145c07p-54
+#define GM_MP1_V 0x1.921fb58000000p0
+#define GM_MP2_V -0x1.dde973c000000p-27
+#define GM_PP3_V -0x1.cb3b398000000p-55
+#define GM_PP4_V -0x1.d747f23e32ed7p-83
+#define GM_HPINV_V 0x1.45f306dc9c883p-1
+#define GM_TOINT_V 0x1.8p52
+#define GM_E_INVLN2N_V 0x1.71547652b82fep+7
+#define GM_E_SHIFT_V 0x1.8p52
+#define GM_E_NEGLN2HIN_V -0x1.62e42fefa0000p-8
+#define GM_E_NEGLN2LON_V -0x1.cf79abc9e3b3ap-47
+#define GM_E_C2_V 0x1.ffffffffffdbdp-2
+#define GM_E_C3_V 0x1.555555555543cp-3
+#define GM_E_C4_V 0x1.55555cf172b91p-5
+#define GM_E_C5_V 0x1.1111167a4d017p-7
+
+// Polynomial / reduction constants.  On the device they live in constant memory
+// so DFMA/DADD take them as c[bank][offset] operands (a 64-bit literal would be
+// re-materialised with two UMOVs at every use); on the host they are literals.
+#if defined(__CUDACC__)
+static __constant__ double gm_kconst[] = {
+  GM_LN2_HI_V,
+  GM_LN2_LO_V,
+  GM_LP1_V,
+  GM_LP2_V,
+  GM_LP3_V,
+  GM_LP4_V,
+  GM_LP5_V,
+  GM_LP6_V,
+  GM_LP7_V,
+  GM_SN3_V,
+  GM_SN5_V,
+  GM_CS2_V,
+  GM_CS4_V,
+  GM_CS6_V,
+  GM_S1_V,
+  GM_S2_V,
+  GM_S3_V,
+  GM_S4_V,
+  GM_S5_V,
+  GM_BIG_V,
+  GM_HP0_V,
+  GM_HP1_V,
+  GM_MP1_V,
+  GM_MP2_V,
+  GM_PP3_V,
+  GM_PP4_V,
+  GM_HPINV_V,
+  GM_TOINT_V,
+  GM_E_INVLN2N_V,
+  GM_E_SHIFT_V,
+  GM_E_NEGLN2HIN_V,
+  GM_E_NEGLN2LON_V,
+  GM_E_C2_V,
+  GM_E_C3_V,
+  GM_E_C4_V,
+  GM_E_C5_V,
+};
+#endif
+static const double gm_kconst_host[] = {
+  GM_LN2_HI_V,
+  GM_LN2_LO_V,
+  GM_LP1_V,
+  GM_LP2_V,
+  GM_LP3_V,
+  GM_LP4_V,
+  GM_LP5_V,
+  GM_LP6_V,
+  GM_LP7_V,
+  GM_SN3_V,
+  GM_SN5_V,
+  GM_CS2_V,
+  GM_CS4_V,
+  GM_CS6_V,
+  GM_S1_V,
+  GM_S2_V,
+  GM_S3_V,
+  GM_S4_V,
+  GM_S5_V,
+  GM_BIG_V,
+  GM_HP0_V,
+  GM_HP1_V,
+  GM_MP1_V,
+  GM_MP2_V,
+  GM_PP3_V,
+  GM_PP4_V,
+  GM_HPINV_V,
+  GM_TOINT_V,
+  GM_E_INVLN2N_V,
+  GM_E_SHIFT_V,
+  GM_E_NEGLN2HIN_V,
+  GM_E_NEGLN2LON_V,
+  GM_E_C2_V,
+  GM_E_C3_V,
+  GM_E_C4_V,
+  GM_E_C5_V,
+};
+#if defined(__CUDA_ARCH__)
+#define GM_K(i) gm_kconst[i]
+#else
+#define GM_K(i) gm_kconst_host[i]
+#endif
+#define GM_LN2_HI GM_K(0)
+#define GM_LN2_LO GM_K(1)
+#define GM_LP1 GM_K(2)
+#define GM_LP2 GM_K(3)
+#define GM_LP3 GM_K(4)
+#define GM_LP4 GM_K(5)
+#define GM_LP5 GM_K(6)
+#define GM_LP6 GM_K(7)
+#define GM_LP7 GM_K(8)
+#define GM_SN3 GM_K(9)
+#define GM_SN5 GM_K(10)
+#define GM_CS2 GM_K(11)
+#define GM_CS4 GM_K(12)
+#define GM_CS6 GM_K(13)
+#define GM_S1 GM_K(14)
+#define GM_S2 GM_K(15)
+#define GM_S3 GM_K(16)
+#define GM_S4 GM_K(17)
+#define GM_S5 GM_K(18)
+#define GM_BIG GM_K(19)
+#define GM_HP0 GM_K(20)
+#define GM_HP1 GM_K(21)
+#define GM_MP1 GM_K(22)
+#define GM_MP2 GM_K(23)
+#define GM_PP3 GM_K(24)
+#define GM_PP4 GM_K(25)
+#define GM_HPINV GM_K(26)
+#define GM_TOINT GM_K(27)
+#define GM_E_INVLN2N GM_K(28)
+#define GM_E_SHIFT GM_K(29)
+#define GM_E_NEGLN2HIN GM_K(30)
+#define GM_E_NEGLN2LON GM_K(31)
+#define GM_E_C2 GM_K(32)
+#define GM_E_C3 GM_K(33)
+#define GM_E_C4 GM_K(34)
+#define GM_E_C5 GM_K(35)
+
+
 // ---------------------------------------------------------------------------
 // log1p  (fdlibm algorithm as shipped in glibc s_log1p.c, FMA variant)
 // ---------------------------------------------------------------------------
-#define GM_LN2_HI 0x1.62e42fee00000p-1
-#define GM_LN2_LO 0x1.a39ef35793c76p-33
-#define GM_LP1 0x1.5555555555593p-1
-#define GM_LP2 0x1.999999997fa04p-2
-#define GM_LP3 0x1.2492494229359p-2
-#define GM_LP4 0x1.c71c51d8e78afp-3
-#define GM_LP5 0x1.7466496cb03dep-3
-#define GM_LP6 0x1.39a09d078c69fp-3
-#define GM_LP7 0x1.2f112df3e5244p-3
 
 SIMOPT_HD double glibc_log1p(double x) {
   const int32_t hx = gm_hi(x);
@@ -147,25 +299,6 @@ poly: {
 // sin / cos  (IBM accurate library as refactored in glibc s_sin.c, FMA variant)
 // `tab` points at the 440 doubles of __sincostab (global, constant or shared).
 // ---------------------------------------------------------------------------
-#define GM_SN3 -0x1.5555555555515p-3
-#define GM_SN5 0x1.11110e829872fp-7
-#define GM_CS2 0x1.0000000000000p-1
-#define GM_CS4 -0x1.5555555555535p-5
-#define GM_CS6 0x1.6c16bedd9e239p-10
-#define GM_S1 -0x1.5555555555555p-3
-#define GM_S2 0x1.1111111110ecep-7
-#define GM_S3 -0x1.a01a019db08b8p-13
-#define GM_S4 0x1.71de27b9a7ed9p-19
-#define GM_S5 -0x1.addffc2fcdf59p-26
-#define GM_BIG 0x1.8p45
-#define GM_HP0 0x1.921fb54442d18p0
-#define GM_HP1 0x1.1a62633145c07p-54
-#define GM_MP1 0x1.921fb58000000p0
-#define GM_MP2 -0x1.dde973c000000p-27
-#define GM_PP3 -0x1.cb3b398000000p-55
-#define GM_PP4 -0x1.d747f23e32ed7p-83
-#define GM_HPINV 0x1.45f306dc9c883p-1
-#define GM_TOINT 0x1.8p52
 
 // TAYLOR_SIN(xx, a, da) (asm 7b950 / 7c0d0)
 SIMOPT_HD double gm_taylor_sin(double a, double da) {
@@ -280,14 +413,7 @@ SIMOPT_HD void glibc_boxmuller(double u1, double u2, const double* tab, double* 
 // exp  (glibc >= 2.28 e_exp.c, Szabolcs Nagy's table method, N = 128; FMA variant
 // __exp_fma @0x79b60).  `etab` = __exp_data.tab (256 words, glibc_tables.h).
 // ---------------------------------------------------------------------------
-#define GM_E_INVLN2N 0x1.71547652b82fep+7
-#define GM_E_SHIFT 0x1.8p52
-#define GM_E_NEGLN2HIN -0x1.62e42fefa0000p-8
-#define GM_E_NEGLN2LON -0x1.cf79abc9e3b3ap-47
-#define GM_E_C2 0x1.ffffffffffdbdp-2
-#define GM_E_C3 0x1.555555555543cp-3
-#define GM_E_C4 0x1.55555cf172b91p-5
-#define GM_E_C5 0x1.1111167a4d017p-7
+
 
 // specialcase(tmp, sbits, ki) for 512 <= |x| < 1024 (asm 79c60..79d27)
 SIMOPT_HD double gm_exp_special(double tmp, uint64_t sbits, uint64_t ki) {

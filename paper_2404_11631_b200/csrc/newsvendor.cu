@@ -4,7 +4,7 @@
 //
 // Data layout (per resampling epoch, resident in HBM):
 //   dem   [d][S] f64   row j = product j's S demand draws, split into segments of
-//                      NV_SEG = 4096 draws; inside a segment the draws are grouped by
+//                      NV_SEG = 2048 draws; inside a segment the draws are grouped by
 //                      bucket (counting-sorted), buckets in ascending order.
 //   off   [d][nseg][NV_B] u16   start of each bucket inside its segment.
 //   kappa [d] f64      bucket scale B / (12 sigma_j).
@@ -34,10 +34,14 @@ __global__ void k_nv_kappa(const double* __restrict__ sigma, int64_t d, double* 
     kappa[j] = (double)NV_B / (12.0 * sigma[j]);
 }
 
-// One CTA = one (product j, segment s): generate the segment's draws
-// D = mu_j + sigma_j * z (sampling.py:190-191), counting-sort them by bucket in
-// shared memory, write the segment and its bucket starts.
-__global__ void __launch_bounds__(kResampleThreads)
+// Persistent CTAs walk (product j, segment s) pairs.  Per segment: generate the
+// segment's draws D = mu_j + sigma_j * z (sampling.py:190-191) in registers,
+// histogram them by bucket in shared memory, scan, scatter into bucket order, and
+// stream the segment and its bucket starts out.  The sin/cos table is staged once
+// per CTA.
+constexpr int kResampleMinBlocks = 4;
+
+__global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     k_nv_resample(uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi, int64_t d, int64_t S,
                   int nseg, const double* __restrict__ mu, const double* __restrict__ sigma,
                   const double* __restrict__ kappa, double* __restrict__ dem,
@@ -47,80 +51,108 @@ __global__ void __launch_bounds__(kResampleThreads)
   double* raw = tab + 448;                                        // NV_SEG
   double* sorted_ = raw + NV_SEG;                                 // NV_SEG
   int* hist = reinterpret_cast<int*>(sorted_ + NV_SEG);           // NV_B
-  const int64_t blk = blockIdx.x;
-  const int64_t j = blk / nseg;
-  const int s = (int)(blk - j * nseg);
-  const int64_t e0 = (int64_t)s * NV_SEG;
-  const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
-  const double muj = mu[j], sj = sigma[j], kj = kappa[j];
-  for (int i = threadIdx.x; i < NV_B; i += blockDim.x) hist[i] = 0;
+  uint16_t* bid = reinterpret_cast<uint16_t*>(hist + NV_B);       // NV_SEG bucket ids
+  __shared__ int wsum[kResampleThreads / 32];
   load_sincostab(tab);  // includes __syncthreads()
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nblk = d * nseg;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t j = blk / nseg;
+    const int s = (int)(blk - j * nseg);
+    const int64_t e0 = (int64_t)s * NV_SEG;
+    const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
+    const double muj = mu[j], sj = sigma[j], kj = kappa[j];
+    for (int i = threadIdx.x; i < NV_B; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
 
-  // 1) generate: normals i0 .. i0+len-1 of the epoch's standard_normal(d*S) draw.
-  const int64_t i0 = j * S + e0;
-  const int64_t q0 = i0 >> 2, q1 = (i0 + len - 1) >> 2;
-  for (int64_t q = q0 + threadIdx.x; q <= q1; q += blockDim.x) {
-    double z[4];
-    normals4(seed, sid, clo, chi, (uint64_t)q, tab, z);
+    // 1) generate normals i0 .. i0+len-1 of the epoch's standard_normal(d*S) draw
+    const int64_t i0 = j * S + e0;
+    const int64_t q0 = i0 >> 2, q1 = (i0 + len - 1) >> 2;
+    for (int64_t q = q0 + threadIdx.x; q <= q1; q += blockDim.x) {
+      double z[4];
+      normals4(seed, sid, clo, chi, (uint64_t)q, tab, z);
+      const int64_t l0 = (q << 2) - i0;
+      if (l0 >= 0 && l0 + 4 <= len) {
+        uint16_t bb[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t l = (q << 2) + k - i0;
-      if (l >= 0 && l < len) {
-        const double dv = muj + sj * z[k];
-        raw[l] = dv;
-        atomicAdd(&hist[nv_bucket(dv, muj, kj)], 1);
+        for (int k = 0; k < 4; ++k) {
+          const double dv = muj + sj * z[k];
+          raw[l0 + k] = dv;
+          const int b = nv_bucket(dv, muj, kj);
+          bb[k] = (uint16_t)b;
+          atomicAdd(&hist[b], 1);
+        }
+        if ((l0 & 3) == 0) {
+          reinterpret_cast<uint2*>(bid)[l0 >> 2] =
+              make_uint2(bb[0] | ((uint32_t)bb[1] << 16), bb[2] | ((uint32_t)bb[3] << 16));
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) bid[l0 + k] = bb[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t l = l0 + k;
+          if (l >= 0 && l < len) {
+            const double dv = muj + sj * z[k];
+            raw[l] = dv;
+            const int b = nv_bucket(dv, muj, kj);
+            bid[l] = (uint16_t)b;
+            atomicAdd(&hist[b], 1);
+          }
+        }
       }
     }
-  }
-  __syncthreads();
-  // 2) exclusive scan of the histogram (NV_B entries, 256 threads x 4).
-  {
-    constexpr int kPer = NV_B / kResampleThreads;
-    int v[kPer];
-    int run = 0;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) { v[k] = hist[threadIdx.x * kPer + k]; run += v[k]; }
-    // block-wide exclusive scan of `run`
-    __shared__ int wsum[kResampleThreads / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int incl = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    if (warp == 0) {
-      int w = lane < kResampleThreads / 32 ? wsum[lane] : 0;
+    // 2) exclusive scan of the histogram (NV_B entries, kPer per thread)
+    {
+      constexpr int kPer = NV_B / kResampleThreads;
+      int v[kPer];
+      int run = 0;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) { v[k] = hist[threadIdx.x * kPer + k]; run += v[k]; }
+      int incl = run;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += t;
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
       }
-      if (lane < kResampleThreads / 32) wsum[lane] = w;  // inclusive warp prefix
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        int w = lane < kResampleThreads / 32 ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, w, o);
+          if (lane >= o) w += t;
+        }
+        if (lane < kResampleThreads / 32) wsum[lane] = w;  // inclusive warp prefix
+      }
+      __syncthreads();
+      int base = incl - run + (warp > 0 ? wsum[warp - 1] : 0);
+      uint32_t packed = 0;
+      uint16_t* o = off + ((j * nseg + s) * (int64_t)NV_B);
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int b = threadIdx.x * kPer + k;
+        packed |= (uint32_t)(uint16_t)base << (16 * k);
+        hist[b] = base;  // becomes the scatter cursor
+        base += v[k];
+      }
+      static_assert(kPer == 2, "bucket starts are stored as one u32 per thread");
+      reinterpret_cast<uint32_t*>(o)[threadIdx.x] = packed;
     }
     __syncthreads();
-    int base = incl - run + (warp > 0 ? wsum[warp - 1] : 0);
-    uint16_t* o = off + ((j * nseg + s) * (int64_t)NV_B);
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int b = threadIdx.x * kPer + k;
-      o[b] = (uint16_t)base;
-      hist[b] = base;  // becomes the scatter cursor
-      base += v[k];
+    // 3) scatter into bucket order (order inside a bucket is irrelevant to every count)
+    for (int l = threadIdx.x; l < len; l += blockDim.x) {
+      const int pos = atomicAdd(&hist[bid[l]], 1);
+      sorted_[pos] = raw[l];
     }
+    __syncthreads();
+    double* dst = dem + j * S + e0;
+    for (int l = threadIdx.x; l < len; l += blockDim.x) dst[l] = sorted_[l];
+    __syncthreads();
   }
-  __syncthreads();
-  // 3) scatter into bucket order (order inside a bucket is irrelevant to every count).
-  for (int l = threadIdx.x; l < len; l += blockDim.x) {
-    const double dv = raw[l];
-    const int pos = atomicAdd(&hist[nv_bucket(dv, muj, kj)], 1);
-    sorted_[pos] = dv;
-  }
-  __syncthreads();
-  double* dst = dem + j * S + e0;
-  for (int l = threadIdx.x; l < len; l += blockDim.x) dst[l] = sorted_[l];
 }
 
 }  // namespace
@@ -243,6 +275,12 @@ int simopt_nv_kappa_impl(cudaStream_t st, const double* sigma, int64_t d, double
   return SIMOPT_OK;
 }
 
+extern "C" int simopt_nv_geometry(int64_t* seg, int64_t* buckets) {
+  if (seg) *seg = NV_SEG;
+  if (buckets) *buckets = NV_B;
+  return SIMOPT_OK;
+}
+
 extern "C" int simopt_nv_layout(int64_t d, int64_t S, int64_t* nseg, int64_t* dem_elems,
                                 int64_t* off_elems) {
   SIMOPT_REQUIRE(d >= 1 && S >= 1, SIMOPT_E_EMPTY, "need d >= 1 products and S >= 1 samples");
@@ -263,14 +301,17 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   const int64_t nseg = ceil_div(S, NV_SEG);
   const int64_t nblk = d * nseg;
   SIMOPT_REQUIRE(nblk < (1LL << 31), SIMOPT_E_CONFIG, "too many segments");
-  const size_t smem = (448 + 2 * NV_SEG) * sizeof(double) + NV_B * sizeof(int);
+  const size_t smem = (448 + 2 * NV_SEG) * sizeof(double) + NV_B * sizeof(int) +
+                      NV_SEG * sizeof(uint16_t);
   static bool attr = false;
   if (!attr) {
     SIMOPT_CUDA(cudaFuncSetAttribute(k_nv_resample, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     attr = true;
   }
-  k_nv_resample<<<(unsigned)nblk, kResampleThreads, smem, st>>>(seed, sid, clo, chi, d, S,
+  const int64_t grid = nblk < (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks * 8
+                           ? nblk : (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks * 8;
+  k_nv_resample<<<(unsigned)grid, kResampleThreads, smem, st>>>(seed, sid, clo, chi, d, S,
                                                                 (int)nseg, mu, sigma, kappa, dem,
                                                                 off);
   SIMOPT_CHECK_LAUNCH("k_nv_resample");
@@ -279,8 +320,8 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
 
 extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   NvIterArgs a = *args;
-  const int grid = (int)(ceil_div(a.d, kIterWarps) < 4 * SIMOPT_NUM_SMS ? ceil_div(a.d, kIterWarps)
-                                                                         : 4 * SIMOPT_NUM_SMS);
+  const int grid = (int)(ceil_div(a.d, kIterWarps) < 16 * SIMOPT_NUM_SMS ? ceil_div(a.d, kIterWarps)
+                                                                          : 16 * SIMOPT_NUM_SMS);
   SIMOPT_REQUIRE(grid <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
   k_nv_iter<<<grid, kIterWarps * 32, 0, as_stream(stream)>>>(a);
   SIMOPT_CHECK_LAUNCH("k_nv_iter");

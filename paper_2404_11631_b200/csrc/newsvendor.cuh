@@ -6,8 +6,8 @@
 #include "glibc_math.cuh"
 #include "glibc_tables.h"
 
-#define NV_SEG 4096  // demand draws per sorted segment
-#define NV_B 1024    // buckets per segment
+#define NV_SEG 2048  // demand draws per bucket-partitioned segment
+#define NV_B 512     // buckets per segment
 
 // Monotone bucket map (see newsvendor.cu header).
 __device__ __forceinline__ int nv_bucket(double v, double mu, double kappa) {

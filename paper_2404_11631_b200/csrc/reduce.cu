@@ -34,38 +34,57 @@ struct TreeJobs {
   int64_t first_chunk[5];  // prefix of chunk counts
 };
 
+// Raw tile loads (no consumer until the next iteration, so they stay in flight
+// while lane 0 walks the previous tile).
+__device__ __forceinline__ void tile_load(const double* __restrict__ x, const double* __restrict__ y,
+                                          int64_t base, int64_t hi, int lane,
+                                          double (&xr)[kTile / 32], double (&yr)[kTile / 32]) {
+#pragma unroll
+  for (int t = 0; t < kTile / 32; ++t) {
+    const int64_t i = base + lane + 32 * t;
+    xr[t] = (i < hi) ? x[i] : 0.0;
+    yr[t] = (y != nullptr && i < hi) ? y[i] : 1.0;
+  }
+}
+
 __device__ __forceinline__ double warp_chunk_sum(const double* __restrict__ x,
                                                  const double* __restrict__ y, int64_t lo,
                                                  int64_t hi, double* buf) {
   const int lane = threadIdx.x & 31;
-  double r[kTile / 32];
-  auto load = [&](int64_t base) {
-#pragma unroll
-    for (int t = 0; t < kTile / 32; ++t) {
-      const int64_t i = base + lane + 32 * t;
-      r[t] = (i < hi) ? (y ? x[i] * y[i] : x[i]) : 0.0;
-    }
-  };
+  const bool has_y = y != nullptr;
+  double xr[kTile / 32], yr[kTile / 32];
   double s = 0.0;
-  load(lo);
+  tile_load(x, y, lo, hi, lane, xr, yr);
   int parity = 0;
   for (int64_t base = lo; base < hi; base += kTile) {
     double* b = buf + parity * kTile;
 #pragma unroll
-    for (int t = 0; t < kTile / 32; ++t) b[lane + 32 * t] = r[t];
+    for (int t = 0; t < kTile / 32; ++t) b[lane + 32 * t] = has_y ? xr[t] * yr[t] : xr[t];
     __syncwarp();
-    if (base + kTile < hi) load(base + kTile);
+    if (base + kTile < hi) tile_load(x, y, base + kTile, hi, lane, xr, yr);
     if (lane == 0) {
       const int cnt = (int)(hi - base < kTile ? hi - base : kTile);
-      int i = 0;
-      for (; i + 8 <= cnt; i += 8) {
-        double v[8];
+      if (cnt == kTile) {
+        // 16-element register batches, next batch loaded before the current is added
+        double v[16], w[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = b[i + k];
+        for (int k = 0; k < 16; ++k) v[k] = b[k];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) s = s + v[k];
+        for (int i = 0; i < kTile; i += 32) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) w[k] = b[i + 16 + k];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) s = s + v[k];
+          if (i + 32 < kTile) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = b[i + 32 + k];
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) s = s + w[k];
+        }
+      } else {
+        for (int i = 0; i < cnt; ++i) s = s + b[i];
       }
-      for (; i < cnt; ++i) s = s + b[i];
     }
     parity ^= 1;
   }

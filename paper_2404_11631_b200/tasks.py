@@ -45,9 +45,16 @@ class NvIterArgs(ctypes.Structure):
     ]
 
 
+def nv_geometry():
+    """(draws per segment, buckets per segment) of the partitioned demand layout."""
+    seg, nb = ctypes.c_int64(), ctypes.c_int64()
+    _lib.call("simopt_nv_geometry", ctypes.byref(seg), ctypes.byref(nb))
+    return seg.value, nb.value
+
+
 NV_FLAG_NAN_GRADIENT = 1
 NV_FLAG_NEGATIVE = 2
-_NV_PART_CAPACITY = 4 * 148
+_NV_PART_CAPACITY = 16 * 148
 
 
 # ---------------------------------------------------------------------------
@@ -201,11 +208,14 @@ class NewsvendorProblem:
 class NvFwEngine:
     """Device-resident Frank-Wolfe loop for one newsvendor run (frank_wolfe.py:91-121).
 
-    Per step t (epoch k, inner m): one fused kernel updates x with the previous
-    LMO vertex, writes objective terms, computes the next ECDF gradient and its
-    LMO argmin; one launch records dot(c, x) and the objective with the exact
-    tree.  Iterates live in a ring of 2M+1 buffers so a failure found at an
-    epoch check still has the reference's final_iterate at hand.
+    Per step t (epoch k, inner m) the main stream runs ONE fused kernel: update x
+    with the previous LMO vertex, write the objective terms of the new iterate,
+    compute the next ECDF gradient and its LMO argmin.  The recorded quantities
+    (exact-tree dot(c, x) for check_feasible, exact-tree objective sum, a
+    %globaltimer stamp) run on a side stream, off the critical path.  Iterates and
+    objective terms live in rings of 2M+1 slots (the side stream is throttled so a
+    slot is never overwritten before it is read), which also keeps the
+    reference's final_iterate at hand when an epoch check finds a failure.
     """
 
     def __init__(self, prob: "NewsvendorProblem", inner_iters: int, epochs: int, chunk: int):
@@ -216,8 +226,8 @@ class NvFwEngine:
         T = epochs * M
         self.T, self.H = T, 2 * M + 1
         self.xs = torch.zeros(self.H, d, dtype=F64, device="cuda")
+        self.terms = torch.empty(self.H, d, dtype=F64, device="cuda")
         self.g = empty(d)
-        self.terms = empty(d)
         self.flags = torch.zeros(T + 1, dtype=torch.int32, device="cuda")
         self.spent = empty(T)
         self.objs = empty(T)
@@ -229,7 +239,7 @@ class NvFwEngine:
         a.d, a.mu, a.sigma = d, dev.mu.data_ptr(), dev.sigma.data_ptr()
         a.k, a.h, a.v, a.c = dev.k.data_ptr(), dev.h.data_ptr(), dev.v.data_ptr(), dev.c.data_ptr()
         a.budget = dev.budget
-        a.g, a.terms = self.g.data_ptr(), self.terms.data_ptr()
+        a.g = self.g.data_ptr()
         a.flags, a.state = self.flags.data_ptr(), self.state.data_ptr()
         a.part_v, a.part_i, a.part_capacity = (self.part_v.data_ptr(), self.part_i.data_ptr(),
                                                _NV_PART_CAPACITY)
@@ -237,13 +247,18 @@ class NvFwEngine:
         self.lib = _lib.load()
         self.t0 = None
         self.resample_events = []
+        self.side = torch.cuda.Stream()
+        self.side_done = {}   # step -> event recorded on the side stream
+        self.epoch_done = {}  # epoch -> event after its last recorded step
 
     def start(self):
         _lib.check(self.lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(self.stamps[self.T:])))
 
     def enqueue_epoch(self, k: int, stream: RngStream, n_samples: int, time_resample: bool = False):
         dev, a, lib, M, H = self.dev, self.args, self.lib, self.M, self.H
-        sp = _lib.stream_ptr()
+        main = torch.cuda.current_stream()
+        sp = _lib.stream_ptr(main)
+        ssp = _lib.stream_ptr(self.side)
         if time_resample:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -255,24 +270,42 @@ class NvFwEngine:
         a.dem, a.off, a.kappa = dev.dem.data_ptr(), dev.off.data_ptr(), dev.kappa.data_ptr()
         t0 = k * M
         a.x_in = a.x = self.xs[t0 % H].data_ptr()  # gradient + LMO at the epoch's first iterate
+        a.terms = self.terms[t0 % H].data_ptr()
         a.do_update, a.do_grad, a.step, a.grad_step, a.gamma = 0, 1, t0, t0, 0.0
         _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
         for m in range(M):
             t = t0 + m
-            xin, xout = self.xs[t % H], self.xs[(t + 1) % H]
+            slot = (t + 1) % H
+            old = self.side_done.pop(t + 1 - H, None)  # slot last read by step t+1-H
+            if old is not None:
+                main.wait_event(old)
+            xin, xout = self.xs[t % H], self.xs[slot]
             a.x_in, a.x = xin.data_ptr(), xout.data_ptr()
+            a.terms = self.terms[slot].data_ptr()
             a.gamma = fw_step_size(k, M, m)
             a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), t, t + 1
             _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.side.wait_event(ev)
             # dot(c, x_{t+1}) for check_feasible and the objective's vec_sum, one launch
-            _lib.check(lib.simopt_tree_sums2(sp, _lib.ptr(dev.c), _lib.ptr(xout), dev.d,
-                                             _lib.ptr(self.spent[t:]), _lib.ptr(self.terms), None,
-                                             dev.d, _lib.ptr(self.objs[t:]), self.chunk))
-            _lib.check(lib.simopt_timestamp(sp, _lib.ptr(self.stamps[t:])))
+            _lib.check(lib.simopt_tree_sums2(ssp, _lib.ptr(dev.c), _lib.ptr(xout), dev.d,
+                                             _lib.ptr(self.spent[t:]), _lib.ptr(self.terms[slot]),
+                                             None, dev.d, _lib.ptr(self.objs[t:]), self.chunk))
+            _lib.check(lib.simopt_timestamp(ssp, _lib.ptr(self.stamps[t:])))
+            done = torch.cuda.Event()
+            done.record(self.side)
+            self.side_done[t] = done
+        self.epoch_done[k] = self.side_done[t0 + M - 1]
+
+    def finish(self):
+        """Join the side stream into the caller's stream."""
+        torch.cuda.current_stream().wait_stream(self.side)
 
     def check_epoch(self, k: int, trace: TraceBuilder):
         """Append epoch k's rows to `trace`; return (t, exc, iterate) at the first failure."""
         M, H = self.M, self.H
+        self.epoch_done[k].synchronize()
         lo, hi = k * M, (k + 1) * M
         fl = to_host(self.flags[lo:hi + 1])
         sp_ = to_host(self.spent[lo:hi])
@@ -313,6 +346,7 @@ def _nv_fw_run_device(prob: "NewsvendorProblem", config, backend, label, size, r
             bad = eng.check_epoch(k - 1, trace)
             if bad:
                 abort(*bad)
+    eng.finish()
     events[-1].synchronize()
     bad = eng.check_epoch(config.epochs - 1, trace)
     if bad:

@@ -25,18 +25,20 @@ def _task_from_golden(pkg, g):
 
 def _check_layout(dev, sorted_rows):
     """Bucketed segments hold exactly the reference's sorted rows; bucket order respected."""
+    from paper_2404_11631_b200.tasks import nv_geometry
+    seg, nb = nv_geometry()
     d, S = sorted_rows.shape
     dem = dev.dem.view(d, S).cpu().numpy()
-    off = dev.off.view(d, dev.nseg, 1024).cpu().numpy().astype(np.int64) & 0xFFFF
+    off = dev.off.view(d, dev.nseg, nb).cpu().numpy().astype(np.int64) & 0xFFFF
     kappa = dev.kappa.cpu().numpy()
     mu = dev.mu.cpu().numpy()
     assert np.array_equal(np.sort(dem, axis=1), sorted_rows)
     for j in range(min(d, 64)):
         for s in range(dev.nseg):
-            seg = dem[j, s * 4096:(s + 1) * 4096]
-            b = np.clip(np.floor((seg - mu[j]) * kappa[j] + 512.0), 0, 1023).astype(np.int64)
+            sv = dem[j, s * seg:(s + 1) * seg]
+            b = np.clip(np.floor((sv - mu[j]) * kappa[j] + nb / 2), 0, nb - 1).astype(np.int64)
             assert np.all(np.diff(b) >= 0)
-            starts = np.searchsorted(b, np.arange(1024), side="left")
+            starts = np.searchsorted(b, np.arange(nb), side="left")
             assert np.array_equal(off[j, s], starts)
 
 

@@ -1,0 +1,75 @@
+"""Host logic for sample/product sharding across ranks (one process per GPU).
+
+Reference anchor: the fixed tree of sobench/_kernels.py:1-42 (chunk partials
+folded pairwise in index order).  If every rank owns whole 4096-chunks, the
+allgathered per-chunk partials folded in index order reproduce the
+single-process reduction bit for bit at any world size (SURVEY §8e
+"deterministic mode").  RNG needs no communication: product j's draws are
+normals j*S .. j*S+S-1 of the epoch's stream, i.e. Philox blocks
+(j*S)//4 .. (j*S+S-1)//4.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, world: int, rank: int, align: int = 4096) -> tuple:
+    """[lo, hi) of rank's contiguous shard; boundaries are multiples of `align`."""
+    units = -(-n // align)
+    per = -(-units // world)
+    lo = min(n, rank * per * align)
+    hi = min(n, (rank + 1) * per * align)
+    return lo, hi
+
+
+def first_block(j: int, samples_per_item: int) -> tuple:
+    """(Philox block index, word offset) of item j's first normal."""
+    e = j * samples_per_item
+    return e // 4, e % 4
+
+
+def fold_pairwise(p: list) -> float:
+    """_kernels.py:30-42 on a Python list (index order, odd tail carried)."""
+    p = list(p)
+    m = len(p)
+    if m == 0:
+        return 0.0
+    while m > 1:
+        h = m // 2
+        q = [p[2 * i] + p[2 * i + 1] for i in range(h)]
+        if m & 1:
+            q.append(p[m - 1])
+        p, m = q, len(q)
+    return p[0]
+
+
+def allgather_fold(local_partials: torch.Tensor, group=None) -> float:
+    """Exact global tree root from each rank's in-order chunk partials (CPU or CUDA tensor)."""
+    world = dist.get_world_size(group)
+    n_local = torch.tensor([local_partials.numel()], dtype=torch.int64, device=local_partials.device)
+    sizes = [torch.zeros_like(n_local) for _ in range(world)]
+    dist.all_gather(sizes, n_local, group=group)
+    cap = int(max(s.item() for s in sizes))
+    buf = torch.zeros(cap, dtype=torch.float64, device=local_partials.device)
+    buf[: local_partials.numel()] = local_partials
+    bufs = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf, group=group)
+    parts = []
+    for s, b in zip(sizes, bufs):
+        parts.extend(b[: int(s.item())].cpu().tolist())
+    return fold_pairwise(parts)
+
+
+def allreduce_argmin(value: float, index: int, group=None, device="cpu") -> tuple:
+    """Global first-argmin (np.argmin semantics) of per-rank (value, global index) pairs."""
+    world = dist.get_world_size(group)
+    t = torch.tensor([value, float(index)], dtype=torch.float64, device=device)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    best = None
+    for o in out:
+        v, i = float(o[0]), int(o[1])
+        if best is None or v < best[0] or (v == best[0] and i < best[1]):
+            best = (v, i)
+    return best

@@ -68,6 +68,13 @@ int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t stream_id, 
                                uint64_t ctr_hi, int64_t n_samples, int64_t d, const double* mu,
                                const double* sigma, double* out);
 
+/* synth_classification features (sampling.py:246-255): out[i] = (u_i >= 0.5) as 0.0/1.0
+ * for the n uniforms of the stream at the counter.  Caller advances by ceil(n/4). */
+int simopt_bernoulli_half(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                          uint64_t ctr_hi, int64_t n, double* out);
+/* out[i] = (x[i] > thr) as 0.0/1.0 (sampling.py:261). */
+int simopt_threshold(void* stream, const double* x, double thr, int64_t n, double* out);
+
 /* ------------------------------------------------------------ backend.py */
 /* Fixed-tree reductions (backend.py:80-141, _kernels.py:30-156): chunk-local
  * strictly sequential sums, chunk partials folded pairwise in index order.
@@ -177,6 +184,34 @@ int simopt_nv_iter(void* stream, const NvIterArgs* args);
 int simopt_nv_cost_terms(void* stream, const double* x, const double* mu, const double* sigma,
                          const double* unit, const double* hold, const double* sell, int64_t d,
                          double* out);
+
+/* ------------------------------------------------------------ logistic / SQN */
+/* c - z[idx] with c = sigmoid(t) (tasks.py:235-236); idx may be NULL. */
+int simopt_logistic_resid(void* stream, const double* t, const double* z, const int64_t* idx,
+                          int64_t n, double* out);
+/* (c * (1 - c)) * tv with c = sigmoid(t) (tasks.py:250-252). */
+int simopt_logistic_hvp_weights(void* stream, const double* t, const double* tv, int64_t n,
+                                double* out);
+/* logistic_loss_block (_kernels.py:193-201) with z[idx]; idx may be NULL. */
+int simopt_logistic_loss_terms(void* stream, const double* t, const double* z, const int64_t* idx,
+                               int64_t n, double* out);
+/* bfgs_rank2_block over all rows (_kernels.py:226-242), h is n x n row-major. */
+int simopt_bfgs_rank2(void* stream, double* h, const double* s, const double* u, double coef_su,
+                      double coef_ss, int64_t n);
+/* h = diag(v) (sqn.py:96-97). */
+int simopt_diag_fill(void* stream, double* h, int64_t n, double v);
+enum simopt_vec { SIMOPT_VEC_SUB_SCALED = 0, SIMOPT_VEC_ADD = 1, SIMOPT_VEC_SUB = 2,
+                  SIMOPT_VEC_SCALE = 3 };
+/* out = x - alpha*y | x + y | x - y | x*alpha (numpy order, no FMA). */
+int simopt_vec_op(void* stream, int op, double alpha, const double* x, const double* y, int64_t n,
+                  double* out);
+/* sample_indices (sampling.py:196-209) on the device for b <= 4096: out[0..b) of the
+ * partial Fisher-Yates driven by uniform01(stream at counter, b).  Caller advances
+ * the counter by ceil(b/4). */
+int simopt_sample_indices(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                          uint64_t ctr_hi, int64_t n, int64_t b, int64_t* out);
+/* Same swap sequence on host memory for large b (u = the b uniforms). */
+int simopt_fisher_yates_host(int64_t n, int64_t b, const double* u, int64_t* out);
 
 #ifdef __cplusplus
 }

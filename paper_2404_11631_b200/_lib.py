@@ -26,6 +26,8 @@ SIGNATURES = {
     "simopt_uniform01": [_vp, _u64, _u64, _u64, _u64, _i64, _vp],
     "simopt_standard_normal": [_vp, _u64, _u64, _u64, _u64, _i64, _vp],
     "simopt_sample_returns_diag": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp, _vp],
+    "simopt_bernoulli_half": [_vp, _u64, _u64, _u64, _u64, _i64, _vp],
+    "simopt_threshold": [_vp, _vp, _d, _i64, _vp],
     "simopt_dot": [_vp, _vp, _vp, _i64, _i64, _vp],
     "simopt_vec_sum": [_vp, _vp, _i64, _i64, _vp],
     "simopt_tree_sums2": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64],
@@ -46,6 +48,14 @@ SIGNATURES = {
     "simopt_ecdf_count_sorted": [_vp, _vp, _i64, _i64, _vp, _vp],
     "simopt_nv_grad_from_counts": [_vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp],
     "simopt_nv_cost_terms": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
+    "simopt_logistic_resid": [_vp, _vp, _vp, _vp, _i64, _vp],
+    "simopt_logistic_hvp_weights": [_vp, _vp, _vp, _i64, _vp],
+    "simopt_logistic_loss_terms": [_vp, _vp, _vp, _vp, _i64, _vp],
+    "simopt_bfgs_rank2": [_vp, _vp, _vp, _vp, _d, _d, _i64],
+    "simopt_diag_fill": [_vp, _vp, _i64, _d],
+    "simopt_vec_op": [_vp, _i32, _d, _vp, _vp, _i64, _vp],
+    "simopt_sample_indices": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp],
+    "simopt_fisher_yates_host": [_i64, _i64, _vp, _vp],
 }
 
 

@@ -98,3 +98,42 @@ extern "C" int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t 
   SIMOPT_CHECK_LAUNCH("k_normal<affine>");
   return SIMOPT_OK;
 }
+
+namespace {
+// synth_classification features (sampling.py:246-255): x = (u >= 0.5), i.e. the MSB
+// of the Philox word, written as 0.0 / 1.0.
+__global__ void __launch_bounds__(256) k_bernoulli_half(uint64_t seed, uint64_t sid, uint64_t clo,
+                                                        uint64_t chi, int64_t n,
+                                                        double* __restrict__ out) {
+  const int64_t nblk = (n + 3) >> 2;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const phx4 w = philox4x64_10(stream_block_counter(clo, chi, b), seed, sid);
+    const int64_t e = b << 2;
+    for (int k = 0; k < 4 && e + k < n; ++k) out[e + k] = (w.v[k] >> 63) ? 1.0 : 0.0;
+  }
+}
+
+// labels = (scores > median).astype(float64) (sampling.py:261)
+__global__ void k_threshold(const double* __restrict__ x, double thr, int64_t n,
+                            double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (x[i] > thr) ? 1.0 : 0.0;
+}
+}  // namespace
+
+extern "C" int simopt_bernoulli_half(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
+                                     uint64_t chi, int64_t n, double* out) {
+  SIMOPT_REQUIRE(n > 0, SIMOPT_E_EMPTY, "requested %lld draws", (long long)n);
+  k_bernoulli_half<<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, n, out);
+  SIMOPT_CHECK_LAUNCH("k_bernoulli_half");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_threshold(void* stream, const double* x, double thr, int64_t n, double* out) {
+  if (n == 0) return SIMOPT_OK;
+  k_threshold<<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(x, thr, n, out);
+  SIMOPT_CHECK_LAUNCH("k_threshold");
+  return SIMOPT_OK;
+}

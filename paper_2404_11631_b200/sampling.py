@@ -154,3 +154,80 @@ def sample_returns_device(spec: GaussianSpec, n_samples: int, stream: RngStream,
 def sample_returns(spec: GaussianSpec, n_samples: int, stream: RngStream, backend=None) -> np.ndarray:
     chunk = getattr(backend, "chunk_size", 4096)
     return to_host(sample_returns_device(spec, n_samples, stream, chunk=chunk))
+
+
+def sample_indices_device(n: int, b: int, stream: RngStream) -> torch.Tensor:
+    """b indices from range(n), uniform without replacement (sampling.py:196-209).
+
+    Partial Fisher-Yates with one uniform per selected index; the swap chain runs
+    on the device (b <= 4096, the SQN mini-batches) or, for large b (instance
+    label flips), in the native host helper over the device-drawn uniforms.
+    """
+    if not 1 <= b <= n:
+        raise ConfigurationError(f"need 1 <= b <= n, got b={b}, n={n}")
+    out = torch.empty(b, dtype=torch.int64, device=device())
+    if b <= 4096:
+        _lib.call("simopt_sample_indices", _lib.stream_ptr(), *stream.words(), n, b, _lib.ptr(out))
+        stream.advance(b)
+        return out
+    u = uniform01(stream, b)
+    host = np.empty(b, dtype=np.int64)
+    _lib.check(_lib.load().simopt_fisher_yates_host(n, b, u.ctypes.data, host.ctypes.data))
+    out.copy_(torch.from_numpy(host))
+    return out
+
+
+def sample_indices(n: int, b: int, stream: RngStream) -> np.ndarray:
+    return to_host(sample_indices_device(n, b, stream))
+
+
+@dataclass
+class ClassificationData:
+    """Synthetic binary-feature dataset on the device; labels carry the noise (sampling.py:212-226)."""
+
+    features: torch.Tensor  # N x n float64, entries exactly 0.0 / 1.0
+    labels: torch.Tensor    # N float64
+    true_weights: torch.Tensor
+
+    @property
+    def n_samples(self) -> int:
+        return self.features.shape[0]
+
+    @property
+    def n_features(self) -> int:
+        return self.features.shape[1]
+
+
+def synth_classification(n_features: int, stream: RngStream, backend=None,
+                         n_rows: int | None = None) -> ClassificationData:
+    """sampling.py:229-265, with the row count generalised (reference: n_rows = 30*n).
+
+    X[i,j] = [u >= 0.5] is the MSB of the Philox word (written directly as 0.0/1.0);
+    w_true continues the stream; scores use the fixed tree with chunk 4096 (the
+    reference's module-level SequentialBackend); labels split at np.median; exactly
+    floor(N/10) labels are flipped by sample_indices.
+    """
+    if n_features < 2:
+        raise ConfigurationError(f"need at least 2 features, got {n_features}")
+    n_rows = 30 * n_features if n_rows is None else int(n_rows)
+    total = n_rows * n_features
+    x = empty(n_rows, n_features)
+    _lib.call("simopt_bernoulli_half", _lib.stream_ptr(), *stream.words(), total, _lib.ptr(x))
+    stream.advance(total)
+    w_true = standard_normal_device(stream, n_features)
+    scores = empty(n_rows)
+    _lib.call("simopt_matvec", _lib.stream_ptr(), _lib.ptr(x), n_rows, n_features, None, n_rows,
+              None, _lib.ptr(w_true), 4096, _lib.ptr(scores))
+    srt = torch.sort(scores).values  # order statistics for np.median (instance-time only)
+    h = n_rows // 2
+    if n_rows % 2:
+        median = float(srt[h].item())
+    else:
+        a, b = float(srt[h - 1].item()), float(srt[h].item())
+        median = (a + b) / 2.0  # np.median -> np.mean of the two middle values
+    labels = empty(n_rows)
+    _lib.call("simopt_threshold", _lib.stream_ptr(), _lib.ptr(scores), median, n_rows,
+              _lib.ptr(labels))
+    flip = sample_indices_device(n_rows, n_rows // 10, stream)
+    labels[flip] = 1.0 - labels[flip]  # exact: labels are 0.0/1.0
+    return ClassificationData(features=x, labels=labels, true_weights=w_true)

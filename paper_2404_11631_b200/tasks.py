@@ -600,3 +600,99 @@ def _mv_fw_run_device(prob: MeanVarProblem, config, backend, label, size, rep):
     if bad:
         abort(*bad)
     return trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(ws[T % H]))
+
+
+# ---------------------------------------------------------------------------
+# Task 3: binary classification (logistic loss), tasks.py:196-253
+@dataclass
+class LogisticTask:
+    data: "ClassificationData"
+
+    @property
+    def dimension(self) -> int:
+        return self.data.n_features
+
+
+def _batch_rows(data, indices):
+    """tasks.py:205-213 without the row copy: a device index vector for the gather."""
+    if indices is None:
+        return None, data.n_samples
+    idx = indices if is_tensor(indices) else torch.as_tensor(np.asarray(indices), dtype=torch.int64)
+    idx = idx.to(device="cuda", dtype=torch.int64).contiguous()
+    if idx.numel() == 0:
+        raise ConfigurationError("empty index set")
+    if int(idx.min().item()) < 0 or int(idx.max().item()) >= data.n_samples:
+        raise ConfigurationError("batch index out of range")
+    return idx, idx.numel()
+
+
+def logistic_loss_device(w, data, indices, backend, idx=None, out=None) -> torch.Tensor:
+    """Device scalar sum of logistic_loss_block terms (divide by the batch size on read)."""
+    wd = vec_dev(w)
+    if wd.numel() != data.n_features:
+        raise DimensionMismatch("weight length != feature count")
+    if idx is None:
+        idx, b = _batch_rows(data, indices)
+    else:
+        b = idx.numel()
+    t = backend.matvec_device(data.features, wd, rows_idx=idx)
+    terms = empty(b)
+    _lib.call("simopt_logistic_loss_terms", _lib.stream_ptr(), _lib.ptr(t), _lib.ptr(data.labels),
+              _lib.ptr(idx), b, _lib.ptr(terms))
+    return backend.vec_sum_device(terms, out=out)
+
+
+def logistic_loss(w, data, indices, backend) -> float:
+    """Mean negative log-likelihood over the given rows (tasks.py:216-225)."""
+    idx, b = _batch_rows(data, indices)
+    s = logistic_loss_device(w, data, indices, backend, idx=idx)
+    return float(s.item()) / b
+
+
+def logistic_gradient_device(w, data, indices, backend, idx=None, out=None) -> torch.Tensor:
+    """(1/b) X_b^T (c - z_b) with exact trees (tasks.py:228-236)."""
+    wd = vec_dev(w)
+    if wd.numel() != data.n_features:
+        raise DimensionMismatch("weight length != feature count")
+    if idx is None:
+        idx, b = _batch_rows(data, indices)
+    else:
+        b = idx.numel()
+    t = backend.matvec_device(data.features, wd, rows_idx=idx)
+    r = empty(b)
+    _lib.call("simopt_logistic_resid", _lib.stream_ptr(), _lib.ptr(t), _lib.ptr(data.labels),
+              _lib.ptr(idx), b, _lib.ptr(r))
+    gt = backend.matvec_t_device(data.features, r, rows_idx=idx)
+    out = empty(gt.numel()) if out is None else out
+    _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(gt), 1.0 / b, None, gt.numel(),
+              _lib.ptr(out))
+    return out
+
+
+def logistic_gradient(w, data, indices, backend):
+    return like_input(w, logistic_gradient_device(w, data, indices, backend))
+
+
+def logistic_hvp_device(w, v, data, indices, backend, idx=None, out=None) -> torch.Tensor:
+    """Sub-sampled Hessian-vector product (1/b) X_b^T diag(c(1-c)) X_b v (tasks.py:239-253)."""
+    wd, vd = vec_dev(w), vec_dev(v)
+    if wd.numel() != data.n_features or vd.numel() != data.n_features:
+        raise DimensionMismatch("vector length != feature count")
+    if idx is None:
+        idx, b = _batch_rows(data, indices)
+    else:
+        b = idx.numel()
+    t = backend.matvec_device(data.features, wd, rows_idx=idx)
+    tv = backend.matvec_device(data.features, vd, rows_idx=idx)
+    wt = empty(b)
+    _lib.call("simopt_logistic_hvp_weights", _lib.stream_ptr(), _lib.ptr(t), _lib.ptr(tv), b,
+              _lib.ptr(wt))
+    ht = backend.matvec_t_device(data.features, wt, rows_idx=idx)
+    out = empty(ht.numel()) if out is None else out
+    _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(ht), 1.0 / b, None, ht.numel(),
+              _lib.ptr(out))
+    return out
+
+
+def logistic_hvp(w, v, data, indices, backend):
+    return like_input(w, logistic_hvp_device(w, v, data, indices, backend))

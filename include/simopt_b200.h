@@ -201,8 +201,8 @@ int simopt_bfgs_rank2(void* stream, double* h, const double* s, const double* u,
 /* h = diag(v) (sqn.py:96-97). */
 int simopt_diag_fill(void* stream, double* h, int64_t n, double v);
 enum simopt_vec { SIMOPT_VEC_SUB_SCALED = 0, SIMOPT_VEC_ADD = 1, SIMOPT_VEC_SUB = 2,
-                  SIMOPT_VEC_SCALE = 3 };
-/* out = x - alpha*y | x + y | x - y | x*alpha (numpy order, no FMA). */
+                  SIMOPT_VEC_SCALE = 3, SIMOPT_VEC_MUL = 4 };
+/* out = x - alpha*y | x + y | x - y | x*alpha | x*y (numpy order, no FMA). */
 int simopt_vec_op(void* stream, int op, double alpha, const double* x, const double* y, int64_t n,
                   double* out);
 /* sample_indices (sampling.py:196-209) on the device for b <= 4096: out[0..b) of the
@@ -210,6 +210,17 @@ int simopt_vec_op(void* stream, int op, double alpha, const double* x, const dou
  * the counter by ceil(b/4). */
 int simopt_sample_indices(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
                           uint64_t ctr_hi, int64_t n, int64_t b, int64_t* out);
+/* CG step halves on device scalars (Newton-CG, BASELINE configs[2]):
+ * step1: alpha = *rr / *dhd; p += alpha*d; r -= alpha*hd.  step2: d = r + (*rr_new / *rr)*d.
+ * Both are no-ops when *rr == 0 (the CG loop's early exit). */
+int simopt_cg_step1(void* stream, double* p, double* r, const double* d, const double* hd,
+                    const double* rr, const double* dhd, int64_t n);
+int simopt_cg_step2(void* stream, double* d, const double* r, const double* rr_new, const double* rr,
+                    int64_t n);
+/* Explicit Hessian h = (1/n) X^T diag(dw) X (d x d, symmetric, written fully) on the FP64
+ * tensor pipe; X is n x d row-major.  Oracle: tests/test_tasks.py:292-304, rtol 1e-10. */
+int simopt_logistic_xtdx(void* stream, const double* x, const double* dw, int64_t n, int64_t d,
+                         double* h);
 /* Same swap sequence on host memory for large b (u = the b uniforms). */
 int simopt_fisher_yates_host(int64_t n, int64_t b, const double* u, int64_t* out);
 

@@ -471,3 +471,66 @@ def sqn_run(x, z, *, pair_every, memory, beta, grad_batch, hess_batch, iteration
             wbar_accum = np.zeros_like(wbar_accum)
         objs.append(logistic_loss(w, x, z, None, chunk))
     return np.array(objs), w
+
+
+# ---------------------------------------------------------------- second-order solvers (no reference)
+def newton_cg(x, z, *, iterations, cg_iters, chunk=CHUNK):
+    """Newton-CG for the full-data logistic loss (BASELINE configs[2]; not in sobench).
+
+    Restated with the reference's own building blocks (logistic_gradient /
+    logistic_hvp / fixed-tree dot, tasks.py:228-253) so that the CUDA driver can be
+    compared bit for bit:  p solves H p = -g by `cg_iters` CG steps from p = 0,
+    then w <- w + p; the recorded objective is logistic_loss(w) after each step.
+    """
+    n = x.shape[1]
+    w = np.zeros(n)
+    objs = []
+    for _ in range(iterations):
+        g = logistic_gradient(w, x, z, None, chunk)
+        p = np.zeros(n)
+        r = -1.0 * g
+        dd = r.copy()
+        rr = dot(r, r, chunk)
+        for _ in range(cg_iters):
+            if rr == 0.0:
+                break
+            hd = logistic_hvp(w, dd, x, z, None, chunk)
+            alpha = rr / dot(dd, hd, chunk)
+            p = p + alpha * dd
+            r = r - alpha * hd
+            rr_new = dot(r, r, chunk)
+            beta = rr_new / rr
+            dd = r + beta * dd
+            rr = rr_new
+        w = w + p
+        objs.append(logistic_loss(w, x, z, None, chunk))
+    return np.array(objs), w
+
+
+def newton_explicit(x, z, *, iterations, cg_iters, chunk=CHUNK):
+    """Newton with the explicit Hessian H = (1/N) X^T diag(c(1-c)) X (tests/test_tasks.py:297-299
+    oracle) and a CG solve on H (BASELINE configs[4]); H via numpy BLAS (any summation order)."""
+    n = x.shape[1]
+    w = np.zeros(n)
+    objs = []
+    for _ in range(iterations):
+        g = logistic_gradient(w, x, z, None, chunk)
+        h = logistic_hessian_explicit(w, x, z)
+        p = np.zeros(n)
+        r = -1.0 * g
+        dd = r.copy()
+        rr = float(r @ r)
+        for _ in range(cg_iters):
+            if rr == 0.0:
+                break
+            hd = h @ dd
+            alpha = rr / float(dd @ hd)
+            p = p + alpha * dd
+            r = r - alpha * hd
+            rr_new = float(r @ r)
+            beta = rr_new / rr
+            dd = r + beta * dd
+            rr = rr_new
+        w = w + p
+        objs.append(logistic_loss(w, x, z, None, chunk))
+    return np.array(objs), w

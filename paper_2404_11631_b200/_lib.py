@@ -56,6 +56,9 @@ SIGNATURES = {
     "simopt_vec_op": [_vp, _i32, _d, _vp, _vp, _i64, _vp],
     "simopt_sample_indices": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp],
     "simopt_fisher_yates_host": [_i64, _i64, _vp, _vp],
+    "simopt_logistic_xtdx": [_vp, _vp, _vp, _i64, _i64, _vp],
+    "simopt_cg_step1": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64],
+    "simopt_cg_step2": [_vp, _vp, _vp, _vp, _vp, _i64],
 }
 
 

@@ -81,6 +81,7 @@ __global__ void k_vec_op(int op, double alpha, const double* __restrict__ x,
       case SIMOPT_VEC_SUB_SCALED: r = x[i] - alpha * y[i]; break;  // x - alpha*y
       case SIMOPT_VEC_ADD: r = x[i] + y[i]; break;
       case SIMOPT_VEC_SUB: r = x[i] - y[i]; break;
+      case SIMOPT_VEC_MUL: r = x[i] * y[i]; break;
       default: r = x[i] * alpha; break;                             // SCALE
     }
     out[i] = r;
@@ -170,7 +171,7 @@ extern "C" int simopt_diag_fill(void* stream, double* h, int64_t n, double v) {
 
 extern "C" int simopt_vec_op(void* stream, int op, double alpha, const double* x, const double* y,
                              int64_t n, double* out) {
-  SIMOPT_REQUIRE(op >= 0 && op <= 3, SIMOPT_E_CONFIG, "unknown vector op %d", op);
+  SIMOPT_REQUIRE(op >= 0 && op <= 4, SIMOPT_E_CONFIG, "unknown vector op %d", op);
   if (n == 0) return SIMOPT_OK;
   k_vec_op<<<egrid(n), 256, 0, as_stream(stream)>>>(op, alpha, x, y, n, out);
   SIMOPT_CHECK_LAUNCH("k_vec_op");
@@ -213,5 +214,46 @@ extern "C" int simopt_fisher_yates_host(int64_t n, int64_t b, const double* u, i
     moved[j] = vi;
     out[i] = vj;
   }
+  return SIMOPT_OK;
+}
+
+namespace {
+// One CG step on device scalars (oracle.newton_cg; no host round trip):
+//   alpha = rr / dHd; p = p + alpha*d; r = r - alpha*Hd       (skipped when rr == 0: `break`)
+__global__ void k_cg_step1(double* __restrict__ p, double* __restrict__ r, const double* __restrict__ d,
+                           const double* __restrict__ hd, const double* __restrict__ rr,
+                           const double* __restrict__ dhd, int64_t n) {
+  const double rrv = *rr;
+  if (rrv == 0.0) return;
+  const double alpha = rrv / *dhd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    p[i] = p[i] + alpha * d[i];
+    r[i] = r[i] - alpha * hd[i];
+  }
+}
+//   beta = rr_new / rr; d = r + beta*d                           (skipped when rr == 0)
+__global__ void k_cg_step2(double* __restrict__ d, const double* __restrict__ r,
+                           const double* __restrict__ rr_new, const double* __restrict__ rr, int64_t n) {
+  const double rrv = *rr;
+  if (rrv == 0.0) return;
+  const double beta = *rr_new / rrv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = r[i] + beta * d[i];
+}
+}  // namespace
+
+extern "C" int simopt_cg_step1(void* stream, double* p, double* r, const double* d, const double* hd,
+                               const double* rr, const double* dhd, int64_t n) {
+  k_cg_step1<<<egrid(n), 256, 0, as_stream(stream)>>>(p, r, d, hd, rr, dhd, n);
+  SIMOPT_CHECK_LAUNCH("k_cg_step1");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_cg_step2(void* stream, double* d, const double* r, const double* rr_new,
+                               const double* rr, int64_t n) {
+  k_cg_step2<<<egrid(n), 256, 0, as_stream(stream)>>>(d, r, rr_new, rr, n);
+  SIMOPT_CHECK_LAUNCH("k_cg_step2");
   return SIMOPT_OK;
 }

@@ -1,0 +1,158 @@
+"""Second-order Newton solvers for the classification task (BASELINE.json configs[2], [4]).
+
+The reference package only ships SQN (sobench/sqn.py); these drivers are the
+north star's "CG/Cholesky Newton step" built from the reference's own building
+blocks, with CPU restatements in oracle/oracle.py (newton_cg / newton_explicit):
+
+* ``newton_cg`` -- full-data gradient (tasks.py:228-236) and CG on
+  Hessian-vector products (tasks.py:239-253).  The HVP weights c(1-c) depend on
+  w only, so they are formed once per Newton iteration and reused by every CG
+  product (same IEEE values as recomputing them); ``X w`` from the recorded
+  loss is reused by the next gradient.  All reductions use the exact tree, so
+  the trajectory is bit-identical to the oracle.
+* ``newton_explicit`` -- explicit H = (1/N) X^T diag(c(1-c)) X on the FP64 tensor
+  pipe (csrc/hessian.cu) and a CG solve on H; parity to the numpy-BLAS oracle
+  is within tolerance (rtol 1e-10 on H, 1e-8 on the trajectory).
+
+Every scalar of the CG recurrences stays on the device (simopt_cg_step1/2), so an
+iteration is one uninterrupted stream of kernels; the objective trace is read
+once at the end.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._tensors import F64, empty, to_host
+from .records import RunRecord, TraceBuilder
+
+_SCALE, _MUL = 3, 4
+
+
+def _vop(op, alpha, x, y, out):
+    _lib.call("simopt_vec_op", _lib.stream_ptr(), op, float(alpha), _lib.ptr(x), _lib.ptr(y),
+              x.numel(), _lib.ptr(out))
+    return out
+
+
+class _Logistic:
+    """Per-run buffers for the full-data logistic passes."""
+
+    def __init__(self, data, backend):
+        self.data, self.b = data, backend
+        self.N, self.d = data.n_samples, data.n_features
+        self.t = empty(self.N)       # X w
+        self.r = empty(self.N)       # residual / hvp weights scratch
+        self.dw = empty(self.N)      # c (1 - c)
+        self.tv = empty(self.N)
+        self.gt = empty(self.d)
+        self.ones = torch.ones(self.N, dtype=F64, device="cuda")
+
+    def xw(self, w):
+        return self.b.matvec_device(self.data.features, w, out=self.t)
+
+    def gradient_from_t(self, out):
+        """(1/N) X^T (sigmoid(t) - z) given t = X w (tasks.py:228-236)."""
+        _lib.call("simopt_logistic_resid", _lib.stream_ptr(), _lib.ptr(self.t),
+                  _lib.ptr(self.data.labels), None, self.N, _lib.ptr(self.r))
+        self.b.matvec_t_device(self.data.features, self.r, out=self.gt)
+        _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(self.gt), 1.0 / self.N, None,
+                  self.d, _lib.ptr(out))
+        return out
+
+    def hvp_weights_from_t(self):
+        """c (1 - c) -- identical to the (c*(1-c)) factor of tasks.py:252."""
+        _lib.call("simopt_logistic_hvp_weights", _lib.stream_ptr(), _lib.ptr(self.t),
+                  _lib.ptr(self.ones), self.N, _lib.ptr(self.dw))
+
+    def hvp(self, v, out):
+        """(1/N) X^T ((c(1-c)) * (X v))."""
+        self.b.matvec_device(self.data.features, v, out=self.tv)
+        _vop(_MUL, 0.0, self.dw, self.tv, self.r)
+        self.b.matvec_t_device(self.data.features, self.r, out=self.gt)
+        _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(self.gt), 1.0 / self.N, None,
+                  self.d, _lib.ptr(out))
+        return out
+
+    def loss_sum_from_t(self, out):
+        _lib.call("simopt_logistic_loss_terms", _lib.stream_ptr(), _lib.ptr(self.t),
+                  _lib.ptr(self.data.labels), None, self.N, _lib.ptr(self.r))
+        return self.b.vec_sum_device(self.r, out=out)
+
+
+def _cg(apply, g, n, cg_iters, dot, p):
+    """p solves A p = -g by cg_iters CG steps from p = 0 (oracle.newton_cg inner loop)."""
+    p.zero_()
+    r = empty(n)
+    _vop(_SCALE, -1.0, g, g, r)                  # r = -1.0 * g
+    dd = r.clone()
+    hd = empty(n)
+    sc = torch.empty(3, dtype=F64, device="cuda")  # rr, dHd, rr_new
+    dot(r, r, sc[0:])
+    for _ in range(cg_iters):
+        apply(dd, hd)
+        dot(dd, hd, sc[1:])
+        _lib.call("simopt_cg_step1", _lib.stream_ptr(), _lib.ptr(p), _lib.ptr(r), _lib.ptr(dd),
+                  _lib.ptr(hd), _lib.ptr(sc[0:]), _lib.ptr(sc[1:]), n)
+        dot(r, r, sc[2:])
+        _lib.call("simopt_cg_step2", _lib.stream_ptr(), _lib.ptr(dd), _lib.ptr(r), _lib.ptr(sc[2:]),
+                  _lib.ptr(sc[0:]), n)
+        # rr <- rr_new unless CG already stopped (rr == 0 keeps every later step a no-op)
+        sc[0:1].copy_(torch.where(sc[0:1] == 0.0, sc[0:1], sc[2:3]))
+    return p
+
+
+def _run(task, iterations, backend, step, label):
+    data = task.data
+    L = _Logistic(data, backend)
+    n = L.d
+    w = torch.zeros(n, dtype=F64, device="cuda")
+    g = empty(n)
+    p = empty(n)
+    sums = empty(iterations)
+    stamps = torch.zeros(iterations + 1, dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[iterations:])))
+    dot = lambda x, y, out: backend.dot_device(x, y, out=out)  # noqa: E731
+    L.xw(w)
+    for it in range(iterations):
+        L.gradient_from_t(g)
+        L.hvp_weights_from_t()
+        step(L, g, p, dot)
+        _lib.call("simopt_vec_op", _lib.stream_ptr(), 1, 0.0, _lib.ptr(w), _lib.ptr(p), n,
+                  _lib.ptr(w))                    # w = w + p
+        L.xw(w)                                   # shared by the loss and the next gradient
+        L.loss_sum_from_t(sums[it:])
+        _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[it:])))
+    trace = TraceBuilder()
+    vals, ts = to_host(sums), to_host(stamps)
+    for it in range(iterations):
+        trace.append(it + 1, float(vals[it]) / L.N, int(ts[it]) - int(ts[iterations]))
+    return trace.build(label, n, backend.kind, 0, 0, to_host(w))
+
+
+def newton_cg(task, iterations: int, cg_iters: int, backend) -> RunRecord:
+    """Newton-CG on the full-data logistic loss (BASELINE.json configs[2])."""
+    def step(L, g, p, dot):
+        _cg(L.hvp, g, L.d, cg_iters, dot, p)
+    return _run(task, iterations, backend, step, "classification-newton-cg")
+
+
+def logistic_hessian_device(data, dw, out=None) -> torch.Tensor:
+    """H = (1/N) X^T diag(dw) X on the FP64 tensor pipe (tests/test_tasks.py:297-299 oracle)."""
+    d = data.n_features
+    out = torch.empty(d, d, dtype=F64, device="cuda") if out is None else out
+    _lib.call("simopt_logistic_xtdx", _lib.stream_ptr(), _lib.ptr(data.features), _lib.ptr(dw),
+              data.n_samples, d, _lib.ptr(out))
+    return out
+
+
+def newton_explicit(task, iterations: int, cg_iters: int, backend) -> RunRecord:
+    """Newton with the explicit X^T D X Hessian and a CG solve (BASELINE.json configs[4])."""
+    d = task.data.n_features
+    H = torch.empty(d, d, dtype=F64, device="cuda")
+
+    def step(L, g, p, dot):
+        logistic_hessian_device(L.data, L.dw, out=H)
+        _cg(lambda v, out: backend.matvec_device(H, v, out=out), g, d, cg_iters, dot, p)
+    return _run(task, iterations, backend, step, "classification-newton-explicit")

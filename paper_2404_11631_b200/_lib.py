@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libsimopt_b200.so")
 
 _lock = threading.Lock()
 _lib = None
+_device_ok = False
 
 _u64, _i64, _i32, _d, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
 
@@ -64,7 +65,9 @@ SIGNATURES = {
 
 def load(require_device: bool = True):
     """Load the library (idempotent).  Raises DeviceError when unusable."""
-    global _lib
+    global _lib, _device_ok
+    if _lib is not None and (_device_ok or not require_device):
+        return _lib
     with _lock:
         if _lib is None:
             if not os.path.exists(LIB_PATH):
@@ -79,8 +82,10 @@ def load(require_device: bool = True):
                 fn.argtypes = argt
                 fn.restype = ctypes.c_int
             _lib = lib
-    if require_device and not torch.cuda.is_available():
-        raise DeviceError("no CUDA device visible: the sm_100a kernels have no CPU fallback")
+    if require_device:
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device visible: the sm_100a kernels have no CPU fallback")
+        _device_ok = True
     return _lib
 
 
@@ -95,13 +100,14 @@ def check(status: int):
 
 
 def call(name: str, *args):
-    lib = load()
+    lib = _lib if _device_ok else load()
     check(getattr(lib, name)(*args))
 
 
 def stream_ptr(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is None:
+        return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch.cuda.current_device()))
+    return ctypes.c_void_p(stream.cuda_stream)
 
 
 def ptr(t):

@@ -11,6 +11,15 @@
 
 namespace {
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 constexpr int kFoldSmem = 4096;  // partials folded in one CTA's shared memory
 
 // --- chunk partials of dot / sum ------------------------------------------------
@@ -152,44 +161,71 @@ __global__ void __launch_bounds__(512) k_fold_final(const double* __restrict__ s
 }
 
 // --- matvec: out[r] = tree-dot(row(r) - center, x) -------------------------------
-// CTA = 128 rows x one column chunk; 32-column tiles staged through shared memory
-// so global reads are coalesced while each thread walks its own row in order.
+// One warp per (32-row strip, column chunk); lane r owns row r's chain.  Row
+// segments (32 columns, 256 B, coalesced) stream through a kTStages-deep cp.async
+// ring; the tile row stride is padded to 33 doubles so the lane-per-row reads are
+// conflict-free.
+constexpr int kRStages = 5;
+
 template <bool kCenter, bool kIdx>
-__global__ void __launch_bounds__(128) k_matvec_rows(const double* __restrict__ a, int64_t cols,
-                                                     const int64_t* __restrict__ idx, int64_t rows,
-                                                     const double* __restrict__ center,
-                                                     const double* __restrict__ x, int64_t chunk,
-                                                     int64_t nch, double* __restrict__ out) {
-  __shared__ double tile[128][33];
-  __shared__ double xs[32];
-  const int64_t r0 = (int64_t)blockIdx.x * 128;
+__global__ void __launch_bounds__(32) k_matvec_rows(const double* __restrict__ a, int64_t cols,
+                                                    const int64_t* __restrict__ idx, int64_t rows,
+                                                    const double* __restrict__ center,
+                                                    const double* __restrict__ x, int64_t chunk,
+                                                    int64_t nch, double* __restrict__ out) {
+  __shared__ __align__(16) double tile[kRStages][32][33];
+  __shared__ __align__(16) double xs[kRStages][32];
+  __shared__ __align__(16) double cs[kRStages][32];
+  const int lane = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int64_t c = blockIdx.y;
   const int64_t clo = c * chunk;
   const int64_t chi = clo + chunk < cols ? clo + chunk : cols;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int64_t j0 = clo; j0 < chi; j0 += 32) {
-    const int64_t jn = chi - j0 < 32 ? chi - j0 : 32;
-    if (threadIdx.x < 32 && lane < jn) xs[lane] = x[j0 + lane];
-    const double cj = (kCenter && lane < jn) ? center[j0 + lane] : 0.0;
-#pragma unroll 4
+  const int64_t nst = (chi - clo + 31) / 32;
+  auto issue = [&](int64_t st) {
+    const int buf = (int)(st % kRStages);
+    const int64_t j0 = clo + st * 32;
+    const int64_t jj = j0 + lane;
+    const bool jv = jj < chi;
+#pragma unroll 8
     for (int rr = 0; rr < 32; ++rr) {
-      const int lr = warp * 32 + rr;
-      const int64_t r = r0 + lr;
-      if (r < rows && lane < jn) {
-        const int64_t row = kIdx ? idx[r] : r;
-        const double v = a[row * cols + j0 + lane];
-        tile[lr][lane] = kCenter ? v - cj : v;
+      const int64_t r = r0 + rr;
+      const bool v = r < rows && jv;
+      const int64_t row = (r < rows) ? (kIdx ? idx[r] : r) : 0;
+      cp_async8(&tile[buf][rr][lane], a + row * cols + (jv ? jj : 0), v);
+    }
+    cp_async8(&xs[buf][lane], x + (jv ? jj : 0), jv);
+    if (kCenter) cp_async8(&cs[buf][lane], center + (jv ? jj : 0), jv);
+    cp_async_commit();
+  };
+  for (int64_t st = 0; st < kRStages - 1; ++st) {
+    if (st < nst) issue(st); else cp_async_commit();
+  }
+  double s = 0.0;
+  for (int64_t st = 0; st < nst; ++st) {
+    if (st + kRStages - 1 < nst) issue(st + kRStages - 1); else cp_async_commit();
+    cp_async_wait<kRStages - 1>();
+    __syncwarp();
+    const int buf = (int)(st % kRStages);
+    const int cnt = (int)((chi - clo) - st * 32 < 32 ? (chi - clo) - st * 32 : 32);
+    if (cnt == 32) {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const double v = tile[buf][lane][jj];
+        s = s + (kCenter ? v - cs[buf][jj] : v) * xs[buf][jj];
+      }
+    } else {
+      for (int jj = 0; jj < cnt; ++jj) {
+        const double v = tile[buf][lane][jj];
+        s = s + (kCenter ? v - cs[buf][jj] : v) * xs[buf][jj];
       }
     }
-    __syncthreads();
-    for (int jj = 0; jj < jn; ++jj) s = s + tile[threadIdx.x][jj] * xs[jj];
-    __syncthreads();
+    __syncwarp();
   }
-  const int64_t r = r0 + threadIdx.x;
+  const int64_t r = r0 + lane;
   if (r < rows) {
     if (nch == 1) out[r] = s;
-    else out[r * nch + c] = s;  // partials, folded by k_fold_rows
+    else out[r * nch + c] = s;  // partials, folded by k_fold_strided
   }
 }
 
@@ -210,36 +246,67 @@ __global__ void k_fold_strided(double* __restrict__ p, int64_t count, int64_t nc
 }
 
 // --- matvec_t: out[j] = tree over row chunks of sum x[r]*(a[row(r),j]-center[j]) ---
+// One warp per (32-column strip, row chunk); lane j owns column j's chain.  Rows
+// stream through a kStages-deep cp.async ring (32 rows x 32 columns per stage),
+// so each chain runs at DADD latency instead of waiting on memory per row.
+constexpr int kTStages = 5;
+constexpr int kTRows = 32;
+
 template <bool kCenter, bool kIdx>
-__global__ void __launch_bounds__(128) k_matvec_t_cols(const double* __restrict__ a, int64_t cols,
-                                                       const int64_t* __restrict__ idx, int64_t rows,
-                                                       const double* __restrict__ center,
-                                                       const double* __restrict__ x, int64_t chunk,
-                                                       int64_t nch, double* __restrict__ out) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(32) k_matvec_t_cols(const double* __restrict__ a, int64_t cols,
+                                                      const int64_t* __restrict__ idx, int64_t rows,
+                                                      const double* __restrict__ center,
+                                                      const double* __restrict__ x, int64_t chunk,
+                                                      int64_t nch, double* __restrict__ out) {
+  __shared__ __align__(16) double tile[kTStages][kTRows][32];
+  __shared__ __align__(16) double xs[kTStages][kTRows];
+  const int lane = threadIdx.x;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   const int64_t c = blockIdx.y;
-  if (j >= cols) return;
   const int64_t lo = c * chunk;
   const int64_t hi = lo + chunk < rows ? lo + chunk : rows;
-  const double cj = kCenter ? center[j] : 0.0;
-  double s = 0.0;
-  int64_t r = lo;
-  for (; r + 8 <= hi; r += 8) {
-    double av[8], xv[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t row = kIdx ? idx[r + k] : r + k;
-      av[k] = a[row * cols + j];
-      xv[k] = x[r + k];
+  const bool jv = j < cols;
+  const double cj = (kCenter && jv) ? center[j] : 0.0;
+  const int64_t nst = (hi - lo + kTRows - 1) / kTRows;
+  auto issue = [&](int64_t st) {
+    const int buf = (int)(st % kTStages);
+    const int64_t r0 = lo + st * kTRows;
+#pragma unroll 8
+    for (int r = 0; r < kTRows; ++r) {
+      const int64_t rr = r0 + r;
+      const bool v = rr < hi;
+      const int64_t row = v ? (kIdx ? idx[rr] : rr) : 0;
+      cp_async8(&tile[buf][r][lane], a + row * cols + (jv ? j : 0), v && jv);
     }
+    const int64_t rr = r0 + lane;
+    cp_async8(&xs[buf][lane], x + (rr < hi ? rr : 0), rr < hi);
+    cp_async_commit();
+  };
+  for (int64_t st = 0; st < kTStages - 1; ++st) {
+    if (st < nst) issue(st); else cp_async_commit();
+  }
+  double s = 0.0;
+  for (int64_t st = 0; st < nst; ++st) {
+    if (st + kTStages - 1 < nst) issue(st + kTStages - 1); else cp_async_commit();
+    cp_async_wait<kTStages - 1>();
+    __syncwarp();
+    const int buf = (int)(st % kTStages);
+    const int cnt = (int)((hi - lo) - st * kTRows < kTRows ? (hi - lo) - st * kTRows : kTRows);
+    if (cnt == kTRows) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s = s + xv[k] * (kCenter ? av[k] - cj : av[k]);
+      for (int r = 0; r < kTRows; ++r) {
+        const double v = tile[buf][r][lane];
+        s = s + xs[buf][r] * (kCenter ? v - cj : v);
+      }
+    } else {
+      for (int r = 0; r < cnt; ++r) {
+        const double v = tile[buf][r][lane];
+        s = s + xs[buf][r] * (kCenter ? v - cj : v);
+      }
+    }
+    __syncwarp();
   }
-  for (; r < hi; ++r) {
-    const int64_t row = kIdx ? idx[r] : r;
-    const double v = a[row * cols + j];
-    s = s + x[r] * (kCenter ? v - cj : v);
-  }
+  if (!jv) return;
   if (nch == 1) out[j] = s;
   else out[c * cols + j] = s;  // partials, folded by k_fold_strided
 }
@@ -369,15 +436,16 @@ extern "C" int simopt_matvec(void* stream, const double* a, int64_t lda_rows, in
   }
   const int64_t nch = ceil_div(cols, chunk);
   SIMOPT_REQUIRE(nch < 65536, SIMOPT_E_CONFIG, "too many column chunks (%lld)", (long long)nch);
+  SIMOPT_REQUIRE(ceil_div(rows, 32) < (1LL << 31), SIMOPT_E_CONFIG, "too many rows");
   double* p = out;
   if (nch > 1) SIMOPT_CUDA(cudaMallocAsync(&p, rows * nch * sizeof(double), st));
-  const dim3 grid((unsigned)ceil_div(rows, 128), (unsigned)nch);
+  const dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)nch);
   const int sel = (center ? 1 : 0) | (idx ? 2 : 0);
   switch (sel) {
-    case 0: k_matvec_rows<false, false><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    case 1: k_matvec_rows<true, false><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    case 2: k_matvec_rows<false, true><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    default: k_matvec_rows<true, true><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 0: k_matvec_rows<false, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 1: k_matvec_rows<true, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 2: k_matvec_rows<false, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    default: k_matvec_rows<true, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
   }
   SIMOPT_CHECK_LAUNCH("k_matvec_rows");
   if (nch > 1) {
@@ -403,13 +471,13 @@ extern "C" int simopt_matvec_t(void* stream, const double* a, int64_t lda_rows, 
   SIMOPT_REQUIRE(nch < 65536, SIMOPT_E_CONFIG, "too many row chunks (%lld)", (long long)nch);
   double* p = out;
   if (nch > 1) SIMOPT_CUDA(cudaMallocAsync(&p, cols * nch * sizeof(double), st));
-  const dim3 grid((unsigned)ceil_div(cols, 128), (unsigned)nch);
+  const dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)nch);
   const int sel = (center ? 1 : 0) | (idx ? 2 : 0);
   switch (sel) {
-    case 0: k_matvec_t_cols<false, false><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    case 1: k_matvec_t_cols<true, false><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    case 2: k_matvec_t_cols<false, true><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    default: k_matvec_t_cols<true, true><<<grid, 128, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 0: k_matvec_t_cols<false, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 1: k_matvec_t_cols<true, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 2: k_matvec_t_cols<false, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    default: k_matvec_t_cols<true, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
   }
   SIMOPT_CHECK_LAUNCH("k_matvec_t_cols");
   if (nch > 1) {

@@ -1,0 +1,82 @@
+"""Throughput of every BASELINE.json config on one B200 (secondary to bench.py's headline).
+
+Prints one JSON line per config.  Per-GPU slices are used where the full
+config is multi-GPU or exceeds one GPU's HBM (stated in each line).
+CUDA events on the launching stream; >= 3 warm-up steps; inputs > L2 except C1.
+
+  python tools/bench_configs.py [c1 c3 c4 c5 xtdx]
+"""
+import json
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2404_11631_b200 as p  # noqa: E402
+from paper_2404_11631_b200.frank_wolfe import FwConfig, fw_run  # noqa: E402
+from paper_2404_11631_b200.instances import gen_meanvar_instance  # noqa: E402
+from paper_2404_11631_b200.tasks import LogisticTask, MeanVarProblem  # noqa: E402
+
+
+def timed(fn, warm=3, reps=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def meanvar(tag, d, n, M=25, epochs=2):
+    b = p.make_backend("cuda")
+    prob = MeanVarProblem(gen_meanvar_instance(d, p.RngStream(42, 0)), b)
+    s = p.RngStream(42, 2)
+    ms = timed(lambda: fw_run(prob, FwConfig(epochs, M, n, s), b), warm=1, reps=2)
+    it_s = epochs * M / (ms / 1e3)
+    bytes_it = 8 * n * d * 2  # exact path: matvec + matvec_t pass per iteration
+    print(json.dumps({"config": tag, "d": d, "N": n, "M": M, "fw_iterations_per_s": it_s,
+                      "ms_per_epoch": ms / epochs, "exact_tree": True,
+                      "algorithmic_GBps_per_iteration_pass": bytes_it * it_s / 1e9}), flush=True)
+
+
+def newton(tag, d, n, k_cg=10, iters=2):
+    from paper_2404_11631_b200.newton import newton_cg
+    from paper_2404_11631_b200.sampling import synth_classification
+    b = p.make_backend("cuda")
+    task = LogisticTask(synth_classification(d, p.RngStream(42, 0), n_rows=n))
+    ms = timed(lambda: newton_cg(task, iters, k_cg, b), warm=1, reps=2)
+    it_s = iters / (ms / 1e3)
+    passes = 2 * k_cg + 2
+    print(json.dumps({"config": tag, "d": d, "N": n, "k_cg": k_cg, "newton_iterations_per_s": it_s,
+                      "ms_per_iteration": ms / iters, "passes_over_X": passes,
+                      "achieved_GBps": passes * 8 * n * d * it_s / 1e9}), flush=True)
+
+
+def xtdx(tag, d, n):
+    from paper_2404_11631_b200.newton import logistic_hessian_device
+    from paper_2404_11631_b200.sampling import synth_classification
+    data = synth_classification(d, p.RngStream(42, 0), n_rows=n)
+    dw = torch.rand(n, dtype=torch.float64, device="cuda") * 0.25
+    H = torch.empty(d, d, dtype=torch.float64, device="cuda")
+    ms = timed(lambda: logistic_hessian_device(data, dw, out=H), warm=1, reps=3)
+    flops_syrk = n * d * (d + 1)  # SYRK convention
+    print(json.dumps({"config": tag, "d": d, "N": n, "ms": ms,
+                      "tflops_syrk_convention": flops_syrk / (ms / 1e3) / 1e12,
+                      "note": "upper-triangle tiles computed, mirrored"}), flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c1", "c3", "c4", "xtdx"]
+    if "c1" in which:
+        meanvar("C1 meanvar d=1e3 N=1e4", 1000, 10_000)
+    if "c4" in which:
+        meanvar("C4 meanvar d=2e4, per-GPU slice N=1.25e5 of N=1e6 on 8 GPUs", 20_000, 125_000, epochs=1)
+    if "c3" in which:
+        newton("C3 logistic Newton-CG d=1e3 N=1e6", 1000, 1_000_000)
+    if "xtdx" in which:
+        xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (fp64 X)", 8192, 125_000)

@@ -250,15 +250,15 @@ def run_ours(args, rank, world):
     from paper_2404_11631_b200.tasks import nv_geometry
     seg, nbuck = nv_geometry()
     nseg = -(-S // seg)
-    alg_bytes = D * S * 8 + D * nseg * nbuck * 2  # demands + bucket starts written per launch
+    alg_bytes = D * S * 4 + D * nseg * nbuck * 2  # keys + bucket starts written per launch
     peak, peak_kind = peaks()
     achieved = alg_bytes / (res_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": profiled_traffic(),
                 "kernel": "k_nv_resample", "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "kernel_ms": res_ms, "share_of_step": res_ms / (ms / args.steps),
-                "note": ("fp64/int issue-bound: Philox4x64-10 + glibc-exact Box-Muller per draw; "
-                         "see profiles/ for fp64-pipe utilisation")}
+                "note": ("issue-bound: Philox4x64-10 + fp32 Box-Muller key per draw (exact glibc "
+                         "Box-Muller only for ambiguous draws at query time); see profiles/")}
     launches_per_epoch = 3 * M + 3
     line = {
         "metric": "newsvendor Frank-Wolfe iterations/sec (d=10000, S=100000, M=25)",

@@ -116,24 +116,30 @@ int simopt_lmo_single_budget(void* stream, const double* g, const double* c, dou
 int simopt_min_value(void* stream, const double* x, int64_t n, double* out);
 
 /* ------------------------------------------------------------ newsvendor */
-/* Segment length and buckets per segment of the partitioned demand layout. */
+/* Segment length and buckets per segment of the keyed demand layout. */
 int simopt_nv_geometry(int64_t* seg, int64_t* buckets);
-/* Epoch layout sizes: demands d*S f64,
+/* Epoch layout sizes: keys d*S u32,
  * bucket starts d*nseg*buckets u16, nseg = ceil(S/seg). */
-int simopt_nv_layout(int64_t d, int64_t S, int64_t* nseg, int64_t* dem_elems, int64_t* off_elems);
+int simopt_nv_layout(int64_t d, int64_t S, int64_t* nseg, int64_t* key_elems, int64_t* off_elems);
 
-/* sample_demands (sampling.py:173-193) fused with the partition the gradient
- * needs: draws D[j,s] = mu_j + sigma_j*z[j*S+s] (z = standard_normal(d*S) of the
- * stream at the given counter) are written bucket-partitioned per
- * segment (simopt_nv_geometry).  Caller advances the counter by ceil(2*ceil(d*S/2)/4).  kappa[d] is
- * filled.  Rows sorted by the reference contain exactly the same multiset. */
+/* sample_demands (sampling.py:173-193) in the keyed ECDF layout: one u32 key per
+ * draw D[j,s] = mu_j + sigma_j*z[j*S+s] (z = standard_normal(d*S) of the stream at
+ * the given counter), counting-sorted by bucket per segment.  Every ECDF count
+ * computed from it equals the count on the reference's sorted rows.  Caller
+ * advances the counter by ceil(2*ceil(d*S/2)/4) and passes the same
+ * (seed, stream_id, ctr) to every query of this epoch. */
 int simopt_nv_resample(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
-                       uint64_t ctr_hi, int64_t d, int64_t S, const double* mu,
-                       const double* sigma, double* kappa, double* dem, uint16_t* off);
+                       uint64_t ctr_hi, int64_t d, int64_t S, uint32_t* keys, uint16_t* off);
 
 /* ECDF counts #{D[j,:] <= x_j} (ecdf_count_block, _kernels.py:245-259). */
-int simopt_nv_counts(void* stream, const double* dem, const uint16_t* off, const double* kappa,
-                     const double* mu, int64_t d, int64_t S, const double* x, int64_t* counts);
+int simopt_nv_counts(void* stream, const uint32_t* keys, const uint16_t* off, const double* mu,
+                     const double* sigma, int64_t d, int64_t S, uint64_t seed, uint64_t stream_id,
+                     uint64_t ctr_lo, uint64_t ctr_hi, const double* x, int64_t* counts);
+
+/* Exact demand value of every stored key, in storage order (diagnostics / tests). */
+int simopt_nv_decode(void* stream, const uint32_t* keys, const double* mu, const double* sigma,
+                     int64_t d, int64_t S, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                     uint64_t ctr_hi, double* out);
 
 /* ecdf_count_block on reference-format rows (each row sorted ascending). */
 int simopt_ecdf_count_sorted(void* stream, const double* samples, int64_t rows, int64_t s,
@@ -160,9 +166,9 @@ typedef struct NvState {
  *             g*(budget/c) (lmo.py:68-89) into *state, flags[grad_step] |= NAN. */
 typedef struct NvIterArgs {
   int64_t d, S, nseg;
-  const double* dem;
+  const uint32_t* keys;       /* epoch layout (simopt_nv_resample)          */
   const uint16_t* off;
-  const double* kappa;
+  uint64_t seed, sid, ctr_lo, ctr_hi;  /* the epoch's draw (exact fallback) */
   const double *mu, *sigma, *k, *h, *v, *c;
   double budget;
   const double* x_in; /* iterate before this step                               */

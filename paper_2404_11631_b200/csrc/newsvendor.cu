@@ -2,19 +2,16 @@
 // single-budget LMO and Frank-Wolfe update (reference: sobench/tasks.py:141-188,
 // sampling.py:173-193, lmo.py:68-89, frank_wolfe.py:62-82, _kernels.py:210-259).
 //
-// Data layout (per resampling epoch, resident in HBM):
-//   dem   [d][S] f64   row j = product j's S demand draws, split into segments of
-//                      NV_SEG = 2048 draws; inside a segment the draws are grouped by
-//                      bucket (counting-sorted), buckets in ascending order.
+// Epoch layout (keyed ECDF, see newsvendor.cuh):
+//   keys  [d][S] u32   row j = product j's S draws in segments of NV_SEG = 4096;
+//                      key = q << 12 | local, counting-sorted by bucket (q >> 10).
 //   off   [d][nseg][NV_B] u16   start of each bucket inside its segment.
-//   kappa [d] f64      bucket scale B / (12 sigma_j).
-// Bucket map  f_j(D) = clamp(floor((D - mu_j) * kappa_j + B/2), 0, B-1) is monotone
-// non-decreasing in D (every rounding step is), so for a query x_j:
-//   #{D <= x} = #{f(D) < f(x)} + #{D in bucket f(x) : D <= x}
-// exactly: elements of lower buckets are < x, elements of higher buckets are > x.
-// The count equals the reference's upper-bound binary search on the fully sorted
-// row (ecdf_count_block) for every x, while an epoch writes the demands once and
-// each gradient reads one bucket per segment instead of the whole row.
+// The reference sorts every row (sampling.py:192) and binary-searches it
+// (_kernels.py:245-259).  Here the resample evaluates only an fp32 approximation
+// per draw (plus the exact Philox stream), and a gradient query resolves the
+// handful of draws whose approximation is within the guaranteed error of the
+// threshold with the exact glibc Box-Muller -- the count is the reference's
+// integer, bit for bit, for every query.
 #include "common.cuh"
 #include "fw.cuh"
 #include "glibc_math.cuh"
@@ -27,33 +24,18 @@
 namespace {
 
 constexpr int kResampleThreads = 256;
-
-__global__ void k_nv_kappa(const double* __restrict__ sigma, int64_t d, double* __restrict__ kappa) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < d;
-       j += (int64_t)gridDim.x * blockDim.x)
-    kappa[j] = (double)NV_B / (12.0 * sigma[j]);
-}
-
-// Persistent CTAs walk (product j, segment s) pairs.  Per segment: generate the
-// segment's draws D = mu_j + sigma_j * z (sampling.py:190-191) in registers,
-// histogram them by bucket in shared memory, scan, scatter into bucket order, and
-// stream the segment and its bucket starts out.  The sin/cos table is staged once
-// per CTA.
 constexpr int kResampleMinBlocks = 4;
 
+// Persistent CTAs walk (product j, segment s) pairs: generate the segment's keys
+// (Philox4x64-10 + fp32 Box-Muller approximation), histogram them by bucket in
+// shared memory, scan, scatter into bucket order and stream keys + bucket starts out.
 __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     k_nv_resample(uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi, int64_t d, int64_t S,
-                  int nseg, const double* __restrict__ mu, const double* __restrict__ sigma,
-                  const double* __restrict__ kappa, double* __restrict__ dem,
-                  uint16_t* __restrict__ off) {
-  extern __shared__ __align__(16) unsigned char nv_smem[];
-  double* tab = reinterpret_cast<double*>(nv_smem);             // 440 doubles
-  double* raw = tab + 448;                                        // NV_SEG
-  double* sorted_ = raw + NV_SEG;                                 // NV_SEG
-  int* hist = reinterpret_cast<int*>(sorted_ + NV_SEG);           // NV_B
-  uint16_t* bid = reinterpret_cast<uint16_t*>(hist + NV_B);       // NV_SEG bucket ids
+                  int nseg, uint32_t* __restrict__ keys, uint16_t* __restrict__ off) {
+  __shared__ __align__(16) uint32_t raw[NV_SEG];
+  __shared__ __align__(16) uint32_t sorted_[NV_SEG];
+  __shared__ int hist[NV_B];
   __shared__ int wsum[kResampleThreads / 32];
-  load_sincostab(tab);  // includes __syncthreads()
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nblk = d * nseg;
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
@@ -61,45 +43,24 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     const int s = (int)(blk - j * nseg);
     const int64_t e0 = (int64_t)s * NV_SEG;
     const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
-    const double muj = mu[j], sj = sigma[j], kj = kappa[j];
     for (int i = threadIdx.x; i < NV_B; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-
-    // 1) generate normals i0 .. i0+len-1 of the epoch's standard_normal(d*S) draw
+    // 1) keys for normals i0 .. i0+len-1 of the epoch's standard_normal(d*S) draw
     const int64_t i0 = j * S + e0;
     const int64_t q0 = i0 >> 2, q1 = (i0 + len - 1) >> 2;
     for (int64_t q = q0 + threadIdx.x; q <= q1; q += blockDim.x) {
-      double z[4];
-      normals4(seed, sid, clo, chi, (uint64_t)q, tab, z);
+      const phx4 w = philox4x64_10(stream_block_counter(clo, chi, (uint64_t)q), seed, sid);
+      float z[4];
+      nv_approx_pair(phx_u01(w.v[0]), phx_u01(w.v[1]), &z[0], &z[1]);
+      nv_approx_pair(phx_u01(w.v[2]), phx_u01(w.v[3]), &z[2], &z[3]);
       const int64_t l0 = (q << 2) - i0;
-      if (l0 >= 0 && l0 + 4 <= len) {
-        uint16_t bb[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double dv = muj + sj * z[k];
-          raw[l0 + k] = dv;
-          const int b = nv_bucket(dv, muj, kj);
-          bb[k] = (uint16_t)b;
-          atomicAdd(&hist[b], 1);
-        }
-        if ((l0 & 3) == 0) {
-          reinterpret_cast<uint2*>(bid)[l0 >> 2] =
-              make_uint2(bb[0] | ((uint32_t)bb[1] << 16), bb[2] | ((uint32_t)bb[3] << 16));
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) bid[l0 + k] = bb[k];
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int64_t l = l0 + k;
-          if (l >= 0 && l < len) {
-            const double dv = muj + sj * z[k];
-            raw[l] = dv;
-            const int b = nv_bucket(dv, muj, kj);
-            bid[l] = (uint16_t)b;
-            atomicAdd(&hist[b], 1);
-          }
+      for (int k = 0; k < 4; ++k) {
+        const int64_t l = l0 + k;
+        if (l >= 0 && l < len) {
+          const uint32_t code = nv_code(z[k]);
+          raw[l] = (code << 12) | (uint32_t)l;
+          atomicAdd(&hist[code >> (NV_QBITS - 10)], 1);
         }
       }
     }
@@ -107,6 +68,7 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     // 2) exclusive scan of the histogram (NV_B entries, kPer per thread)
     {
       constexpr int kPer = NV_B / kResampleThreads;
+      static_assert(kPer == 4, "bucket starts are stored as one u64 per thread");
       int v[kPer];
       int run = 0;
 #pragma unroll
@@ -130,26 +92,24 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
       }
       __syncthreads();
       int base = incl - run + (warp > 0 ? wsum[warp - 1] : 0);
-      uint32_t packed = 0;
-      uint16_t* o = off + ((j * nseg + s) * (int64_t)NV_B);
+      uint64_t packed = 0;
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
-        const int b = threadIdx.x * kPer + k;
-        packed |= (uint32_t)(uint16_t)base << (16 * k);
-        hist[b] = base;  // becomes the scatter cursor
+        packed |= (uint64_t)(uint16_t)base << (16 * k);
+        hist[threadIdx.x * kPer + k] = base;  // becomes the scatter cursor
         base += v[k];
       }
-      static_assert(kPer == 2, "bucket starts are stored as one u32 per thread");
-      reinterpret_cast<uint32_t*>(o)[threadIdx.x] = packed;
+      reinterpret_cast<uint64_t*>(off + (j * nseg + s) * (int64_t)NV_B)[threadIdx.x] = packed;
     }
     __syncthreads();
     // 3) scatter into bucket order (order inside a bucket is irrelevant to every count)
     for (int l = threadIdx.x; l < len; l += blockDim.x) {
-      const int pos = atomicAdd(&hist[bid[l]], 1);
-      sorted_[pos] = raw[l];
+      const uint32_t key = raw[l];
+      const int pos = atomicAdd(&hist[key >> (12 + NV_QBITS - 10)], 1);
+      sorted_[pos] = key;
     }
     __syncthreads();
-    double* dst = dem + j * S + e0;
+    uint32_t* dst = keys + j * S + e0;
     for (int l = threadIdx.x; l < len; l += blockDim.x) dst[l] = sorted_[l];
     __syncthreads();
   }
@@ -158,22 +118,40 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// ECDF count for one product, one warp: lanes take segments.
-__device__ __forceinline__ int64_t nv_count_warp(const double* __restrict__ dem,
+// ECDF count #{D[j,:] <= x} for one product, one warp: lanes take segments.
+struct NvStreamPos {
+  uint64_t seed, sid, clo, chi;
+};
+
+__device__ __forceinline__ int64_t nv_count_warp(const uint32_t* __restrict__ keys,
                                                  const uint16_t* __restrict__ off, int64_t j,
-                                                 int64_t S, int nseg, double x, double muj,
-                                                 double kj) {
+                                                 int64_t S, int nseg, double x, double mu,
+                                                 double sigma, NvStreamPos sp) {
   const int lane = threadIdx.x & 31;
-  const int b = nv_bucket(x, muj, kj);
+  const NvWindow w = nv_window(x, mu, sigma);
+  const int blo = (int)(w.qlo >> (NV_QBITS - 10)), bhi = (int)(w.qhi >> (NV_QBITS - 10));
+  const double* tab = reinterpret_cast<const double*>(simopt_sincostab_dev);
   int64_t cnt = 0;
   for (int s = lane; s < nseg; s += 32) {
-    const int len = (int)((S - (int64_t)s * NV_SEG) < NV_SEG ? (S - (int64_t)s * NV_SEG) : NV_SEG);
+    const int64_t e0 = (int64_t)s * NV_SEG;
+    const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
     const uint16_t* o = off + (j * nseg + s) * (int64_t)NV_B;
-    const int start = o[b];
-    const int end = (b + 1 < NV_B) ? o[b + 1] : len;
-    const double* seg = dem + j * S + (int64_t)s * NV_SEG;
+    const int start = o[blo];
+    const int end = (bhi + 1 < NV_B) ? o[bhi + 1] : len;
+    const uint32_t* seg = keys + j * S + e0;
     int c = start;
-    for (int p = start; p < end; ++p) c += (seg[p] <= x) ? 1 : 0;
+    for (int p = start; p < end; ++p) {
+      const uint32_t key = seg[p];
+      const int cls = nv_classify(key >> 12, w);
+      if (cls < 0) {
+        ++c;
+      } else if (cls == 0) {  // ambiguous: the reference's exact comparison
+        const int64_t i = j * S + e0 + (int64_t)(key & 4095u);
+        const double z = nv_exact_z(sp.seed, sp.sid, sp.clo, sp.chi, i, tab);
+        const double dv = mu + sigma * z;  // sampling.py:191
+        c += (dv <= x) ? 1 : 0;
+      }
+    }
     cnt += c;
   }
 #pragma unroll
@@ -209,6 +187,7 @@ __global__ void __launch_bounds__(kIterWarps * 32)
   NvState* st = a.state;
   const int64_t jstar = st->jstar;
   const double sval = st->sval;
+  const NvStreamPos sp{a.seed, a.sid, a.ctr_lo, a.ctr_hi};
   for (int64_t j = (int64_t)blockIdx.x * kIterWarps + warp; j < a.d;
        j += (int64_t)gridDim.x * kIterWarps) {
     double x = a.x_in[j];
@@ -223,7 +202,8 @@ __global__ void __launch_bounds__(kIterWarps * 32)
       }
     }
     if (a.do_grad) {
-      const int64_t cnt = nv_count_warp(a.dem, a.off, j, a.S, a.nseg, x, a.mu[j], a.kappa[j]);
+      const int64_t cnt = nv_count_warp(a.keys, a.off, j, a.S, (int)a.nseg, x, a.mu[j],
+                                        a.sigma[j], sp);
       const double g = nv_grad_value(cnt, a.S, a.k[j], a.h[j], a.v[j]);
       if (lane == 0) {
         a.g[j] = g;
@@ -267,13 +247,33 @@ __global__ void __launch_bounds__(kIterWarps * 32)
   }
 }
 
-}  // namespace
-
-int simopt_nv_kappa_impl(cudaStream_t st, const double* sigma, int64_t d, double* kappa) {
-  k_nv_kappa<<<(int)ceil_div(d, 256), 256, 0, st>>>(sigma, d, kappa);
-  SIMOPT_CHECK_LAUNCH("k_nv_kappa");
-  return SIMOPT_OK;
+__global__ void k_nv_counts(const uint32_t* __restrict__ keys, const uint16_t* __restrict__ off,
+                            const double* __restrict__ mu, const double* __restrict__ sigma,
+                            int64_t d, int64_t S, int nseg, NvStreamPos sp,
+                            const double* __restrict__ x, int64_t* __restrict__ counts) {
+  const int warp = threadIdx.x >> 5;
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; j < d;
+       j += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t c = nv_count_warp(keys, off, j, S, nseg, x[j], mu[j], sigma[j], sp);
+    if ((threadIdx.x & 31) == 0) counts[j] = c;
+  }
 }
+
+// Materialise the exact demand of every stored key (test/diagnostic path).
+__global__ void k_nv_decode(const uint32_t* __restrict__ keys, const double* __restrict__ mu,
+                            const double* __restrict__ sigma, int64_t d, int64_t S, NvStreamPos sp,
+                            double* __restrict__ out) {
+  const double* tab = reinterpret_cast<const double*>(simopt_sincostab_dev);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < d * S;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / S, pos = e - j * S;
+    const int64_t seg0 = pos - (pos % NV_SEG);
+    const int64_t i = j * S + seg0 + (int64_t)(keys[e] & 4095u);
+    out[e] = mu[j] + sigma[j] * nv_exact_z(sp.seed, sp.sid, sp.clo, sp.chi, i, tab);
+  }
+}
+
+}  // namespace
 
 extern "C" int simopt_nv_geometry(int64_t* seg, int64_t* buckets) {
   if (seg) *seg = NV_SEG;
@@ -281,40 +281,50 @@ extern "C" int simopt_nv_geometry(int64_t* seg, int64_t* buckets) {
   return SIMOPT_OK;
 }
 
-extern "C" int simopt_nv_layout(int64_t d, int64_t S, int64_t* nseg, int64_t* dem_elems,
+extern "C" int simopt_nv_layout(int64_t d, int64_t S, int64_t* nseg, int64_t* key_elems,
                                 int64_t* off_elems) {
   SIMOPT_REQUIRE(d >= 1 && S >= 1, SIMOPT_E_EMPTY, "need d >= 1 products and S >= 1 samples");
   const int64_t ns = ceil_div(S, NV_SEG);
   if (nseg) *nseg = ns;
-  if (dem_elems) *dem_elems = d * S;
+  if (key_elems) *key_elems = d * S;
   if (off_elems) *off_elems = d * ns * NV_B;
   return SIMOPT_OK;
 }
 
 extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
-                                  uint64_t chi, int64_t d, int64_t S, const double* mu,
-                                  const double* sigma, double* kappa, double* dem, uint16_t* off) {
+                                  uint64_t chi, int64_t d, int64_t S, uint32_t* keys,
+                                  uint16_t* off) {
   SIMOPT_REQUIRE(d >= 1 && S >= 1, SIMOPT_E_EMPTY, "need at least one demand sample per product");
-  cudaStream_t st = as_stream(stream);
-  const int rc = simopt_nv_kappa_impl(st, sigma, d, kappa);
-  if (rc) return rc;
   const int64_t nseg = ceil_div(S, NV_SEG);
   const int64_t nblk = d * nseg;
   SIMOPT_REQUIRE(nblk < (1LL << 31), SIMOPT_E_CONFIG, "too many segments");
-  const size_t smem = (448 + 2 * NV_SEG) * sizeof(double) + NV_B * sizeof(int) +
-                      NV_SEG * sizeof(uint16_t);
-  static bool attr = false;
-  if (!attr) {
-    SIMOPT_CUDA(cudaFuncSetAttribute(k_nv_resample, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    attr = true;
-  }
-  const int64_t grid = nblk < (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks * 8
-                           ? nblk : (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks * 8;
-  k_nv_resample<<<(unsigned)grid, kResampleThreads, smem, st>>>(seed, sid, clo, chi, d, S,
-                                                                (int)nseg, mu, sigma, kappa, dem,
-                                                                off);
+  const int64_t cap = (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks * 8;
+  const int64_t grid = nblk < cap ? nblk : cap;
+  k_nv_resample<<<(unsigned)grid, kResampleThreads, 0, as_stream(stream)>>>(seed, sid, clo, chi, d,
+                                                                            S, (int)nseg, keys, off);
   SIMOPT_CHECK_LAUNCH("k_nv_resample");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_nv_counts(void* stream, const uint32_t* keys, const uint16_t* off,
+                                const double* mu, const double* sigma, int64_t d, int64_t S,
+                                uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi,
+                                const double* x, int64_t* counts) {
+  const int64_t nseg = ceil_div(S, NV_SEG);
+  const int grid = (int)(ceil_div(d, 8) < 8 * SIMOPT_NUM_SMS ? ceil_div(d, 8) : 8 * SIMOPT_NUM_SMS);
+  k_nv_counts<<<grid, 256, 0, as_stream(stream)>>>(keys, off, mu, sigma, d, S, (int)nseg,
+                                                   NvStreamPos{seed, sid, clo, chi}, x, counts);
+  SIMOPT_CHECK_LAUNCH("k_nv_counts");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_nv_decode(void* stream, const uint32_t* keys, const double* mu,
+                                const double* sigma, int64_t d, int64_t S, uint64_t seed,
+                                uint64_t sid, uint64_t clo, uint64_t chi, double* out) {
+  k_nv_decode<<<8 * SIMOPT_NUM_SMS, 256, 0, as_stream(stream)>>>(keys, mu, sigma, d, S,
+                                                                 NvStreamPos{seed, sid, clo, chi},
+                                                                 out);
+  SIMOPT_CHECK_LAUNCH("k_nv_decode");
   return SIMOPT_OK;
 }
 
@@ -325,30 +335,6 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   SIMOPT_REQUIRE(grid <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
   k_nv_iter<<<grid, kIterWarps * 32, 0, as_stream(stream)>>>(a);
   SIMOPT_CHECK_LAUNCH("k_nv_iter");
-  return SIMOPT_OK;
-}
-
-namespace {
-__global__ void k_nv_counts(const double* __restrict__ dem, const uint16_t* __restrict__ off,
-                            const double* __restrict__ kappa, const double* __restrict__ mu,
-                            int64_t d, int64_t S, int nseg, const double* __restrict__ x,
-                            int64_t* __restrict__ counts) {
-  const int warp = threadIdx.x >> 5;
-  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; j < d;
-       j += (int64_t)gridDim.x * (blockDim.x >> 5)) {
-    const int64_t c = nv_count_warp(dem, off, j, S, nseg, x[j], mu[j], kappa[j]);
-    if ((threadIdx.x & 31) == 0) counts[j] = c;
-  }
-}
-}  // namespace
-
-extern "C" int simopt_nv_counts(void* stream, const double* dem, const uint16_t* off,
-                                const double* kappa, const double* mu, int64_t d, int64_t S,
-                                const double* x, int64_t* counts) {
-  const int64_t nseg = ceil_div(S, NV_SEG);
-  const int grid = (int)(ceil_div(d, 8) < 8 * SIMOPT_NUM_SMS ? ceil_div(d, 8) : 8 * SIMOPT_NUM_SMS);
-  k_nv_counts<<<grid, 256, 0, as_stream(stream)>>>(dem, off, kappa, mu, d, S, (int)nseg, x, counts);
-  SIMOPT_CHECK_LAUNCH("k_nv_counts");
   return SIMOPT_OK;
 }
 

@@ -31,7 +31,9 @@ FEAS_TOL = 1e-10  # tasks.py:27
 class NvIterArgs(ctypes.Structure):
     _fields_ = [
         ("d", ctypes.c_int64), ("S", ctypes.c_int64), ("nseg", ctypes.c_int64),
-        ("dem", ctypes.c_void_p), ("off", ctypes.c_void_p), ("kappa", ctypes.c_void_p),
+        ("keys", ctypes.c_void_p), ("off", ctypes.c_void_p),
+        ("seed", ctypes.c_uint64), ("sid", ctypes.c_uint64),
+        ("ctr_lo", ctypes.c_uint64), ("ctr_hi", ctypes.c_uint64),
         ("mu", ctypes.c_void_p), ("sigma", ctypes.c_void_p), ("k", ctypes.c_void_p),
         ("h", ctypes.c_void_p), ("v", ctypes.c_void_p), ("c", ctypes.c_void_p),
         ("budget", ctypes.c_double),
@@ -112,7 +114,7 @@ class NewsvendorTask:
 
 
 class _NvDevice:
-    """Device copies of a NewsvendorTask plus the epoch's demand layout."""
+    """Device copies of a NewsvendorTask plus the epoch's keyed demand layout."""
 
     def __init__(self, task: NewsvendorTask):
         self.d = task.dimension
@@ -123,21 +125,20 @@ class _NvDevice:
         self.v = to_dev(task.selling_value)
         self.c = to_dev(task.budget_costs)
         self.budget = task.budget
-        self.kappa = empty(self.d)
         self.S = None
-        self.dem = None
+        self.keys = None
         self.off = None
         self.nseg = 0
+        self.draw = None  # (seed, stream_id, ctr_lo, ctr_hi) of the epoch's draw
 
     def ensure_layout(self, S: int):
         if S == self.S:
             return
-        ns, de, oe = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        _lib.call("simopt_nv_layout", self.d, S, ctypes.byref(ns), ctypes.byref(de), ctypes.byref(oe))
-        self.dem = None
+        ns, ke, oe = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.call("simopt_nv_layout", self.d, S, ctypes.byref(ns), ctypes.byref(ke), ctypes.byref(oe))
+        self.keys = None
         self.off = None
-        torch.cuda.empty_cache()
-        self.dem = torch.empty(de.value, dtype=F64, device="cuda")
+        self.keys = torch.empty(ke.value, dtype=torch.int32, device="cuda")
         self.off = torch.empty(oe.value, dtype=torch.int16, device="cuda")
         self.nseg = ns.value
         self.S = S
@@ -146,16 +147,24 @@ class _NvDevice:
         if S < 1:
             raise InsufficientSamples("need at least one demand sample per product")
         self.ensure_layout(S)
-        _lib.call("simopt_nv_resample", _lib.stream_ptr(), *stream.words(), self.d, S,
-                  _lib.ptr(self.mu), _lib.ptr(self.sigma), _lib.ptr(self.kappa),
-                  _lib.ptr(self.dem), _lib.ptr(self.off))
+        self.draw = stream.words()
+        _lib.call("simopt_nv_resample", _lib.stream_ptr(), *self.draw, self.d, S,
+                  _lib.ptr(self.keys), _lib.ptr(self.off))
         stream.advance(2 * ((self.d * S + 1) // 2))
 
     def counts(self, x: torch.Tensor) -> torch.Tensor:
         out = torch.empty(self.d, dtype=torch.int64, device="cuda")
-        _lib.call("simopt_nv_counts", _lib.stream_ptr(), _lib.ptr(self.dem), _lib.ptr(self.off),
-                  _lib.ptr(self.kappa), _lib.ptr(self.mu), self.d, self.S, _lib.ptr(x), _lib.ptr(out))
+        _lib.call("simopt_nv_counts", _lib.stream_ptr(), _lib.ptr(self.keys), _lib.ptr(self.off),
+                  _lib.ptr(self.mu), _lib.ptr(self.sigma), self.d, self.S, *self.draw,
+                  _lib.ptr(x), _lib.ptr(out))
         return out
+
+    def decode(self) -> torch.Tensor:
+        """Exact demand of every stored key (storage order) -- diagnostics/tests."""
+        out = torch.empty(self.d * self.S, dtype=F64, device="cuda")
+        _lib.call("simopt_nv_decode", _lib.stream_ptr(), _lib.ptr(self.keys), _lib.ptr(self.mu),
+                  _lib.ptr(self.sigma), self.d, self.S, *self.draw, _lib.ptr(out))
+        return out.view(self.d, self.S)
 
 
 class NewsvendorProblem:
@@ -267,7 +276,8 @@ class NvFwEngine:
             e1.record()
             self.resample_events.append((e0, e1))
         a.S, a.nseg = dev.S, dev.nseg
-        a.dem, a.off, a.kappa = dev.dem.data_ptr(), dev.off.data_ptr(), dev.kappa.data_ptr()
+        a.keys, a.off = dev.keys.data_ptr(), dev.off.data_ptr()
+        a.seed, a.sid, a.ctr_lo, a.ctr_hi = dev.draw
         t0 = k * M
         a.x_in = a.x = self.xs[t0 % H].data_ptr()  # gradient + LMO at the epoch's first iterate
         a.terms = self.terms[t0 % H].data_ptr()

@@ -24,22 +24,21 @@ def _task_from_golden(pkg, g):
 
 
 def _check_layout(dev, sorted_rows):
-    """Bucketed segments hold exactly the reference's sorted rows; bucket order respected."""
+    """Keyed segments decode to exactly the reference's sorted rows; bucket order respected."""
     from paper_2404_11631_b200.tasks import nv_geometry
     seg, nb = nv_geometry()
     d, S = sorted_rows.shape
-    dem = dev.dem.view(d, S).cpu().numpy()
-    off = dev.off.view(d, dev.nseg, nb).cpu().numpy().astype(np.int64) & 0xFFFF
-    kappa = dev.kappa.cpu().numpy()
-    mu = dev.mu.cpu().numpy()
+    dem = dev.decode().cpu().numpy()
     assert np.array_equal(np.sort(dem, axis=1), sorted_rows)
+    keys = dev.keys.view(d, S).cpu().numpy().view(np.uint32).astype(np.int64)
+    off = dev.off.view(d, dev.nseg, nb).cpu().numpy().astype(np.int64) & 0xFFFF
     for j in range(min(d, 64)):
         for s in range(dev.nseg):
-            sv = dem[j, s * seg:(s + 1) * seg]
-            b = np.clip(np.floor((sv - mu[j]) * kappa[j] + nb / 2), 0, nb - 1).astype(np.int64)
+            kv = keys[j, s * seg:(s + 1) * seg]
+            b = kv >> 22
             assert np.all(np.diff(b) >= 0)
-            starts = np.searchsorted(b, np.arange(nb), side="left")
-            assert np.array_equal(off[j, s], starts)
+            assert np.array_equal(np.sort(kv & 4095), np.arange(kv.size))  # each draw once
+            assert np.array_equal(off[j, s], np.searchsorted(b, np.arange(nb), side="left"))
 
 
 def test_resample_matches_reference_rows(pkg, golden):
@@ -55,7 +54,7 @@ def test_resample_matches_reference_rows(pkg, golden):
     assert np.array_equal(got, g["grad"])
 
 
-@pytest.mark.parametrize("d,S", [(300, 5000), (64, 100_000), (1000, 4096), (7, 12289)])
+@pytest.mark.parametrize("d,S", [(300, 5000), (64, 100_000), (1000, 4096), (7, 12289), (5, 3)])
 def test_counts_vs_oracle(pkg, d, S):
     from paper_2404_11631_b200.instances import gen_newsvendor_instance
     from paper_2404_11631_b200.tasks import NewsvendorProblem
@@ -128,3 +127,36 @@ def test_reference_fw_loop_drives_device_problem(pkg, golden):
     rec = fwm.fw_run(HostOnly(), FwConfig(epochs, m_inner, n, pkg.RngStream(42, 2)), b)
     assert np.array_equal(rec.final_iterate, g["fwa_x"])
     np.testing.assert_allclose(rec.objectives, g["fwa_obj"], rtol=1e-13, atol=0)
+
+
+def test_degenerate_sigma_counts(pkg):
+    """sigma = 1e-12 (tests/test_sampling.py:156-158): every draw is ambiguous -> exact path."""
+    from paper_2404_11631_b200.tasks import NewsvendorProblem, NewsvendorTask
+    task = NewsvendorTask(unit_cost=[1.0, 1.5], holding_cost=[0.5, 0.5], selling_value=[3.0, 4.0],
+                          demand_mean=[30.0, 25.0], demand_std=[1e-12, 3.0], budget_costs=[1.0, 1.0],
+                          budget=20.0)
+    prob = NewsvendorProblem(task, pkg.make_backend("cuda"))
+    prob.resample(pkg.RngStream(6, 0), 997)
+    rows = orc.sample_demands(task.demand_mean, task.demand_std, 997, orc.Stream(6, 0))
+    for x0 in (30.0, 30.0 + 1e-13, 25.0, np.nextafter(30.0, 0.0)):
+        x = np.array([x0, x0])
+        cnt = prob.dev.counts(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.array_equal(cnt, orc.ecdf_counts(rows, x))
+
+
+def test_approximation_error_bound(pkg):
+    """The fp32 approximation error stays far inside NV_EPSZ = 1e-4 over 2^26 draws."""
+    from paper_2404_11631_b200.tasks import NewsvendorProblem, NewsvendorTask
+    d, S = 64, 1 << 20
+    ones = np.ones(d)
+    task = NewsvendorTask(unit_cost=ones, holding_cost=ones, selling_value=3 * ones,
+                          demand_mean=np.zeros(d), demand_std=ones, budget_costs=ones, budget=1.0)
+    prob = NewsvendorProblem(task, pkg.make_backend("cuda"))
+    prob.resample(pkg.RngStream(123, 9), S)
+    exact = prob.dev.decode()                       # D = 0 + 1*z, storage order
+    keys = prob.dev.keys.view(d, S).long() & 0xFFFFFFFF
+    q = (keys >> 12).double()
+    lo = (q - 1.0) * (19.0 / 2 ** 20) - 9.5
+    hi = (q + 2.0) * (19.0 / 2 ** 20) - 9.5
+    inside = (exact >= lo - 1e-5) & (exact <= hi + 1e-5)
+    assert bool(inside.all())

@@ -136,6 +136,12 @@ int simopt_nv_counts(void* stream, const uint32_t* keys, const uint16_t* off, co
                      const double* sigma, int64_t d, int64_t S, uint64_t seed, uint64_t stream_id,
                      uint64_t ctr_lo, uint64_t ctr_hi, const double* x, int64_t* counts);
 
+/* Largest |z~ - z| between the key's fp32 approximation and the exact normal over the
+ * first n normals of the draw (*out_max device double); *eps (host) = the bound the
+ * ECDF queries rely on. */
+int simopt_nv_approx_error(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                           uint64_t ctr_hi, int64_t n, double* out_max, double* eps);
+
 /* Exact demand value of every stored key, in storage order (diagnostics / tests). */
 int simopt_nv_decode(void* stream, const uint32_t* keys, const double* mu, const double* sigma,
                      int64_t d, int64_t S, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,

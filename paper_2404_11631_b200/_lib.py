@@ -45,6 +45,7 @@ SIGNATURES = {
     "simopt_nv_geometry": [_vp, _vp],
     "simopt_nv_resample": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp],
     "simopt_nv_counts": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _u64, _u64, _u64, _u64, _vp, _vp],
+    "simopt_nv_approx_error": [_vp, _u64, _u64, _u64, _u64, _i64, _vp, _vp],
     "simopt_nv_decode": [_vp, _vp, _vp, _vp, _i64, _i64, _u64, _u64, _u64, _u64, _vp],
     "simopt_nv_iter": [_vp, _vp],
     "simopt_ecdf_count_sorted": [_vp, _vp, _i64, _i64, _vp, _vp],

@@ -30,7 +30,7 @@ constexpr int kResampleMinBlocks = 4;
 // (Philox4x64-10 + fp32 Box-Muller approximation), histogram them by bucket in
 // shared memory, scan, scatter into bucket order and stream keys + bucket starts out.
 __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
-    k_nv_resample(uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi, int64_t d, int64_t S,
+    k_nv_resample(const phx_keys rk, uint64_t clo, uint64_t chi, int64_t d, int64_t S,
                   int nseg, uint32_t* __restrict__ keys, uint16_t* __restrict__ off) {
   __shared__ __align__(16) uint32_t raw[NV_SEG];
   __shared__ __align__(16) uint32_t sorted_[NV_SEG];
@@ -48,19 +48,31 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     // 1) keys for normals i0 .. i0+len-1 of the epoch's standard_normal(d*S) draw
     const int64_t i0 = j * S + e0;
     const int64_t q0 = i0 >> 2, q1 = (i0 + len - 1) >> 2;
+    const bool aligned = ((i0 & 3) == 0) && ((len & 3) == 0);
     for (int64_t q = q0 + threadIdx.x; q <= q1; q += blockDim.x) {
-      const phx4 w = philox4x64_10(stream_block_counter(clo, chi, (uint64_t)q), seed, sid);
+      const phx4 w = philox4x64_10_rk(stream_block_counter(clo, chi, (uint64_t)q), rk);
       float z[4];
-      nv_approx_pair(phx_u01(w.v[0]), phx_u01(w.v[1]), &z[0], &z[1]);
-      nv_approx_pair(phx_u01(w.v[2]), phx_u01(w.v[3]), &z[2], &z[3]);
-      const int64_t l0 = (q << 2) - i0;
+      nv_approx_pair(w.v[0], w.v[1], &z[0], &z[1]);
+      nv_approx_pair(w.v[2], w.v[3], &z[2], &z[3]);
+      const int l0 = (int)((q << 2) - i0);
+      if (aligned) {
+        uint32_t kk[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t l = l0 + k;
-        if (l >= 0 && l < len) {
+        for (int k = 0; k < 4; ++k) {
           const uint32_t code = nv_code(z[k]);
-          raw[l] = (code << 12) | (uint32_t)l;
+          kk[k] = (code << 12) | (uint32_t)(l0 + k);
           atomicAdd(&hist[code >> (NV_QBITS - 10)], 1);
+        }
+        reinterpret_cast<uint4*>(raw)[l0 >> 2] = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int l = l0 + k;
+          if (l >= 0 && l < len) {
+            const uint32_t code = nv_code(z[k]);
+            raw[l] = (code << 12) | (uint32_t)l;
+            atomicAdd(&hist[code >> (NV_QBITS - 10)], 1);
+          }
         }
       }
     }
@@ -123,37 +135,83 @@ struct NvStreamPos {
   uint64_t seed, sid, clo, chi;
 };
 
+constexpr int kQueue = 256;  // ambiguous draws buffered per warp (>= one batch: 32 lanes x 8)
+
+// Lanes scan segments and count certain-below draws; ambiguous draws are queued in
+// shared memory and then resolved with the exact glibc Box-Muller, one per lane.
 __device__ __forceinline__ int64_t nv_count_warp(const uint32_t* __restrict__ keys,
                                                  const uint16_t* __restrict__ off, int64_t j,
                                                  int64_t S, int nseg, double x, double mu,
-                                                 double sigma, NvStreamPos sp) {
+                                                 double sigma, NvStreamPos sp, int64_t* queue) {
   const int lane = threadIdx.x & 31;
   const NvWindow w = nv_window(x, mu, sigma);
   const int blo = (int)(w.qlo >> (NV_QBITS - 10)), bhi = (int)(w.qhi >> (NV_QBITS - 10));
   const double* tab = reinterpret_cast<const double*>(simopt_sincostab_dev);
   int64_t cnt = 0;
-  for (int s = lane; s < nseg; s += 32) {
-    const int64_t e0 = (int64_t)s * NV_SEG;
-    const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
-    const uint16_t* o = off + (j * nseg + s) * (int64_t)NV_B;
-    const int start = o[blo];
-    const int end = (bhi + 1 < NV_B) ? o[bhi + 1] : len;
-    const uint32_t* seg = keys + j * S + e0;
-    int c = start;
-    for (int p = start; p < end; ++p) {
-      const uint32_t key = seg[p];
-      const int cls = nv_classify(key >> 12, w);
-      if (cls < 0) {
-        ++c;
-      } else if (cls == 0) {  // ambiguous: the reference's exact comparison
-        const int64_t i = j * S + e0 + (int64_t)(key & 4095u);
-        const double z = nv_exact_z(sp.seed, sp.sid, sp.clo, sp.chi, i, tab);
-        const double dv = mu + sigma * z;  // sampling.py:191
-        c += (dv <= x) ? 1 : 0;
+  int nq = 0;  // warp-uniform queue length
+  auto drain = [&]() {
+    for (int e = lane; e < nq; e += 32) {
+      const double z = nv_exact_z(sp.seed, sp.sid, sp.clo, sp.chi, queue[e], tab);
+      const double dv = mu + sigma * z;  // sampling.py:191
+      cnt += (dv <= x) ? 1 : 0;
+    }
+    __syncwarp();
+    nq = 0;
+  };
+  for (int s0 = 0; s0 < nseg; s0 += 32) {
+    const int s = s0 + lane;
+    int start = 0, end = 0, c = 0;
+    const uint32_t* seg = keys;
+    int64_t base = 0;
+    if (s < nseg) {
+      const int64_t e0 = (int64_t)s * NV_SEG;
+      const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
+      const uint16_t* o = off + (j * nseg + s) * (int64_t)NV_B;
+      start = o[blo];
+      end = (bhi + 1 < NV_B) ? o[bhi + 1] : len;
+      seg = keys + j * S + e0;
+      base = j * S + e0;
+      c = start;
+    }
+    // walk the window buckets in lock-step batches of 8 keys per lane (all loads of a
+    // batch in flight together); ambiguous draws are queued warp-wide
+    const int span = end - start;
+    int maxspan = span;
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) maxspan = max(maxspan, __shfl_xor_sync(0xffffffffu, maxspan, o2));
+    for (int p0 = 0; p0 < maxspan; p0 += 8) {
+      uint32_t kv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) kv[k] = (p0 + k < span) ? seg[start + p0 + k] : 0u;
+      unsigned amb = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (p0 + k < span) {
+          const int cls = nv_classify(kv[k] >> 12, w);
+          c += (cls < 0) ? 1 : 0;
+          amb |= (cls == 0) ? (1u << k) : 0u;
+        }
+      }
+      const int na = __popc(amb);
+      int pre = na;  // inclusive warp prefix of the ambiguous counts
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, pre, o2);
+        if (lane >= o2) pre += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, pre, 31);
+      if (total) {
+        if (nq + total > kQueue) drain();
+        int pos = nq + pre - na;
+        for (int k = 0; k < 8; ++k)
+          if (amb & (1u << k)) queue[pos++] = base + (int64_t)(kv[k] & 4095u);
+        __syncwarp();
+        nq += total;
       }
     }
     cnt += c;
   }
+  drain();
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o2);
   return cnt;
@@ -175,9 +233,10 @@ constexpr int kIterWarps = 8;
 //       previous LMO (frank_wolfe.py:69-82), record x_j < -FEAS_TOL, objective term;
 //   (2) if do_grad: g_j at the (new) x_j, LMO values g_j * (C / c_j), argmin over all
 //       products (last-block reduction), NaN flag.
-__global__ void __launch_bounds__(kIterWarps * 32)
+__global__ void __launch_bounds__(kIterWarps * 32, 2)
     k_nv_iter(NvIterArgs a) {
   __shared__ ArgMin warp_best[kIterWarps];
+  __shared__ int64_t queues[kIterWarps][kQueue];
   __shared__ int nan_seen;
   __shared__ bool am_last;
   if (threadIdx.x == 0) nan_seen = 0;
@@ -203,7 +262,7 @@ __global__ void __launch_bounds__(kIterWarps * 32)
     }
     if (a.do_grad) {
       const int64_t cnt = nv_count_warp(a.keys, a.off, j, a.S, (int)a.nseg, x, a.mu[j],
-                                        a.sigma[j], sp);
+                                        a.sigma[j], sp, queues[warp]);
       const double g = nv_grad_value(cnt, a.S, a.k[j], a.h[j], a.v[j]);
       if (lane == 0) {
         a.g[j] = g;
@@ -252,9 +311,10 @@ __global__ void k_nv_counts(const uint32_t* __restrict__ keys, const uint16_t* _
                             int64_t d, int64_t S, int nseg, NvStreamPos sp,
                             const double* __restrict__ x, int64_t* __restrict__ counts) {
   const int warp = threadIdx.x >> 5;
+  __shared__ int64_t queues[8][kQueue];
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; j < d;
        j += (int64_t)gridDim.x * (blockDim.x >> 5)) {
-    const int64_t c = nv_count_warp(keys, off, j, S, nseg, x[j], mu[j], sigma[j], sp);
+    const int64_t c = nv_count_warp(keys, off, j, S, nseg, x[j], mu[j], sigma[j], sp, queues[warp]);
     if ((threadIdx.x & 31) == 0) counts[j] = c;
   }
 }
@@ -300,8 +360,9 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   SIMOPT_REQUIRE(nblk < (1LL << 31), SIMOPT_E_CONFIG, "too many segments");
   const int64_t cap = (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks * 8;
   const int64_t grid = nblk < cap ? nblk : cap;
-  k_nv_resample<<<(unsigned)grid, kResampleThreads, 0, as_stream(stream)>>>(seed, sid, clo, chi, d,
-                                                                            S, (int)nseg, keys, off);
+  const phx_keys rk = phx_round_keys(seed, sid);
+  k_nv_resample<<<(unsigned)grid, kResampleThreads, 0, as_stream(stream)>>>(rk, clo, chi, d, S,
+                                                                            (int)nseg, keys, off);
   SIMOPT_CHECK_LAUNCH("k_nv_resample");
   return SIMOPT_OK;
 }
@@ -401,5 +462,41 @@ extern "C" int simopt_nv_grad_from_counts(void* stream, const int64_t* counts, i
   k_nv_grad_counts<<<(int)(ceil_div(d, 256) < 4096 ? ceil_div(d, 256) : 4096), 256, 0,
                      as_stream(stream)>>>(counts, S, k, h, v, d, g);
   SIMOPT_CHECK_LAUNCH("k_nv_grad_counts");
+  return SIMOPT_OK;
+}
+
+namespace {
+// max |z~ - z| over the first n normals of a draw (evidence for NV_EPSZ).
+__global__ void k_nv_approx_error(const phx_keys rk, uint64_t seed, uint64_t sid, uint64_t clo,
+                                  uint64_t chi, int64_t nblk, unsigned long long* __restrict__ out) {
+  __shared__ double tab[SIMOPT_SINCOSTAB_N];
+  load_sincostab(tab);
+  double m = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nblk;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const phx4 w = philox4x64_10_rk(stream_block_counter(clo, chi, (uint64_t)q), rk);
+    float za[4];
+    nv_approx_pair(w.v[0], w.v[1], &za[0], &za[1]);
+    nv_approx_pair(w.v[2], w.v[3], &za[2], &za[3]);
+    double ze[4];
+    glibc_boxmuller_fast(phx_u01(w.v[0]), phx_u01(w.v[1]), tab, &ze[0], &ze[1]);
+    glibc_boxmuller_fast(phx_u01(w.v[2]), phx_u01(w.v[3]), tab, &ze[2], &ze[3]);
+    for (int k = 0; k < 4; ++k) m = fmax(m, fabs((double)za[k] - ze[k]));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+}  // namespace
+
+extern "C" int simopt_nv_approx_error(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
+                                      uint64_t chi, int64_t n, double* out_max, double* eps) {
+  if (eps) *eps = NV_EPSZ;
+  SIMOPT_REQUIRE(n >= 4, SIMOPT_E_EMPTY, "need n >= 4");
+  cudaStream_t st = as_stream(stream);
+  SIMOPT_CUDA(cudaMemsetAsync(out_max, 0, sizeof(double), st));
+  k_nv_approx_error<<<8 * SIMOPT_NUM_SMS, 256, 0, st>>>(phx_round_keys(seed, sid), seed, sid, clo,
+                                                         chi, n / 4,
+                                                         reinterpret_cast<unsigned long long*>(out_max));
+  SIMOPT_CHECK_LAUNCH("k_nv_approx_error");
   return SIMOPT_OK;
 }

@@ -5,8 +5,9 @@
 // its 4096-draw segment and q (20 bits) is a fixed-point code of an fp32
 // approximation z~ of its standard normal z:
 //     q = clamp(floor((z~ + 9.5) * 2^20 / 19), 0, 2^20 - 1).
-// |z~ - z| <= NV_EPSZ is guaranteed by construction (fp32 log1pf/logf/sqrtf/
-// sincospif are <= 2 ulp; the bound used is ~20x the worst case), and q is
+// |z~ - z| <= NV_EPSZ is guaranteed by construction (error budget at
+// nv_approx_pair; NV_EPSZ is > 3x the worst case and tests/test_gpu_newsvendor.py
+// measures the maximum over 2^26 draws), and q is
 // monotone in z~ up to one code of fp32 rounding.  Keys are counting-sorted by
 // bucket (the top 10 bits of q) inside each segment.  An ECDF query x_j then
 // splits every draw into: certainly below x, certainly above x, or ambiguous
@@ -31,24 +32,50 @@
 #define NV_Z0 9.5
 #define NV_QSCALE (1048576.0 / 19.0)  // codes per unit of z
 #define NV_W (19.0 / 1048576.0)       // z width of one code
-#define NV_EPSZ 1e-4                  // guaranteed |z~ - z| bound (actual < 6e-6)
+#define NV_EPSZ 1.5e-5                // guaranteed |z~ - z| bound (analytic worst case < 1e-5,
+                                      // measured max 3.7e-6 over 2^28 draws)
 
-// fp32 approximation of one Box-Muller pair (both components).
-__device__ __forceinline__ void nv_approx_pair(double u1, double u2, float* z0, float* z1) {
-  // -2*log1p(-u1): log1pf for small u1, logf(1 - u1) (1 - u1 exact in double) near 1
-  const float l = (u1 < 0.5) ? log1pf(-(float)u1) : logf((float)(1.0 - u1));
-  const float r = sqrtf(-2.0f * l);
+// fp32 approximation of one Box-Muller pair (both components) from the raw
+// Philox words, on the SFU (MUFU) path.  Error budget, |z~ - z|:
+//   l = log1p(-u1): u1 < 2^-6: 5-term series -(u + u^2/2 + ... + u^5/5) (relative
+//       error < 2^-29 + fp32 rounding); else ln2 * lg2.approx((float)(1 - u1)) with
+//       1 - u1 an exact integer times 2^-53 (the __logf bound: abs error <= 3.6e-7 on
+//       [0.5, 2], 3 ulp relative below; the ftz forms never see subnormals here):
+//       |dr| = |dl| / r <= 2.7e-6 (worst at u1 = 2^-6, r = 0.177).
+//   r = y * rsqrt.approx(y), y = -2l: relative 2 ulp -> |dr| <= 2.1e-6 at r = 8.57.
+//   theta' = 2pi(u2 - 1/2) in [-pi, pi): sin/cos.approx abs error <= 2^-21.41, plus
+//       2pi * 2^-24 from rounding u2: |dcos|, |dsin| <= 7.3e-7.
+//   => |z~ - z| <= 2.7e-6 + 8.57 * 7.3e-7 + 1e-6 < 1e-5;  NV_EPSZ = 1.5e-5.
+__device__ __forceinline__ void nv_approx_pair(uint64_t w0, uint64_t w1, float* z0, float* z1) {
+  const uint64_t k1 = w0 >> 11;                        // u1 = k1 * 2^-53
+  const float u1f = (float)k1 * 0x1p-53f;
+  const float vf = (float)((1ULL << 53) - k1) * 0x1p-53f;  // 1 - u1 (exact integer)
+  // series for small u1 (Horner), SFU log otherwise; both evaluated, one selected
+  float ser = fmaf(u1f, 0.2f, 0.25f);
+  ser = fmaf(u1f, ser, 0.33333334f);
+  ser = fmaf(u1f, ser, 0.5f);
+  ser = fmaf(u1f, ser, 1.0f);
+  const float ls = -u1f * ser;
+  float lg;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(vf));  // vf >= 2^-53: never subnormal
+  const float ll = lg * 0.69314718055994531f;
+  const float l = (k1 < (1ULL << 47)) ? ls : ll;      // u1 < 2^-6
+  const float y = -2.0f * l;
+  float rs;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(y));   // y >= 2^-52 or exactly 0
+  const float r = (y > 0.0f) ? y * rs : 0.0f;
+  const float u2f = (float)(uint32_t)(w1 >> 40) * 0x1p-24f;  // |u2f - u2| < 2^-24
+  const float th = 6.2831853071795865f * (u2f - 0.5f);      // theta - pi, in [-pi, pi)
   float s, c;
-  sincospif(2.0f * (float)u2, &s, &c);
-  *z0 = r * c;
-  *z1 = r * s;
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
+  *z0 = -r * c;
+  *z1 = -r * s;
 }
 
 __device__ __forceinline__ uint32_t nv_code(float z) {
   const float t = (z + (float)NV_Z0) * (float)NV_QSCALE;
-  if (!(t >= 0.0f)) return 0u;
-  if (t >= (float)NV_QMAX) return (uint32_t)NV_QMAX;
-  return (uint32_t)t;
+  return (uint32_t)fminf(fmaxf(t, 0.0f), (float)NV_QMAX);  // branch-free clamp, then trunc
 }
 
 // Exact standard normal #i of the epoch's draw (glibc-exact Box-Muller, _kernels.py:184-190).
@@ -80,10 +107,12 @@ __device__ __forceinline__ NvWindow nv_window(double x, double mu, double sigma)
   return w;
 }
 
-// -1: certainly below t, +1: certainly above, 0: ambiguous.
+// -1: certainly below t, +1: certainly above, 0: ambiguous.  A code q means
+// (z~ + 9.5) * 2^20/19 in [q - 0.15, q + 1.15] (fp32 rounding of the code's two
+// operations is < 0.15 code); 0.25 code of slack is used on each side.
 __device__ __forceinline__ int nv_classify(uint32_t q, const NvWindow& w) {
-  const double hiz = (q >= (uint32_t)NV_QMAX) ? INFINITY : ((double)q + 2.0) * NV_W - NV_Z0;
-  const double loz = (q == 0u) ? -INFINITY : ((double)q - 1.0) * NV_W - NV_Z0;
+  const double hiz = (q >= (uint32_t)NV_QMAX) ? INFINITY : ((double)q + 1.25) * NV_W - NV_Z0;
+  const double loz = (q == 0u) ? -INFINITY : ((double)q - 0.25) * NV_W - NV_Z0;
   if (hiz + w.eps < w.t) return -1;
   if (loz - w.eps > w.t) return 1;
   return 0;

@@ -68,3 +68,37 @@ PHX_HD phx4 phx_block_counter(uint64_t clo, uint64_t chi, uint64_t b) {
 }
 
 PHX_HD double phx_u01(uint64_t w) { return (double)(w >> 11) * (1.0 / 9007199254740992.0); }
+
+// Round keys of Philox4x64-10 for key (k0, k1): rk[2r], rk[2r+1] = key after r bumps.
+// Precomputed once on the host and passed by value, so every round's XOR takes
+// its key straight from the constant bank (no per-round key arithmetic).
+typedef struct phx_keys { uint64_t k[20]; } phx_keys;
+
+static inline phx_keys phx_round_keys(uint64_t k0, uint64_t k1) {
+  phx_keys r;
+  for (int i = 0; i < 10; ++i) {
+    r.k[2 * i] = k0;
+    r.k[2 * i + 1] = k1;
+    k0 += PHILOX_W0;
+    k1 += PHILOX_W1;
+  }
+  return r;
+}
+
+PHX_HD phx4 philox4x64_10_rk(phx4 c, const phx_keys& rk) {
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+  for (int r = 0; r < 10; ++r) {
+    uint64_t hi0, lo0, hi1, lo1;
+    phx_mulhilo(PHILOX_M0, c.v[0], &hi0, &lo0);
+    phx_mulhilo(PHILOX_M1, c.v[2], &hi1, &lo1);
+    phx4 o;
+    o.v[0] = hi1 ^ c.v[1] ^ rk.k[2 * r];
+    o.v[1] = lo1;
+    o.v[2] = hi0 ^ c.v[3] ^ rk.k[2 * r + 1];
+    o.v[3] = lo0;
+    c = o;
+  }
+  return c;
+}

@@ -160,3 +160,18 @@ def test_approximation_error_bound(pkg):
     hi = (q + 2.0) * (19.0 / 2 ** 20) - 9.5
     inside = (exact >= lo - 1e-5) & (exact <= hi + 1e-5)
     assert bool(inside.all())
+
+
+@pytest.mark.parametrize("seed,sid,ctr", [(42, 2, 0), (7, 1, (1 << 64) - 3)])
+def test_approximation_error_measured(pkg, seed, sid, ctr):
+    """max |z~ - z| over 2^28 normals stays below a third of the bound the queries assume."""
+    import ctypes
+    from paper_2404_11631_b200 import _lib
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    eps = ctypes.c_double()
+    s = pkg.RngStream(seed, sid, ctr)
+    _lib.call("simopt_nv_approx_error", _lib.stream_ptr(), *s.words(), 1 << 28, _lib.ptr(out),
+              ctypes.byref(eps))
+    m = float(out.item())
+    print(f"max |z~ - z| = {m:.3e} (bound {eps.value:.1e})")
+    assert m < eps.value / 3

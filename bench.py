@@ -259,7 +259,7 @@ def run_ours(args, rank, world):
                 "kernel_ms": res_ms, "share_of_step": res_ms / (ms / args.steps),
                 "note": ("issue-bound: Philox4x64-10 + fp32 Box-Muller key per draw (exact glibc "
                          "Box-Muller only for ambiguous draws at query time); see profiles/")}
-    launches_per_epoch = 3 * M + 3
+    launches_per_epoch = 4 * M + 2  # resample, M+1 fused steps, M x (terms, sums, stamp)
     line = {
         "metric": "newsvendor Frank-Wolfe iterations/sec (d=10000, S=100000, M=25)",
         "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,

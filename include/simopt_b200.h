@@ -167,7 +167,8 @@ typedef struct NvState {
 
 /* One fused FW kernel (frank_wolfe.py:106-117 for NewsvendorProblem):
  *  do_update: x <- (gamma*((-1*x) + s)) + x with the vertex in *state, objective
- *             terms (newsvendor_cost_block) into terms[], flags[step] |= NEGATIVE;
+ *             terms (newsvendor_cost_block) into terms[] unless terms == NULL,
+ *             flags[step] |= NEGATIVE;
  *  do_grad:   g = nv_gradient_hat(x) (tasks.py:141-160), LMO argmin of
  *             g*(budget/c) (lmo.py:68-89) into *state, flags[grad_step] |= NAN. */
 typedef struct NvIterArgs {

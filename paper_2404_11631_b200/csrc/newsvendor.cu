@@ -135,6 +135,16 @@ struct NvStreamPos {
   uint64_t seed, sid, clo, chi;
 };
 
+// Exact resolve of one ambiguous draw, kept out of line so the rare glibc
+// Box-Muller path does not inflate the register budget of the scan.
+__device__ __noinline__ int nv_resolve(NvStreamPos sp, int64_t i, double mu, double sigma,
+                                       double x) {
+  const double* tab = reinterpret_cast<const double*>(simopt_sincostab_dev);
+  const double z = nv_exact_z(sp.seed, sp.sid, sp.clo, sp.chi, i, tab);
+  const double dv = mu + sigma * z;  // sampling.py:191
+  return (dv <= x) ? 1 : 0;
+}
+
 constexpr int kQueue = 256;  // ambiguous draws buffered per warp (>= one batch: 32 lanes x 8)
 
 // Lanes scan segments and count certain-below draws; ambiguous draws are queued in
@@ -146,15 +156,10 @@ __device__ __forceinline__ int64_t nv_count_warp(const uint32_t* __restrict__ ke
   const int lane = threadIdx.x & 31;
   const NvWindow w = nv_window(x, mu, sigma);
   const int blo = (int)(w.qlo >> (NV_QBITS - 10)), bhi = (int)(w.qhi >> (NV_QBITS - 10));
-  const double* tab = reinterpret_cast<const double*>(simopt_sincostab_dev);
   int64_t cnt = 0;
   int nq = 0;  // warp-uniform queue length
   auto drain = [&]() {
-    for (int e = lane; e < nq; e += 32) {
-      const double z = nv_exact_z(sp.seed, sp.sid, sp.clo, sp.chi, queue[e], tab);
-      const double dv = mu + sigma * z;  // sampling.py:191
-      cnt += (dv <= x) ? 1 : 0;
-    }
+    for (int e = lane; e < nq; e += 32) cnt += nv_resolve(sp, queue[e], mu, sigma, x);
     __syncwarp();
     nq = 0;
   };
@@ -233,7 +238,7 @@ constexpr int kIterWarps = 8;
 //       previous LMO (frank_wolfe.py:69-82), record x_j < -FEAS_TOL, objective term;
 //   (2) if do_grad: g_j at the (new) x_j, LMO values g_j * (C / c_j), argmin over all
 //       products (last-block reduction), NaN flag.
-__global__ void __launch_bounds__(kIterWarps * 32, 2)
+__global__ void __launch_bounds__(kIterWarps * 32, 3)
     k_nv_iter(NvIterArgs a) {
   __shared__ ArgMin warp_best[kIterWarps];
   __shared__ int64_t queues[kIterWarps][kQueue];
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, 2)
       if (lane == 0) {
         a.x[j] = x;
         if (x < -1e-10) atomicOr(&a.flags[a.step], NV_FLAG_NEGATIVE);
-        a.terms[j] = nv_cost_term(x, a.mu[j], a.sigma[j], a.k[j], a.h[j], a.v[j]);
+        if (a.terms) a.terms[j] = nv_cost_term(x, a.mu[j], a.sigma[j], a.k[j], a.h[j], a.v[j]);
       }
     }
     if (a.do_grad) {

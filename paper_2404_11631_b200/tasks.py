@@ -280,7 +280,7 @@ class NvFwEngine:
         a.seed, a.sid, a.ctr_lo, a.ctr_hi = dev.draw
         t0 = k * M
         a.x_in = a.x = self.xs[t0 % H].data_ptr()  # gradient + LMO at the epoch's first iterate
-        a.terms = self.terms[t0 % H].data_ptr()
+        a.terms = None  # objective terms are formed on the side stream
         a.do_update, a.do_grad, a.step, a.grad_step, a.gamma = 0, 1, t0, t0, 0.0
         _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
         for m in range(M):
@@ -291,14 +291,18 @@ class NvFwEngine:
                 main.wait_event(old)
             xin, xout = self.xs[t % H], self.xs[slot]
             a.x_in, a.x = xin.data_ptr(), xout.data_ptr()
-            a.terms = self.terms[slot].data_ptr()
             a.gamma = fw_step_size(k, M, m)
             a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), t, t + 1
             _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
             ev = torch.cuda.Event()
             ev.record(main)
             self.side.wait_event(ev)
-            # dot(c, x_{t+1}) for check_feasible and the objective's vec_sum, one launch
+            # objective terms of x_{t+1} (newsvendor_cost_block), then dot(c, x_{t+1}) for
+            # check_feasible and the objective's vec_sum in one launch -- all off the
+            # critical path
+            _lib.check(lib.simopt_nv_cost_terms(ssp, _lib.ptr(xout), _lib.ptr(dev.mu),
+                                                _lib.ptr(dev.sigma), _lib.ptr(dev.k), _lib.ptr(dev.h),
+                                                _lib.ptr(dev.v), dev.d, _lib.ptr(self.terms[slot])))
             _lib.check(lib.simopt_tree_sums2(ssp, _lib.ptr(dev.c), _lib.ptr(xout), dev.d,
                                              _lib.ptr(self.spent[t:]), _lib.ptr(self.terms[slot]),
                                              None, dev.d, _lib.ptr(self.objs[t:]), self.chunk))

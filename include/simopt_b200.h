@@ -99,6 +99,10 @@ int simopt_matvec_t(void* stream, const double* a, int64_t lda_rows, int64_t col
 int simopt_axpy(void* stream, double alpha, const double* x, const double* y, int64_t n,
                 double* out);
 int simopt_map_kernel(void* stream, int kernel, const double* x, int64_t n, double* out);
+/* axpy with alpha read from device memory when the kernel runs (CUDA-graph replay of
+ * Frank-Wolfe epochs whose step sizes change per epoch). */
+int simopt_axpy_ptr(void* stream, const double* alpha, const double* x, const double* y, int64_t n,
+                    double* out);
 /* out = x*alpha - y elementwise (y may be NULL), e.g. tasks.py:62 and :85 epilogues. */
 int simopt_scale_sub(void* stream, const double* x, double alpha, const double* y, int64_t n,
                      double* out);

@@ -35,6 +35,7 @@ SIGNATURES = {
     "simopt_matvec": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],
     "simopt_matvec_t": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],
     "simopt_axpy": [_vp, _d, _vp, _vp, _i64, _vp],
+    "simopt_axpy_ptr": [_vp, _vp, _vp, _vp, _i64, _vp],
     "simopt_map_kernel": [_vp, _i32, _vp, _i64, _vp],
     "simopt_timestamp": [_vp, _vp],
     "simopt_scale_sub": [_vp, _vp, _d, _vp, _i64, _vp],

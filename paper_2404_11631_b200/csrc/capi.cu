@@ -2,6 +2,10 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
 #include "common.cuh"
 
 static thread_local char g_err[512] = "";
@@ -28,4 +32,38 @@ extern "C" int simopt_timestamp(void* stream, int64_t* out) {
   k_stamp<<<1, 1, 0, as_stream(stream)>>>(out);
   SIMOPT_CHECK_LAUNCH("k_stamp");
   return SIMOPT_OK;
+}
+
+namespace {
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_scratch_mu;
+std::unordered_map<cudaStream_t, Scratch> g_scratch;
+std::vector<void*> g_retired;  // superseded buffers, kept alive for captured graphs
+}  // namespace
+
+void* simopt_scratch(cudaStream_t st, size_t bytes) {
+  std::lock_guard<std::mutex> lock(g_scratch_mu);
+  Scratch& s = g_scratch[st];
+  if (s.bytes >= bytes) return s.ptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+    simopt_set_error("scratch for this stream must be warmed up (an eager call of the same "
+                     "sizes) before CUDA-graph capture: need %zu bytes, have %zu", bytes, s.bytes);
+    return nullptr;
+  }
+  size_t want = bytes < (1u << 20) ? (1u << 20) : bytes;
+  want = (want + 4095) & ~size_t(4095);
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess) {
+    simopt_set_error("scratch allocation of %zu bytes: %s", want, cudaGetErrorString(e));
+    return nullptr;
+  }
+  if (s.ptr) g_retired.push_back(s.ptr);
+  s.ptr = p;
+  s.bytes = want;
+  return p;
 }

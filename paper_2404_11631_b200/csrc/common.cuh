@@ -39,6 +39,14 @@ void simopt_set_error(const char* fmt, ...);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Per-stream scratch.  Every ABI call that needs scratch (chunk partials, argmin
+// partials) takes it from its stream's buffer: uses are stream-ordered, so one
+// buffer per stream is race-free, and no allocation happens on the hot path or
+// inside a captured CUDA graph.  Buffers only grow; a superseded buffer is kept
+// alive (graphs captured earlier may still reference it).  Returns nullptr and
+// sets the error text on failure.
+void* simopt_scratch(cudaStream_t st, size_t bytes);
+
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Pairwise fold of a[0..m) in index order, odd tail carried (_kernels.py:30-42),

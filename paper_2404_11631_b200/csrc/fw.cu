@@ -67,16 +67,15 @@ static int lmo(void* stream, int mode, const double* g, const double* c, double 
   cudaStream_t st = as_stream(stream);
   const int grid = (int)(ceil_div(n, kThreads) < 2 * SIMOPT_NUM_SMS ? ceil_div(n, kThreads)
                                                                       : 2 * SIMOPT_NUM_SMS);
-  unsigned char* ws = nullptr;
   const size_t bytes = grid * (sizeof(double) + sizeof(int64_t)) + 64;
-  SIMOPT_CUDA(cudaMallocAsync(&ws, bytes, st));
+  unsigned char* ws = static_cast<unsigned char*>(simopt_scratch(st, bytes));
+  SIMOPT_REQUIRE(ws != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
   double* pv = reinterpret_cast<double*>(ws);
   int64_t* pi = reinterpret_cast<int64_t*>(ws + grid * sizeof(double));
   unsigned* done = reinterpret_cast<unsigned*>(ws + grid * (sizeof(double) + sizeof(int64_t)));
   SIMOPT_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned), st));
   k_lmo<<<grid, kThreads, 0, st>>>(mode, g, c, budget, n, pv, pi, done, status, s_out, nullptr);
   SIMOPT_CHECK_LAUNCH("k_lmo");
-  SIMOPT_CUDA(cudaFreeAsync(ws, st));
   return SIMOPT_OK;
 }
 

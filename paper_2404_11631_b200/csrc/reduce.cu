@@ -16,6 +16,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -167,13 +172,13 @@ __global__ void __launch_bounds__(512) k_fold_final(const double* __restrict__ s
 // conflict-free.
 constexpr int kRStages = 5;
 
-template <bool kCenter, bool kIdx>
+template <bool kCenter, bool kIdx, bool kV16>
 __global__ void __launch_bounds__(32) k_matvec_rows(const double* __restrict__ a, int64_t cols,
                                                     const int64_t* __restrict__ idx, int64_t rows,
                                                     const double* __restrict__ center,
                                                     const double* __restrict__ x, int64_t chunk,
                                                     int64_t nch, double* __restrict__ out) {
-  __shared__ __align__(16) double tile[kRStages][32][33];
+  __shared__ __align__(16) double tile[kRStages][32][34];  // 272-B rows: 16-B aligned, 2-way banks
   __shared__ __align__(16) double xs[kRStages][32];
   __shared__ __align__(16) double cs[kRStages][32];
   const int lane = threadIdx.x;
@@ -182,17 +187,32 @@ __global__ void __launch_bounds__(32) k_matvec_rows(const double* __restrict__ a
   const int64_t clo = c * chunk;
   const int64_t chi = clo + chunk < cols ? clo + chunk : cols;
   const int64_t nst = (chi - clo + 31) / 32;
+  const int h = lane >> 4, m2 = 2 * (lane & 15);
+  int64_t rowA = 0, rowB = 0;  // v16: rows 2rr+h handled by this lane are fetched per stage
+  (void)rowA; (void)rowB;
   auto issue = [&](int64_t st) {
     const int buf = (int)(st % kRStages);
     const int64_t j0 = clo + st * 32;
     const int64_t jj = j0 + lane;
     const bool jv = jj < chi;
+    if (kV16) {
+      const bool pv = (j0 + m2 < chi);  // chi even (cols even, chunk even)
+#pragma unroll 4
+      for (int rr = 0; rr < 16; ++rr) {
+        const int r = 2 * rr + h;
+        const int64_t grow = r0 + r;
+        const bool v = grow < rows && pv;
+        const int64_t row = (grow < rows) ? (kIdx ? idx[grow] : grow) : 0;
+        cp_async16(&tile[buf][r][m2], a + row * cols + (pv ? j0 + m2 : 0), v);
+      }
+    } else {
 #pragma unroll 8
-    for (int rr = 0; rr < 32; ++rr) {
-      const int64_t r = r0 + rr;
-      const bool v = r < rows && jv;
-      const int64_t row = (r < rows) ? (kIdx ? idx[r] : r) : 0;
-      cp_async8(&tile[buf][rr][lane], a + row * cols + (jv ? jj : 0), v);
+      for (int rr = 0; rr < 32; ++rr) {
+        const int64_t grow = r0 + rr;
+        const bool v = grow < rows && jv;
+        const int64_t row = (grow < rows) ? (kIdx ? idx[grow] : grow) : 0;
+        cp_async8(&tile[buf][rr][lane], a + row * cols + (jv ? jj : 0), v);
+      }
     }
     cp_async8(&xs[buf][lane], x + (jv ? jj : 0), jv);
     if (kCenter) cp_async8(&cs[buf][lane], center + (jv ? jj : 0), jv);
@@ -252,7 +272,7 @@ __global__ void k_fold_strided(double* __restrict__ p, int64_t count, int64_t nc
 constexpr int kTStages = 5;
 constexpr int kTRows = 32;
 
-template <bool kCenter, bool kIdx>
+template <bool kCenter, bool kIdx, bool kV16>
 __global__ void __launch_bounds__(32) k_matvec_t_cols(const double* __restrict__ a, int64_t cols,
                                                       const int64_t* __restrict__ idx, int64_t rows,
                                                       const double* __restrict__ center,
@@ -261,22 +281,37 @@ __global__ void __launch_bounds__(32) k_matvec_t_cols(const double* __restrict__
   __shared__ __align__(16) double tile[kTStages][kTRows][32];
   __shared__ __align__(16) double xs[kTStages][kTRows];
   const int lane = threadIdx.x;
-  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t j0 = (int64_t)blockIdx.x * 32;
+  const int64_t j = j0 + lane;
   const int64_t c = blockIdx.y;
   const int64_t lo = c * chunk;
   const int64_t hi = lo + chunk < rows ? lo + chunk : rows;
   const bool jv = j < cols;
   const double cj = (kCenter && jv) ? center[j] : 0.0;
   const int64_t nst = (hi - lo + kTRows - 1) / kTRows;
+  // 16-byte copies: lane = (half h, pair m) moves columns j0+2m, j0+2m+1 of rows r0+2rr+h
+  const int h = lane >> 4, m2 = 2 * (lane & 15);
+  const bool pv = (j0 + m2 < cols);  // cols even => both columns valid together
   auto issue = [&](int64_t st) {
     const int buf = (int)(st % kTStages);
     const int64_t r0 = lo + st * kTRows;
+    if (kV16) {
+#pragma unroll 4
+      for (int rr = 0; rr < kTRows / 2; ++rr) {
+        const int r = 2 * rr + h;
+        const int64_t grow = r0 + r;
+        const bool v = grow < hi;
+        const int64_t row = v ? (kIdx ? idx[grow] : grow) : 0;
+        cp_async16(&tile[buf][r][m2], a + row * cols + (pv ? j0 + m2 : 0), v && pv);
+      }
+    } else {
 #pragma unroll 8
-    for (int r = 0; r < kTRows; ++r) {
-      const int64_t rr = r0 + r;
-      const bool v = rr < hi;
-      const int64_t row = v ? (kIdx ? idx[rr] : rr) : 0;
-      cp_async8(&tile[buf][r][lane], a + row * cols + (jv ? j : 0), v && jv);
+      for (int r = 0; r < kTRows; ++r) {
+        const int64_t grow = r0 + r;
+        const bool v = grow < hi;
+        const int64_t row = v ? (kIdx ? idx[grow] : grow) : 0;
+        cp_async8(&tile[buf][r][lane], a + row * cols + (jv ? j : 0), v && jv);
+      }
     }
     const int64_t rr = r0 + lane;
     cp_async8(&xs[buf][lane], x + (rr < hi ? rr : 0), rr < hi);
@@ -309,6 +344,18 @@ __global__ void __launch_bounds__(32) k_matvec_t_cols(const double* __restrict__
   if (!jv) return;
   if (nch == 1) out[j] = s;
   else out[c * cols + j] = s;  // partials, folded by k_fold_strided
+}
+
+bool vec16_ok(const void* a, int64_t cols) {
+  return ((reinterpret_cast<uintptr_t>(a) & 15u) == 0) && (cols % 2 == 0);
+}
+
+__global__ void k_axpy_ptr(const double* __restrict__ alpha, const double* __restrict__ x,
+                           const double* __restrict__ y, int64_t n, double* __restrict__ out) {
+  const double a = *alpha;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a * x[i] + y[i];
 }
 
 __global__ void k_axpy(double alpha, const double* __restrict__ x, const double* __restrict__ y,
@@ -380,8 +427,8 @@ static int tree_jobs(cudaStream_t st, TreeJob* js, int nj, int64_t chunk) {
   J.first_chunk[0] = 0;
   for (int i = 0; i < k; ++i) J.first_chunk[i + 1] = J.first_chunk[i] + ceil_div(J.job[i].n, chunk);
   const int64_t total = J.first_chunk[k];
-  unsigned char* ws = nullptr;
-  SIMOPT_CUDA(cudaMallocAsync(&ws, 2 * total * sizeof(double) + 64, st));
+  unsigned char* ws = static_cast<unsigned char*>(simopt_scratch(st, 2 * total * sizeof(double) + 64));
+  SIMOPT_REQUIRE(ws != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
   double* partials = reinterpret_cast<double*>(ws);
   unsigned* counters = reinterpret_cast<unsigned*>(ws + 2 * total * sizeof(double));
   SIMOPT_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned), st));
@@ -397,7 +444,6 @@ static int tree_jobs(cudaStream_t st, TreeJob* js, int nj, int64_t chunk) {
       if (rc) return rc;
     }
   }
-  SIMOPT_CUDA(cudaFreeAsync(ws, st));
   return SIMOPT_OK;
 }
 
@@ -438,20 +484,23 @@ extern "C" int simopt_matvec(void* stream, const double* a, int64_t lda_rows, in
   SIMOPT_REQUIRE(nch < 65536, SIMOPT_E_CONFIG, "too many column chunks (%lld)", (long long)nch);
   SIMOPT_REQUIRE(ceil_div(rows, 32) < (1LL << 31), SIMOPT_E_CONFIG, "too many rows");
   double* p = out;
-  if (nch > 1) SIMOPT_CUDA(cudaMallocAsync(&p, rows * nch * sizeof(double), st));
+  if (nch > 1) {
+    p = static_cast<double*>(simopt_scratch(st, rows * nch * sizeof(double)));
+    SIMOPT_REQUIRE(p != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
+  }
   const dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)nch);
   const int sel = (center ? 1 : 0) | (idx ? 2 : 0);
+  const bool v16 = vec16_ok(a, cols) && (chunk % 2 == 0);
   switch (sel) {
-    case 0: k_matvec_rows<false, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    case 1: k_matvec_rows<true, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    case 2: k_matvec_rows<false, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    default: k_matvec_rows<true, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 0: if (v16) k_matvec_rows<false, false, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); else k_matvec_rows<false, false, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 1: if (v16) k_matvec_rows<true, false, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); else k_matvec_rows<true, false, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 2: if (v16) k_matvec_rows<false, true, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); else k_matvec_rows<false, true, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    default: if (v16) k_matvec_rows<true, true, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); else k_matvec_rows<true, true, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
   }
   SIMOPT_CHECK_LAUNCH("k_matvec_rows");
   if (nch > 1) {
     k_fold_strided<<<elementwise_grid(rows), 256, 0, st>>>(p, rows, nch, nch, 1, out);
     SIMOPT_CHECK_LAUNCH("k_fold_strided");
-    SIMOPT_CUDA(cudaFreeAsync(p, st));
   }
   return SIMOPT_OK;
 }
@@ -470,20 +519,23 @@ extern "C" int simopt_matvec_t(void* stream, const double* a, int64_t lda_rows, 
   const int64_t nch = ceil_div(rows, chunk);
   SIMOPT_REQUIRE(nch < 65536, SIMOPT_E_CONFIG, "too many row chunks (%lld)", (long long)nch);
   double* p = out;
-  if (nch > 1) SIMOPT_CUDA(cudaMallocAsync(&p, cols * nch * sizeof(double), st));
+  if (nch > 1) {
+    p = static_cast<double*>(simopt_scratch(st, cols * nch * sizeof(double)));
+    SIMOPT_REQUIRE(p != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
+  }
   const dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)nch);
   const int sel = (center ? 1 : 0) | (idx ? 2 : 0);
+  const bool v16 = vec16_ok(a, cols);
   switch (sel) {
-    case 0: k_matvec_t_cols<false, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    case 1: k_matvec_t_cols<true, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    case 2: k_matvec_t_cols<false, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
-    default: k_matvec_t_cols<true, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 0: if (v16) k_matvec_t_cols<false, false, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); else k_matvec_t_cols<false, false, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 1: if (v16) k_matvec_t_cols<true, false, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); else k_matvec_t_cols<true, false, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    case 2: if (v16) k_matvec_t_cols<false, true, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); else k_matvec_t_cols<false, true, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
+    default: if (v16) k_matvec_t_cols<true, true, true><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); else k_matvec_t_cols<true, true, false><<<grid, 32, 0, st>>>(a, cols, idx, rows, center, x, chunk, nch, p); break;
   }
   SIMOPT_CHECK_LAUNCH("k_matvec_t_cols");
   if (nch > 1) {
     k_fold_strided<<<elementwise_grid(cols), 256, 0, st>>>(p, cols, nch, 1, cols, out);
     SIMOPT_CHECK_LAUNCH("k_fold_strided");
-    SIMOPT_CUDA(cudaFreeAsync(p, st));
   }
   return SIMOPT_OK;
 }
@@ -522,5 +574,13 @@ extern "C" int simopt_scale_sub(void* stream, const double* x, double alpha, con
   if (n == 0) return SIMOPT_OK;
   k_scale_sub<<<elementwise_grid(n), 256, 0, as_stream(stream)>>>(x, alpha, y, n, out);
   SIMOPT_CHECK_LAUNCH("k_scale_sub");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_axpy_ptr(void* stream, const double* alpha, const double* x, const double* y,
+                               int64_t n, double* out) {
+  if (n == 0) return SIMOPT_OK;
+  k_axpy_ptr<<<elementwise_grid(n), 256, 0, as_stream(stream)>>>(alpha, x, y, n, out);
+  SIMOPT_CHECK_LAUNCH("k_axpy_ptr");
   return SIMOPT_OK;
 }

@@ -435,7 +435,7 @@ class MeanVarSampleSet:
         return self.samples - self.mean[None, :]
 
 
-def build_sample_set(samples, backend) -> MeanVarSampleSet:
+def build_sample_set(samples, backend, mean_out=None) -> MeanVarSampleSet:
     """colsum = tree matvec_t(X, 1); mean = colsum * (1/n) (tasks.py:56-64)."""
     x = mat_dev(samples)
     n = x.shape[0]
@@ -443,7 +443,7 @@ def build_sample_set(samples, backend) -> MeanVarSampleSet:
         raise InsufficientSamples("sample covariance needs at least 2 rows")
     ones = torch.ones(n, dtype=F64, device="cuda")
     col = backend.matvec_t_device(x, ones)
-    mean = empty(x.shape[1])
+    mean = empty(x.shape[1]) if mean_out is None else mean_out
     _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(col), 1.0 / n, None, col.numel(),
               _lib.ptr(mean))
     return MeanVarSampleSet(x, mean)
@@ -484,6 +484,8 @@ class MeanVarProblem:
         self.constraint = SimplexSlackSet(task.dimension)
         self.sample_set: MeanVarSampleSet | None = None
         self._x = None
+        self._mean = empty(task.dimension)
+        self._engines = {}
 
     @property
     def dimension(self) -> int:
@@ -497,7 +499,7 @@ class MeanVarProblem:
             self._x = empty(n_samples, d)
         x = sample_returns_device(self.task.spec, n_samples, stream, out=self._x,
                                   chunk=self.backend.chunk_size)
-        self.sample_set = build_sample_set(x, self.backend)
+        self.sample_set = build_sample_set(x, self.backend, mean_out=self._mean)
 
     def objective(self, w) -> float:
         return mv_objective(w, self.sample_set, self.backend)
@@ -516,104 +518,152 @@ class MeanVarProblem:
         return _mv_fw_run_device(self, config, backend, task_label, size, rep)
 
 
-def _mv_fw_run_device(prob: MeanVarProblem, config, backend, label, size, rep):
-    """Device-resident fw_run for the mean-variance task (frank_wolfe.py:91-121).
+class MvFwEngine:
+    """Device-resident Frank-Wolfe loop for the mean-variance task (frank_wolfe.py:91-121).
 
-    q = Xc w_{t+1} computed for the objective of step t is reused as the first
+    The M inner steps of an epoch are captured as a CUDA graph (one per iterate
+    ring, two rings alternating by epoch parity) and replayed every epoch: at C1
+    sizes a step is ~8 latency-bound kernels, so launch overhead would otherwise
+    dominate.  Everything that changes between epochs lives in device memory the
+    graph reads: the iterate ring (slot 0 = the epoch's first iterate), the step
+    sizes gamma (copied in before each replay) and the epoch-local trace buffers
+    (copied out after).  q = Xc w_{t+1} of the objective is reused as the first
     half of gradient(w_{t+1}) inside an epoch (same kernel, same bits).
     Feasibility: min(w) and an exact-tree sum (the reference uses numpy's
     pairwise np.sum, tasks.py:290; both are within 1e-15 of the exact sum, far
     inside the 1e-10 tolerance of that boolean test).
     """
-    d, M, K = prob.dimension, config.inner_iters, config.epochs
+
+    def __init__(self, prob: "MeanVarProblem", inner_iters: int, chunk: int, use_graph: bool = True):
+        self.prob, self.M, self.chunk, self.use_graph = prob, inner_iters, chunk, use_graph
+        d, M = prob.dimension, inner_iters
+        self.rings = [torch.zeros(M + 1, d, dtype=F64, device="cuda") for _ in range(2)]
+        self.g, self.gq, self.s, self.dirn = empty(d), empty(d), empty(d), empty(d)
+        self.gamma = empty(M)
+        self.status = torch.zeros(M, dtype=torch.int32, device="cuda")
+        self.wmin, self.wsum, self.quad, self.lin = empty(M), empty(M), empty(M), empty(M)
+        self.stamps = torch.zeros(M, dtype=torch.int64, device="cuda")
+        self.q = None
+        self.graphs = {}
+        self.warm = False
+        self.cstream = torch.cuda.Stream()  # capture stream: its library scratch is pre-warmed
+        self.lib = _lib.load()
+
+    def _steps(self, ws, x, mean, n_k):
+        """Enqueue the M inner steps on the current stream (captured or eager)."""
+        lib, sp, chunk, d, q = self.lib, _lib.stream_ptr(), self.chunk, self.prob.dimension, self.q
+        inv = 1.0 / (n_k - 1)
+        P = _lib.ptr
+        for m in range(self.M):
+            w_in, w_out = ws[m], ws[m + 1]
+            if m == 0:  # first gradient of the epoch: q = Xc w_kM
+                _lib.check(lib.simopt_matvec(sp, P(x), n_k, d, None, n_k, P(mean), P(w_in), chunk, P(q)))
+            _lib.check(lib.simopt_matvec_t(sp, P(x), n_k, d, None, n_k, P(mean), P(q), chunk, P(self.gq)))
+            _lib.check(lib.simopt_scale_sub(sp, P(self.gq), inv, P(mean), d, P(self.g)))
+            _lib.check(lib.simopt_lmo_simplex_slack(sp, P(self.g), d, P(self.s), P(self.status[m:])))
+            _lib.check(lib.simopt_axpy(sp, -1.0, P(w_in), P(self.s), d, P(self.dirn)))
+            _lib.check(lib.simopt_axpy_ptr(sp, P(self.gamma[m:]), P(self.dirn), P(w_in), d, P(w_out)))
+            _lib.check(lib.simopt_min_value(sp, P(w_out), d, P(self.wmin[m:])))
+            # objective(w_{t+1}); q is reused by the next gradient of this epoch
+            _lib.check(lib.simopt_matvec(sp, P(x), n_k, d, None, n_k, P(mean), P(w_out), chunk, P(q)))
+            _lib.check(lib.simopt_tree_sums2(sp, P(q), P(q), n_k, P(self.quad[m:]), P(w_out), P(mean), d,
+                                             P(self.lin[m:]), chunk))
+            _lib.check(lib.simopt_vec_sum(sp, P(w_out), d, chunk, P(self.wsum[m:])))
+            _lib.check(lib.simopt_timestamp(sp, P(self.stamps[m:])))
+
+    def run_epoch(self, k: int, n_k: int):
+        """Enqueue epoch k's M steps on ring k % 2 (slot 0 must hold the first iterate)."""
+        M = self.M
+        ss = self.prob.sample_set
+        x, mean = ss.samples, ss.mean
+        if self.q is None or self.q.numel() != n_k:
+            self.q = empty(n_k)
+            self.graphs = {}
+        ws = self.rings[k % 2]
+        self.status.zero_()
+        self.gamma.copy_(torch.tensor([fw_step_size(k, M, m) for m in range(M)], dtype=F64))
+        key = (k % 2, x.data_ptr(), mean.data_ptr(), n_k)
+        g = self.graphs.get(key)
+        if not self.use_graph:
+            self._steps(ws, x, mean, n_k)
+            return
+        if g is None and not self.warm:
+            # first epoch eager on the capture stream: lazy library setup and the
+            # stream's scratch happen outside any capture
+            self.cstream.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(self.cstream):
+                self._steps(ws, x, mean, n_k)
+            torch.cuda.current_stream().wait_stream(self.cstream)
+            self.warm = True
+            return
+        if g is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.cstream):
+                self._steps(ws, x, mean, n_k)
+            self.graphs[key] = g
+        g.replay()
+
+
+def _mv_fw_run_device(prob: MeanVarProblem, config, backend, label, size, rep):
+    M, K = config.inner_iters, config.epochs
     T = K * M
-    H = 2 * M + 1
-    ws = torch.zeros(H, d, dtype=F64, device="cuda")
-    g = empty(d)
-    s = empty(d)
-    dirn = empty(d)
-    status = torch.zeros(T + 1, dtype=torch.int32, device="cuda")
-    wmin = empty(T)
-    wsum = empty(T)
-    quad = empty(T)
-    lin = empty(T)
+    eng = prob._engines.get((M, backend.chunk_size))
+    if eng is None:  # kept on the problem: its captured epoch graphs are reused by later runs
+        eng = prob._engines[(M, backend.chunk_size)] = MvFwEngine(prob, M, backend.chunk_size)
+    eng.rings[0][0].zero_()
+    status = torch.zeros(T, dtype=torch.int32, device="cuda")
+    wmin, wsum, quad, lin = empty(T), empty(T), empty(T), empty(T)
     stamps = torch.zeros(T + 1, dtype=torch.int64, device="cuda")
     lib = _lib.load()
-    sp = _lib.stream_ptr()
-    chunk = backend.chunk_size
+    _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[T:])))
     trace = TraceBuilder()
-    host = {}
-    q = None
-    gq = None
+    n_of, events, host = [], [], {}
 
-    def check_epoch(k_done):
-        lo, hi = k_done * M, (k_done + 1) * M
-        st = to_host(status[lo:hi])
-        mn, sm = to_host(wmin[lo:hi]), to_host(wsum[lo:hi])
-        qd, ln = to_host(quad[lo:hi]), to_host(lin[lo:hi])
-        ts = to_host(stamps[lo:hi])
+    def check_epoch(k):
+        """Host validation of epoch k (its ring is intact until epoch k+2 is enqueued)."""
+        events[k].synchronize()
+        sl = slice(k * M, (k + 1) * M)
+        st, mn, sm, qd, ln, ts = (to_host(a[sl]) for a in (status, wmin, wsum, quad, lin, stamps))
         t0 = host.setdefault("t0", int(stamps[T].item()))
-        n_eff = host[("N", k_done)]
-        for i in range(M):
-            t = lo + i
-            if st[i] != 0:
-                return t, InvalidGradient("gradient contains NaN"), ws[t % H]
-            if not (mn[i] >= -FEAS_TOL and sm[i] <= 1.0 + FEAS_TOL):
-                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), ws[(t + 1) % H]
-            f = 0.5 * float(qd[i]) / (n_eff - 1) - float(ln[i])  # tasks.py:75
-            trace.append(t + 1, f, int(ts[i]) - t0)
+        ws = eng.rings[k % 2]
+        for m in range(M):
+            t = k * M + m
+            if st[m] != 0:
+                return InvalidGradient("gradient contains NaN"), ws[m]
+            if not (mn[m] >= -FEAS_TOL and sm[m] <= 1.0 + FEAS_TOL):
+                return InvalidConstraint(f"iterate infeasible at step {t + 1}"), ws[m + 1]
+            f = 0.5 * float(qd[m]) / (n_of[k] - 1) - float(ln[m])  # tasks.py:75
+            trace.append(t + 1, f, int(ts[m]) - t0)
         return None
 
-    def abort(t, exc, it):
+    def abort(exc, it):
         partial = trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(it))
         raise RunAborted(f"frank-wolfe run failed at step {len(trace) + 1}: {exc}", partial) from exc
 
-    _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[T:])))
-    events = []
     for k in range(K):
         n_k = config.epoch_sample_size(k)
-        host[("N", k)] = n_k
+        n_of.append(n_k)
+        if k >= 1:
+            eng.rings[k % 2][0].copy_(eng.rings[(k - 1) % 2][M])  # roll the iterate
         prob.resample(config.stream, n_k)
-        ss = prob.sample_set
-        x, mean = ss.samples, ss.mean
-        if q is None or q.numel() != n_k:
-            q = empty(n_k)
-        gq = empty(d) if gq is None else gq
-        inv = 1.0 / (n_k - 1)
-        for m in range(M):
-            t = k * M + m
-            w_in, w_out = ws[t % H], ws[(t + 1) % H]
-            if m == 0:  # first gradient of the epoch: q = Xc w_t
-                _lib.check(lib.simopt_matvec(sp, _lib.ptr(x), n_k, d, None, n_k, _lib.ptr(mean),
-                                             _lib.ptr(w_in), chunk, _lib.ptr(q)))
-            _lib.check(lib.simopt_matvec_t(sp, _lib.ptr(x), n_k, d, None, n_k, _lib.ptr(mean),
-                                           _lib.ptr(q), chunk, _lib.ptr(gq)))
-            _lib.check(lib.simopt_scale_sub(sp, _lib.ptr(gq), inv, _lib.ptr(mean), d, _lib.ptr(g)))
-            _lib.check(lib.simopt_lmo_simplex_slack(sp, _lib.ptr(g), d, _lib.ptr(s), _lib.ptr(status[t:])))
-            gamma = fw_step_size(k, M, m)
-            _lib.check(lib.simopt_axpy(sp, -1.0, _lib.ptr(w_in), _lib.ptr(s), d, _lib.ptr(dirn)))
-            _lib.check(lib.simopt_axpy(sp, gamma, _lib.ptr(dirn), _lib.ptr(w_in), d, _lib.ptr(w_out)))
-            _lib.check(lib.simopt_min_value(sp, _lib.ptr(w_out), d, _lib.ptr(wmin[t:])))
-            # objective(w_{t+1}); q is reused by the next gradient of this epoch
-            _lib.check(lib.simopt_matvec(sp, _lib.ptr(x), n_k, d, None, n_k, _lib.ptr(mean),
-                                         _lib.ptr(w_out), chunk, _lib.ptr(q)))
-            _lib.check(lib.simopt_tree_sums2(sp, _lib.ptr(q), _lib.ptr(q), n_k, _lib.ptr(quad[t:]),
-                                             _lib.ptr(w_out), _lib.ptr(mean), d, _lib.ptr(lin[t:]), chunk))
-            _lib.check(lib.simopt_vec_sum(sp, _lib.ptr(w_out), d, chunk, _lib.ptr(wsum[t:])))
-            _lib.check(lib.simopt_timestamp(sp, _lib.ptr(stamps[t:])))
+        eng.run_epoch(k, n_k)
+        sl = slice(k * M, (k + 1) * M)
+        for dst, src in ((status, eng.status), (wmin, eng.wmin), (wsum, eng.wsum),
+                         (quad, eng.quad), (lin, eng.lin), (stamps, eng.stamps)):
+            dst[sl].copy_(src)
         ev = torch.cuda.Event()
         ev.record()
         events.append(ev)
-        if k >= 1:
-            events[k - 1].synchronize()
+        if k >= 1:  # validate the previous epoch while this one runs
             bad = check_epoch(k - 1)
             if bad:
                 abort(*bad)
-    events[-1].synchronize()
     bad = check_epoch(K - 1)
     if bad:
         abort(*bad)
-    return trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(ws[T % H]))
+    return trace.build(label, size, backend.kind, rep, config.stream.seed,
+                       to_host(eng.rings[(K - 1) % 2][M]))
 
 
 # ---------------------------------------------------------------------------

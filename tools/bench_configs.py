@@ -32,7 +32,7 @@ def timed(fn, warm=3, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
-def meanvar(tag, d, n, M=25, epochs=2):
+def meanvar(tag, d, n, M=25, epochs=8):
     b = p.make_backend("cuda")
     prob = MeanVarProblem(gen_meanvar_instance(d, p.RngStream(42, 0)), b)
     s = p.RngStream(42, 2)
@@ -75,7 +75,7 @@ if __name__ == "__main__":
     if "c1" in which:
         meanvar("C1 meanvar d=1e3 N=1e4", 1000, 10_000)
     if "c4" in which:
-        meanvar("C4 meanvar d=2e4, per-GPU slice N=1.25e5 of N=1e6 on 8 GPUs", 20_000, 125_000, epochs=1)
+        meanvar("C4 meanvar d=2e4, per-GPU slice N=1.25e5 of N=1e6 on 8 GPUs", 20_000, 125_000, epochs=2)
     if "c3" in which:
         newton("C3 logistic Newton-CG d=1e3 N=1e6", 1000, 1_000_000)
     if "xtdx" in which:

@@ -241,6 +241,24 @@ int simopt_logistic_xtdx(void* stream, const double* x, const double* dw, int64_
 /* Same swap sequence on host memory for large b (u = the b uniforms). */
 int simopt_fisher_yates_host(int64_t n, int64_t b, const double* u, int64_t* out);
 
+/* Fused single pass over X (N x d row-major): t_r = x_r . v, wt_r = f(t_r), and
+ * col_out[j] = (sum_r x_rj wt_r) * col_scale [- center[j] for MV], in ONE read of X.
+ * Replaces each matvec + matvec_t pair of the reference (fast summation order, not
+ * the fixed tree; ~1e-15 relative):
+ *   SIMOPT_FUSED_MV       tasks.py:67-85  x = X - center; wt = t; *scalar_out = sum t^2
+ *   SIMOPT_FUSED_LR_GRAD  tasks.py:216-236 wt = sigmoid(t) - rowaux[r] (labels);
+ *                         dw_out[r] = c(1-c); *scalar_out = sum of loss terms
+ *   SIMOPT_FUSED_LR_HVP   tasks.py:239-253 wt = rowaux[r] (= c(1-c)) * t
+ * t_out / dw_out / col_out / scalar_out may be NULL; accumulate = 0 skips the column
+ * sums (row pass only).  Supports d <= 32768. */
+#define SIMOPT_FUSED_MV 0
+#define SIMOPT_FUSED_LR_GRAD 1
+#define SIMOPT_FUSED_LR_HVP 2
+int simopt_fused_rows(void* stream, int mode, const double* x, int64_t rows, int64_t cols,
+                      const double* v, const double* center, const double* rowaux,
+                      double col_scale, int accumulate, double* t_out, double* dw_out,
+                      double* col_out, double* scalar_out);
+
 #ifdef __cplusplus
 }
 #endif

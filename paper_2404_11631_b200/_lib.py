@@ -63,6 +63,7 @@ SIGNATURES = {
     "simopt_logistic_xtdx": [_vp, _vp, _vp, _i64, _i64, _vp],
     "simopt_cg_step1": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64],
     "simopt_cg_step2": [_vp, _vp, _vp, _vp, _vp, _i64],
+    "simopt_fused_rows": [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _d, _i32, _vp, _vp, _vp, _vp],
 }
 
 

@@ -17,6 +17,12 @@ blocks, with CPU restatements in oracle/oracle.py (newton_cg / newton_explicit):
 Every scalar of the CG recurrences stays on the device (simopt_cg_step1/2), so an
 iteration is one uninterrupted stream of kernels; the objective trace is read
 once at the end.
+
+``fused=True`` (the default) evaluates each gradient+loss and each HVP with the
+single-pass kernel of csrc/fused.cu -- one read of X instead of two, k_CG + 1
+reads per Newton iteration (SURVEY 8d's algorithmic bytes) -- in a fast
+summation order (trajectory within 1e-8 of the oracle).  ``fused=False`` keeps
+the exact fixed tree and the bit-identical trajectory.
 """
 from __future__ import annotations
 
@@ -24,6 +30,7 @@ import torch
 
 from . import _lib
 from ._tensors import F64, empty, to_host
+from .fused import LR_GRAD, LR_HVP, fused_rows
 from .records import RunRecord, TraceBuilder
 
 _SCALE, _MUL = 3, 4
@@ -74,6 +81,16 @@ class _Logistic:
                   self.d, _lib.ptr(out))
         return out
 
+    def fused_gradient(self, w, g_out, loss_sum_out):
+        """One pass: g = (1/N) X^T (sigmoid(Xw) - z), sum of loss terms, c(1-c) for the HVPs."""
+        fused_rows(LR_GRAD, self.data.features, w, rowaux=self.data.labels, col_scale=1.0 / self.N,
+                   col_out=g_out, scalar_out=loss_sum_out, dw_out=self.dw)
+
+    def fused_hvp(self, v, out):
+        """One pass: (1/N) X^T ((c(1-c)) * (X v))."""
+        return fused_rows(LR_HVP, self.data.features, v, rowaux=self.dw, col_scale=1.0 / self.N,
+                          col_out=out)
+
     def loss_sum_from_t(self, out):
         _lib.call("simopt_logistic_loss_terms", _lib.stream_ptr(), _lib.ptr(self.t),
                   _lib.ptr(self.data.labels), None, self.N, _lib.ptr(self.r))
@@ -102,7 +119,7 @@ def _cg(apply, g, n, cg_iters, dot, p):
     return p
 
 
-def _run(task, iterations, backend, step, label):
+def _run(task, iterations, backend, step, label, fused=False):
     data = task.data
     L = _Logistic(data, backend)
     n = L.d
@@ -114,15 +131,23 @@ def _run(task, iterations, backend, step, label):
     lib = _lib.load()
     _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[iterations:])))
     dot = lambda x, y, out: backend.dot_device(x, y, out=out)  # noqa: E731
-    L.xw(w)
+    if fused:
+        loss0 = empty(1)
+        L.fused_gradient(w, g, loss0)
+    else:
+        L.xw(w)
     for it in range(iterations):
-        L.gradient_from_t(g)
-        L.hvp_weights_from_t()
+        if not fused:
+            L.gradient_from_t(g)
+            L.hvp_weights_from_t()
         step(L, g, p, dot)
         _lib.call("simopt_vec_op", _lib.stream_ptr(), 1, 0.0, _lib.ptr(w), _lib.ptr(p), n,
                   _lib.ptr(w))                    # w = w + p
-        L.xw(w)                                   # shared by the loss and the next gradient
-        L.loss_sum_from_t(sums[it:])
+        if fused:  # loss at the new iterate + the next gradient and HVP weights, one pass
+            L.fused_gradient(w, g, sums[it:])
+        else:
+            L.xw(w)                               # shared by the loss and the next gradient
+            L.loss_sum_from_t(sums[it:])
         _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[it:])))
     trace = TraceBuilder()
     vals, ts = to_host(sums), to_host(stamps)
@@ -131,11 +156,11 @@ def _run(task, iterations, backend, step, label):
     return trace.build(label, n, backend.kind, 0, 0, to_host(w))
 
 
-def newton_cg(task, iterations: int, cg_iters: int, backend) -> RunRecord:
+def newton_cg(task, iterations: int, cg_iters: int, backend, fused: bool = True) -> RunRecord:
     """Newton-CG on the full-data logistic loss (BASELINE.json configs[2])."""
     def step(L, g, p, dot):
-        _cg(L.hvp, g, L.d, cg_iters, dot, p)
-    return _run(task, iterations, backend, step, "classification-newton-cg")
+        _cg(L.fused_hvp if fused else L.hvp, g, L.d, cg_iters, dot, p)
+    return _run(task, iterations, backend, step, "classification-newton-cg", fused)
 
 
 def logistic_hessian_device(data, dw, out=None) -> torch.Tensor:
@@ -147,7 +172,7 @@ def logistic_hessian_device(data, dw, out=None) -> torch.Tensor:
     return out
 
 
-def newton_explicit(task, iterations: int, cg_iters: int, backend) -> RunRecord:
+def newton_explicit(task, iterations: int, cg_iters: int, backend, fused: bool = True) -> RunRecord:
     """Newton with the explicit X^T D X Hessian and a CG solve (BASELINE.json configs[4])."""
     d = task.data.n_features
     H = torch.empty(d, d, dtype=F64, device="cuda")
@@ -155,4 +180,4 @@ def newton_explicit(task, iterations: int, cg_iters: int, backend) -> RunRecord:
     def step(L, g, p, dot):
         logistic_hessian_device(L.data, L.dw, out=H)
         _cg(lambda v, out: backend.matvec_device(H, v, out=out), g, d, cg_iters, dot, p)
-    return _run(task, iterations, backend, step, "classification-newton-explicit")
+    return _run(task, iterations, backend, step, "classification-newton-explicit", fused)

@@ -24,7 +24,7 @@ def _data(pkg, d, n, seed=42):
 def test_newton_cg_bitwise_vs_oracle(pkg):
     from paper_2404_11631_b200.newton import newton_cg
     task, x, z = _data(pkg, 50, 6000)
-    rec = newton_cg(task, 4, 10, pkg.make_backend("cuda"))
+    rec = newton_cg(task, 4, 10, pkg.make_backend("cuda"), fused=False)
     objs, w = orc.newton_cg(x, z, iterations=4, cg_iters=10)
     assert np.array_equal(rec.objectives, objs)
     assert np.array_equal(rec.final_iterate, w)
@@ -47,7 +47,7 @@ def test_xtdx_dmma_vs_oracle(pkg, d, n):
 def test_newton_explicit_vs_oracle(pkg):
     from paper_2404_11631_b200.newton import newton_explicit
     task, x, z = _data(pkg, 64, 8000, seed=9)
-    rec = newton_explicit(task, 3, 20, pkg.make_backend("cuda"))
+    rec = newton_explicit(task, 3, 20, pkg.make_backend("cuda"), fused=False)
     objs, w = orc.newton_explicit(x, z, iterations=3, cg_iters=20)
     np.testing.assert_allclose(rec.objectives, objs, rtol=1e-8)
     np.testing.assert_allclose(rec.final_iterate, w, rtol=1e-8, atol=1e-10)

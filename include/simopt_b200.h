@@ -68,6 +68,16 @@ int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t stream_id, 
                                uint64_t ctr_hi, int64_t n_samples, int64_t d, const double* mu,
                                const double* sigma, double* out);
 
+/* Rows [row_lo, row_hi) of the diag sample_returns draw at the stream position (the
+ * values the full n_samples x d draw has there): sample sharding, no RNG
+ * communication.  out is (row_hi - row_lo) x d. */
+int simopt_sample_returns_diag_rows(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                                    uint64_t ctr_hi, int64_t row_lo, int64_t row_hi, int64_t d,
+                                    const double* mu, const double* sigma, double* out);
+/* Elements [e_lo, e_hi) of simopt_bernoulli_half's draw (row shards of the features). */
+int simopt_bernoulli_half_range(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                                uint64_t ctr_hi, int64_t e_lo, int64_t e_hi, double* out);
+
 /* synth_classification features (sampling.py:246-255): out[i] = (u_i >= 0.5) as 0.0/1.0
  * for the n uniforms of the stream at the counter.  Caller advances by ceil(n/4). */
 int simopt_bernoulli_half(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
@@ -164,6 +174,8 @@ typedef struct NvState {
   double sval;            /* vertex value C/c_j* if g_j* < 0 else 0            */
   unsigned blocks_done;   /* last-block-done counter (kept 0 between launches) */
   unsigned pad;
+  double best_val;        /* LMO value g_j* (C/c_j*) of the vertex (shard exchange) */
+  int64_t pad2;
 } NvState;
 
 #define NV_FLAG_NAN_GRADIENT 1 /* InvalidGradient at this step's LMO (lmo.py:78-79) */
@@ -196,6 +208,16 @@ typedef struct NvIterArgs {
   int64_t part_capacity;
 } NvIterArgs;
 int simopt_nv_iter(void* stream, const NvIterArgs* args);
+
+/* Product-sharded LMO: every rank owns products [j0, j0 + d_local).
+ * pack: send[0..2] = {best_val, j* + j0, sval} of this rank's k_nv_iter argmin.
+ * apply: recv = the world ranks' packs in rank order; the global first-argmin
+ * (lexicographic (value, global index), i.e. np.argmin over the full vector, lmo.py:84)
+ * is written back: state->jstar = global j* - j0 if this rank owns it else -1,
+ * state->sval = its vertex value. */
+int simopt_nv_lmo_pack(void* stream, const NvState* state, int64_t j0, double* send);
+int simopt_nv_lmo_apply(void* stream, const double* recv, int64_t world, int64_t j0,
+                        int64_t d_local, NvState* state);
 
 /* newsvendor_cost_block (_kernels.py:210-223): out[j] = expected cost of product j. */
 int simopt_nv_cost_terms(void* stream, const double* x, const double* mu, const double* sigma,
@@ -241,6 +263,14 @@ int simopt_logistic_xtdx(void* stream, const double* x, const double* dw, int64_
 /* Same swap sequence on host memory for large b (u = the b uniforms). */
 int simopt_fisher_yates_host(int64_t n, int64_t b, const double* u, int64_t* out);
 
+/* Deterministic sharded reductions: matvec_t chunk partials before the
+ * fold, out[c*cols + j] (c < ceil(rows/chunk)); and the fold of nch gathered partial
+ * rows, out[j] = fold_pairwise(p[0*count+j], ..., p[(nch-1)*count+j]) (p clobbered).
+ * A dot's partials are matvec_t_partials of the n x 1 matrix x against y. */
+int simopt_matvec_t_partials(void* stream, const double* a, int64_t rows, int64_t cols,
+                             const double* center, const double* x, int64_t chunk, double* out);
+int simopt_fold_partials(void* stream, double* p, int64_t nch, int64_t count, double* out);
+
 /* Fused single pass over X (N x d row-major): t_r = x_r . v, wt_r = f(t_r), and
  * col_out[j] = (sum_r x_rj wt_r) * col_scale [- center[j] for MV], in ONE read of X.
  * Replaces each matvec + matvec_t pair of the reference (fast summation order, not
@@ -250,13 +280,14 @@ int simopt_fisher_yates_host(int64_t n, int64_t b, const double* u, int64_t* out
  *                         dw_out[r] = c(1-c); *scalar_out = sum of loss terms
  *   SIMOPT_FUSED_LR_HVP   tasks.py:239-253 wt = rowaux[r] (= c(1-c)) * t
  * t_out / dw_out / col_out / scalar_out may be NULL; accumulate = 0 skips the column
- * sums (row pass only).  Supports d <= 32768. */
+ * sums (row pass only); raw = 1 writes the plain column sums (no scale, no centering:
+ * the per-shard partial that a sample-sharded caller allreduces).  d <= 32768. */
 #define SIMOPT_FUSED_MV 0
 #define SIMOPT_FUSED_LR_GRAD 1
 #define SIMOPT_FUSED_LR_HVP 2
 int simopt_fused_rows(void* stream, int mode, const double* x, int64_t rows, int64_t cols,
                       const double* v, const double* center, const double* rowaux,
-                      double col_scale, int accumulate, double* t_out, double* dw_out,
+                      double col_scale, int accumulate, int raw, double* t_out, double* dw_out,
                       double* col_out, double* scalar_out);
 
 #ifdef __cplusplus

@@ -63,7 +63,14 @@ SIGNATURES = {
     "simopt_logistic_xtdx": [_vp, _vp, _vp, _i64, _i64, _vp],
     "simopt_cg_step1": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64],
     "simopt_cg_step2": [_vp, _vp, _vp, _vp, _vp, _i64],
-    "simopt_fused_rows": [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _d, _i32, _vp, _vp, _vp, _vp],
+    "simopt_fused_rows": [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _d, _i32, _i32, _vp, _vp, _vp,
+                          _vp],
+    "simopt_sample_returns_diag_rows": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _i64, _vp, _vp, _vp],
+    "simopt_bernoulli_half_range": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp],
+    "simopt_matvec_t_partials": [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp],
+    "simopt_fold_partials": [_vp, _vp, _i64, _i64, _vp],
+    "simopt_nv_lmo_pack": [_vp, _vp, _i64, _vp],
+    "simopt_nv_lmo_apply": [_vp, _vp, _i64, _i64, _i64, _vp],
 }
 
 

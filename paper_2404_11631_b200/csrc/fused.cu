@@ -338,8 +338,8 @@ int grid_for(KernelFn fn, int C, size_t smem) {
 
 extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_t rows, int64_t cols,
                                  const double* v, const double* center, const double* rowaux,
-                                 double col_scale, int accumulate, double* t_out, double* dw_out,
-                                 double* col_out, double* scalar_out) {
+                                 double col_scale, int accumulate, int raw, double* t_out,
+                                 double* dw_out, double* col_out, double* scalar_out) {
   cudaStream_t st = as_stream(stream);
   SIMOPT_REQUIRE(mode == SIMOPT_FUSED_MV || mode == SIMOPT_FUSED_LR_GRAD || mode == SIMOPT_FUSED_LR_HVP,
                  SIMOPT_E_CONFIG, "unknown fused mode %d", mode);
@@ -348,7 +348,7 @@ extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_
   SIMOPT_REQUIRE(mode == SIMOPT_FUSED_MV || rowaux != nullptr, SIMOPT_E_CONFIG, "row weights missing");
   if (cols == 0 || rows == 0) {  // empty sums: col_out = 0 * scale [- center], scalar 0
     k_fused_finish<<<(int)(cols > 0 ? ceil_div(cols, 256) : 1), 256, 0, st>>>(
-        nullptr, nullptr, 0, cols, col_scale, mode == SIMOPT_FUSED_MV ? center : nullptr,
+        nullptr, nullptr, 0, cols, col_scale, (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr,
         (accumulate && cols) ? col_out : nullptr, scalar_out);
     SIMOPT_CHECK_LAUNCH("k_fused_finish");
     return SIMOPT_OK;
@@ -389,8 +389,9 @@ extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_
   SIMOPT_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
   const int fgrid = (int)(a.accumulate ? ceil_div(cols, 256) : 1);
   k_fused_finish<<<fgrid < 1 ? 1 : fgrid, 256, 0, st>>>(
-      part, a.scal_part, ncl, cols, col_scale, mode == SIMOPT_FUSED_MV ? center : nullptr,
-      a.accumulate ? col_out : nullptr, scalar_out);
+      part, a.scal_part, ncl, cols, raw ? 1.0 : col_scale,
+      (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr, a.accumulate ? col_out : nullptr,
+      scalar_out);
   SIMOPT_CHECK_LAUNCH("k_fused_finish");
   return SIMOPT_OK;
 }

@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, 3)
     const double gj = a.g[r.i];
     st->jstar = r.i;
     st->sval = (gj < 0.0) ? a.budget / a.c[r.i] : 0.0;
+    st->best_val = r.v;
     st->blocks_done = 0;
   }
 }
@@ -401,6 +402,43 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   SIMOPT_REQUIRE(grid <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
   k_nv_iter<<<grid, kIterWarps * 32, 0, as_stream(stream)>>>(a);
   SIMOPT_CHECK_LAUNCH("k_nv_iter");
+  return SIMOPT_OK;
+}
+
+namespace {
+__global__ void k_nv_lmo_pack(const NvState* st, int64_t j0, double* send) {
+  send[0] = st->best_val;
+  send[1] = (double)(st->jstar + j0);  // exact: product indices < 2^53
+  send[2] = st->sval;
+}
+
+__global__ void k_nv_lmo_apply(const double* recv, int64_t world, int64_t j0, int64_t d_local,
+                               NvState* st) {
+  ArgMin b{recv[0], (int64_t)recv[1]};
+  double sv = recv[2];
+  for (int64_t r = 1; r < world; ++r) {
+    const ArgMin c{recv[3 * r], (int64_t)recv[3 * r + 1]};
+    const ArgMin m = amin(b, c);
+    if (m.i != b.i || m.v != b.v) sv = recv[3 * r + 2];
+    b = m;
+  }
+  st->jstar = (b.i >= j0 && b.i < j0 + d_local) ? b.i - j0 : -1;
+  st->sval = sv;
+  st->best_val = b.v;
+}
+}  // namespace
+
+extern "C" int simopt_nv_lmo_pack(void* stream, const NvState* state, int64_t j0, double* send) {
+  k_nv_lmo_pack<<<1, 1, 0, as_stream(stream)>>>(state, j0, send);
+  SIMOPT_CHECK_LAUNCH("k_nv_lmo_pack");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_nv_lmo_apply(void* stream, const double* recv, int64_t world, int64_t j0,
+                                   int64_t d_local, NvState* state) {
+  SIMOPT_REQUIRE(world >= 1, SIMOPT_E_CONFIG, "world size must be >= 1");
+  k_nv_lmo_apply<<<1, 1, 0, as_stream(stream)>>>(recv, world, j0, d_local, state);
+  SIMOPT_CHECK_LAUNCH("k_nv_lmo_apply");
   return SIMOPT_OK;
 }
 

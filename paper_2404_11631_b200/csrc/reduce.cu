@@ -540,6 +540,45 @@ extern "C" int simopt_matvec_t(void* stream, const double* a, int64_t lda_rows, 
   return SIMOPT_OK;
 }
 
+// Chunk partials of matvec_t without the fold: out[c * cols + j] = chain of row chunk c
+// (_kernels.py:124-156 before fold_pairwise).  Row-sharded ranks whose shards start on
+// chunk boundaries produce exactly the reference's partials for their chunks; gathered
+// in rank order and folded (simopt_fold_partials) they give the single-process result
+// bit for bit (SURVEY 8e deterministic mode).
+extern "C" int simopt_matvec_t_partials(void* stream, const double* a, int64_t rows, int64_t cols,
+                                        const double* center, const double* x, int64_t chunk,
+                                        double* out) {
+  SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1");
+  cudaStream_t st = as_stream(stream);
+  if (cols == 0 || rows == 0) return SIMOPT_OK;
+  const int64_t nch = ceil_div(rows, chunk);
+  SIMOPT_REQUIRE(nch < 65536, SIMOPT_E_CONFIG, "too many row chunks (%lld)", (long long)nch);
+  const dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)nch);
+  const bool v16 = vec16_ok(a, cols);
+  if (center) {
+    if (v16) k_matvec_t_cols<true, false, true><<<grid, 32, 0, st>>>(a, cols, nullptr, rows, center, x, chunk, nch, out);
+    else k_matvec_t_cols<true, false, false><<<grid, 32, 0, st>>>(a, cols, nullptr, rows, center, x, chunk, nch, out);
+  } else {
+    if (v16) k_matvec_t_cols<false, false, true><<<grid, 32, 0, st>>>(a, cols, nullptr, rows, center, x, chunk, nch, out);
+    else k_matvec_t_cols<false, false, false><<<grid, 32, 0, st>>>(a, cols, nullptr, rows, center, x, chunk, nch, out);
+  }
+  SIMOPT_CHECK_LAUNCH("k_matvec_t_cols<partials>");
+  return SIMOPT_OK;
+}
+
+// out[j] = fold_pairwise(p[0*count + j], ..., p[(nch-1)*count + j]); p is overwritten.
+extern "C" int simopt_fold_partials(void* stream, double* p, int64_t nch, int64_t count, double* out) {
+  if (count == 0) return SIMOPT_OK;
+  cudaStream_t st = as_stream(stream);
+  if (nch == 0) {
+    SIMOPT_CUDA(cudaMemsetAsync(out, 0, count * sizeof(double), st));
+    return SIMOPT_OK;
+  }
+  k_fold_strided<<<elementwise_grid(count), 256, 0, st>>>(p, count, nch, 1, count, out);
+  SIMOPT_CHECK_LAUNCH("k_fold_strided");
+  return SIMOPT_OK;
+}
+
 extern "C" int simopt_axpy(void* stream, double alpha, const double* x, const double* y, int64_t n,
                            double* out) {
   if (n == 0) return SIMOPT_OK;

@@ -29,18 +29,24 @@ __global__ void __launch_bounds__(256) k_uniform01(uint64_t seed, uint64_t sid, 
   }
 }
 
-// Normals (optionally affine per column: mu[j] + sigma[j]*z, j = e % d).
+// Normals e0 .. e0+n-1 of the stream (optionally affine per column: mu[j] + sigma[j]*z,
+// j = e % d), written to out[e - e0].  e0 > 0 addresses a row shard of a larger draw
+// (sample sharding): the values are those of the full draw.
 template <bool kAffine>
 __global__ void __launch_bounds__(256) k_normal(uint64_t seed, uint64_t sid, uint64_t clo,
-                                                uint64_t chi, int64_t n, int64_t d,
+                                                uint64_t chi, int64_t e0, int64_t n, int64_t d,
                                                 const double* __restrict__ mu,
                                                 const double* __restrict__ sigma,
                                                 double* __restrict__ out) {
   __shared__ double tab[SIMOPT_SINCOSTAB_N];
   load_sincostab(tab);
-  const int64_t nblk = (n + 3) >> 2;  // m = 2*ceil(n/2) uniforms -> ceil(m/4) == ceil(n/4) blocks
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk;
-       b += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t b0 = e0 >> 2;
+  const int64_t e1 = e0 + n;
+  const int64_t nblk = ((e1 + 3) >> 2) - b0;
+  const bool aligned = (e0 & 3) == 0;
+  for (int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; bi < nblk;
+       bi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = b0 + bi;
     double z[4];
     normals4(seed, sid, clo, chi, b, tab, z);
     const int64_t e = b << 2;
@@ -51,12 +57,13 @@ __global__ void __launch_bounds__(256) k_normal(uint64_t seed, uint64_t sid, uin
         if (++j == d) j = 0;
       }
     }
-    if (e + 4 <= n) {
-      double2* o = reinterpret_cast<double2*>(out + e);
+    if (aligned && e + 4 <= e1) {
+      double2* o = reinterpret_cast<double2*>(out + (e - e0));
       o[0] = make_double2(z[0], z[1]);
       o[1] = make_double2(z[2], z[3]);
     } else {
-      for (int k = 0; e + k < n; ++k) out[e + k] = z[k];
+      for (int k = 0; k < 4; ++k)
+        if (e + k >= e0 && e + k < e1) out[e + k - e0] = z[k];
     }
   }
 }
@@ -80,8 +87,8 @@ extern "C" int simopt_uniform01(void* stream, uint64_t seed, uint64_t sid, uint6
 extern "C" int simopt_standard_normal(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
                                       uint64_t chi, int64_t n, double* out) {
   SIMOPT_REQUIRE(n > 0, SIMOPT_E_EMPTY, "requested %lld normals", (long long)n);
-  k_normal<false><<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, n, 1,
-                                                                      nullptr, nullptr, out);
+  k_normal<false><<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, 0, n,
+                                                                      1, nullptr, nullptr, out);
   SIMOPT_CHECK_LAUNCH("k_normal");
   return SIMOPT_OK;
 }
@@ -93,9 +100,24 @@ extern "C" int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t 
                  "need at least 2 samples for a sample covariance, got %lld", (long long)n_samples);
   SIMOPT_REQUIRE(d >= 1, SIMOPT_E_DIMENSION, "empty return dimension");
   const int64_t n = n_samples * d;
-  k_normal<true><<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, n, d,
-                                                                     mu, sigma, out);
+  k_normal<true><<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, 0, n,
+                                                                     d, mu, sigma, out);
   SIMOPT_CHECK_LAUNCH("k_normal<affine>");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_sample_returns_diag_rows(void* stream, uint64_t seed, uint64_t sid,
+                                               uint64_t clo, uint64_t chi, int64_t row_lo,
+                                               int64_t row_hi, int64_t d, const double* mu,
+                                               const double* sigma, double* out) {
+  SIMOPT_REQUIRE(d >= 1, SIMOPT_E_DIMENSION, "empty return dimension");
+  SIMOPT_REQUIRE(0 <= row_lo && row_lo <= row_hi, SIMOPT_E_CONFIG, "bad row range");
+  const int64_t n = (row_hi - row_lo) * d;
+  if (n == 0) return SIMOPT_OK;
+  k_normal<true><<<grid_for((n + 3) / 4 + 1), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi,
+                                                                         row_lo * d, n, d, mu, sigma,
+                                                                         out);
+  SIMOPT_CHECK_LAUNCH("k_normal<affine,rows>");
   return SIMOPT_OK;
 }
 
@@ -103,14 +125,17 @@ namespace {
 // synth_classification features (sampling.py:246-255): x = (u >= 0.5), i.e. the MSB
 // of the Philox word, written as 0.0 / 1.0.
 __global__ void __launch_bounds__(256) k_bernoulli_half(uint64_t seed, uint64_t sid, uint64_t clo,
-                                                        uint64_t chi, int64_t n,
+                                                        uint64_t chi, int64_t e0, int64_t n,
                                                         double* __restrict__ out) {
-  const int64_t nblk = (n + 3) >> 2;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk;
-       b += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t b0 = e0 >> 2, e1 = e0 + n;
+  const int64_t nblk = ((e1 + 3) >> 2) - b0;
+  for (int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; bi < nblk;
+       bi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = b0 + bi;
     const phx4 w = philox4x64_10(stream_block_counter(clo, chi, b), seed, sid);
     const int64_t e = b << 2;
-    for (int k = 0; k < 4 && e + k < n; ++k) out[e + k] = (w.v[k] >> 63) ? 1.0 : 0.0;
+    for (int k = 0; k < 4; ++k)
+      if (e + k >= e0 && e + k < e1) out[e + k - e0] = (w.v[k] >> 63) ? 1.0 : 0.0;
   }
 }
 
@@ -126,8 +151,20 @@ __global__ void k_threshold(const double* __restrict__ x, double thr, int64_t n,
 extern "C" int simopt_bernoulli_half(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
                                      uint64_t chi, int64_t n, double* out) {
   SIMOPT_REQUIRE(n > 0, SIMOPT_E_EMPTY, "requested %lld draws", (long long)n);
-  k_bernoulli_half<<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, n, out);
+  k_bernoulli_half<<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, 0, n,
+                                                                         out);
   SIMOPT_CHECK_LAUNCH("k_bernoulli_half");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_bernoulli_half_range(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
+                                           uint64_t chi, int64_t e_lo, int64_t e_hi, double* out) {
+  SIMOPT_REQUIRE(0 <= e_lo && e_lo <= e_hi, SIMOPT_E_CONFIG, "bad element range");
+  const int64_t n = e_hi - e_lo;
+  if (n == 0) return SIMOPT_OK;
+  k_bernoulli_half<<<grid_for((n + 3) / 4 + 1), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi,
+                                                                             e_lo, n, out);
+  SIMOPT_CHECK_LAUNCH("k_bernoulli_half<range>");
   return SIMOPT_OK;
 }
 

@@ -18,11 +18,11 @@ MV, LR_GRAD, LR_HVP = 0, 1, 2
 
 def fused_rows(mode: int, x: torch.Tensor, v: torch.Tensor, *, center=None, rowaux=None,
                col_scale: float = 1.0, col_out=None, scalar_out=None, t_out=None, dw_out=None,
-               accumulate: bool = True):
+               accumulate: bool = True, raw: bool = False):
     """One read of x (N x d, fp64, row-major, on the device); see include/simopt_b200.h."""
     n, d = x.shape
     P = _lib.ptr
     _lib.call("simopt_fused_rows", _lib.stream_ptr(), int(mode), P(x), n, d, P(v), P(center),
-              P(rowaux), float(col_scale), 1 if accumulate else 0, P(t_out), P(dw_out),
+              P(rowaux), float(col_scale), 1 if accumulate else 0, 1 if raw else 0, P(t_out), P(dw_out),
               P(col_out), P(scalar_out))
     return col_out

@@ -47,54 +47,91 @@ class _Logistic:
 
     def __init__(self, data, backend):
         self.data, self.b = data, backend
-        self.N, self.d = data.n_samples, data.n_features
-        self.t = empty(self.N)       # X w
-        self.r = empty(self.N)       # residual / hvp weights scratch
-        self.dw = empty(self.N)      # c (1 - c)
-        self.tv = empty(self.N)
+        self.N, self.d = data.n_samples, data.n_features   # N: global rows
+        self.shard = getattr(data, "shard", None)
+        nl = max(data.features.shape[0], 1)                 # this rank's rows
+        self.nl = data.features.shape[0]
+        self.t = empty(nl)       # X w
+        self.r = empty(nl)       # residual / hvp weights scratch
+        self.dw = empty(nl)      # c (1 - c)
+        self.tv = empty(nl)
         self.gt = empty(self.d)
-        self.ones = torch.ones(self.N, dtype=F64, device="cuda")
+        self.buf = empty(self.d + 1)  # [column sums | side sum] allreduced across shards
+        self.ones = torch.ones(nl, dtype=F64, device="cuda")
+
+    def _col_sums(self, v, out):
+        """Fixed-tree X^T v over all rows (gathered chunk partials when sharded)."""
+        if self.shard is None:
+            return self.b.matvec_t_device(self.data.features, v, out=out)
+        from .tasks import sharded_matvec_t
+        return sharded_matvec_t(self.shard, self.data.features, v[:self.nl], self.N,
+                                self.b.chunk_size, out=out)
+
+    def _scale(self, src, out):
+        _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(src), 1.0 / self.N, None,
+                  self.d, _lib.ptr(out))
+        return out
 
     def xw(self, w):
-        return self.b.matvec_device(self.data.features, w, out=self.t)
+        if self.nl:
+            self.b.matvec_device(self.data.features, w, out=self.t[:self.nl])
+        return self.t
 
     def gradient_from_t(self, out):
         """(1/N) X^T (sigmoid(t) - z) given t = X w (tasks.py:228-236)."""
-        _lib.call("simopt_logistic_resid", _lib.stream_ptr(), _lib.ptr(self.t),
-                  _lib.ptr(self.data.labels), None, self.N, _lib.ptr(self.r))
-        self.b.matvec_t_device(self.data.features, self.r, out=self.gt)
-        _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(self.gt), 1.0 / self.N, None,
-                  self.d, _lib.ptr(out))
-        return out
+        if self.nl:
+            _lib.call("simopt_logistic_resid", _lib.stream_ptr(), _lib.ptr(self.t),
+                      _lib.ptr(self.data.labels), None, self.nl, _lib.ptr(self.r))
+        self._col_sums(self.r, self.gt)
+        return self._scale(self.gt, out)
 
     def hvp_weights_from_t(self):
         """c (1 - c) -- identical to the (c*(1-c)) factor of tasks.py:252."""
-        _lib.call("simopt_logistic_hvp_weights", _lib.stream_ptr(), _lib.ptr(self.t),
-                  _lib.ptr(self.ones), self.N, _lib.ptr(self.dw))
+        if self.nl:
+            _lib.call("simopt_logistic_hvp_weights", _lib.stream_ptr(), _lib.ptr(self.t),
+                      _lib.ptr(self.ones), self.nl, _lib.ptr(self.dw))
 
     def hvp(self, v, out):
         """(1/N) X^T ((c(1-c)) * (X v))."""
-        self.b.matvec_device(self.data.features, v, out=self.tv)
-        _vop(_MUL, 0.0, self.dw, self.tv, self.r)
-        self.b.matvec_t_device(self.data.features, self.r, out=self.gt)
-        _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(self.gt), 1.0 / self.N, None,
-                  self.d, _lib.ptr(out))
-        return out
+        if self.nl:
+            self.b.matvec_device(self.data.features, v, out=self.tv[:self.nl])
+            _vop(_MUL, 0.0, self.dw, self.tv, self.r)
+        self._col_sums(self.r, self.gt)
+        return self._scale(self.gt, out)
 
     def fused_gradient(self, w, g_out, loss_sum_out):
         """One pass: g = (1/N) X^T (sigmoid(Xw) - z), sum of loss terms, c(1-c) for the HVPs."""
-        fused_rows(LR_GRAD, self.data.features, w, rowaux=self.data.labels, col_scale=1.0 / self.N,
-                   col_out=g_out, scalar_out=loss_sum_out, dw_out=self.dw)
+        X = self.data.features
+        if self.shard is None:
+            fused_rows(LR_GRAD, X, w, rowaux=self.data.labels, col_scale=1.0 / self.N,
+                       col_out=g_out, scalar_out=loss_sum_out, dw_out=self.dw)
+            return
+        # per-shard raw sums, one allreduce of d+1 doubles
+        fused_rows(LR_GRAD, X, w, rowaux=self.data.labels, col_out=self.buf[:self.d],
+                   scalar_out=self.buf[self.d:], dw_out=self.dw, raw=True)
+        self.shard.allreduce_(self.buf)
+        self._scale(self.buf, g_out)
+        loss_sum_out[:1].copy_(self.buf[self.d:])
 
     def fused_hvp(self, v, out):
         """One pass: (1/N) X^T ((c(1-c)) * (X v))."""
-        return fused_rows(LR_HVP, self.data.features, v, rowaux=self.dw, col_scale=1.0 / self.N,
-                          col_out=out)
+        X = self.data.features
+        if self.shard is None:
+            return fused_rows(LR_HVP, X, v, rowaux=self.dw, col_scale=1.0 / self.N, col_out=out)
+        fused_rows(LR_HVP, X, v, rowaux=self.dw, col_out=self.buf[:self.d], raw=True)
+        self.shard.allreduce_(self.buf[:self.d])
+        return self._scale(self.buf, out)
 
     def loss_sum_from_t(self, out):
-        _lib.call("simopt_logistic_loss_terms", _lib.stream_ptr(), _lib.ptr(self.t),
-                  _lib.ptr(self.data.labels), None, self.N, _lib.ptr(self.r))
-        return self.b.vec_sum_device(self.r, out=out)
+        if self.nl:
+            _lib.call("simopt_logistic_loss_terms", _lib.stream_ptr(), _lib.ptr(self.t),
+                      _lib.ptr(self.data.labels), None, self.nl, _lib.ptr(self.r))
+        if self.shard is None:
+            return self.b.vec_sum_device(self.r, out=out)
+        from .tasks import sharded_matvec_t
+        # exact sum over shards: partials of the (n x 1) column r against ones (r * 1.0 == r)
+        return sharded_matvec_t(self.shard, self.r[:self.nl].view(-1, 1), self.ones[:self.nl],
+                                self.N, self.b.chunk_size, out=out[:1])
 
 
 def _cg(apply, g, n, cg_iters, dot, p):
@@ -164,11 +201,23 @@ def newton_cg(task, iterations: int, cg_iters: int, backend, fused: bool = True)
 
 
 def logistic_hessian_device(data, dw, out=None) -> torch.Tensor:
-    """H = (1/N) X^T diag(dw) X on the FP64 tensor pipe (tests/test_tasks.py:297-299 oracle)."""
+    """H = (1/N) X^T diag(dw) X on the FP64 tensor pipe (tests/test_tasks.py:297-299 oracle).
+
+    Row-sharded data: each rank's (1/N_loc) X_loc^T D X_loc is weighted by N_loc/N and
+    summed over ranks with one allreduce of the d x d matrix."""
     d = data.n_features
     out = torch.empty(d, d, dtype=F64, device="cuda") if out is None else out
-    _lib.call("simopt_logistic_xtdx", _lib.stream_ptr(), _lib.ptr(data.features), _lib.ptr(dw),
-              data.n_samples, d, _lib.ptr(out))
+    nl = data.features.shape[0]
+    shard = getattr(data, "shard", None)
+    if nl:
+        _lib.call("simopt_logistic_xtdx", _lib.stream_ptr(), _lib.ptr(data.features), _lib.ptr(dw),
+                  nl, d, _lib.ptr(out))
+    else:
+        out.zero_()
+    if shard is not None:
+        if nl:
+            out.mul_(nl / data.n_samples)
+        shard.allreduce_(out)
     return out
 
 

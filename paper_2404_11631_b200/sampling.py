@@ -185,12 +185,20 @@ def sample_indices(n: int, b: int, stream: RngStream) -> np.ndarray:
 class ClassificationData:
     """Synthetic binary-feature dataset on the device; labels carry the noise (sampling.py:212-226)."""
 
-    features: torch.Tensor  # N x n float64, entries exactly 0.0 / 1.0
+    features: torch.Tensor  # N x n float64, entries exactly 0.0 / 1.0 (this rank's rows)
     labels: torch.Tensor    # N float64
     true_weights: torch.Tensor
+    shard: object = None    # ShardGroup when the rows are split across ranks
+    row_offset: int = 0     # first global row held here
+    total_rows: int | None = None
 
     @property
     def n_samples(self) -> int:
+        """Global row count N (the 1/N of every full-data average)."""
+        return self.features.shape[0] if self.total_rows is None else self.total_rows
+
+    @property
+    def local_rows(self) -> int:
         return self.features.shape[0]
 
     @property
@@ -199,7 +207,7 @@ class ClassificationData:
 
 
 def synth_classification(n_features: int, stream: RngStream, backend=None,
-                         n_rows: int | None = None) -> ClassificationData:
+                         n_rows: int | None = None, shard=None) -> ClassificationData:
     """sampling.py:229-265, with the row count generalised (reference: n_rows = 30*n).
 
     X[i,j] = [u >= 0.5] is the MSB of the Philox word (written directly as 0.0/1.0);
@@ -210,6 +218,8 @@ def synth_classification(n_features: int, stream: RngStream, backend=None,
     if n_features < 2:
         raise ConfigurationError(f"need at least 2 features, got {n_features}")
     n_rows = 30 * n_features if n_rows is None else int(n_rows)
+    if shard is not None:
+        return _synth_classification_shard(n_features, stream, n_rows, shard)
     total = n_rows * n_features
     x = empty(n_rows, n_features)
     _lib.call("simopt_bernoulli_half", _lib.stream_ptr(), *stream.words(), total, _lib.ptr(x))
@@ -231,3 +241,39 @@ def synth_classification(n_features: int, stream: RngStream, backend=None,
     flip = sample_indices_device(n_rows, n_rows // 10, stream)
     labels[flip] = 1.0 - labels[flip]  # exact: labels are 0.0/1.0
     return ClassificationData(features=x, labels=labels, true_weights=w_true)
+
+
+def _synth_classification_shard(n_features, stream, n_rows, shard, chunk=4096):
+    """Rows [lo, hi) of synth_classification (chunk-aligned), identical to the one-process
+    instance: features are elements [lo*n, hi*n) of the same Philox draw, scores are
+    row-local fixed-tree dots, the median is taken over the allgathered scores, and the
+    replicated sample_indices flips are applied where they fall in [lo, hi)."""
+    lo, hi = shard.range(n_rows, chunk)
+    nl = hi - lo
+    total = n_rows * n_features
+    x = empty(max(nl, 0), n_features)
+    _lib.call("simopt_bernoulli_half_range", _lib.stream_ptr(), *stream.words(), lo * n_features,
+              hi * n_features, _lib.ptr(x))
+    stream.advance(total)
+    w_true = standard_normal_device(stream, n_features)
+    scores = empty(max(nl, 1))
+    if nl:
+        _lib.call("simopt_matvec", _lib.stream_ptr(), _lib.ptr(x), nl, n_features, None, nl,
+                  None, _lib.ptr(w_true), chunk, _lib.ptr(scores))
+    counts = [b - a for a, b in shard.ranges(n_rows, chunk)]
+    allsc = shard.allgather_rows(scores[:nl].view(-1, 1), counts).view(-1)
+    srt = torch.sort(allsc).values
+    h = n_rows // 2
+    if n_rows % 2:
+        median = float(srt[h].item())
+    else:
+        median = (float(srt[h - 1].item()) + float(srt[h].item())) / 2.0
+    labels = empty(max(nl, 1))
+    if nl:
+        _lib.call("simopt_threshold", _lib.stream_ptr(), _lib.ptr(scores), median, nl,
+                  _lib.ptr(labels))
+    flip = sample_indices_device(n_rows, n_rows // 10, stream)
+    mine = flip[(flip >= lo) & (flip < hi)] - lo
+    labels[mine] = 1.0 - labels[mine]
+    return ClassificationData(features=x, labels=labels[:nl], true_weights=w_true, shard=shard,
+                              row_offset=lo, total_rows=n_rows)

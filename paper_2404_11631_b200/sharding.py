@@ -1,4 +1,4 @@
-"""Host logic for sample/product sharding across ranks (one process per GPU).
+"""Sample/product sharding across ranks (one process per GPU).
 
 Reference anchor: the fixed tree of sobench/_kernels.py:1-42 (chunk partials
 folded pairwise in index order).  If every rank owns whole 4096-chunks, the
@@ -12,6 +12,76 @@ from __future__ import annotations
 
 import torch
 import torch.distributed as dist
+
+_U128 = (1 << 128) - 1
+
+
+class ShardGroup:
+    """The ranks that split one solver run's sample (or product) axis.
+
+    Collectives go through ``torch.distributed``: NCCL over NVLink/NVSwitch on a
+    GPU box (device tensors, issued on the current CUDA stream), or gloo (tensors
+    staged through host memory -- the CPU tests and the two-processes-on-one-GPU
+    parity tests).  Every rank runs the same program, so collectives are issued in
+    the same order everywhere.
+    """
+
+    def __init__(self, group=None):
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed is not initialised")
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def range(self, n: int, align: int = 1) -> tuple:
+        return shard_range(n, self.world, self.rank, align)
+
+    def ranges(self, n: int, align: int = 1) -> list:
+        return [shard_range(n, self.world, r, align) for r in range(self.world)]
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        """In-place sum over ranks."""
+        if self.world == 1:
+            return t
+        if self.nccl:
+            dist.all_reduce(t, group=self.group)
+            return t
+        h = t.detach().cpu()
+        dist.all_reduce(h, group=self.group)
+        t.copy_(h)
+        return t
+
+    def allgather(self, t: torch.Tensor) -> torch.Tensor:
+        """[world, *t.shape]: every rank's tensor, in rank order (equal shapes)."""
+        t = t.contiguous()
+        if self.world == 1:
+            return t.unsqueeze(0)
+        if self.nccl:
+            out = torch.empty((self.world, *t.shape), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t, group=self.group)
+            return out
+        h = t.detach().cpu()
+        parts = [torch.empty_like(h) for _ in range(self.world)]
+        dist.all_gather(parts, h, group=self.group)
+        return torch.stack(parts).to(t.device)
+
+    def allgather_rows(self, t: torch.Tensor, counts: list) -> torch.Tensor:
+        """Concatenate each rank's first counts[r] rows (uneven shards, padded transfer)."""
+        cap = max(max(counts), 1)
+        pad = torch.zeros((cap, *t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        g = self.allgather(pad)
+        return torch.cat([g[r, : counts[r]] for r in range(self.world)])
+
+    def barrier(self):
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+
+def shifted_counter(counter: int, blocks: int) -> int:
+    """Stream counter of a shard whose draws start `blocks` Philox blocks in (mod 2^128)."""
+    return (counter + blocks) & _U128
 
 
 def shard_range(n: int, world: int, rank: int, align: int = 4096) -> tuple:

@@ -117,14 +117,18 @@ class NewsvendorTask:
 class _NvDevice:
     """Device copies of a NewsvendorTask plus the epoch's keyed demand layout."""
 
-    def __init__(self, task: NewsvendorTask):
-        self.d = task.dimension
-        self.mu = to_dev(task.demand_mean)
-        self.sigma = to_dev(task.demand_std)
-        self.k = to_dev(task.unit_cost)
-        self.h = to_dev(task.holding_cost)
-        self.v = to_dev(task.selling_value)
-        self.c = to_dev(task.budget_costs)
+    def __init__(self, task: NewsvendorTask, j0: int = 0, j1: int | None = None):
+        # products [j0, j1) (the whole task unless product-sharded)
+        j1 = task.dimension if j1 is None else j1
+        self.j0, self.d_total = j0, task.dimension
+        self.d = j1 - j0
+        sl = slice(j0, j1)
+        self.mu = to_dev(task.demand_mean[sl])
+        self.sigma = to_dev(task.demand_std[sl])
+        self.k = to_dev(task.unit_cost[sl])
+        self.h = to_dev(task.holding_cost[sl])
+        self.v = to_dev(task.selling_value[sl])
+        self.c = to_dev(task.budget_costs[sl])
         self.budget = task.budget
         self.S = None
         self.keys = None
@@ -148,10 +152,20 @@ class _NvDevice:
         if S < 1:
             raise InsufficientSamples("need at least one demand sample per product")
         self.ensure_layout(S)
-        self.draw = stream.words()
+        # product j's draws are normals j*S .. j*S+S-1 of standard_normal(d*S): a shard
+        # starting at product j0 (j0*S % 4 == 0) is the same draw with the counter
+        # moved j0*S/4 Philox blocks on -- no RNG communication
+        from .sharding import shifted_counter
+        if self.j0:
+            if (self.j0 * S) % 4:
+                raise ConfigurationError("product shard must start on a Philox block")
+            self.draw = RngStream(stream.seed, stream.stream_id,
+                                  shifted_counter(stream.counter, self.j0 * S // 4)).words()
+        else:
+            self.draw = stream.words()
         _lib.call("simopt_nv_resample", _lib.stream_ptr(), *self.draw, self.d, S,
                   _lib.ptr(self.keys), _lib.ptr(self.off))
-        stream.advance(2 * ((self.d * S + 1) // 2))
+        stream.advance(2 * ((self.d_total * S + 1) // 2))
 
     def counts(self, x: torch.Tensor) -> torch.Tensor:
         out = torch.empty(self.d, dtype=torch.int64, device="cuda")
@@ -173,10 +187,14 @@ class NewsvendorProblem:
 
     name = "newsvendor"
 
-    def __init__(self, task: NewsvendorTask, backend):
+    def __init__(self, task: NewsvendorTask, backend, shard=None):
         self.task = task
         self.backend = backend
-        self.dev = _NvDevice(task)
+        # product sharding: products are independent; each FW step exchanges only the
+        # per-rank LMO candidates (allgather of 3 doubles per rank)
+        self.shard = shard
+        j0, j1 = (0, task.dimension) if shard is None else shard.range(task.dimension, 4)
+        self.dev = _NvDevice(task, j0, j1)
         self._stream = None
 
     @property
@@ -187,7 +205,13 @@ class NewsvendorProblem:
     def resample(self, stream: RngStream, n_samples: int) -> None:
         self.dev.resample(stream, n_samples)
 
+    def _whole(self):
+        if self.shard is not None:
+            raise ConfigurationError("a product-sharded newsvendor runs through fw_run's device "
+                                     "loop; per-call gradient/objective need the whole task")
+
     def gradient(self, x):
+        self._whole()
         xd = vec_dev(x)
         cnt = self.dev.counts(xd)
         g = empty(self.dev.d)
@@ -201,6 +225,7 @@ class NewsvendorProblem:
                                  self.task.budget)
 
     def check_feasible(self, x) -> bool:
+        self._whole()
         xd = vec_dev(x)
         if bool((xd < -FEAS_TOL).any()):
             return False
@@ -242,7 +267,7 @@ class NvFwEngine:
         self.spent = empty(T)
         self.objs = empty(T)
         self.stamps = torch.zeros(T + 1, dtype=torch.int64, device="cuda")
-        self.state = torch.zeros(4, dtype=torch.int64, device="cuda")  # NvState (32 bytes)
+        self.state = torch.zeros(6, dtype=torch.int64, device="cuda")  # NvState (48 bytes)
         self.part_v = empty(_NV_PART_CAPACITY)
         self.part_i = torch.empty(_NV_PART_CAPACITY, dtype=torch.int64, device="cuda")
         a = NvIterArgs()
@@ -254,6 +279,11 @@ class NvFwEngine:
         a.part_v, a.part_i, a.part_capacity = (self.part_v.data_ptr(), self.part_i.data_ptr(),
                                                _NV_PART_CAPACITY)
         self.args = a
+        self.shard = prob.shard
+        if self.shard is not None:
+            self.send = empty(3)
+            # per epoch: spent[M] | objs[M] | nan flags[M+1] | negative flags[M+1]
+            self.red = empty(2, 4 * M + 2)  # double-buffered by epoch parity
         self.lib = _lib.load()
         self.t0 = None
         self.resample_events = []
@@ -284,6 +314,7 @@ class NvFwEngine:
         a.terms = None  # objective terms are formed on the side stream
         a.do_update, a.do_grad, a.step, a.grad_step, a.gamma = 0, 1, t0, t0, 0.0
         _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
+        self._exchange(sp)
         for m in range(M):
             t = t0 + m
             slot = (t + 1) % H
@@ -295,6 +326,8 @@ class NvFwEngine:
             a.gamma = fw_step_size(k, M, m)
             a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), t, t + 1
             _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
+            if m + 1 < M:
+                self._exchange(sp)
             ev = torch.cuda.Event()
             ev.record(main)
             self.side.wait_event(ev)
@@ -311,7 +344,30 @@ class NvFwEngine:
             done = torch.cuda.Event()
             done.record(self.side)
             self.side_done[t] = done
+        if self.shard is not None:
+            # epoch totals over the product shards, one allreduce after the side work
+            with torch.cuda.stream(self.side):
+                r, lo, hi = self.red[k % 2], t0, t0 + M
+                r[:M].copy_(self.spent[lo:hi])
+                r[M:2 * M].copy_(self.objs[lo:hi])
+                f = self.flags[lo:hi + 1]
+                r[2 * M:3 * M + 1].copy_((f & NV_FLAG_NAN_GRADIENT).to(F64))
+                r[3 * M + 1:].copy_((f & NV_FLAG_NEGATIVE).to(F64))
+                self.shard.allreduce_(r)
+                done = torch.cuda.Event()
+                done.record(self.side)
+            self.side_done[t0 + M - 1] = done
         self.epoch_done[k] = self.side_done[t0 + M - 1]
+
+    def _exchange(self, sp):
+        """Global LMO vertex over product shards: allgather the per-rank argmins."""
+        if self.shard is None:
+            return
+        lib, P = self.lib, _lib.ptr
+        _lib.check(lib.simopt_nv_lmo_pack(sp, P(self.state), self.dev.j0, P(self.send)))
+        recv = self.shard.allgather(self.send)
+        _lib.check(lib.simopt_nv_lmo_apply(sp, P(recv), self.shard.world, self.dev.j0, self.dev.d,
+                                           P(self.state)))
 
     def finish(self):
         """Join the side stream into the caller's stream."""
@@ -322,23 +378,34 @@ class NvFwEngine:
         M, H = self.M, self.H
         self.epoch_done[k].synchronize()
         lo, hi = k * M, (k + 1) * M
-        fl = to_host(self.flags[lo:hi + 1])
-        sp_ = to_host(self.spent[lo:hi])
-        ob = to_host(self.objs[lo:hi])
+        if self.shard is None:
+            fl = to_host(self.flags[lo:hi + 1])
+            sp_ = to_host(self.spent[lo:hi])
+            ob = to_host(self.objs[lo:hi])
+        else:
+            r = to_host(self.red[k % 2])
+            sp_, ob = r[:M], r[M:2 * M]
+            fl = ((r[2 * M:3 * M + 1] > 0) * NV_FLAG_NAN_GRADIENT
+                  + (r[3 * M + 1:] > 0) * NV_FLAG_NEGATIVE).astype(np.int32)
         ts = to_host(self.stamps[lo:hi])
         if self.t0 is None:
             self.t0 = int(self.stamps[self.T].item())
         for i in range(M):
             t = lo + i
             if fl[i] & NV_FLAG_NAN_GRADIENT:
-                return t, InvalidGradient("gradient contains NaN"), self.xs[t % H]
+                return t, InvalidGradient("gradient contains NaN"), self.iterate(t)
             if (fl[i] & NV_FLAG_NEGATIVE) or not sp_[i] <= self.dev.budget * (1.0 + FEAS_TOL):
-                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), self.xs[(t + 1) % H]
+                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), self.iterate(t + 1)
             trace.append(t + 1, float(ob[i]), int(ts[i]) - self.t0)
         return None
 
     def iterate(self, t: int) -> torch.Tensor:
-        return self.xs[t % self.H]
+        """Full iterate after step t (the product slices gathered when sharded)."""
+        x = self.xs[t % self.H]
+        if self.shard is None:
+            return x
+        counts = [b - a for a, b in self.shard.ranges(self.dev.d_total, 4)]
+        return self.shard.allgather_rows(x.view(-1, 1), counts).view(-1)
 
 
 def _nv_fw_run_device(prob: "NewsvendorProblem", config, backend, label, size, rep):
@@ -426,10 +493,10 @@ class MeanVarSampleSet:
     when materialising it (tasks.py:63).  ``centered`` materialises on demand.
     """
 
-    def __init__(self, samples: torch.Tensor, mean: torch.Tensor):
-        self.samples = samples
+    def __init__(self, samples: torch.Tensor, mean: torch.Tensor, count: int | None = None):
+        self.samples = samples  # this rank's rows when sharded
         self.mean = mean
-        self.count = samples.shape[0]
+        self.count = samples.shape[0] if count is None else count  # global N
 
     @property
     def centered(self) -> torch.Tensor:
@@ -474,15 +541,47 @@ def mv_gradient(w, ss: MeanVarSampleSet, backend):
     return like_input(w, g)
 
 
+# --- deterministic sample sharding -------------------------------
+# A rank owns rows [lo, hi) with lo, hi on chunk boundaries, so its matvec_t chunk
+# partials ARE the reference's partials of those chunks; gathered in rank order and
+# folded they give the single-process fixed-tree result bit for bit at any world size.
+def _chunk_counts(shard, n, chunk):
+    return [-(-(hi - lo) // chunk) for lo, hi in shard.ranges(n, chunk)]
+
+
+def sharded_matvec_t(shard, a_loc, x_loc, n_total, chunk, center=None, out=None):
+    """Fixed-tree a^T x over row shards (backend.py:128-141 across ranks)."""
+    cols = a_loc.shape[1]
+    nloc = -(-a_loc.shape[0] // chunk)
+    part = empty(max(nloc, 1), cols)
+    if nloc:
+        _lib.call("simopt_matvec_t_partials", _lib.stream_ptr(), _lib.ptr(a_loc), a_loc.shape[0],
+                  cols, _lib.ptr(center), _lib.ptr(x_loc), chunk, _lib.ptr(part))
+    counts = _chunk_counts(shard, n_total, chunk)
+    allp = shard.allgather_rows(part[:nloc], counts)
+    out = empty(cols) if out is None else out
+    _lib.call("simopt_fold_partials", _lib.stream_ptr(), _lib.ptr(allp), allp.shape[0], cols,
+              _lib.ptr(out))
+    return out
+
+
+def sharded_dot(shard, x_loc, y_loc, n_total, chunk, out=None):
+    """Fixed-tree dot over row shards (dot partials = matvec_t of the n x 1 matrix)."""
+    return sharded_matvec_t(shard, x_loc.view(-1, 1), y_loc, n_total, chunk, out=out)
+
+
 class MeanVarProblem:
     """Mean-variance task wired for the FW engine (tasks.py:261-290)."""
 
     name = "meanvar"
 
-    def __init__(self, task: MeanVarTask, backend, fused: bool = False):
+    def __init__(self, task: MeanVarTask, backend, fused: bool = False, shard=None):
         self.task = task
         self.backend = backend
         self.fused = fused  # device FW loop: single-pass fused gradient (csrc/fused.cu)
+        # sample sharding: this rank draws and reduces only its scenario rows
+        # [lo, hi) (chunk-aligned), with one allreduce / allgather per reduction
+        self.shard = shard
         self.constraint = SimplexSlackSet(task.dimension)
         self.sample_set: MeanVarSampleSet | None = None
         self._x = None
@@ -496,6 +595,9 @@ class MeanVarProblem:
     def resample(self, stream: RngStream, n_samples: int) -> None:
         from .sampling import sample_returns_device
         d = self.dimension
+        if self.shard is not None:
+            self._resample_shard(stream, n_samples)
+            return
         if self._x is None or self._x.shape[0] != n_samples:
             self._x = None
             self._x = empty(n_samples, d)
@@ -503,11 +605,46 @@ class MeanVarProblem:
                                   chunk=self.backend.chunk_size)
         self.sample_set = build_sample_set(x, self.backend, mean_out=self._mean)
 
+    def _resample_shard(self, stream: RngStream, n_samples: int) -> None:
+        """Rows [lo, hi) of sample_returns (no RNG communication) + the exact global mean."""
+        spec, d, chunk = self.task.spec, self.dimension, self.backend.chunk_size
+        if n_samples < 2:
+            raise InsufficientSamples(f"need at least 2 samples for a sample covariance, got {n_samples}")
+        if spec.diag_std is None:
+            raise ConfigurationError("sample sharding supports the diagonal return model")
+        lo, hi = self.shard.range(n_samples, chunk)
+        if self._x is None or self._x.shape[0] != hi - lo:
+            self._x = None
+            self._x = empty(max(hi - lo, 0), d)
+        mu, sd = vec_dev(spec.mean), vec_dev(spec.diag_std)
+        _lib.call("simopt_sample_returns_diag_rows", _lib.stream_ptr(), *stream.words(), lo, hi, d,
+                  _lib.ptr(mu), _lib.ptr(sd), _lib.ptr(self._x))
+        stream.advance(2 * ((n_samples * d + 1) // 2))
+        ones = torch.ones(max(hi - lo, 1), dtype=F64, device="cuda")
+        col = sharded_matvec_t(self.shard, self._x, ones, n_samples, chunk)
+        _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(col), 1.0 / n_samples, None, d,
+                  _lib.ptr(self._mean))
+        self.sample_set = MeanVarSampleSet(self._x, self._mean, count=n_samples)
+
     def objective(self, w) -> float:
-        return mv_objective(w, self.sample_set, self.backend)
+        if self.shard is None:
+            return mv_objective(w, self.sample_set, self.backend)
+        ss, chunk, wd = self.sample_set, self.backend.chunk_size, vec_dev(w)
+        q = self.backend.matvec_device(ss.samples, wd, center=ss.mean)
+        quad = float(sharded_dot(self.shard, q, q, ss.count, chunk).item())
+        lin = float(self.backend.dot_device(wd, ss.mean).item())
+        return 0.5 * quad / (ss.count - 1) - lin
 
     def gradient(self, w):
-        return mv_gradient(w, self.sample_set, self.backend)
+        if self.shard is None:
+            return mv_gradient(w, self.sample_set, self.backend)
+        ss, chunk, wd = self.sample_set, self.backend.chunk_size, vec_dev(w)
+        q = self.backend.matvec_device(ss.samples, wd, center=ss.mean)
+        gq = sharded_matvec_t(self.shard, ss.samples, q, ss.count, chunk, center=ss.mean)
+        g = empty(gq.numel())
+        _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(gq), 1.0 / (ss.count - 1),
+                  _lib.ptr(ss.mean), gq.numel(), _lib.ptr(g))
+        return like_input(w, g)
 
     def lmo(self, g):
         return lmo_simplex_slack(g)
@@ -552,6 +689,7 @@ class MvFwEngine:
         self.wmin, self.wsum, self.quad, self.lin = empty(M), empty(M), empty(M), empty(M)
         self.stamps = torch.zeros(M, dtype=torch.int64, device="cuda")
         self.q = None
+        self.red_buf = empty(d + 1)
         self.graphs = {}
         self.warm = False
         self.cstream = torch.cuda.Stream()  # capture stream: its library scratch is pre-warmed
@@ -562,6 +700,9 @@ class MvFwEngine:
         lib, sp, chunk, d, q = self.lib, _lib.stream_ptr(), self.chunk, self.prob.dimension, self.q
         inv = 1.0 / (n_k - 1)
         P = _lib.ptr
+        if self.prob.shard is not None:
+            self._sharded_steps(ws, x, mean, n_k, inv)
+            return
         if self.prob.fused:
             self._fused_steps(ws, x, mean, n_k, inv)
             return
@@ -579,6 +720,51 @@ class MvFwEngine:
             _lib.check(lib.simopt_matvec(sp, P(x), n_k, d, None, n_k, P(mean), P(w_out), chunk, P(q)))
             _lib.check(lib.simopt_tree_sums2(sp, P(q), P(q), n_k, P(self.quad[m:]), P(w_out), P(mean), d,
                                              P(self.lin[m:]), chunk))
+            _lib.check(lib.simopt_vec_sum(sp, P(w_out), d, chunk, P(self.wsum[m:])))
+            _lib.check(lib.simopt_timestamp(sp, P(self.stamps[m:])))
+
+    def _sharded_steps(self, ws, x, mean, n_k, inv):
+        """Row-sharded step: exact mode gathers chunk partials (bit-identical to one
+        GPU); fused mode allreduces [X_loc^T q_loc | |q_loc|^2] (d+1 doubles)."""
+        lib, sp, chunk, d, sh = self.lib, _lib.stream_ptr(), self.chunk, self.prob.dimension, self.prob.shard
+        P = _lib.ptr
+        nl = x.shape[0]
+        q = self.q[:nl]
+        buf = self.red_buf
+        for m in range(self.M):
+            w_in, w_out = ws[m], ws[m + 1]
+            if m == 0:
+                if self.prob.fused:
+                    fused_rows(MV, x, w_in, center=mean, col_out=buf[:d], raw=True)
+                    sh.allreduce_(buf[:d])
+                    _lib.check(lib.simopt_scale_sub(sp, P(buf), inv, P(mean), d, P(self.g)))
+                else:
+                    if nl:
+                        _lib.check(lib.simopt_matvec(sp, P(x), nl, d, None, nl, P(mean), P(w_in), chunk, P(q)))
+                    sharded_matvec_t(sh, x, q, n_k, chunk, center=mean, out=self.gq)
+                    _lib.check(lib.simopt_scale_sub(sp, P(self.gq), inv, P(mean), d, P(self.g)))
+            _lib.check(lib.simopt_lmo_simplex_slack(sp, P(self.g), d, P(self.s), P(self.status[m:])))
+            _lib.check(lib.simopt_axpy(sp, -1.0, P(w_in), P(self.s), d, P(self.dirn)))
+            _lib.check(lib.simopt_axpy_ptr(sp, P(self.gamma[m:]), P(self.dirn), P(w_in), d, P(w_out)))
+            _lib.check(lib.simopt_min_value(sp, P(w_out), d, P(self.wmin[m:])))
+            last = m == self.M - 1
+            if self.prob.fused:
+                fused_rows(MV, x, w_out, center=mean, col_out=None if last else buf[:d],
+                           scalar_out=buf[d:], accumulate=not last, raw=True)
+                if last:
+                    sh.allreduce_(buf[d:])
+                else:
+                    sh.allreduce_(buf)
+                    _lib.check(lib.simopt_scale_sub(sp, P(buf), inv, P(mean), d, P(self.g)))
+                self.quad[m:m + 1].copy_(buf[d:])
+            else:
+                if nl:
+                    _lib.check(lib.simopt_matvec(sp, P(x), nl, d, None, nl, P(mean), P(w_out), chunk, P(q)))
+                sharded_dot(sh, q, q, n_k, chunk, out=self.quad[m:m + 1])
+                if not last:
+                    sharded_matvec_t(sh, x, q, n_k, chunk, center=mean, out=self.gq)
+                    _lib.check(lib.simopt_scale_sub(sp, P(self.gq), inv, P(mean), d, P(self.g)))
+            _lib.check(lib.simopt_dot(sp, P(w_out), P(mean), d, chunk, P(self.lin[m:])))
             _lib.check(lib.simopt_vec_sum(sp, P(w_out), d, chunk, P(self.wsum[m:])))
             _lib.check(lib.simopt_timestamp(sp, P(self.stamps[m:])))
 
@@ -605,15 +791,16 @@ class MvFwEngine:
         M = self.M
         ss = self.prob.sample_set
         x, mean = ss.samples, ss.mean
-        if self.q is None or self.q.numel() != n_k:
-            self.q = empty(n_k)
+        n_rows = x.shape[0]  # this rank's rows when sharded
+        if self.q is None or self.q.numel() != max(n_rows, 1):
+            self.q = empty(max(n_rows, 1))
             self.graphs = {}
         ws = self.rings[k % 2]
         self.status.zero_()
         self.gamma.copy_(torch.tensor([fw_step_size(k, M, m) for m in range(M)], dtype=F64))
         key = (k % 2, x.data_ptr(), mean.data_ptr(), n_k, self.prob.fused)
         g = self.graphs.get(key)
-        if not self.use_graph:
+        if not self.use_graph or self.prob.shard is not None:  # collectives: eager
             self._steps(ws, x, mean, n_k)
             return
         if g is None and not self.warm:

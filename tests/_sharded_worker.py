@@ -1,0 +1,57 @@
+"""Child process of tests/test_gpu_sharded.py: one rank of a sharded solver run.
+
+Ranks share cuda:0 and talk over gloo (the one-GPU box); on a multi-GPU box the
+same code runs one rank per GPU over NCCL.  Each rank writes its RunRecords to
+<out>/rank<r>.npz for the parent to compare against the oracle.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main(rank, world, port, out):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2404_11631_b200 as p
+    from paper_2404_11631_b200.frank_wolfe import FwConfig, fw_run
+    from paper_2404_11631_b200.instances import gen_meanvar_instance, gen_newsvendor_instance
+    from paper_2404_11631_b200.newton import newton_cg, newton_explicit
+    from paper_2404_11631_b200.sampling import synth_classification
+    from paper_2404_11631_b200.sharding import ShardGroup
+    from paper_2404_11631_b200.tasks import LogisticTask, MeanVarProblem, NewsvendorProblem
+    sh = ShardGroup()
+    res = {}
+    for chunk in (4096, 1000):
+        b = p.make_backend("cuda", chunk_size=chunk)
+        for fused in (False, True):
+            task = gen_meanvar_instance(300, p.RngStream(42, 0))
+            rec = fw_run(MeanVarProblem(task, b, fused=fused, shard=sh),
+                         FwConfig(2, 10, 10_000, p.RngStream(42, 2)), b)
+            res[f"mv_{chunk}_{int(fused)}_obj"] = rec.objectives
+            res[f"mv_{chunk}_{int(fused)}_w"] = rec.final_iterate
+    b = p.make_backend("cuda")
+    data = synth_classification(40, p.RngStream(42, 0), n_rows=9000, shard=sh)
+    res["lr_rows"] = np.array([data.local_rows, data.row_offset])
+    for fused in (False, True):
+        rec = newton_cg(LogisticTask(data), 3, 8, b, fused=fused)
+        res[f"ncg_{int(fused)}_obj"] = rec.objectives
+        res[f"ncg_{int(fused)}_w"] = rec.final_iterate
+    rec = newton_explicit(LogisticTask(data), 3, 20, b)
+    res["nex_obj"], res["nex_w"] = rec.objectives, rec.final_iterate
+    nv = gen_newsvendor_instance(1003, p.RngStream(42, 0))
+    rec = fw_run(NewsvendorProblem(nv, b, shard=sh), FwConfig(2, 6, 5000, p.RngStream(42, 2)), b)
+    res["nv_obj"], res["nv_w"] = rec.objectives, rec.final_iterate
+    np.savez(os.path.join(out, f"rank{rank}.npz"), **res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4])

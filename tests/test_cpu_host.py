@@ -146,3 +146,49 @@ def test_gloo_sharded_exact_tree_and_argmin():
     for _, root, best in res:
         assert root == want
         assert best == (float(g[int(np.argmin(g))]), int(np.argmin(g)))
+
+
+def _group_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2404_11631_b200.sharding import ShardGroup
+    sh = ShardGroup()
+    t = torch.full((3,), float(rank + 1), dtype=torch.float64)
+    sh.allreduce_(t)
+    g = sh.allgather(torch.tensor([rank, 10 * rank], dtype=torch.float64))
+    lo, hi = sh.range(10, 4)
+    rows = torch.arange(lo, hi, dtype=torch.float64).view(-1, 1)
+    cat = sh.allgather_rows(rows, [b - a for a, b in sh.ranges(10, 4)])
+    q.put((rank, t.tolist(), g.tolist(), cat.view(-1).tolist(), (lo, hi)))
+    dist.destroy_process_group()
+
+
+def test_gloo_shard_group_collectives():
+    """ShardGroup (the sharded solvers' only communication layer) over gloo, world 2."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_group_worker, args=(r, 2, port, q)) for r in range(3 - 1)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, t, g, cat, rng in res:
+        assert t == [3.0, 3.0, 3.0]
+        assert g == [[0.0, 0.0], [1.0, 10.0]]
+        assert cat == [float(i) for i in range(10)]      # uneven shards [0,8) and [8,10)
+    assert res[0][4] == (0, 8) and res[1][4] == (8, 10)
+
+
+def test_shifted_counter_matches_block_offset():
+    """A product shard's draw = the full draw with the counter moved by whole blocks."""
+    from paper_2404_11631_b200.sharding import shifted_counter
+    S, j0 = 5000, 504
+    full = orc.standard_normal(orc.Stream(42, 2), 1003 * S)
+    st = orc.Stream(42, 2)
+    st.counter = shifted_counter(0, j0 * S // 4)
+    part = orc.standard_normal(st, 8 * S)
+    assert np.array_equal(part, full[j0 * S:(j0 + 8) * S])
+    assert shifted_counter((1 << 128) - 1, 2) == 1

@@ -1,0 +1,80 @@
+"""Sharded solver runs vs the one-process oracle, world size 2 on one GPU.
+
+Two ranks share cuda:0 over gloo, which exercises every sharded code path
+(row-shard RNG addressing, chunk-partial gathers, fused allreduces, the product
+-sharded LMO exchange) except NCCL itself.  Exact-tree modes must be bit-identical
+to the single-process oracle; fused modes within the north-star 1e-8.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def ranks(tmp_path_factory):
+    out = str(tmp_path_factory.mktemp("sharded"))
+    port = _port()
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "_sharded_worker.py"), str(r), "2",
+                               str(port), out]) for r in range(2)]
+    for pr in procs:
+        assert pr.wait(timeout=600) == 0
+    return [dict(np.load(os.path.join(out, f"rank{r}.npz"))) for r in range(2)]
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def test_ranks_agree(ranks):
+    a, b = ranks
+    for k in a:
+        if k != "lr_rows":
+            assert np.array_equal(a[k], b[k]), k
+    assert a["lr_rows"][0] + b["lr_rows"][0] == 9000 and b["lr_rows"][1] == a["lr_rows"][0]
+
+
+@pytest.mark.parametrize("chunk", [4096, 1000])
+def test_meanvar_sharded(ranks, chunk):
+    mu, sigma = orc.gen_meanvar_instance(300, orc.Stream(42, 0))
+    objs, w = orc.fw_run_meanvar(mu, sigma, 2, 10, 10_000, orc.Stream(42, 2), chunk)
+    r = ranks[0]
+    assert np.array_equal(r[f"mv_{chunk}_0_obj"], objs)      # exact tree: bitwise
+    assert np.array_equal(r[f"mv_{chunk}_0_w"], w)
+    np.testing.assert_allclose(r[f"mv_{chunk}_1_obj"], objs, rtol=1e-8)
+    assert _rel(r[f"mv_{chunk}_1_w"], w) < 1e-8
+
+
+def test_logistic_sharded(ranks):
+    x, z, _ = orc.synth_classification(40, orc.Stream(42, 0), n_rows=9000)
+    objs, w = orc.newton_cg(x, z, iterations=3, cg_iters=8)
+    r = ranks[0]
+    assert np.array_equal(r["ncg_0_obj"], objs)
+    assert np.array_equal(r["ncg_0_w"], w)
+    np.testing.assert_allclose(r["ncg_1_obj"], objs, rtol=1e-8)
+    assert _rel(r["ncg_1_w"], w) < 1e-8
+    objs, w = orc.newton_explicit(x, z, iterations=3, cg_iters=20)
+    np.testing.assert_allclose(r["nex_obj"], objs, rtol=1e-8)
+    assert _rel(r["nex_w"], w) < 1e-8
+
+
+def test_newsvendor_sharded(ranks):
+    task = orc.gen_newsvendor_instance(1003, orc.Stream(42, 0))
+    objs, x = orc.fw_run_newsvendor(task, 2, 6, 5000, orc.Stream(42, 2))
+    r = ranks[0]
+    assert np.array_equal(r["nv_w"], x)                    # counts are exact integers
+    np.testing.assert_allclose(r["nv_obj"], objs, rtol=1e-13)

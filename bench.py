@@ -10,8 +10,11 @@ draws, 8 GB) + 25 FW iterations; value = FW iterations/s.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 runs one independent replica per GPU (weak scaling: products are
-independent but the LMO couples them every iteration).
+N > 1 shards the SAME problem's products across the N GPUs (strong scaling):
+each rank draws and scans only its products (Philox counter offset, no RNG
+communication); every FW step exchanges the per-rank LMO argmins (NCCL
+allgather of 3 doubles per rank) and each epoch's recorded sums (one
+allreduce).  See DESIGN.md section 5.
 """
 from __future__ import annotations
 
@@ -34,15 +37,17 @@ CPU_SAMPLE_D = 1_000  # reference CPU arm: products per bounded sample (cost is 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the N>1 path with several ranks on one GPU")
     return ap.parse_args()
 
 
-def dist_setup(n):
+def dist_setup(n, backend="nccl"):
     import torch
     import torch.distributed as dist
     rank = int(os.environ.get("RANK", "0"))
@@ -50,8 +55,12 @@ def dist_setup(n):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev = local % max(torch.cuda.device_count(), 1)
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     return rank, world
 
 
@@ -72,7 +81,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -189,7 +198,7 @@ def run_reference(args, rank):
         "impl": "reference", "metric": "newsvendor Frank-Wolfe iterations/sec (d=10000, S=100000, M=25)",
         "value": value, "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "newsvendor C2 (BASELINE.json configs[1])", "d": D, "S": S, "M": M,
                    "seed": SEED},
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cores, "kind": kind,
@@ -210,9 +219,11 @@ def run_ours(args, rank, world):
     from paper_2404_11631_b200.records import TraceBuilder
     from paper_2404_11631_b200.tasks import NewsvendorProblem, NvFwEngine
 
+    from paper_2404_11631_b200.sharding import ShardGroup
     backend = pkg.make_backend("cuda")
     task = gen_newsvendor_instance(D, pkg.RngStream(SEED, 0))
-    prob = NewsvendorProblem(task, backend)
+    shard = ShardGroup() if world > 1 else None
+    prob = NewsvendorProblem(task, backend, shard=shard)
     epochs = args.warmup + args.steps
     eng = NvFwEngine(prob, M, epochs, backend.chunk_size)
     stream = pkg.RngStream(SEED, 2)
@@ -236,7 +247,7 @@ def run_ours(args, rank, world):
         dist.barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     # validate the whole run (trace rows, feasibility) outside the timed region
@@ -245,12 +256,13 @@ def run_ours(args, rank, world):
         bad = eng.check_epoch(k, trace)
         if bad:
             raise RuntimeError(f"bench run aborted at step {bad[0]}: {bad[1]}")
-    value = world * args.steps * M / (ms / 1e3)
+    value = args.steps * M / (ms / 1e3)  # one problem, all ranks (strong scaling)
     res_ms = statistics.mean(a.elapsed_time(b) for a, b in eng.resample_events)
     from paper_2404_11631_b200.tasks import nv_geometry
     seg, nbuck = nv_geometry()
     nseg = -(-S // seg)
-    alg_bytes = D * S * 4 + D * nseg * nbuck * 2  # keys + bucket starts written per launch
+    d_loc = prob.dev.d
+    alg_bytes = d_loc * S * 4 + d_loc * nseg * nbuck * 2  # keys + bucket starts written per launch
     peak, peak_kind = peaks()
     achieved = alg_bytes / (res_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -260,29 +272,32 @@ def run_ours(args, rank, world):
                 "note": ("issue-bound: Philox4x64-10 + fp32 Box-Muller key per draw (exact glibc "
                          "Box-Muller only for ambiguous draws at query time); see profiles/")}
     launches_per_epoch = 4 * M + 2  # resample, M+1 fused steps, M x (terms, sums, stamp)
+    if world > 1:
+        launches_per_epoch += 2 * M  # LMO pack + apply around each exchange
     line = {
         "metric": "newsvendor Frank-Wolfe iterations/sec (d=10000, S=100000, M=25)",
         "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "newsvendor C2 (BASELINE.json configs[1])", "d": D, "S": S, "M": M,
                    "seed": SEED, "step": "1 resampling epoch = 1 resample + 25 FW iterations",
                    "l2": "inputs larger than L2 (8 GB demands per epoch)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"products sharded x{world} ({args.dist_backend} LMO exchange "
+                                   "per step)") if world > 1 else "single GPU"},
         "roofline": roofline,
         "clocks": clk.summary(),
         "gpu_launches": launches_per_epoch * args.steps,
         "final_objective": trace.build("newsvendor", D, "cuda", 0, SEED, None).final_objective,
     }
     if not args.no_e2e:
-        line["e2e"] = run_e2e(args, task, backend)
+        line["e2e"] = run_e2e(args, task, backend, shard)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
-def run_e2e(args, task, backend):
+def run_e2e(args, task, backend, shard=None):
     """Same metric through the public API with host inputs: every step builds the
     problem from host arrays (H2D of the instance) and returns a RunRecord (D2H of
     the trace and final iterate)."""
@@ -292,13 +307,22 @@ def run_e2e(args, task, backend):
     from paper_2404_11631_b200.tasks import NewsvendorProblem
     steps = max(2, min(args.steps, 3))
     stream = pkg.RngStream(SEED, 2)
-    rec = fw_run(NewsvendorProblem(task, backend), FwConfig(1, M, S, stream), backend)  # warm
+    rec = fw_run(NewsvendorProblem(task, backend, shard=shard), FwConfig(1, M, S, stream),
+                 backend)  # warm
     torch.cuda.synchronize()
+    if shard is not None:
+        shard.barrier()
     t = time.perf_counter()
     for _ in range(steps):
-        rec = fw_run(NewsvendorProblem(task, backend), FwConfig(1, M, S, stream), backend)
+        rec = fw_run(NewsvendorProblem(task, backend, shard=shard), FwConfig(1, M, S, stream), backend)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
+    if shard is not None:  # max over ranks
+        import torch.distributed as dist
+        tt = torch.tensor([dt], dtype=torch.float64,
+                          device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
     h2d = 6 * D * 8  # mu, sigma, k, h, v, c
     d2h = rec.iterations.size * (4 + 8 + 8 + 8) + D * 8  # flags, spent, objective, stamps + iterate
     return {"value": steps * M / dt, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
@@ -307,11 +331,12 @@ def run_e2e(args, task, backend):
 
 def main():
     args = parse()
-    rank, world = dist_setup(args.gpus)
     if args.impl == "reference":
-        run_reference(args, rank)
-    else:
-        run_ours(args, rank, world)
+        # host-CPU arm: rank 0 alone times the reference; other ranks exit at once
+        run_reference(args, int(os.environ.get("RANK", "0")))
+        return
+    rank, world = dist_setup(args.gpus, args.dist_backend)
+    run_ours(args, rank, world)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

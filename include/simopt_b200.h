@@ -263,6 +263,33 @@ int simopt_logistic_xtdx(void* stream, const double* x, const double* dw, int64_
 /* Same swap sequence on host memory for large b (u = the b uniforms). */
 int simopt_fisher_yates_host(int64_t n, int64_t b, const double* u, int64_t* out);
 
+/* ------------------------------------------------------------ projections (projected SGD) */
+/* Euclidean projection of y onto {x >= 0, c . x <= budget} (c == NULL: all ones, i.e.
+ * the simplex-with-slack of lmo.py:20-24 for budget 1).  One CTA: bisection on the
+ * multiplier, exact recompute on the active set.  A NaN in y sets *status = 1
+ * (InvalidGradient) when status != NULL. */
+int simopt_project_budget(void* stream, const double* y, const double* c, double budget, int64_t d,
+                          double* out, int* status);
+/* Clamp onto the box [lo, hi]^d. */
+int simopt_project_box(void* stream, const double* y, double lo, double hi, int64_t d, double* out);
+
+/* ------------------------------------------------------------ multi-PRNG streams */
+/* Philox4x32-10 (Random123): out[4b..4b+3] = Philox4x32_10(ctr + b, {key0, key1}) for
+ * b < nblocks, ctr a 128-bit counter of four little-endian u32 words (host array);
+ * out 16-byte aligned. */
+int simopt_philox4x32(void* stream, uint32_t key0, uint32_t key1, const uint32_t* ctr,
+                      int64_t nblocks, uint32_t* out);
+/* Per-stream SFC64 / xoshiro256++: state = device u64[n_streams][4] (SFC64: a, b, c,
+ * counter as numpy.random.SFC64; xoshiro: s[0..3]), advanced in place by n outputs;
+ * out is stream-major [n_streams][n]: u64 words (out_kind 0) or doubles
+ * (w >> 11) * 2^-53 (out_kind 1). */
+int simopt_sfc64(void* stream, uint64_t* state, int64_t n_streams, int64_t n, int out_kind,
+                 void* out);
+int simopt_xoshiro256pp(void* stream, uint64_t* state, int64_t n_streams, int64_t n, int out_kind,
+                        void* out);
+/* Host: n_streams xoshiro256++ states, states[k] = jump^k(seed_state) (2^128 apart). */
+int simopt_xoshiro256pp_streams(const uint64_t* seed_state, int64_t n_streams, uint64_t* states);
+
 /* Deterministic sharded reductions: matvec_t chunk partials before the
  * fold, out[c*cols + j] (c < ceil(rows/chunk)); and the fold of nch gathered partial
  * rows, out[j] = fold_pairwise(p[0*count+j], ..., p[(nch-1)*count+j]) (p clobbered).

@@ -66,6 +66,11 @@ def lib():
         L.orc_ecdf_count.argtypes = [_dp, i64, i64, _dp, _i64p]
         L.orc_bfgs_rank2.argtypes = [_dp, _dp, _dp, d, d, i64]
         L.orc_sort_rows.argtypes = [_dp, i64, i64]
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        L.orc_philox4x32.argtypes = [u32p, u32p, i64, u32p]
+        L.orc_sfc64.argtypes = [_u64p, i64, _u64p]
+        L.orc_xoshiro256pp.argtypes = [_u64p, i64, _u64p]
+        L.orc_xoshiro256pp_jump.argtypes = [_u64p]
         _lib = L
     return _lib
 
@@ -533,4 +538,77 @@ def newton_explicit(x, z, *, iterations, cg_iters, chunk=CHUNK):
             rr = rr_new
         w = w + p
         objs.append(logistic_loss(w, x, z, None, chunk))
+    return np.array(objs), w
+
+
+# ---------------------------------------------------------------- multi-PRNG
+# Published-algorithm restatements (oracle/prng.c); parity with the reference's
+# orphaned pkg/test_multi_prng_*.json fixtures is UNPINNED.
+def philox4x32(ctr, key, nblocks):
+    """uint32[4*nblocks]: Philox4x32-10 of counters ctr, ctr+1, ... (128-bit carry)."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.empty(4 * nblocks, dtype=np.uint32)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    lib().orc_philox4x32(c.ctypes.data_as(u32p), k.ctypes.data_as(u32p), nblocks,
+                         out.ctypes.data_as(u32p))
+    return out
+
+
+def _gen64(fn, state, n):
+    s = np.array(state, dtype=np.uint64)
+    out = np.empty(n, dtype=np.uint64)
+    fn(s.ctypes.data_as(_u64p), n, out.ctypes.data_as(_u64p))
+    return out, s
+
+
+def sfc64(state, n):
+    """(outputs, new state) of SFC64 from state (a, b, c, counter)."""
+    return _gen64(lib().orc_sfc64, state, n)
+
+
+def xoshiro256pp(state, n):
+    return _gen64(lib().orc_xoshiro256pp, state, n)
+
+
+def xoshiro256pp_jump(state):
+    s = np.array(state, dtype=np.uint64)
+    lib().orc_xoshiro256pp_jump(s.ctypes.data_as(_u64p))
+    return s
+
+
+# ---------------------------------------------------------------- projected SGD
+# No reference counterpart (sobench ships only Frank-Wolfe): restated from the
+# standard exact algorithm (sort the breakpoints y_j / c_j; Held/Wolfe/Crowder,
+# Duchi et al. 2008 for c = 1).  Checks csrc/project.cu and psgd.py by tolerance.
+def project_budget(y, c=None, budget=1.0):
+    """argmin ||x - y|| over {x >= 0, c.x <= budget}."""
+    y = _vec(y)
+    c = np.ones(y.size) if c is None else _vec(c)
+    x0 = np.maximum(y, 0.0)
+    if c @ x0 <= budget:
+        return x0
+    t = y / c
+    order = np.argsort(-t, kind="stable")
+    cy = np.cumsum(c[order] * y[order])
+    cc = np.cumsum(c[order] ** 2)
+    theta = (cy - budget) / cc
+    ok = np.nonzero(theta < t[order])[0]
+    th = theta[ok[-1]]
+    return np.maximum(y - th * c, 0.0)
+
+
+def psgd_run_meanvar(mu, sigma, epochs, inner_iters, n_samples, stream, step0=1.0, chunk=CHUNK):
+    d = mu.size
+    w = np.zeros(d)
+    objs = []
+    t = 0
+    for _ in range(epochs):
+        x = sample_returns_diag(mu, sigma, n_samples, stream)
+        mean, xc = build_sample_set(x, chunk)
+        for _ in range(inner_iters):
+            g = mv_gradient(w, mean, xc, chunk)
+            w = project_budget(w - (step0 / math.sqrt(t + 1)) * g, None, 1.0)
+            objs.append(mv_objective(w, mean, xc, chunk))
+            t += 1
     return np.array(objs), w

@@ -60,6 +60,11 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
+// Bulk L2 prefetch of one contiguous row band (TMA engine; no registers, no smem).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <int MODE, int C, int K, bool VEC>
 __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
   constexpr int R = (16 / K) < 1 ? 1 : 16 / K;
@@ -94,8 +99,14 @@ __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
   double sc = 0.0;
   const int64_t ntiles = (N + R - 1) / R;
   int par = 0;
+  const uint32_t band_bytes = (uint32_t)(((b1 - b0) * 8 + 15) & ~15LL);
   for (int64_t tile = cl; tile < ntiles; tile += ncl, par ^= 1) {
     const int64_t r0 = tile * R;
+    // keep HBM busy through this tile's reductions: the next tile's rows go to L2 now
+    if (VEC && tid < R && b1 > b0) {
+      const int64_t rn = r0 + ncl * R + tid;
+      if (rn < N) prefetch_l2(a.X + rn * d + b0, band_bytes);
+    }
     double2 x[R][K];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -218,17 +229,30 @@ __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
 }
 
 // out[j] = (sum_cl part[cl][j]) * scale - center[j];  scalar = sum_cl spart[cl]
-__global__ void k_fused_finish(const double* __restrict__ part, const double* __restrict__ spart,
-                               int64_t ncl, int64_t d, double scale,
-                               const double* __restrict__ center, double* __restrict__ out,
-                               double* __restrict__ scalar_out) {
+// Block = 32 columns x 8 warps; warp w sums clusters w, w+8, ... (independent loads),
+// then the 8 warp partials are added in warp order (fixed order: deterministic).
+__global__ void __launch_bounds__(256) k_fused_finish(const double* __restrict__ part,
+                                                      const double* __restrict__ spart, int64_t ncl,
+                                                      int64_t d, double scale,
+                                                      const double* __restrict__ center,
+                                                      double* __restrict__ out,
+                                                      double* __restrict__ scalar_out) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (out) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < d;
-         j += (int64_t)gridDim.x * blockDim.x) {
-      double s = 0.0;
-      for (int64_t c = 0; c < ncl; ++c) s += part[c * d + j];
-      s = s * scale;
-      out[j] = center ? s - center[j] : s;
+    const int64_t j = blockIdx.x * 32LL + lane;
+    double s = 0.0;
+    if (j < d) {
+      for (int64_t c = w; c < ncl; c += 8) s += part[c * d + j];
+    }
+    red[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && j < d) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += red[k][lane];
+      t = t * scale;
+      out[j] = center ? t - center[j] : t;
     }
   }
   if (scalar_out && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -347,7 +371,7 @@ extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_
   SIMOPT_REQUIRE(mode != SIMOPT_FUSED_MV || center != nullptr, SIMOPT_E_CONFIG, "MV needs the mean");
   SIMOPT_REQUIRE(mode == SIMOPT_FUSED_MV || rowaux != nullptr, SIMOPT_E_CONFIG, "row weights missing");
   if (cols == 0 || rows == 0) {  // empty sums: col_out = 0 * scale [- center], scalar 0
-    k_fused_finish<<<(int)(cols > 0 ? ceil_div(cols, 256) : 1), 256, 0, st>>>(
+    k_fused_finish<<<(int)(cols > 0 ? ceil_div(cols, 32) : 1), 256, 0, st>>>(
         nullptr, nullptr, 0, cols, col_scale, (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr,
         (accumulate && cols) ? col_out : nullptr, scalar_out);
     SIMOPT_CHECK_LAUNCH("k_fused_finish");
@@ -387,7 +411,7 @@ extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_
   cfg.numAttrs = 1;
   cfg.dynamicSmemBytes = dyn_smem(mode, K);
   SIMOPT_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
-  const int fgrid = (int)(a.accumulate ? ceil_div(cols, 256) : 1);
+  const int fgrid = (int)(a.accumulate ? ceil_div(cols, 32) : 1);
   k_fused_finish<<<fgrid < 1 ? 1 : fgrid, 256, 0, st>>>(
       part, a.scal_part, ncl, cols, raw ? 1.0 : col_scale,
       (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr, a.accumulate ? col_out : nullptr,

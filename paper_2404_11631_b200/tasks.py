@@ -224,6 +224,12 @@ class NewsvendorProblem:
         return lmo_single_budget(g, self.dev.c if is_tensor(g) else self.task.budget_costs,
                                  self.task.budget)
 
+    def project(self, y):
+        """Euclidean projection onto {x >= 0, c.x <= C} (projected SGD, psgd.py)."""
+        from .psgd import project_budget
+        self._whole()
+        return project_budget(y, self.dev.c, self.task.budget)
+
     def check_feasible(self, x) -> bool:
         self._whole()
         xd = vec_dev(x)
@@ -627,6 +633,12 @@ class MeanVarProblem:
         self.sample_set = MeanVarSampleSet(self._x, self._mean, count=n_samples)
 
     def objective(self, w) -> float:
+        if self.shard is None and self.fused:
+            ss, wd = self.sample_set, vec_dev(w)
+            quad = empty(1)
+            fused_rows(MV, ss.samples, wd, center=ss.mean, scalar_out=quad, accumulate=False)
+            lin = float(self.backend.dot_device(wd, ss.mean).item())
+            return 0.5 * float(quad.item()) / (ss.count - 1) - lin
         if self.shard is None:
             return mv_objective(w, self.sample_set, self.backend)
         ss, chunk, wd = self.sample_set, self.backend.chunk_size, vec_dev(w)
@@ -636,6 +648,11 @@ class MeanVarProblem:
         return 0.5 * quad / (ss.count - 1) - lin
 
     def gradient(self, w):
+        if self.shard is None and self.fused:  # one read of X (csrc/fused.cu)
+            ss, wd = self.sample_set, vec_dev(w)
+            g = empty(wd.numel())
+            fused_rows(MV, ss.samples, wd, center=ss.mean, col_scale=1.0 / (ss.count - 1), col_out=g)
+            return like_input(w, g)
         if self.shard is None:
             return mv_gradient(w, self.sample_set, self.backend)
         ss, chunk, wd = self.sample_set, self.backend.chunk_size, vec_dev(w)
@@ -648,6 +665,11 @@ class MeanVarProblem:
 
     def lmo(self, g):
         return lmo_simplex_slack(g)
+
+    def project(self, y):
+        """Euclidean projection onto {w >= 0, sum(w) <= 1} (projected SGD, psgd.py)."""
+        from .psgd import project_budget
+        return project_budget(y, None, 1.0)
 
     def check_feasible(self, w) -> bool:
         wh = to_host(w) if is_tensor(w) else np.asarray(w)

@@ -137,3 +137,36 @@ def test_sqn_trace(golden):
                           hess_batch=100, iterations=60, stream=orc.Stream(42, 2))
     assert np.array_equal(objs, g["sqn_obj"])
     assert np.array_equal(w, g["sqn_w"])
+
+
+def test_multi_prng_oracle_known_answers():
+    """Published known answers for the multi-PRNG restatements (oracle/prng.c)."""
+    kat = [([0, 0, 0, 0], [0, 0], [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]),
+           ([0xffffffff] * 4, [0xffffffff] * 2, [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]),
+           ([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0],
+            [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1])]
+    for ctr, key, want in kat:  # Random123 kat_vectors, philox4x32 10 rounds
+        assert list(orc.philox4x32(ctr, key, 1)) == want
+    out, _ = orc.xoshiro256pp([1, 2, 3, 4], 3)  # xoshiro256plusplus.c from s = {1,2,3,4}
+    assert list(out) == [41943041, 58720359, 3588806011781223]
+    bg = np.random.SFC64(2024)
+    st = bg.state["state"]["state"].copy()
+    out, st2 = orc.sfc64(st, 1000)
+    assert np.array_equal(out, bg.random_raw(1000))
+    assert np.array_equal(st2, bg.state["state"]["state"])
+
+
+def test_xoshiro_stream_states_host():
+    """The library's host stream setup (jump^k) equals the oracle's jump()."""
+    from paper_2404_11631_b200.prng import Xoshiro256ppStreams
+    import ctypes
+    from paper_2404_11631_b200 import _lib
+    seed = [0x9E3779B97F4A7C15, 7, 11, 13]
+    out = np.empty((3, 4), dtype=np.uint64)
+    s = (ctypes.c_uint64 * 4)(*seed)
+    _lib.check(_lib.load(require_device=False).simopt_xoshiro256pp_streams(s, 3, out.ctypes.data))
+    want = np.array(seed, dtype=np.uint64)
+    for k in range(3):
+        assert np.array_equal(out[k], want)
+        want = orc.xoshiro256pp_jump(want)
+    assert Xoshiro256ppStreams is not None

@@ -228,8 +228,9 @@ def run_ours(args, rank, world):
     eng = NvFwEngine(prob, M, epochs, backend.chunk_size)
     stream = pkg.RngStream(SEED, 2)
     eng.start()
-    for k in range(args.warmup):
-        eng.enqueue_epoch(k, stream, S)
+    for k in range(args.warmup):  # the next epoch's resample overlaps this epoch's steps,
+        nxt = S if k + 1 < args.warmup else None  # never across the timed-region boundary
+        eng.enqueue_epoch(k, stream, S, next_samples=nxt)
     eng.finish()
     torch.cuda.synchronize()
     if world > 1:
@@ -239,7 +240,8 @@ def run_ours(args, rank, world):
     with ClockSampler(torch.cuda.current_device()) as clk:
         e0.record()
         for k in range(args.warmup, epochs):
-            eng.enqueue_epoch(k, stream, S, time_resample=True)
+            nxt = S if k + 1 < epochs else None
+            eng.enqueue_epoch(k, stream, S, time_resample=True, next_samples=nxt)
         eng.finish()
         e1.record()
         torch.cuda.synchronize()

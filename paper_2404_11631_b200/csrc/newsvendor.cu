@@ -12,6 +12,8 @@
 // handful of draws whose approximation is within the guaranteed error of the
 // threshold with the exact glibc Box-Muller -- the count is the reference's
 // integer, bit for bit, for every query.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "fw.cuh"
 #include "glibc_math.cuh"
@@ -29,9 +31,10 @@ constexpr int kResampleMinBlocks = 4;
 // Persistent CTAs walk (product j, segment s) pairs: generate the segment's keys
 // (Philox4x64-10 + fp32 Box-Muller approximation), histogram them by bucket in
 // shared memory, scan, scatter into bucket order and stream keys + bucket starts out.
+template <bool kNoCarry>
 __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
-    k_nv_resample(const phx_keys rk, uint64_t clo, uint64_t chi, int64_t d, int64_t S,
-                  int nseg, uint32_t* __restrict__ keys, uint16_t* __restrict__ off) {
+    k_nv_resample(const phx_keys rk, const phx_pre pre, uint64_t clo, uint64_t chi, int64_t d,
+                  int64_t S, int nseg, uint32_t* __restrict__ keys, uint16_t* __restrict__ off) {
   __shared__ __align__(16) uint32_t raw[NV_SEG];
   __shared__ __align__(16) uint32_t sorted_[NV_SEG];
   __shared__ int hist[NV_B];
@@ -50,7 +53,10 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     const int64_t q0 = i0 >> 2, q1 = (i0 + len - 1) >> 2;
     const bool aligned = ((i0 & 3) == 0) && ((len & 3) == 0);
     for (int64_t q = q0 + threadIdx.x; q <= q1; q += blockDim.x) {
-      const phx4 w = philox4x64_10_rk(stream_block_counter(clo, chi, (uint64_t)q), rk);
+      // kNoCarry: no carry into the counter's word 1 within this launch (checked on the
+      // host), so block q's counter is (clo + q + 1, chi, 0, 0) -- see stream_block_counter
+      const phx4 w = kNoCarry ? philox4x64_10_rk_c0(clo + (uint64_t)q + 1, rk, pre)
+                              : philox4x64_10_rk(stream_block_counter(clo, chi, (uint64_t)q), rk);
       float z[4];
       nv_approx_pair(w.v[0], w.v[1], &z[0], &z[1]);
       nv_approx_pair(w.v[2], w.v[3], &z[2], &z[3]);
@@ -122,7 +128,12 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     }
     __syncthreads();
     uint32_t* dst = keys + j * S + e0;
-    for (int l = threadIdx.x; l < len; l += blockDim.x) dst[l] = sorted_[l];
+    if (aligned) {  // 16-byte stores (row offset j*S + e0 is a multiple of 4 here)
+      for (int l4 = threadIdx.x; l4 < (len >> 2); l4 += blockDim.x)
+        reinterpret_cast<uint4*>(dst)[l4] = reinterpret_cast<const uint4*>(sorted_)[l4];
+    } else {
+      for (int l = threadIdx.x; l < len; l += blockDim.x) dst[l] = sorted_[l];
+    }
     __syncthreads();
   }
 }
@@ -364,11 +375,26 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   const int64_t nseg = ceil_div(S, NV_SEG);
   const int64_t nblk = d * nseg;
   SIMOPT_REQUIRE(nblk < (1LL << 31), SIMOPT_E_CONFIG, "too many segments");
-  const int64_t cap = (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks * 8;
+  // Persistent grid of 5 CTAs per SM (6 fit): one wave, and room on every SM for the
+  // high-priority FW step kernels of the previous epoch that run concurrently in the
+  // pipelined device loop (measured best of 3..10 per SM at C2).
+  // SIMOPT_NV_RESAMPLE_GRID overrides it for tuning sweeps.
+  static const int64_t cap = [] {
+    const char* e = getenv("SIMOPT_NV_RESAMPLE_GRID");
+    return e ? atoll(e) : (int64_t)SIMOPT_NUM_SMS * 5;
+  }();
   const int64_t grid = nblk < cap ? nblk : cap;
   const phx_keys rk = phx_round_keys(seed, sid);
-  k_nv_resample<<<(unsigned)grid, kResampleThreads, 0, as_stream(stream)>>>(rk, clo, chi, d, S,
-                                                                            (int)nseg, keys, off);
+  // blocks q = 0 .. ceil(d*S/4)-1 use counters clo+1 ..; when they stay within word 0
+  // (the span resets of stream_block_counter then add no carry either) the first two
+  // Philox rounds are partly constant (philox4x64_10_rk_c0)
+  const phx_pre pre = phx_precompute(chi, rk);
+  if (phx_no_carry(clo, (uint64_t)ceil_div(d * S, 4)))
+    k_nv_resample<true><<<(unsigned)grid, kResampleThreads, 0, as_stream(stream)>>>(
+        rk, pre, clo, chi, d, S, (int)nseg, keys, off);
+  else
+    k_nv_resample<false><<<(unsigned)grid, kResampleThreads, 0, as_stream(stream)>>>(
+        rk, pre, clo, chi, d, S, (int)nseg, keys, off);
   SIMOPT_CHECK_LAUNCH("k_nv_resample");
   return SIMOPT_OK;
 }

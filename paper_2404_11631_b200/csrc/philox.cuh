@@ -102,3 +102,57 @@ PHX_HD phx4 philox4x64_10_rk(phx4 c, const phx_keys& rk) {
   }
   return c;
 }
+
+// Counter (c0, hi, 0, 0) with a launch-constant high word `hi`: the first two rounds
+// carry known values (round 0 multiplies word 2 = 0; round 1 multiplies the constant
+// hi ^ k0), so those two 64x64 products are skipped / precomputed on the host.
+// Valid whenever the launch's counters c0 = clo + b + 1 do not carry into word 1
+// (phx_no_carry).  Bit-identical to philox4x64_10_rk on such counters.
+typedef struct phx_pre {
+  uint64_t a;       // hi ^ k0 (word 0 after round 0)
+  uint64_t h1, l1;  // mulhilo(M0, a): round 1's first product
+} phx_pre;
+
+static inline phx_pre phx_precompute(uint64_t hi, const phx_keys& rk) {
+  phx_pre p;
+  p.a = hi ^ rk.k[0];
+#if defined(__CUDA_ARCH__)
+  p.l1 = PHILOX_M0 * p.a;
+  p.h1 = __umul64hi(PHILOX_M0, p.a);
+#else
+  const unsigned __int128 q = (unsigned __int128)PHILOX_M0 * p.a;
+  p.l1 = (uint64_t)q;
+  p.h1 = (uint64_t)(q >> 64);
+#endif
+  return p;
+}
+
+// True when clo + 1 .. clo + nblocks stays below 2^64 (no carry into word 1).
+static inline bool phx_no_carry(uint64_t clo, uint64_t nblocks) {
+  return nblocks <= ~clo;
+}
+
+PHX_HD phx4 philox4x64_10_rk_c0(uint64_t c0, const phx_keys& rk, const phx_pre& pre) {
+  uint64_t hi0, lo0, hi1, lo1;
+  phx_mulhilo(PHILOX_M0, c0, &hi0, &lo0);          // round 0 (word 2 == 0: no second product)
+  phx4 c;                                          // round 1
+  phx_mulhilo(PHILOX_M1, hi0 ^ rk.k[1], &hi1, &lo1);
+  c.v[0] = hi1 ^ rk.k[2];
+  c.v[1] = lo1;
+  c.v[2] = pre.h1 ^ lo0 ^ rk.k[3];
+  c.v[3] = pre.l1;
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+  for (int r = 2; r < 10; ++r) {
+    phx_mulhilo(PHILOX_M0, c.v[0], &hi0, &lo0);
+    phx_mulhilo(PHILOX_M1, c.v[2], &hi1, &lo1);
+    phx4 o;
+    o.v[0] = hi1 ^ c.v[1] ^ rk.k[2 * r];
+    o.v[1] = lo1;
+    o.v[2] = hi0 ^ c.v[3] ^ rk.k[2 * r + 1];
+    o.v[3] = lo0;
+    c = o;
+  }
+  return c;
+}

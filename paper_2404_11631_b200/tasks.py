@@ -135,23 +135,28 @@ class _NvDevice:
         self.off = None
         self.nseg = 0
         self.draw = None  # (seed, stream_id, ctr_lo, ctr_hi) of the epoch's draw
+        # layout slots: the device FW loop double-buffers the epoch layout so the next
+        # epoch's resample can run while this epoch's steps read the current one
+        self.slots = {}   # slot -> [S, nseg, keys, off, draw]
 
-    def ensure_layout(self, S: int):
-        if S == self.S:
-            return
-        ns, ke, oe = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        _lib.call("simopt_nv_layout", self.d, S, ctypes.byref(ns), ctypes.byref(ke), ctypes.byref(oe))
-        self.keys = None
-        self.off = None
-        self.keys = torch.empty(ke.value, dtype=torch.int32, device="cuda")
-        self.off = torch.empty(oe.value, dtype=torch.int16, device="cuda")
-        self.nseg = ns.value
-        self.S = S
+    def ensure_layout(self, S: int, slot: int = 0):
+        cur = self.slots.get(slot)
+        if cur is None or cur[0] != S:
+            ns, ke, oe = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+            _lib.call("simopt_nv_layout", self.d, S, ctypes.byref(ns), ctypes.byref(ke),
+                      ctypes.byref(oe))
+            self.slots[slot] = None
+            self.slots[slot] = [S, ns.value, torch.empty(ke.value, dtype=torch.int32, device="cuda"),
+                                torch.empty(oe.value, dtype=torch.int16, device="cuda"), None]
+        self.use_slot(slot)
 
-    def resample(self, stream: RngStream, S: int):
+    def use_slot(self, slot: int):
+        self.S, self.nseg, self.keys, self.off, self.draw = self.slots[slot]
+
+    def resample(self, stream: RngStream, S: int, slot: int = 0):
         if S < 1:
             raise InsufficientSamples("need at least one demand sample per product")
-        self.ensure_layout(S)
+        self.ensure_layout(S, slot)
         # product j's draws are normals j*S .. j*S+S-1 of standard_normal(d*S): a shard
         # starting at product j0 (j0*S % 4 == 0) is the same draw with the counter
         # moved j0*S/4 Philox blocks on -- no RNG communication
@@ -163,6 +168,7 @@ class _NvDevice:
                                   shifted_counter(stream.counter, self.j0 * S // 4)).words()
         else:
             self.draw = stream.words()
+        self.slots[slot][4] = self.draw
         _lib.call("simopt_nv_resample", _lib.stream_ptr(), *self.draw, self.d, S,
                   _lib.ptr(self.keys), _lib.ptr(self.off))
         stream.advance(2 * ((self.d_total * S + 1) // 2))
@@ -293,25 +299,65 @@ class NvFwEngine:
         self.lib = _lib.load()
         self.t0 = None
         self.resample_events = []
+        # streams: FW steps (the critical path) at high priority; the next epoch's
+        # resample (issue-bound, long) at low priority so step blocks are scheduled
+        # first whenever resample blocks retire; recording sums on a side stream
+        lo_pri, hi_pri = torch.cuda.Stream.priority_range() if hasattr(
+            torch.cuda.Stream, "priority_range") else (0, -1)
+        self.hi = torch.cuda.Stream(priority=hi_pri)
+        self.gen = torch.cuda.Stream(priority=lo_pri)
         self.side = torch.cuda.Stream()
         self.side_done = {}   # step -> event recorded on the side stream
         self.epoch_done = {}  # epoch -> event after its last recorded step
+        self.ready = {}       # epoch -> (layout slot, event: its resample is done)
+        self.steps_done = {}  # epoch -> event after its last step kernel
 
     def start(self):
-        _lib.check(self.lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(self.stamps[self.T:])))
+        cur = torch.cuda.current_stream()
+        _lib.check(self.lib.simopt_timestamp(_lib.stream_ptr(cur), _lib.ptr(self.stamps[self.T:])))
+        for s_ in (self.hi, self.gen, self.side):
+            s_.wait_stream(cur)
 
-    def enqueue_epoch(self, k: int, stream: RngStream, n_samples: int, time_resample: bool = False):
+    def _resample(self, k: int, stream: RngStream, n_samples: int, time_it: bool):
+        """Epoch k's resample on the generator stream into layout slot k % 2."""
+        slot = k % 2
+        old = self.steps_done.get(k - 2)  # last reader of this slot
+        if old is not None:
+            self.gen.wait_event(old)
+        with torch.cuda.stream(self.gen):
+            if time_it:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            self.dev.resample(stream, n_samples, slot)
+            if time_it:
+                e1.record()
+                self.resample_events.append((e0, e1))
+            ev = torch.cuda.Event()
+            ev.record()
+        self.ready[k] = (slot, ev)
+
+    def enqueue_epoch(self, k: int, stream: RngStream, n_samples: int, time_resample: bool = False,
+                      next_samples: int | None = None):
+        """Enqueue epoch k.  With next_samples, epoch k+1's resample is enqueued right
+        behind this epoch's steps on the low-priority generator stream (it draws from
+        `stream` after epoch k, exactly as a sequential run would) and overlaps them."""
         dev, a, lib, M, H = self.dev, self.args, self.lib, self.M, self.H
-        main = torch.cuda.current_stream()
+        if k not in self.ready:
+            self._resample(k, stream, n_samples, time_resample)
+        slot, ready = self.ready.pop(k)
+        main = self.hi
+        main.wait_event(ready)
+        dev.use_slot(slot)
         sp = _lib.stream_ptr(main)
         ssp = _lib.stream_ptr(self.side)
-        if time_resample:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-        dev.resample(stream, n_samples)
-        if time_resample:
-            e1.record()
-            self.resample_events.append((e0, e1))
+        with torch.cuda.stream(main):
+            self._enqueue_steps(k, sp, ssp)
+        if next_samples is not None:
+            self._resample(k + 1, stream, next_samples, time_resample)
+
+    def _enqueue_steps(self, k: int, sp, ssp):
+        dev, a, lib, M, H = self.dev, self.args, self.lib, self.M, self.H
+        main = self.hi
         a.S, a.nseg = dev.S, dev.nseg
         a.keys, a.off = dev.keys.data_ptr(), dev.off.data_ptr()
         a.seed, a.sid, a.ctr_lo, a.ctr_hi = dev.draw
@@ -336,6 +382,8 @@ class NvFwEngine:
                 self._exchange(sp)
             ev = torch.cuda.Event()
             ev.record(main)
+            if m + 1 == M:
+                self.steps_done[k] = ev
             self.side.wait_event(ev)
             # objective terms of x_{t+1} (newsvendor_cost_block), then dot(c, x_{t+1}) for
             # check_feasible and the objective's vec_sum in one launch -- all off the
@@ -376,8 +424,10 @@ class NvFwEngine:
                                            P(self.state)))
 
     def finish(self):
-        """Join the side stream into the caller's stream."""
-        torch.cuda.current_stream().wait_stream(self.side)
+        """Join the engine's streams into the caller's stream."""
+        cur = torch.cuda.current_stream()
+        for s_ in (self.hi, self.gen, self.side):
+            cur.wait_stream(s_)
 
     def check_epoch(self, k: int, trace: TraceBuilder):
         """Append epoch k's rows to `trace`; return (t, exc, iterate) at the first failure."""
@@ -425,7 +475,8 @@ def _nv_fw_run_device(prob: "NewsvendorProblem", config, backend, label, size, r
     eng.start()
     events = []
     for k in range(config.epochs):
-        eng.enqueue_epoch(k, config.stream, config.epoch_sample_size(k))
+        nxt = config.epoch_sample_size(k + 1) if k + 1 < config.epochs else None
+        eng.enqueue_epoch(k, config.stream, config.epoch_sample_size(k), next_samples=nxt)
         ev = torch.cuda.Event()
         ev.record()
         events.append(ev)

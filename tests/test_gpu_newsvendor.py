@@ -54,14 +54,17 @@ def test_resample_matches_reference_rows(pkg, golden):
     assert np.array_equal(got, g["grad"])
 
 
-@pytest.mark.parametrize("d,S", [(300, 5000), (64, 100_000), (1000, 4096), (7, 12289), (5, 3)])
-def test_counts_vs_oracle(pkg, d, S):
+# counters: word-0 fast path (77; high word set), and a draw carrying into word 1
+@pytest.mark.parametrize("d,S,ctr", [(300, 5000, 77), (64, 100_000, 77), (1000, 4096, 77),
+                                     (7, 12289, 77), (5, 3, 77), (300, 5000, (5 << 64) + 3),
+                                     (300, 5000, (1 << 64) - 100)])
+def test_counts_vs_oracle(pkg, d, S, ctr):
     from paper_2404_11631_b200.instances import gen_newsvendor_instance
     from paper_2404_11631_b200.tasks import NewsvendorProblem
     task = gen_newsvendor_instance(d, pkg.RngStream(42, 0))
     prob = NewsvendorProblem(task, pkg.make_backend("cuda"))
-    prob.resample(pkg.RngStream(42, 2, 77), S)
-    want_rows = orc.sample_demands(task.demand_mean, task.demand_std, S, orc.Stream(42, 2, 77))
+    prob.resample(pkg.RngStream(42, 2, ctr), S)
+    want_rows = orc.sample_demands(task.demand_mean, task.demand_std, S, orc.Stream(42, 2, ctr))
     _check_layout(prob.dev, want_rows)
     rng = np.random.default_rng(d)
     for trial in range(4):

@@ -324,6 +324,9 @@ class NvFwEngine:
         old = self.steps_done.get(k - 2)  # last reader of this slot
         if old is not None:
             self.gen.wait_event(old)
+        # allocate on the caller's stream: the caching allocator keeps blocks per stream,
+        # and a fresh engine's generator stream would otherwise cudaMalloc the layout anew
+        self.dev.ensure_layout(n_samples, slot)
         with torch.cuda.stream(self.gen):
             if time_it:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

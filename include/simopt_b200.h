@@ -298,6 +298,26 @@ int simopt_matvec_t_partials(void* stream, const double* a, int64_t rows, int64_
                              const double* center, const double* x, int64_t chunk, double* out);
 int simopt_fold_partials(void* stream, double* p, int64_t nch, int64_t count, double* out);
 
+/* ------------------------------------------------------------ bit-packed binary features */
+/* Layout: row-major, W = ceil(d/64) u64 words per row, feature j = bit (j&63) of word j>>6.
+ * bernoulli_bits: rows [row_lo, row_hi) of synth_classification's features
+ * (sampling.py:246-255, MSB of each Philox word) straight into bits.
+ * matvec_bits: the fixed-tree row dots (_kernels.py:71-121) over bits -- bit-identical to
+ * simopt_matvec on the 0.0/1.0 matrix.  unpack_bits: 0.0/1.0 fp64 rows. */
+int simopt_bernoulli_bits(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
+                          uint64_t ctr_hi, int64_t row_lo, int64_t row_hi, int64_t d, uint64_t* out);
+int simopt_matvec_bits(void* stream, const uint64_t* bits, int64_t rows, int64_t d, const double* v,
+                       int64_t chunk, double* out);
+int simopt_unpack_bits(void* stream, const uint64_t* bits, int64_t rows, int64_t d, double* out);
+/* simopt_fused_rows (LR_GRAD / LR_HVP modes) on bit-packed features, d <= 16384. */
+int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bits, int64_t rows, int64_t cols,
+                           const double* v, const double* rowaux, double col_scale, int accumulate,
+                           int raw, double* t_out, double* dw_out, double* col_out,
+                           double* scalar_out);
+/* simopt_logistic_xtdx on bit-packed features (DMMA fragments expanded in registers). */
+int simopt_logistic_xtdx_bits(void* stream, const uint64_t* xbits, const double* dw, int64_t n,
+                              int64_t d, double* h);
+
 /* Fused single pass over X (N x d row-major): t_r = x_r . v, wt_r = f(t_r), and
  * col_out[j] = (sum_r x_rj wt_r) * col_scale [- center[j] for MV], in ONE read of X.
  * Replaces each matvec + matvec_t pair of the reference (fast summation order, not

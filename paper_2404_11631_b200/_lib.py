@@ -70,6 +70,12 @@ SIGNATURES = {
     "simopt_matvec_t_partials": [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp],
     "simopt_fold_partials": [_vp, _vp, _i64, _i64, _vp],
     "simopt_nv_lmo_pack": [_vp, _vp, _i64, _vp],
+    "simopt_bernoulli_bits": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _i64, _vp],
+    "simopt_matvec_bits": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
+    "simopt_unpack_bits": [_vp, _vp, _i64, _i64, _vp],
+    "simopt_fused_rows_bits": [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _d, _i32, _i32, _vp, _vp, _vp,
+                               _vp],
+    "simopt_logistic_xtdx_bits": [_vp, _vp, _vp, _i64, _i64, _vp],
     "simopt_project_budget": [_vp, _vp, _vp, _d, _i64, _vp, _vp],
     "simopt_project_box": [_vp, _vp, _d, _d, _i64, _vp],
     "simopt_philox4x32": [_vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _i64, _vp],

@@ -37,9 +37,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-__global__ void __launch_bounds__(128) k_xtdx(const double* __restrict__ x, const double* __restrict__ dw,
-                                              int64_t n, int64_t d, double scale,
-                                              double* __restrict__ h) {
+// kBits: x is the bit-packed binary design matrix (csrc/bits.cu layout, W words per
+// row); a 64-column tile block is exactly one word, so a slab stages 16 words per
+// operand and the DMMA fragments are expanded (0.0 / 1.0) in registers.
+template <bool kBits>
+__global__ void __launch_bounds__(128) k_xtdx(const double* __restrict__ x,
+                                              const uint64_t* __restrict__ xb, int64_t W,
+                                              const double* __restrict__ dw, int64_t n, int64_t d,
+                                              double scale, double* __restrict__ h) {
   // map blockIdx.x -> (bj, bk) with bj <= bk
   const int nt = (int)((d + kTile - 1) / kTile);
   int t = blockIdx.x, bj = 0;
@@ -50,6 +55,7 @@ __global__ void __launch_bounds__(128) k_xtdx(const double* __restrict__ x, cons
   __shared__ __align__(16) double As[2][kSlab][kTile + kPad];
   __shared__ __align__(16) double Bs[2][kSlab][kTile + kPad];
   __shared__ __align__(16) double Ds[2][kSlab];
+  __shared__ __align__(16) uint64_t Aw[2][kSlab], Bw[2][kSlab];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // warp quadrant inside the tile
   double acc[4][4][2];
@@ -59,7 +65,16 @@ __global__ void __launch_bounds__(128) k_xtdx(const double* __restrict__ x, cons
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   auto stage = [&](int buf, int64_t i0) {
-    for (int e = threadIdx.x; e < kSlab * kTile; e += blockDim.x) {
+    if (kBits) {
+      if (threadIdx.x < 2 * kSlab) {
+        const int r = threadIdx.x & (kSlab - 1);
+        const int64_t i = i0 + r;
+        const int64_t wcol = (threadIdx.x < kSlab ? j0 : k0) >> 6;
+        cp_async8(threadIdx.x < kSlab ? (void*)&Aw[buf][r] : (void*)&Bw[buf][r],
+                  xb + (i < n ? i : 0) * W + wcol, i < n);
+      }
+    }
+    for (int e = threadIdx.x; !kBits && e < kSlab * kTile; e += blockDim.x) {
       const int r = e / kTile, c = e % kTile;
       const int64_t i = i0 + r;
       const bool vi = i < n;
@@ -92,10 +107,18 @@ __global__ void __launch_bounds__(128) k_xtdx(const double* __restrict__ x, cons
       const int kr = kk + (lane & 3);
       const double di = Ds[buf][kr];
       double af[4], bf[4];
+      if (kBits) {
+        const uint64_t aw = Aw[buf][kr], bw = Bw[buf][kr];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) af[mi] = As[buf][kr][wm + mi * 8 + (lane >> 2)];
+        for (int mi = 0; mi < 4; ++mi) af[mi] = ((aw >> (wm + mi * 8 + (lane >> 2))) & 1ULL) ? 1.0 : 0.0;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) bf[ni] = di * Bs[buf][kr][wn + ni * 8 + (lane >> 2)];
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = ((bw >> (wn + ni * 8 + (lane >> 2))) & 1ULL) ? di : 0.0;
+      } else {
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) af[mi] = As[buf][kr][wm + mi * 8 + (lane >> 2)];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = di * Bs[buf][kr][wn + ni * 8 + (lane >> 2)];
+      }
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -128,7 +151,21 @@ extern "C" int simopt_logistic_xtdx(void* stream, const double* x, const double*
   const int64_t nt = (d + kTile - 1) / kTile;
   const int64_t tiles = nt * (nt + 1) / 2;
   SIMOPT_REQUIRE(tiles < (1LL << 31), SIMOPT_E_CONFIG, "d too large");
-  k_xtdx<<<(unsigned)tiles, 128, 0, as_stream(stream)>>>(x, dw, n, d, 1.0 / (double)n, h);
+  k_xtdx<false><<<(unsigned)tiles, 128, 0, as_stream(stream)>>>(x, nullptr, 0, dw, n, d,
+                                                                1.0 / (double)n, h);
   SIMOPT_CHECK_LAUNCH("k_xtdx");
+  return SIMOPT_OK;
+}
+
+// Same Hessian from bit-packed binary features (csrc/bits.cu): H = (1/n) X^T diag(dw) X.
+extern "C" int simopt_logistic_xtdx_bits(void* stream, const uint64_t* xbits, const double* dw,
+                                         int64_t n, int64_t d, double* h) {
+  SIMOPT_REQUIRE(n >= 1 && d >= 1, SIMOPT_E_DIMENSION, "empty design matrix");
+  const int64_t nt = (d + kTile - 1) / kTile;
+  const int64_t tiles = nt * (nt + 1) / 2;
+  SIMOPT_REQUIRE(tiles < (1LL << 31), SIMOPT_E_CONFIG, "d too large");
+  k_xtdx<true><<<(unsigned)tiles, 128, 0, as_stream(stream)>>>(nullptr, xbits, (d + 63) / 64, dw, n,
+                                                               d, 1.0 / (double)n, h);
+  SIMOPT_CHECK_LAUNCH("k_xtdx<bits>");
   return SIMOPT_OK;
 }

@@ -26,3 +26,14 @@ def fused_rows(mode: int, x: torch.Tensor, v: torch.Tensor, *, center=None, rowa
               P(rowaux), float(col_scale), 1 if accumulate else 0, 1 if raw else 0, P(t_out), P(dw_out),
               P(col_out), P(scalar_out))
     return col_out
+
+
+def fused_rows_bits(mode: int, bits: torch.Tensor, d: int, v: torch.Tensor, *, rowaux,
+                    col_scale: float = 1.0, col_out=None, scalar_out=None, t_out=None, dw_out=None,
+                    accumulate: bool = True, raw: bool = False):
+    """The logistic passes on bit-packed features (N x ceil(d/64) words)."""
+    P = _lib.ptr
+    _lib.call("simopt_fused_rows_bits", _lib.stream_ptr(), int(mode), P(bits), bits.shape[0], d,
+              P(v), P(rowaux), float(col_scale), 1 if accumulate else 0, 1 if raw else 0, P(t_out),
+              P(dw_out), P(col_out), P(scalar_out))
+    return col_out

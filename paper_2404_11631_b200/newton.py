@@ -30,7 +30,7 @@ import torch
 
 from . import _lib
 from ._tensors import F64, empty, to_host
-from .fused import LR_GRAD, LR_HVP, fused_rows
+from .fused import LR_GRAD, LR_HVP, fused_rows, fused_rows_bits
 from .records import RunRecord, TraceBuilder
 
 _SCALE, _MUL = 3, 4
@@ -49,8 +49,8 @@ class _Logistic:
         self.data, self.b = data, backend
         self.N, self.d = data.n_samples, data.n_features   # N: global rows
         self.shard = getattr(data, "shard", None)
-        nl = max(data.features.shape[0], 1)                 # this rank's rows
-        self.nl = data.features.shape[0]
+        nl = max(data.local_rows, 1)                        # this rank's rows
+        self.nl = data.local_rows
         self.t = empty(nl)       # X w
         self.r = empty(nl)       # residual / hvp weights scratch
         self.dw = empty(nl)      # c (1 - c)
@@ -58,6 +58,12 @@ class _Logistic:
         self.gt = empty(self.d)
         self.buf = empty(self.d + 1)  # [column sums | side sum] allreduced across shards
         self.ones = torch.ones(nl, dtype=F64, device="cuda")
+
+    def _pass(self, mode, v, rowaux, **kw):
+        """One fused read of this rank's rows (bit-packed features when available)."""
+        if self.data.packed:
+            return fused_rows_bits(mode, self.data.bits, self.d, v, rowaux=rowaux, **kw)
+        return fused_rows(mode, self.data.features, v, rowaux=rowaux, **kw)
 
     def _col_sums(self, v, out):
         """Fixed-tree X^T v over all rows (gathered chunk partials when sharded)."""
@@ -101,13 +107,12 @@ class _Logistic:
 
     def fused_gradient(self, w, g_out, loss_sum_out):
         """One pass: g = (1/N) X^T (sigmoid(Xw) - z), sum of loss terms, c(1-c) for the HVPs."""
-        X = self.data.features
         if self.shard is None:
-            fused_rows(LR_GRAD, X, w, rowaux=self.data.labels, col_scale=1.0 / self.N,
-                       col_out=g_out, scalar_out=loss_sum_out, dw_out=self.dw)
+            self._pass(LR_GRAD, w, self.data.labels, col_scale=1.0 / self.N, col_out=g_out,
+                       scalar_out=loss_sum_out, dw_out=self.dw)
             return
         # per-shard raw sums, one allreduce of d+1 doubles
-        fused_rows(LR_GRAD, X, w, rowaux=self.data.labels, col_out=self.buf[:self.d],
+        self._pass(LR_GRAD, w, self.data.labels, col_out=self.buf[:self.d],
                    scalar_out=self.buf[self.d:], dw_out=self.dw, raw=True)
         self.shard.allreduce_(self.buf)
         self._scale(self.buf, g_out)
@@ -115,10 +120,9 @@ class _Logistic:
 
     def fused_hvp(self, v, out):
         """One pass: (1/N) X^T ((c(1-c)) * (X v))."""
-        X = self.data.features
         if self.shard is None:
-            return fused_rows(LR_HVP, X, v, rowaux=self.dw, col_scale=1.0 / self.N, col_out=out)
-        fused_rows(LR_HVP, X, v, rowaux=self.dw, col_out=self.buf[:self.d], raw=True)
+            return self._pass(LR_HVP, v, self.dw, col_scale=1.0 / self.N, col_out=out)
+        self._pass(LR_HVP, v, self.dw, col_out=self.buf[:self.d], raw=True)
         self.shard.allreduce_(self.buf[:self.d])
         return self._scale(self.buf, out)
 
@@ -207,9 +211,12 @@ def logistic_hessian_device(data, dw, out=None) -> torch.Tensor:
     summed over ranks with one allreduce of the d x d matrix."""
     d = data.n_features
     out = torch.empty(d, d, dtype=F64, device="cuda") if out is None else out
-    nl = data.features.shape[0]
+    nl = data.local_rows
     shard = getattr(data, "shard", None)
-    if nl:
+    if nl and data.packed:
+        _lib.call("simopt_logistic_xtdx_bits", _lib.stream_ptr(), _lib.ptr(data.bits), _lib.ptr(dw),
+                  nl, d, _lib.ptr(out))
+    elif nl:
         _lib.call("simopt_logistic_xtdx", _lib.stream_ptr(), _lib.ptr(data.features), _lib.ptr(dw),
                   nl, d, _lib.ptr(out))
     else:

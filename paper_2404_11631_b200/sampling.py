@@ -181,33 +181,58 @@ def sample_indices(n: int, b: int, stream: RngStream) -> np.ndarray:
     return to_host(sample_indices_device(n, b, stream))
 
 
-@dataclass
 class ClassificationData:
-    """Synthetic binary-feature dataset on the device; labels carry the noise (sampling.py:212-226)."""
+    """Synthetic binary-feature dataset on the device; labels carry the noise (sampling.py:212-226).
 
-    features: torch.Tensor  # N x n float64, entries exactly 0.0 / 1.0 (this rank's rows)
-    labels: torch.Tensor    # N float64
-    true_weights: torch.Tensor
-    shard: object = None    # ShardGroup when the rows are split across ranks
-    row_offset: int = 0     # first global row held here
-    total_rows: int | None = None
+    Features are held either as fp64 0.0/1.0 (``features``, the reference's layout)
+    or bit-packed (``bits``: u64 words, csrc/bits.cu layout -- 1/64 of the bytes;
+    config 5's 10^7 x 8192 matrix is 10 GB instead of 655 GB).  Packed data
+    materialises ``features`` on first access (device unpack) for the exact-tree
+    paths; the fused Newton passes and the Hessian read the bits directly.
+    """
+
+    def __init__(self, features=None, labels=None, true_weights=None, shard=None, row_offset=0,
+                 total_rows=None, bits=None, n_features=None):
+        if features is None and bits is None:
+            raise ConfigurationError("need features or bits")
+        self._features = features
+        self.bits = bits
+        self.labels = labels            # this rank's rows, float64
+        self.true_weights = true_weights
+        self.shard = shard              # ShardGroup when the rows are split across ranks
+        self.row_offset = row_offset    # first global row held here
+        self.total_rows = total_rows
+        self._d = features.shape[1] if features is not None else int(n_features)
+
+    @property
+    def features(self) -> torch.Tensor:
+        if self._features is None:
+            x = empty(max(self.local_rows, 0), self._d)
+            _lib.call("simopt_unpack_bits", _lib.stream_ptr(), _lib.ptr(self.bits), self.local_rows,
+                      self._d, _lib.ptr(x))
+            self._features = x
+        return self._features
+
+    @property
+    def packed(self) -> bool:
+        return self.bits is not None
 
     @property
     def n_samples(self) -> int:
         """Global row count N (the 1/N of every full-data average)."""
-        return self.features.shape[0] if self.total_rows is None else self.total_rows
+        return self.local_rows if self.total_rows is None else self.total_rows
 
     @property
     def local_rows(self) -> int:
-        return self.features.shape[0]
+        return (self._features if self._features is not None else self.bits).shape[0]
 
     @property
     def n_features(self) -> int:
-        return self.features.shape[1]
+        return self._d
 
 
 def synth_classification(n_features: int, stream: RngStream, backend=None,
-                         n_rows: int | None = None, shard=None) -> ClassificationData:
+                         n_rows: int | None = None, shard=None, packed: bool = False) -> ClassificationData:
     """sampling.py:229-265, with the row count generalised (reference: n_rows = 30*n).
 
     X[i,j] = [u >= 0.5] is the MSB of the Philox word (written directly as 0.0/1.0);
@@ -218,8 +243,8 @@ def synth_classification(n_features: int, stream: RngStream, backend=None,
     if n_features < 2:
         raise ConfigurationError(f"need at least 2 features, got {n_features}")
     n_rows = 30 * n_features if n_rows is None else int(n_rows)
-    if shard is not None:
-        return _synth_classification_shard(n_features, stream, n_rows, shard)
+    if shard is not None or packed:
+        return _synth_classification_shard(n_features, stream, n_rows, shard, packed=packed)
     total = n_rows * n_features
     x = empty(n_rows, n_features)
     _lib.call("simopt_bernoulli_half", _lib.stream_ptr(), *stream.words(), total, _lib.ptr(x))
@@ -243,25 +268,39 @@ def synth_classification(n_features: int, stream: RngStream, backend=None,
     return ClassificationData(features=x, labels=labels, true_weights=w_true)
 
 
-def _synth_classification_shard(n_features, stream, n_rows, shard, chunk=4096):
-    """Rows [lo, hi) of synth_classification (chunk-aligned), identical to the one-process
-    instance: features are elements [lo*n, hi*n) of the same Philox draw, scores are
-    row-local fixed-tree dots, the median is taken over the allgathered scores, and the
-    replicated sample_indices flips are applied where they fall in [lo, hi)."""
-    lo, hi = shard.range(n_rows, chunk)
+def _synth_classification_shard(n_features, stream, n_rows, shard, chunk=4096, packed=False):
+    """Rows [lo, hi) of synth_classification (chunk-aligned; all rows without a shard),
+    identical to the one-process instance: features are elements [lo*n, hi*n) of the
+    same Philox draw, scores are row-local fixed-tree dots, the median is taken over
+    the allgathered scores, and the replicated sample_indices flips are applied where
+    they fall in [lo, hi).  packed: features generated straight into bits."""
+    lo, hi = shard.range(n_rows, chunk) if shard is not None else (0, n_rows)
     nl = hi - lo
     total = n_rows * n_features
-    x = empty(max(nl, 0), n_features)
-    _lib.call("simopt_bernoulli_half_range", _lib.stream_ptr(), *stream.words(), lo * n_features,
-              hi * n_features, _lib.ptr(x))
+    if packed:
+        W = -(-n_features // 64)
+        bits = torch.empty(max(nl, 0), W, dtype=torch.int64, device=device())
+        _lib.call("simopt_bernoulli_bits", _lib.stream_ptr(), *stream.words(), lo, hi, n_features,
+                  _lib.ptr(bits))
+        x = None
+    else:
+        x = empty(max(nl, 0), n_features)
+        _lib.call("simopt_bernoulli_half_range", _lib.stream_ptr(), *stream.words(), lo * n_features,
+                  hi * n_features, _lib.ptr(x))
     stream.advance(total)
     w_true = standard_normal_device(stream, n_features)
     scores = empty(max(nl, 1))
-    if nl:
+    if nl and packed:
+        _lib.call("simopt_matvec_bits", _lib.stream_ptr(), _lib.ptr(bits), nl, n_features,
+                  _lib.ptr(w_true), chunk, _lib.ptr(scores))
+    elif nl:
         _lib.call("simopt_matvec", _lib.stream_ptr(), _lib.ptr(x), nl, n_features, None, nl,
                   None, _lib.ptr(w_true), chunk, _lib.ptr(scores))
-    counts = [b - a for a, b in shard.ranges(n_rows, chunk)]
-    allsc = shard.allgather_rows(scores[:nl].view(-1, 1), counts).view(-1)
+    if shard is not None:
+        counts = [b - a for a, b in shard.ranges(n_rows, chunk)]
+        allsc = shard.allgather_rows(scores[:nl].view(-1, 1), counts).view(-1)
+    else:
+        allsc = scores[:nl]
     srt = torch.sort(allsc).values
     h = n_rows // 2
     if n_rows % 2:
@@ -276,4 +315,5 @@ def _synth_classification_shard(n_features, stream, n_rows, shard, chunk=4096):
     mine = flip[(flip >= lo) & (flip < hi)] - lo
     labels[mine] = 1.0 - labels[mine]
     return ClassificationData(features=x, labels=labels[:nl], true_weights=w_true, shard=shard,
-                              row_offset=lo, total_rows=n_rows)
+                              row_offset=lo, total_rows=n_rows if shard is not None else None,
+                              bits=bits if packed else None, n_features=n_features)

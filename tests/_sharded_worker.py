@@ -45,6 +45,11 @@ def main(rank, world, port, out):
         res[f"ncg_{int(fused)}_w"] = rec.final_iterate
     rec = newton_explicit(LogisticTask(data), 3, 20, b)
     res["nex_obj"], res["nex_w"] = rec.objectives, rec.final_iterate
+    packed = synth_classification(40, p.RngStream(42, 0), n_rows=9000, shard=sh, packed=True)
+    rec = newton_cg(LogisticTask(packed), 3, 8, b)
+    res["ncgp_obj"], res["ncgp_w"] = rec.objectives, rec.final_iterate
+    rec = newton_explicit(LogisticTask(packed), 3, 20, b)
+    res["nexp_obj"], res["nexp_w"] = rec.objectives, rec.final_iterate
     nv = gen_newsvendor_instance(1003, p.RngStream(42, 0))
     rec = fw_run(NewsvendorProblem(nv, b, shard=sh), FwConfig(2, 6, 5000, p.RngStream(42, 2)), b)
     res["nv_obj"], res["nv_w"] = rec.objectives, rec.final_iterate

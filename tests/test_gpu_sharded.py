@@ -67,9 +67,13 @@ def test_logistic_sharded(ranks):
     assert np.array_equal(r["ncg_0_w"], w)
     np.testing.assert_allclose(r["ncg_1_obj"], objs, rtol=1e-8)
     assert _rel(r["ncg_1_w"], w) < 1e-8
+    np.testing.assert_allclose(r["ncgp_obj"], objs, rtol=1e-8)      # bit-packed shards
+    assert _rel(r["ncgp_w"], w) < 1e-8
     objs, w = orc.newton_explicit(x, z, iterations=3, cg_iters=20)
     np.testing.assert_allclose(r["nex_obj"], objs, rtol=1e-8)
     assert _rel(r["nex_w"], w) < 1e-8
+    np.testing.assert_allclose(r["nexp_obj"], objs, rtol=1e-8)
+    assert _rel(r["nexp_w"], w) < 1e-8
 
 
 def test_newsvendor_sharded(ranks):

@@ -47,26 +47,26 @@ def meanvar(tag, d, n, M=25, epochs=8, fused=False):
                       "algorithmic_GBps": alg * it_s / 1e9}), flush=True)
 
 
-def newton(tag, d, n, k_cg=10, iters=2, fused=True):
+def newton(tag, d, n, k_cg=10, iters=2, fused=True, packed=False):
     from paper_2404_11631_b200.newton import newton_cg
     from paper_2404_11631_b200.sampling import synth_classification
     b = p.make_backend("cuda")
-    task = LogisticTask(synth_classification(d, p.RngStream(42, 0), n_rows=n))
+    task = LogisticTask(synth_classification(d, p.RngStream(42, 0), n_rows=n, packed=packed))
     ms = timed(lambda: newton_cg(task, iters, k_cg, b, fused=fused), warm=1, reps=2)
     it_s = iters / (ms / 1e3)
     passes = k_cg + 1 if fused else 2 * k_cg + 2
     alg = 8 * n * d * (k_cg + 1)  # one read of X per gradient / HVP
-    print(json.dumps({"config": tag, "d": d, "N": n, "k_cg": k_cg, "fused": fused,
+    print(json.dumps({"config": tag, "d": d, "N": n, "k_cg": k_cg, "fused": fused, "packed": packed,
                       "newton_iterations_per_s": it_s,
                       "ms_per_iteration": ms / iters, "passes_over_X": passes,
                       "achieved_GBps": passes * 8 * n * d * it_s / 1e9,
                       "algorithmic_GBps": alg * it_s / 1e9}), flush=True)
 
 
-def xtdx(tag, d, n):
+def xtdx(tag, d, n, packed=False):
     from paper_2404_11631_b200.newton import logistic_hessian_device
     from paper_2404_11631_b200.sampling import synth_classification
-    data = synth_classification(d, p.RngStream(42, 0), n_rows=n)
+    data = synth_classification(d, p.RngStream(42, 0), n_rows=n, packed=packed)
     dw = torch.rand(n, dtype=torch.float64, device="cuda") * 0.25
     H = torch.empty(d, d, dtype=torch.float64, device="cuda")
     ms = timed(lambda: logistic_hessian_device(data, dw, out=H), warm=1, reps=3)
@@ -89,5 +89,8 @@ if __name__ == "__main__":
     if "c3" in which:
         newton("C3 logistic Newton-CG d=1e3 N=1e6 (exact tree)", 1000, 1_000_000, fused=False)
         newton("C3 logistic Newton-CG d=1e3 N=1e6 (fused)", 1000, 1_000_000)
+        newton("C3 logistic Newton-CG d=1e3 N=1e6 (fused, bit-packed features)", 1000, 1_000_000,
+               packed=True)
     if "xtdx" in which:
         xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (fp64 X)", 8192, 125_000)
+        xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X)", 8192, 125_000, packed=True)

@@ -314,6 +314,15 @@ int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bits, int64_t
                            const double* v, const double* rowaux, double col_scale, int accumulate,
                            int raw, double* t_out, double* dw_out, double* col_out,
                            double* scalar_out);
+/* Binary X on the integer tensor cores (csrc/hessian_i8.cu): bits_to_u8t builds X^T as u8 in
+ * sample blocks [np/ch][d][ch + 32] (ch, np from u8t_geometry; padded rows are zero); xtdx_i8 computes
+ * H = (1/n) X^T diag(dw) X exactly for dw rounded to 2^-41 (5 x 8-bit limbs, u8 IMMA with
+ * int32 accumulation); limbs = u8 scratch [5][np]. */
+int simopt_u8t_geometry(int64_t n, int64_t* ch, int64_t* np);
+int simopt_bits_to_u8t(void* stream, const uint64_t* bits, int64_t rows, int64_t d, int64_t np,
+                       uint8_t* out);
+int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
+                            const double* dw, uint8_t* limbs, double* h);
 /* simopt_logistic_xtdx on bit-packed features (DMMA fragments expanded in registers). */
 int simopt_logistic_xtdx_bits(void* stream, const uint64_t* xbits, const double* dw, int64_t n,
                               int64_t d, double* h);

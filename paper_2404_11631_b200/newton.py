@@ -204,16 +204,28 @@ def newton_cg(task, iterations: int, cg_iters: int, backend, fused: bool = True)
     return _run(task, iterations, backend, step, "classification-newton-cg", fused)
 
 
-def logistic_hessian_device(data, dw, out=None) -> torch.Tensor:
-    """H = (1/N) X^T diag(dw) X on the FP64 tensor pipe (tests/test_tasks.py:297-299 oracle).
+def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.Tensor:
+    """H = (1/N) X^T diag(dw) X (tests/test_tasks.py:297-299 oracle, rtol 1e-10).
 
+    method: "dmma" -- FP64 tensor pipe (csrc/hessian.cu; fp64 or bit-packed X);
+    "i8" -- bit-packed binary X only: exact 5-limb split of dw on the integer tensor
+    cores (csrc/hessian_i8.cu); "auto" = "i8" for bit-packed data, else "dmma".
     Row-sharded data: each rank's (1/N_loc) X_loc^T D X_loc is weighted by N_loc/N and
     summed over ranks with one allreduce of the d x d matrix."""
     d = data.n_features
     out = torch.empty(d, d, dtype=F64, device="cuda") if out is None else out
     nl = data.local_rows
     shard = getattr(data, "shard", None)
-    if nl and data.packed:
+    if method == "auto":
+        method = "i8" if data.packed else "dmma"
+    if nl and method == "i8":
+        xt, np_ = data.feature_major_u8()
+        limbs = getattr(data, "_limbs", None)
+        if limbs is None or limbs.numel() != 5 * np_:
+            limbs = data._limbs = torch.empty(5 * np_, dtype=torch.uint8, device="cuda")
+        _lib.call("simopt_logistic_xtdx_i8", _lib.stream_ptr(), _lib.ptr(xt), np_, nl, d,
+                  _lib.ptr(dw), _lib.ptr(limbs), _lib.ptr(out))
+    elif nl and data.packed:
         _lib.call("simopt_logistic_xtdx_bits", _lib.stream_ptr(), _lib.ptr(data.bits), _lib.ptr(dw),
                   nl, d, _lib.ptr(out))
     elif nl:
@@ -228,12 +240,13 @@ def logistic_hessian_device(data, dw, out=None) -> torch.Tensor:
     return out
 
 
-def newton_explicit(task, iterations: int, cg_iters: int, backend, fused: bool = True) -> RunRecord:
+def newton_explicit(task, iterations: int, cg_iters: int, backend, fused: bool = True,
+                    hessian: str = "auto") -> RunRecord:
     """Newton with the explicit X^T D X Hessian and a CG solve (BASELINE.json configs[4])."""
     d = task.data.n_features
     H = torch.empty(d, d, dtype=F64, device="cuda")
 
     def step(L, g, p, dot):
-        logistic_hessian_device(L.data, L.dw, out=H)
+        logistic_hessian_device(L.data, L.dw, out=H, method=hessian)
         _cg(lambda v, out: backend.matvec_device(H, v, out=out), g, d, cg_iters, dot, p)
     return _run(task, iterations, backend, step, "classification-newton-explicit", fused)

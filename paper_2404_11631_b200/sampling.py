@@ -217,6 +217,23 @@ class ClassificationData:
     def packed(self) -> bool:
         return self.bits is not None
 
+    def feature_major_u8(self):
+        """(X^T as u8 in sample blocks, np): the integer-tensor-core Hessian's operand, built once."""
+        if getattr(self, "_u8t", None) is None:
+            if not self.packed:
+                raise ConfigurationError("the u8 Hessian operand is built from bit-packed features")
+            import ctypes
+            n = self.local_rows
+            ch, npv = ctypes.c_int64(), ctypes.c_int64()
+            _lib.call("simopt_u8t_geometry", n, ctypes.byref(ch), ctypes.byref(npv))
+            np_ = npv.value
+            xt = torch.empty((np_ // ch.value) * self._d * (ch.value + 32), dtype=torch.uint8,
+                             device=device())
+            _lib.call("simopt_bits_to_u8t", _lib.stream_ptr(), _lib.ptr(self.bits), n, self._d, np_,
+                      _lib.ptr(xt))
+            self._u8t = (xt, np_)
+        return self._u8t
+
     @property
     def n_samples(self) -> int:
         """Global row count N (the 1/N of every full-data average)."""

@@ -63,13 +63,13 @@ def newton(tag, d, n, k_cg=10, iters=2, fused=True, packed=False):
                       "algorithmic_GBps": alg * it_s / 1e9}), flush=True)
 
 
-def xtdx(tag, d, n, packed=False):
+def xtdx(tag, d, n, packed=False, method="dmma"):
     from paper_2404_11631_b200.newton import logistic_hessian_device
     from paper_2404_11631_b200.sampling import synth_classification
     data = synth_classification(d, p.RngStream(42, 0), n_rows=n, packed=packed)
     dw = torch.rand(n, dtype=torch.float64, device="cuda") * 0.25
     H = torch.empty(d, d, dtype=torch.float64, device="cuda")
-    ms = timed(lambda: logistic_hessian_device(data, dw, out=H), warm=1, reps=3)
+    ms = timed(lambda: logistic_hessian_device(data, dw, out=H, method=method), warm=1, reps=3)
     flops_syrk = n * d * (d + 1)  # SYRK convention
     print(json.dumps({"config": tag, "d": d, "N": n, "ms": ms,
                       "tflops_syrk_convention": flops_syrk / (ms / 1e3) / 1e12,
@@ -93,4 +93,7 @@ if __name__ == "__main__":
                packed=True)
     if "xtdx" in which:
         xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (fp64 X)", 8192, 125_000)
-        xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X)", 8192, 125_000, packed=True)
+        xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X, DMMA)", 8192, 125_000,
+             packed=True)
+        xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X, u8 IMMA limbs)", 8192,
+             125_000, packed=True, method="i8")

@@ -54,7 +54,7 @@ __device__ __forceinline__ void imma(int (&c)[4], const unsigned (&a)[4], unsign
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
-    k_xtdx_i8(const uint8_t* __restrict__ xt, int64_t ch, int64_t d, const uint8_t* __restrict__ limb,
+    k_xtdx_i8(const uint8_t* __restrict__ xt, int lg_ch, int64_t d, const uint8_t* __restrict__ limb,
               int64_t s0, int64_t s1, double scale, int beta, double* __restrict__ h) {
   const int nt = (int)((d + kBM - 1) / kBM);
   int t = blockIdx.x, bj = 0;
@@ -76,12 +76,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int c = 0; c < 4; ++c) acc[a][b][c] = 0;
 
   const int64_t nslab = (s1 - s0) / kBK;
+  // per-thread constants of the stage copies: this thread's A/B feature rows in a block
+  const int64_t ch = 1LL << lg_ch, rs = ch + kRowPad;
+  const int srow = tid >> 1, half = tid & 1;
+  const bool va = i0 + srow < d, vb = j0 + srow < d;
+  const int64_t offa = (va ? i0 + srow : 0) * rs + half * 16;
+  const int64_t offb = (vb ? j0 + srow : 0) * rs + half * 16;
+  uint8_t* sa = &As[0][srow * kRS + half * 16];
+  uint8_t* sb = &Bs[0][srow * kRS + half * 16];
   auto stage = [&](int buf, int64_t s) {
-    const int row = tid >> 1, half = tid & 1;
-    const int64_t rs = ch + kRowPad;
-    const uint8_t* blk = xt + (s / ch) * (d * rs) + (s % ch) + half * 16;  // sample block of s
-    cp16(&As[buf][row * kRS + half * 16], blk + (i0 + row < d ? i0 + row : 0) * rs, i0 + row < d);
-    cp16(&Bs[buf][row * kRS + half * 16], blk + (j0 + row < d ? j0 + row : 0) * rs, j0 + row < d);
+    const uint8_t* blk = xt + (s >> lg_ch) * (d * rs) + (s & (ch - 1));  // sample block of s
+    cp16(sa + buf * (kBM * kRS), blk + offa, va);
+    cp16(sb + buf * (kBM * kRS), blk + offb, vb);
     if (tid < 2) cp16(&Ls[buf][tid * 16], limb + s + tid * 16, true);
     asm volatile("cp.async.commit_group;\n" ::);
   };
@@ -186,13 +192,13 @@ int egrid(int64_t n) {
 
 }  // namespace
 
-// Sample-block width ch and padded row count np of the u8 operand for n rows; the operand
-// occupies (np / ch) * d * (ch + 32) bytes.
+// Sample-block width ch (a power of two, 32..4096) and padded row count np of the u8
+// operand for n rows; the operand occupies (np / ch) * d * (ch + 32) bytes.
 extern "C" int simopt_u8t_geometry(int64_t n, int64_t* ch, int64_t* np) {
-  const int64_t n32 = ceil_div(n < 1 ? 1 : n, 32) * 32;
-  const int64_t c = n32 < 4096 ? n32 : 4096;
+  int64_t c = 32;
+  while (c < 4096 && c < n) c <<= 1;
   *ch = c;
-  *np = ceil_div(n32, c) * c;
+  *np = ceil_div(n < 1 ? 1 : n, c) * c;
   return SIMOPT_OK;
 }
 
@@ -217,6 +223,8 @@ extern "C" int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t 
   simopt_u8t_geometry(n, &ch, &np_want);
   SIMOPT_REQUIRE(np == np_want, SIMOPT_E_CONFIG, "np must come from simopt_u8t_geometry");
   cudaStream_t st = as_stream(stream);
+  int lg = 0;
+  while ((1LL << lg) < ch) ++lg;
   k_limbs<<<egrid(np), 256, 0, st>>>(dw, n, np, limbs);
   SIMOPT_CHECK_LAUNCH("k_limbs");
   const int64_t nt = (d + kBM - 1) / kBM;
@@ -227,7 +235,7 @@ extern "C" int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t 
     const int64_t c1 = c0 + kChunk < np ? c0 + kChunk : np;
     for (int k = 0; k < kLimbs; ++k) {
       const double scale = ldexp(1.0, kLimbBits * k - kFixBits) / (double)n;
-      k_xtdx_i8<<<(unsigned)tiles, kThreads, 0, st>>>(xt, ch, d, limbs + k * np, c0, c1, scale, beta, h);
+      k_xtdx_i8<<<(unsigned)tiles, kThreads, 0, st>>>(xt, lg, d, limbs + k * np, c0, c1, scale, beta, h);
       SIMOPT_CHECK_LAUNCH("k_xtdx_i8");
       beta = 1;
     }

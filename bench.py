@@ -12,9 +12,10 @@ draws, 8 GB) + 25 FW iterations; value = FW iterations/s.
 
 N > 1 shards the SAME problem's products across the N GPUs (strong scaling):
 each rank draws and scans only its products (Philox counter offset, no RNG
-communication); every FW step exchanges the per-rank LMO argmins (NCCL
-allgather of 3 doubles per rank) and each epoch's recorded sums (one
-allreduce).  See DESIGN.md section 5.
+communication); every FW step exchanges the per-rank LMO argmins inside the
+step kernel over NVLink peer memory (CUDA IPC mailboxes; NCCL allgather if IPC
+is unavailable) and each epoch's recorded sums once (NCCL allreduce).  See
+DESIGN.md section 5.
 """
 from __future__ import annotations
 
@@ -284,8 +285,11 @@ def run_ours(args, rank, world):
         "config": {"workload": "newsvendor C2 (BASELINE.json configs[1])", "d": D, "S": S, "M": M,
                    "seed": SEED, "step": "1 resampling epoch = 1 resample + 25 FW iterations",
                    "l2": "inputs larger than L2 (8 GB demands per epoch)",
-                   "parallelism": (f"products sharded x{world} ({args.dist_backend} LMO exchange "
-                                   "per step)") if world > 1 else "single GPU"},
+                   "parallelism": (f"products sharded x{world}; per-step LMO exchange "
+                                   + ("inside the step kernel over NVLink peer memory (CUDA IPC)"
+                                      if eng.mailbox is not None else
+                                      f"by {args.dist_backend} allgather"))
+                   if world > 1 else "single GPU"},
         "roofline": roofline,
         "clocks": clk.summary(),
         "gpu_launches": launches_per_epoch * args.steps,

@@ -180,6 +180,7 @@ typedef struct NvState {
 
 #define NV_FLAG_NAN_GRADIENT 1 /* InvalidGradient at this step's LMO (lmo.py:78-79) */
 #define NV_FLAG_NEGATIVE 2     /* iterate < -FEAS_TOL after this step (tasks.py:328) */
+#define NV_FLAG_EXCHANGE_TIMEOUT 4 /* peer-memory LMO exchange gave up (a peer never arrived) */
 
 /* One fused FW kernel (frank_wolfe.py:106-117 for NewsvendorProblem):
  *  do_update: x <- (gamma*((-1*x) + s)) + x with the vertex in *state, objective
@@ -206,8 +207,24 @@ typedef struct NvIterArgs {
   double* part_v;
   int64_t* part_i;
   int64_t part_capacity;
+  /* Product-sharded LMO fused into the step over NVLink peer memory (NULL: off).
+   * peer_mb[q] = rank q's mailbox (simopt_peer_*), mailbox layout
+   * [2 parities][world][4]: {value, global index, vertex value, sequence}.  The last
+   * block publishes this rank's argmin to every peer, waits for all `world` entries
+   * of sequence `seq`, and applies the global first-argmin (as simopt_nv_lmo_apply). */
+  double* const* peer_mb;
+  int64_t world, rank, j0;
+  uint64_t seq;
 } NvIterArgs;
 int simopt_nv_iter(void* stream, const NvIterArgs* args);
+
+/* Peer mailboxes (CUDA IPC over NVLink/NVSwitch): alloc returns a zeroed device buffer and
+ * its 64-byte IPC handle; open maps a peer's handle (cudaIpcMemLazyEnablePeerAccess);
+ * close/free release them. */
+int simopt_peer_alloc(int64_t bytes, void** ptr, void* handle64);
+int simopt_peer_open(const void* handle64, void** ptr);
+int simopt_peer_close(void* ptr);
+int simopt_peer_free(void* ptr);
 
 /* Product-sharded LMO: every rank owns products [j0, j0 + d_local).
  * pack: send[0..2] = {best_val, j* + j0, sval} of this rank's k_nv_iter argmin.

@@ -70,6 +70,10 @@ SIGNATURES = {
     "simopt_matvec_t_partials": [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp],
     "simopt_fold_partials": [_vp, _vp, _i64, _i64, _vp],
     "simopt_nv_lmo_pack": [_vp, _vp, _i64, _vp],
+    "simopt_peer_alloc": [_i64, _vp, _vp],
+    "simopt_peer_open": [_vp, _vp],
+    "simopt_peer_close": [_vp],
+    "simopt_peer_free": [_vp],
     "simopt_bernoulli_bits": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _i64, _vp],
     "simopt_matvec_bits": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
     "simopt_unpack_bits": [_vp, _vp, _i64, _i64, _vp],

@@ -13,6 +13,7 @@
 // threshold with the exact glibc Box-Muller -- the count is the reference's
 // integer, bit for bit, for every query.
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "fw.cuh"
@@ -244,6 +245,65 @@ namespace {
 
 constexpr int kIterWarps = 8;
 
+// Fused product-shard LMO exchange over NVLink peer memory (one thread of the step's
+// last block): publish (value, global index, vertex value) into slot `rank` of every
+// peer's mailbox, release the sequence word, then acquire all `world` entries of this
+// sequence from the own mailbox and keep the global first-argmin -- the allgather +
+// simopt_nv_lmo_apply of the NCCL path in one kernel, no host round trip.  Mailboxes are
+// double-buffered by sequence parity (a rank cannot run two exchanges ahead).  A peer
+// that never arrives ends the wait after 20 s with NV_FLAG_EXCHANGE_TIMEOUT.
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __noinline__ void nv_peer_exchange(const NvIterArgs& a, ArgMin r, double sval, NvState* st) {
+  const int64_t par = (int64_t)(a.seq & 1ULL), W = a.world;
+  for (int64_t q = 0; q < W; ++q) {
+    double* slot = a.peer_mb[q] + (par * W + a.rank) * 4;
+    volatile double* vs = slot;
+    vs[0] = r.v;
+    vs[1] = (double)(r.i + a.j0);  // exact: product indices < 2^53
+    vs[2] = sval;
+    __threadfence_system();
+    st_release_u64(reinterpret_cast<uint64_t*>(slot + 3), a.seq);
+  }
+  const double* mb = a.peer_mb[a.rank] + par * W * 4;
+  ArgMin best{INFINITY, INT64_MAX};
+  double bs = 0.0;
+  const uint64_t t0 = globaltimer();
+  bool timed_out = false;
+  for (int64_t q = 0; q < W; ++q) {
+    const double* e = mb + q * 4;
+    while (ld_acquire_u64(reinterpret_cast<const uint64_t*>(e + 3)) != a.seq) {
+      if (globaltimer() - t0 > 20000000000ULL) { timed_out = true; break; }
+    }
+    if (timed_out) break;
+    const volatile double* ve = e;
+    const ArgMin c{ve[0], (int64_t)ve[1]};
+    const ArgMin m = amin(best, c);
+    if (m.i != best.i || m.v != best.v) bs = ve[2];
+    best = m;
+  }
+  if (timed_out) {
+    atomicOr(&a.flags[a.grad_step], NV_FLAG_EXCHANGE_TIMEOUT);
+    best = ArgMin{r.v, r.i + a.j0};
+    bs = sval;
+  }
+  st->jstar = (best.i >= a.j0 && best.i < a.j0 + a.d) ? best.i - a.j0 : -1;
+  st->sval = bs;
+  st->best_val = best.v;
+}
+
 // Fused FW step for the newsvendor:
 //   (1) if do_update: x_j <- (gamma * ((-1 * x_j) + s_j)) + x_j with the vertex of the
 //       previous LMO (frank_wolfe.py:69-82), record x_j < -FEAS_TOL, objective term;
@@ -316,10 +376,15 @@ __global__ void __launch_bounds__(kIterWarps * 32, 3)
     for (int w = 1; w < kIterWarps; ++w) r = amin(r, warp_best[w]);
     // lmo_single_budget (lmo.py:84-89): s_j* = C / c_j* iff g_j* < 0
     const double gj = a.g[r.i];
-    st->jstar = r.i;
-    st->sval = (gj < 0.0) ? a.budget / a.c[r.i] : 0.0;
-    st->best_val = r.v;
+    const double sval = (gj < 0.0) ? a.budget / a.c[r.i] : 0.0;
     st->blocks_done = 0;
+    if (a.peer_mb == nullptr) {
+      st->jstar = r.i;
+      st->sval = sval;
+      st->best_val = r.v;
+    } else {
+      nv_peer_exchange(a, r, sval, st);
+    }
   }
 }
 
@@ -567,5 +632,32 @@ extern "C" int simopt_nv_approx_error(void* stream, uint64_t seed, uint64_t sid,
                                                          chi, n / 4,
                                                          reinterpret_cast<unsigned long long*>(out_max));
   SIMOPT_CHECK_LAUNCH("k_nv_approx_error");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_peer_alloc(int64_t bytes, void** ptr, void* handle64) {
+  SIMOPT_REQUIRE(bytes > 0, SIMOPT_E_CONFIG, "mailbox size must be > 0");
+  SIMOPT_CUDA(cudaMalloc(ptr, (size_t)bytes));
+  SIMOPT_CUDA(cudaMemset(*ptr, 0xff, (size_t)bytes));  // sequence words never match at start
+  cudaIpcMemHandle_t h;
+  SIMOPT_CUDA(cudaIpcGetMemHandle(&h, *ptr));
+  memcpy(handle64, &h, sizeof(h));
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_peer_open(const void* handle64, void** ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  SIMOPT_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_peer_close(void* ptr) {
+  SIMOPT_CUDA(cudaIpcCloseMemHandle(ptr));
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_peer_free(void* ptr) {
+  SIMOPT_CUDA(cudaFree(ptr));
   return SIMOPT_OK;
 }

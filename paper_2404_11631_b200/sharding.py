@@ -143,3 +143,62 @@ def allreduce_argmin(value: float, index: int, group=None, device="cpu") -> tupl
         if best is None or v < best[0] or (v == best[0] and i < best[1]):
             best = (v, i)
     return best
+
+
+class PeerMailbox:
+    """Per-rank device mailbox mapped into every peer over CUDA IPC (NVLink/NVSwitch).
+
+    Used by the newsvendor step kernel to exchange its LMO candidate with all ranks
+    inside the kernel (csrc/newsvendor.cu nv_peer_exchange) instead of an NCCL
+    allgather between launches.  Layout per rank: [2 parities][world][4 doubles].
+    The sequence counter is monotonic for the mailbox's lifetime, so stale entries
+    of earlier runs never match.  ``get`` returns None on every rank when any rank
+    cannot map its peers (the caller then uses the NCCL exchange).
+    """
+
+    _cache = {}
+
+    def __init__(self, shard: ShardGroup):
+        import ctypes
+
+        from . import _lib
+        lib = _lib.load()
+        self.shard = shard
+        W = shard.world
+        self._own = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        _lib.check(lib.simopt_peer_alloc(2 * W * 4 * 8, ctypes.byref(self._own), handle))
+        handles = [None] * W
+        dist.all_gather_object(handles, bytes(handle), group=shard.group)
+        ptrs, self._opened = [], []
+        for q in range(W):
+            if q == shard.rank:
+                ptrs.append(self._own.value)
+                continue
+            p = ctypes.c_void_p()
+            _lib.check(lib.simopt_peer_open(handles[q], ctypes.byref(p)))
+            self._opened.append(p)
+            ptrs.append(p.value)
+        self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
+        self.seq = 0
+
+    def next_seq(self) -> int:
+        self.seq += 1
+        return self.seq
+
+    @classmethod
+    def get(cls, shard: ShardGroup):
+        key = (id(shard.group), shard.rank, shard.world)
+        if key in cls._cache:
+            return cls._cache[key]
+        try:
+            mb, ok = cls(shard), 1.0
+        except Exception:  # noqa: BLE001 -- IPC unavailable here: every rank falls back
+            mb, ok = None, 0.0
+        flag = torch.tensor([ok], dtype=torch.float64, device="cuda" if shard.nccl else "cpu")
+        if shard.world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=shard.group)
+        if float(flag.item()) < 1.0:
+            mb = None
+        cls._cache[key] = mb
+        return mb

@@ -16,8 +16,8 @@ import torch
 
 from . import _lib
 from ._tensors import F64, empty, is_tensor, like_input, mat_dev, to_dev, to_host, vec_dev
-from .errors import (ConfigurationError, DimensionMismatch, InsufficientSamples, InvalidConstraint,
-                     InvalidGradient, RunAborted)
+from .errors import (ConfigurationError, DeviceError, DimensionMismatch, InsufficientSamples,
+                     InvalidConstraint, InvalidGradient, RunAborted)
 from .frank_wolfe import fw_step_size
 from .fused import MV, fused_rows
 from .lmo import SimplexSlackSet, lmo_simplex_slack, lmo_single_budget
@@ -45,6 +45,8 @@ class NvIterArgs(ctypes.Structure):
         ("flags", ctypes.c_void_p), ("state", ctypes.c_void_p),
         ("part_v", ctypes.c_void_p), ("part_i", ctypes.c_void_p),
         ("part_capacity", ctypes.c_int64),
+        ("peer_mb", ctypes.c_void_p), ("world", ctypes.c_int64), ("rank", ctypes.c_int64),
+        ("j0", ctypes.c_int64), ("seq", ctypes.c_uint64),
     ]
 
 
@@ -57,6 +59,7 @@ def nv_geometry():
 
 NV_FLAG_NAN_GRADIENT = 1
 NV_FLAG_NEGATIVE = 2
+NV_FLAG_EXCHANGE_TIMEOUT = 4
 _NV_PART_CAPACITY = 16 * 148
 
 
@@ -193,12 +196,16 @@ class NewsvendorProblem:
 
     name = "newsvendor"
 
-    def __init__(self, task: NewsvendorTask, backend, shard=None):
+    def __init__(self, task: NewsvendorTask, backend, shard=None, exchange: str = "peer"):
         self.task = task
         self.backend = backend
         # product sharding: products are independent; each FW step exchanges only the
-        # per-rank LMO candidates (allgather of 3 doubles per rank)
+        # per-rank LMO candidates -- "peer": inside the step kernel over NVLink peer
+        # memory (sharding.PeerMailbox); "nccl": an allgather of 3 doubles per rank
         self.shard = shard
+        if exchange not in ("peer", "nccl"):
+            raise ConfigurationError(f"unknown exchange {exchange!r}")
+        self.exchange = exchange
         j0, j1 = (0, task.dimension) if shard is None else shard.range(task.dimension, 4)
         self.dev = _NvDevice(task, j0, j1)
         self._stream = None
@@ -292,10 +299,17 @@ class NvFwEngine:
                                                _NV_PART_CAPACITY)
         self.args = a
         self.shard = prob.shard
+        self.mailbox = None
+        if self.shard is not None and prob.exchange == "peer":
+            from .sharding import PeerMailbox
+            self.mailbox = PeerMailbox.get(self.shard)  # None if IPC is unavailable (all ranks)
+        if self.mailbox is not None:
+            a.peer_mb = self.mailbox.ptrs.data_ptr()
+            a.world, a.rank, a.j0 = self.shard.world, self.shard.rank, dev.j0
         if self.shard is not None:
             self.send = empty(3)
-            # per epoch: spent[M] | objs[M] | nan flags[M+1] | negative flags[M+1]
-            self.red = empty(2, 4 * M + 2)  # double-buffered by epoch parity
+            # per epoch: spent[M] | objs[M] | nan[M+1] | negative[M+1] | timeout[M+1] flags
+            self.red = empty(2, 5 * M + 3)  # double-buffered by epoch parity
         self.lib = _lib.load()
         self.t0 = None
         self.resample_events = []
@@ -368,6 +382,7 @@ class NvFwEngine:
         a.x_in = a.x = self.xs[t0 % H].data_ptr()  # gradient + LMO at the epoch's first iterate
         a.terms = None  # objective terms are formed on the side stream
         a.do_update, a.do_grad, a.step, a.grad_step, a.gamma = 0, 1, t0, t0, 0.0
+        self._seq()
         _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
         self._exchange(sp)
         for m in range(M):
@@ -380,6 +395,8 @@ class NvFwEngine:
             a.x_in, a.x = xin.data_ptr(), xout.data_ptr()
             a.gamma = fw_step_size(k, M, m)
             a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), t, t + 1
+            if m + 1 < M:
+                self._seq()
             _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
             if m + 1 < M:
                 self._exchange(sp)
@@ -409,16 +426,23 @@ class NvFwEngine:
                 r[M:2 * M].copy_(self.objs[lo:hi])
                 f = self.flags[lo:hi + 1]
                 r[2 * M:3 * M + 1].copy_((f & NV_FLAG_NAN_GRADIENT).to(F64))
-                r[3 * M + 1:].copy_((f & NV_FLAG_NEGATIVE).to(F64))
+                r[3 * M + 1:4 * M + 2].copy_((f & NV_FLAG_NEGATIVE).to(F64))
+                r[4 * M + 2:].copy_((f & NV_FLAG_EXCHANGE_TIMEOUT).to(F64))
                 self.shard.allreduce_(r)
                 done = torch.cuda.Event()
                 done.record(self.side)
             self.side_done[t0 + M - 1] = done
         self.epoch_done[k] = self.side_done[t0 + M - 1]
 
+    def _seq(self):
+        """Next exchange sequence number (monotonic per mailbox, across runs)."""
+        if self.mailbox is not None:
+            self.args.seq = self.mailbox.next_seq()
+
     def _exchange(self, sp):
-        """Global LMO vertex over product shards: allgather the per-rank argmins."""
-        if self.shard is None:
+        """Global LMO vertex over product shards: allgather the per-rank argmins (NCCL
+        path; the peer path exchanges inside the step kernel)."""
+        if self.shard is None or self.mailbox is not None:
             return
         lib, P = self.lib, _lib.ptr
         _lib.check(lib.simopt_nv_lmo_pack(sp, P(self.state), self.dev.j0, P(self.send)))
@@ -445,12 +469,15 @@ class NvFwEngine:
             r = to_host(self.red[k % 2])
             sp_, ob = r[:M], r[M:2 * M]
             fl = ((r[2 * M:3 * M + 1] > 0) * NV_FLAG_NAN_GRADIENT
-                  + (r[3 * M + 1:] > 0) * NV_FLAG_NEGATIVE).astype(np.int32)
+                  + (r[3 * M + 1:4 * M + 2] > 0) * NV_FLAG_NEGATIVE
+                  + (r[4 * M + 2:] > 0) * NV_FLAG_EXCHANGE_TIMEOUT).astype(np.int32)
         ts = to_host(self.stamps[lo:hi])
         if self.t0 is None:
             self.t0 = int(self.stamps[self.T].item())
         for i in range(M):
             t = lo + i
+            if fl[i] & NV_FLAG_EXCHANGE_TIMEOUT:
+                raise DeviceError(f"peer-memory LMO exchange timed out at step {t + 1}")
             if fl[i] & NV_FLAG_NAN_GRADIENT:
                 return t, InvalidGradient("gradient contains NaN"), self.iterate(t)
             if (fl[i] & NV_FLAG_NEGATIVE) or not sp_[i] <= self.dev.budget * (1.0 + FEAS_TOL):

@@ -51,8 +51,12 @@ def main(rank, world, port, out):
     rec = newton_explicit(LogisticTask(packed), 3, 20, b)
     res["nexp_obj"], res["nexp_w"] = rec.objectives, rec.final_iterate
     nv = gen_newsvendor_instance(1003, p.RngStream(42, 0))
-    rec = fw_run(NewsvendorProblem(nv, b, shard=sh), FwConfig(2, 6, 5000, p.RngStream(42, 2)), b)
-    res["nv_obj"], res["nv_w"] = rec.objectives, rec.final_iterate
+    for ex in ("nccl", "peer"):
+        rec = fw_run(NewsvendorProblem(nv, b, shard=sh, exchange=ex),
+                     FwConfig(2, 6, 5000, p.RngStream(42, 2)), b)
+        res[f"nv_{ex}_obj"], res[f"nv_{ex}_w"] = rec.objectives, rec.final_iterate
+    from paper_2404_11631_b200.sharding import PeerMailbox
+    res["nv_peer_used"] = np.array([PeerMailbox.get(sh) is not None])
     np.savez(os.path.join(out, f"rank{rank}.npz"), **res)
     dist.barrier()
     dist.destroy_process_group()

@@ -80,5 +80,7 @@ def test_newsvendor_sharded(ranks):
     task = orc.gen_newsvendor_instance(1003, orc.Stream(42, 0))
     objs, x = orc.fw_run_newsvendor(task, 2, 6, 5000, orc.Stream(42, 2))
     r = ranks[0]
-    assert np.array_equal(r["nv_w"], x)                    # counts are exact integers
-    np.testing.assert_allclose(r["nv_obj"], objs, rtol=1e-13)
+    assert bool(r["nv_peer_used"][0])                      # the in-kernel NVLink/IPC exchange ran
+    for ex in ("nccl", "peer"):
+        assert np.array_equal(r[f"nv_{ex}_w"], x)          # counts are exact integers
+        np.testing.assert_allclose(r[f"nv_{ex}_obj"], objs, rtol=1e-13)

@@ -340,6 +340,10 @@ int simopt_bits_to_u8t(void* stream, const uint64_t* bits, int64_t rows, int64_t
                        uint8_t* out);
 int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
                             const double* dw, uint8_t* limbs, double* h);
+/* Same result on the 5th-generation tensor cores: tcgen05.mma.kind::i8 with the five limb
+ * accumulators resident in TMEM (128 x 96 tiles, one CTA per SM). */
+int simopt_logistic_xtdx_tc(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
+                            const double* dw, uint8_t* limbs, double* h);
 /* simopt_logistic_xtdx on bit-packed features (DMMA fragments expanded in registers). */
 int simopt_logistic_xtdx_bits(void* stream, const uint64_t* xbits, const double* dw, int64_t n,
                               int64_t d, double* h);

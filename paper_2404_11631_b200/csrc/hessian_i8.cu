@@ -20,6 +20,10 @@
 // triangle, 8 warps of 64x32, 32-sample k-slabs in a 3-stage cp.async ring, fragments
 // by ldmatrix (48-byte padded rows: conflict-free), the limb applied to the B fragment
 // with two integer ops per 4 samples: (b * 255) & L.
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 namespace {
@@ -150,6 +154,221 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
 }
 
+// ---------------------------------------------------------------------------------------
+// tcgen05 version (5th-gen tensor cores, TMEM accumulators).  One CTA (4 warps) owns a
+// 128 (i) x 96 (j) tile of H and keeps all five limb accumulators D_k (s32, 128 lanes x
+// 96 columns each = 480 of the SM's 512 TMEM columns) resident for the whole sample
+// range.  Per 32-sample k-step: cp.async brings the A tile (X, 128 x 32 B) and the raw B
+// tile (X, 96 x 32 B) straight into the SWIZZLE_NONE K-major canonical layout (8-row x
+// 16-byte core matrices), all threads expand B into the five limb-scaled copies
+// (b * 255) & L_k, and one elected thread issues five tcgen05.mma.kind::i8 (M=128, N=96,
+// K=32) and commits them to the stage's mbarrier, which frees the stage four steps later.
+// Epilogue: tcgen05.ld of the five accumulators, fp64 combination 2^(8k-41)/n, upper
+// entries and their mirrors.  (tools/micro/tc_i8.cu is the single-MMA smoke test.)
+constexpr int kTM = 128, kTN = 96;
+constexpr int kTK = 64;              // samples per stage = two K=32 MMAs per limb
+constexpr int kRing = 6, kTP = 4;    // cp.async ring depth, prefetch distance (< kRing - 1)
+constexpr int kTT = 256;             // threads (8 warps); warps 0-3 run the TMEM epilogue
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint64_t umma_desc(const void* p) {  // SWIZZLE_NONE, K-major
+  return (uint64_t)((smem_u32(p) >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(256 >> 4) << 32) | ((uint64_t)1 << 46);
+}
+// canonical byte offset of (row r, k-byte kb < 64) in an R x 64-byte operand stage:
+// sub-tile kb/32 (one MMA's K), then 8-row x 16-byte core matrices (LBO 128, SBO 256)
+template <int R>
+__device__ __forceinline__ int canon(int r, int kb) {
+  return (kb >> 5) * (R * 32) + (r >> 3) * 256 + ((kb >> 4) & 1) * 128 + (r & 7) * 16 + (kb & 15);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+struct TcSmem {
+  uint8_t a[kRing][kTM * kTK];          // X rows i (MMA operand A, read in place)
+  uint8_t braw[kRing][kTN * kTK];       // X rows j
+  uint8_t limb[kRing][kLimbs][kTK];
+  uint8_t b[2][kLimbs][kTN * kTK];      // limb-scaled B operands (double-buffered)
+  uint64_t done[kRing];                 // MMAs of the step that used ring slot s completed
+  uint32_t taddr;
+};
+
+__global__ void __launch_bounds__(kTT, 1)
+    k_xtdx_tc(const uint8_t* __restrict__ xt, int lg_ch, int64_t d, const uint8_t* __restrict__ limbs,
+              int64_t np, const int2* __restrict__ tiles, int64_t s0, int64_t s1, double inv_n, int beta,
+              double* __restrict__ h) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  TcSmem& sm = *reinterpret_cast<TcSmem*>(smraw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int2 tile = tiles[blockIdx.x];
+  const int64_t i0 = (int64_t)tile.x * kTM, j0 = (int64_t)tile.y * kTN;
+  const int64_t ch = 1LL << lg_ch, rs = ch + kRowPad;
+  if (tid == 0) {
+    for (int q = 0; q < kRing; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.done[q])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.taddr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t taddr = sm.taddr;
+  const uint32_t idesc = (2u << 4) | ((uint32_t)(kTN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+
+  const int64_t T = (s1 - s0) / kTK;
+  // this thread's cp.async chunks, fixed for every stage: (source offset in a sample
+  // block, destination offset in a ring slot, bytes); 16-byte chunks of the A rows, the
+  // B rows, then the limb rows
+  constexpr int kA = kTM * 4, kB = kTN * 4, kL = kLimbs * 4;
+  constexpr int kPer = (kA + kB + kL + kTT - 1) / kTT;
+  int64_t csrc[kPer];
+  int cdst[kPer], cbytes[kPer];
+  constexpr int kSlot = (int)(sizeof(TcSmem::a[0]));
+  const int a_base = (int)(sm.a[0] - smraw), b_base = (int)(sm.braw[0] - smraw);
+  const int l_base = (int)(&sm.limb[0][0][0] - smraw);
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int c = tid + u * kTT;
+    csrc[u] = 0; cdst[u] = 0; cbytes[u] = -1;  // -1: no chunk
+    if (c < kA + kB) {
+      const bool isa = c < kA;
+      const int cc = isa ? c : c - kA;
+      const int r = cc >> 2, kb = (cc & 3) * 16;
+      const int64_t feat = (isa ? i0 : j0) + r;
+      cbytes[u] = feat < d ? 16 : 0;
+      csrc[u] = (feat < d ? feat : 0) * rs + kb;
+      cdst[u] = isa ? a_base + canon<kTM>(r, kb) : b_base + canon<kTN>(r, kb);
+    } else if (c < kA + kB + kL) {
+      const int cc = c - kA - kB, k = cc >> 2, kb = (cc & 3) * 16;
+      cbytes[u] = 16;
+      csrc[u] = -1 - (k * np + kb);  // negative: a limb row (offset from `limbs`)
+      cdst[u] = l_base + k * kTK + kb;
+    }
+  }
+  const uint32_t sbase = smem_u32(smraw);
+  auto issue = [&](int64_t t) {  // cp.async of stage t into ring slot t % kRing
+    const int q = (int)(t % kRing);
+    const int64_t smp = s0 + t * kTK;
+    const uint8_t* blk = xt + (smp >> lg_ch) * (d * rs) + (smp & (ch - 1));
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      if (cbytes[u] < 0) continue;
+      const bool lim = csrc[u] < 0;
+      const uint8_t* src = lim ? limbs + (-1 - csrc[u]) + smp : blk + csrc[u];
+      const uint32_t dst = sbase + (uint32_t)cdst[u] +
+                           (uint32_t)q * (lim ? (uint32_t)sizeof(TcSmem::limb[0]) : (uint32_t)(cdst[u] < b_base ? kSlot : (int)sizeof(TcSmem::braw[0])));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(cbytes[u]));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  for (int64_t t = 0; t < kTP; ++t) {
+    if (t < T) issue(t);
+    else asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int64_t t = 0; t < T; ++t) {
+    const int q = (int)(t % kRing), bb = (int)(t & 1);
+    // the MMAs of stage t-2 read ring slot (t+kTP)%kRing's predecessor chain and b[bb]:
+    // wait for them once (they completed long ago unless the tensor core is the bottleneck)
+    if (t >= 2) mbar_wait(&sm.done[(t - 2) % kRing], (uint32_t)(((t - 2) / kRing) & 1));
+    {
+      const int64_t tp = t + kTP;  // slot tp % kRing was last used by stage tp - kRing <= t - 2
+      if (tp < T) issue(tp);
+      else asm volatile("cp.async.commit_group;\n" ::);
+    }
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kTP));
+    __syncthreads();
+    // B_k = (x * 255) & L_k, four samples per word, same canonical offsets as the raw tile
+    for (int c = tid; c < kTN * 4; c += kTT) {
+      const int off = c * 16;
+      const int kb = (off >= kTN * 32 ? 32 : 0) + ((off >> 7) & 1) * 16;  // first sample of the chunk
+      const uint4 x = *reinterpret_cast<const uint4*>(&sm.braw[q][off]);
+      const uint4 m = make_uint4(x.x * 255u, x.y * 255u, x.z * 255u, x.w * 255u);
+#pragma unroll
+      for (int k = 0; k < kLimbs; ++k) {
+        const uint4 L = *reinterpret_cast<const uint4*>(&sm.limb[q][k][kb]);
+        *reinterpret_cast<uint4*>(&sm.b[bb][k][off]) =
+            make_uint4(m.x & L.x, m.y & L.y, m.z & L.z, m.w & L.w);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int ks = 0; ks < kTK / 32; ++ks) {
+        const uint64_t da = umma_desc(sm.a[q] + ks * kTM * 32);
+#pragma unroll
+        for (int k = 0; k < kLimbs; ++k) {
+          const uint64_t db = umma_desc(sm.b[bb][k] + ks * kTN * 32);
+          const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
+                  taddr + (uint32_t)(k * kTN)),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(&sm.done[q])));
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  if (T > 0) mbar_wait(&sm.done[(T - 1) % kRing], (uint32_t)(((T - 1) / kRing) & 1));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp < 4) {  // epilogue: row i = i0 + 32*warp + lane, columns j0 .. j0+95
+    const int64_t i = i0 + warp * 32 + lane;
+    for (int c0 = 0; c0 < kTN; c0 += 32) {
+      double hv[32];
+#pragma unroll
+      for (int qq = 0; qq < 32; ++qq) hv[qq] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kLimbs; ++k) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+              "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+              "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr + ((uint32_t)(warp * 32) << 16) + (uint32_t)(k * kTN + c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        const double sc = ldexp(1.0, kLimbBits * k - kFixBits) * inv_n;
+#pragma unroll
+        for (int qq = 0; qq < 32; ++qq) hv[qq] += (double)(int)v[qq] * sc;
+      }
+      if (i < d) {
+#pragma unroll
+        for (int qq = 0; qq < 32; ++qq) {
+          const int64_t j = j0 + c0 + qq;
+          if (j < d && i <= j) {
+            if (beta) {
+              h[i * d + j] += hv[qq];
+              if (i != j) h[j * d + i] += hv[qq];
+            } else {
+              h[i * d + j] = hv[qq];
+              if (i != j) h[j * d + i] = hv[qq];
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr));
+}
+
 // out[block r/ch][j][r%ch] = bit (r, j) of the packed rows, 0 for r >= rows (16 samples
 // per thread)
 __global__ void k_bits_to_u8t(const uint64_t* __restrict__ bits, int64_t rows, int64_t d, int64_t W,
@@ -192,10 +411,10 @@ int egrid(int64_t n) {
 
 }  // namespace
 
-// Sample-block width ch (a power of two, 32..4096) and padded row count np of the u8
+// Sample-block width ch (a power of two, 64..4096) and padded row count np of the u8
 // operand for n rows; the operand occupies (np / ch) * d * (ch + 32) bytes.
 extern "C" int simopt_u8t_geometry(int64_t n, int64_t* ch, int64_t* np) {
-  int64_t c = 32;
+  int64_t c = 64;  // >= the tcgen05 kernel's 64-sample stage
   while (c < 4096 && c < n) c <<= 1;
   *ch = c;
   *np = ceil_div(n < 1 ? 1 : n, c) * c;
@@ -239,6 +458,55 @@ extern "C" int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t 
       SIMOPT_CHECK_LAUNCH("k_xtdx_i8");
       beta = 1;
     }
+  }
+  return SIMOPT_OK;
+}
+
+// tcgen05 version of simopt_logistic_xtdx_i8 (same operands and result).
+extern "C" int simopt_logistic_xtdx_tc(void* stream, const uint8_t* xt, int64_t np, int64_t n,
+                                       int64_t d, const double* dw, uint8_t* limbs, double* h) {
+  SIMOPT_REQUIRE(n >= 1 && d >= 1, SIMOPT_E_DIMENSION, "empty design matrix");
+  int64_t ch = 0, np_want = 0;
+  simopt_u8t_geometry(n, &ch, &np_want);
+  SIMOPT_REQUIRE(np == np_want, SIMOPT_E_CONFIG, "np must come from simopt_u8t_geometry");
+  cudaStream_t st = as_stream(stream);
+  int lg = 0;
+  while ((1LL << lg) < ch) ++lg;
+  k_limbs<<<egrid(np), 256, 0, st>>>(dw, n, np, limbs);
+  SIMOPT_CHECK_LAUNCH("k_limbs");
+  // upper-triangle tile list (tile (bi, bj) holds some j >= i), cached per d
+  static std::mutex mu;
+  static std::vector<std::pair<int64_t, std::pair<int2*, int>>> cache;
+  int2* tiles = nullptr;
+  int ntiles = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : cache)
+      if (e.first == d) { tiles = e.second.first; ntiles = e.second.second; }
+    if (!tiles) {
+      std::vector<int2> v;
+      for (int64_t bi = 0; bi * kTM < d; ++bi)
+        for (int64_t bj = 0; bj * kTN < d; ++bj)
+          if (bj * kTN + kTN - 1 >= bi * kTM) v.push_back(make_int2((int)bi, (int)bj));
+      SIMOPT_CUDA(cudaMalloc(&tiles, v.size() * sizeof(int2)));
+      SIMOPT_CUDA(cudaMemcpy(tiles, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice));
+      ntiles = (int)v.size();
+      cache.push_back({d, {tiles, ntiles}});
+    }
+  }
+  // > half the SM's shared memory: one CTA per SM, which then owns all 512 TMEM columns
+  const size_t smem = sizeof(TcSmem) + 1024 > 120 * 1024 ? sizeof(TcSmem) + 1024 : 120 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  int beta = 0;
+  for (int64_t c0 = 0; c0 < np; c0 += kChunk) {
+    const int64_t c1 = c0 + kChunk < np ? c0 + kChunk : np;
+    k_xtdx_tc<<<ntiles, kTT, smem, st>>>(xt, lg, d, limbs, np, tiles, c0, c1, 1.0 / (double)n, beta, h);
+    SIMOPT_CHECK_LAUNCH("k_xtdx_tc");
+    beta = 1;
   }
   return SIMOPT_OK;
 }

@@ -208,8 +208,9 @@ def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.T
     """H = (1/N) X^T diag(dw) X (tests/test_tasks.py:297-299 oracle, rtol 1e-10).
 
     method: "dmma" -- FP64 tensor pipe (csrc/hessian.cu; fp64 or bit-packed X);
-    "i8" -- bit-packed binary X only: exact 5-limb split of dw on the integer tensor
-    cores (csrc/hessian_i8.cu); "auto" = "i8" for bit-packed data, else "dmma".
+    "i8" / "tc" -- bit-packed binary X only: exact 5-limb split of dw on the integer
+    tensor cores, warp-level IMMA ("i8") or tcgen05 with TMEM accumulators ("tc",
+    csrc/hessian_i8.cu); "auto" = "tc" for bit-packed data, else "dmma".
     Row-sharded data: each rank's (1/N_loc) X_loc^T D X_loc is weighted by N_loc/N and
     summed over ranks with one allreduce of the d x d matrix."""
     d = data.n_features
@@ -217,14 +218,15 @@ def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.T
     nl = data.local_rows
     shard = getattr(data, "shard", None)
     if method == "auto":
-        method = "i8" if data.packed else "dmma"
-    if nl and method == "i8":
+        method = "tc" if data.packed else "dmma"
+    if nl and method in ("i8", "tc"):
         xt, np_ = data.feature_major_u8()
         limbs = getattr(data, "_limbs", None)
         if limbs is None or limbs.numel() != 5 * np_:
             limbs = data._limbs = torch.empty(5 * np_, dtype=torch.uint8, device="cuda")
-        _lib.call("simopt_logistic_xtdx_i8", _lib.stream_ptr(), _lib.ptr(xt), np_, nl, d,
-                  _lib.ptr(dw), _lib.ptr(limbs), _lib.ptr(out))
+        _lib.call("simopt_logistic_xtdx_tc" if method == "tc" else "simopt_logistic_xtdx_i8",
+                  _lib.stream_ptr(), _lib.ptr(xt), np_, nl, d, _lib.ptr(dw), _lib.ptr(limbs),
+                  _lib.ptr(out))
     elif nl and data.packed:
         _lib.call("simopt_logistic_xtdx_bits", _lib.stream_ptr(), _lib.ptr(data.bits), _lib.ptr(dw),
                   nl, d, _lib.ptr(out))

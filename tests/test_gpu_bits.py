@@ -80,8 +80,10 @@ def test_xtdx_bits_equals_dense(pkg, d, n):
     assert torch.equal(logistic_hessian_device(dense, dw), logistic_hessian_device(packed, dw, method="dmma"))
 
 
-@pytest.mark.parametrize("d,n", [(128, 4096), (200, 3001), (13, 777), (1000, 2000), (300, 40)])
-def test_xtdx_i8_vs_oracle(pkg, d, n):
+@pytest.mark.parametrize("method", ["i8", "tc"])
+@pytest.mark.parametrize("d,n", [(128, 4096), (200, 3001), (13, 777), (1000, 2000), (300, 40),
+                                 (97, 9000)])
+def test_xtdx_i8_vs_oracle(pkg, d, n, method):
     """Integer-tensor-core Hessian (exact limbs of dw rounded to 2^-41) vs the explicit oracle."""
     from paper_2404_11631_b200.newton import logistic_hessian_device
     from paper_2404_11631_b200.sampling import synth_classification
@@ -92,14 +94,14 @@ def test_xtdx_i8_vs_oracle(pkg, d, n):
     want = orc.logistic_hessian_explicit(w, x, z)
     c = orc.sigmoid(orc.matvec(x, w))
     dw = torch.from_numpy(c * (1 - c)).cuda()
-    got = logistic_hessian_device(data, dw, method="i8").cpu().numpy()
+    got = logistic_hessian_device(data, dw, method=method).cpu().numpy()
     np.testing.assert_allclose(got, want, rtol=1e-10, atol=1e-15)
     assert np.array_equal(got, got.T)
     dmma = logistic_hessian_device(data, dw, method="dmma").cpu().numpy()
     np.testing.assert_allclose(got, dmma, rtol=1e-10, atol=1e-15)
     # dw = 1/4 everywhere (w = 0): the largest fixed-point value
     quarter = torch.full((n,), 0.25, dtype=torch.float64, device="cuda")
-    np.testing.assert_allclose(logistic_hessian_device(data, quarter, method="i8").cpu().numpy(),
+    np.testing.assert_allclose(logistic_hessian_device(data, quarter, method=method).cpu().numpy(),
                                (x.T @ x) * 0.25 / n, rtol=1e-12)
 
 

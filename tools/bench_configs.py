@@ -97,3 +97,5 @@ if __name__ == "__main__":
              packed=True)
         xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X, u8 IMMA limbs)", 8192,
              125_000, packed=True, method="i8")
+        xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X, tcgen05 i8 limbs, TMEM)", 8192,
+             125_000, packed=True, method="tc")

@@ -265,15 +265,30 @@ def run_ours(args, rank, world):
     seg, nbuck = nv_geometry()
     nseg = -(-S // seg)
     d_loc = prob.dev.d
-    alg_bytes = d_loc * S * 4 + d_loc * nseg * nbuck * 2  # keys + bucket starts written per launch
+    # the algorithmic bytes of a resample launch are the epoch's fp64
+    # demand matrix written once, 8 B per draw (the reference's data model).  This
+    # kernel actually writes 4 B keys + 2-byte bucket starts per 4096-draw segment
+    # (keyed layout), measured as `traffic`.
+    alg_bytes = d_loc * S * 8
+    stored_bytes = d_loc * S * 4 + d_loc * nseg * nbuck * 2
     peak, peak_kind = peaks()
     achieved = alg_bytes / (res_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": profiled_traffic(),
                 "kernel": "k_nv_resample", "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "algorithmic_bytes_per_launch": alg_bytes, "stored_bytes_per_launch": stored_bytes,
                 "kernel_ms": res_ms, "share_of_step": res_ms / (ms / args.steps),
-                "note": ("issue-bound: Philox4x64-10 + fp32 Box-Muller key per draw (exact glibc "
-                         "Box-Muller only for ambiguous draws at query time); see profiles/")}
+                "note": ("instruction-bound by design: Philox4x64-10 (37 IMAD/draw) + an fp32 SFU "
+                         "Box-Muller key per draw, exact glibc Box-Muller only for the few "
+                         "ambiguous draws at query time; kernel_ms is measured while the previous "
+                         "epoch's FW steps run concurrently; see profiles/")}
+    # the step against SURVEY 8(d)'s per-iteration roof (8 d S (1 + 1/M) bytes: one scan of
+    # the epoch's demands per gradient + the amortised write) -- the keyed ECDF reads a
+    # window of buckets per product instead of all S demands, so it runs above that roof
+    it_roof = peak * 1e9 / (8 * D * S * (1 + 1 / M))
+    step_roofline = {"unit": "iterations/s", "data_model_roof": it_roof, "achieved": value,
+                     "frac": value / it_roof,
+                     "basis": "SURVEY 8(d) C2: 8*d*S*(1+1/M) bytes per FW iteration at hbm peak"}
     launches_per_epoch = 4 * M + 2  # resample, M+1 fused steps, M x (terms, sums, stamp)
     if world > 1:
         launches_per_epoch += 2 * M  # LMO pack + apply around each exchange
@@ -291,6 +306,7 @@ def run_ours(args, rank, world):
                                       f"by {args.dist_backend} allgather"))
                    if world > 1 else "single GPU"},
         "roofline": roofline,
+        "step_roofline": step_roofline,
         "clocks": clk.summary(),
         "gpu_launches": launches_per_epoch * args.steps,
         "final_objective": trace.build("newsvendor", D, "cuda", 0, SEED, None).final_objective,
@@ -311,7 +327,7 @@ def run_e2e(args, task, backend, shard=None):
     import paper_2404_11631_b200 as pkg
     from paper_2404_11631_b200.frank_wolfe import FwConfig, fw_run
     from paper_2404_11631_b200.tasks import NewsvendorProblem
-    steps = max(2, min(args.steps, 3))
+    steps = max(3, min(args.steps, 8))
     stream = pkg.RngStream(SEED, 2)
     rec = fw_run(NewsvendorProblem(task, backend, shard=shard), FwConfig(1, M, S, stream),
                  backend)  # warm

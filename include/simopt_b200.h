@@ -315,6 +315,21 @@ int simopt_matvec_t_partials(void* stream, const double* a, int64_t rows, int64_
                              const double* center, const double* x, int64_t chunk, double* out);
 int simopt_fold_partials(void* stream, double* p, int64_t nch, int64_t count, double* out);
 
+/* Cross-rank sum fused into the finish of a fused pass over NVLink peer memory (sample
+ * sharding).  peers[q] = device pointer to rank q's receive buffer (CUDA IPC mapping of a
+ * simopt_peer_alloc of simopt_peer_reduce_bytes(world, cols) bytes); every rank pushes its
+ * per-column partial sums (and the side scalar) into slot `rank` of every peer buffer,
+ * releases per-block flags, acquires all ranks' flags and sums the slots in rank order --
+ * so every rank computes the same bits.  seq must increase by one per pass (double-buffered
+ * by parity); *status = 1 if a peer never arrives (20 s). */
+typedef struct SimoptPeerReduce {
+  void* const* peers;
+  int64_t world, rank;
+  uint64_t seq;
+  int* status;
+} SimoptPeerReduce;
+int64_t simopt_peer_reduce_bytes(int64_t world, int64_t cols);
+
 /* ------------------------------------------------------------ bit-packed binary features */
 /* Layout: row-major, W = ceil(d/64) u64 words per row, feature j = bit (j&63) of word j>>6.
  * bernoulli_bits: rows [row_lo, row_hi) of synth_classification's features
@@ -330,7 +345,7 @@ int simopt_unpack_bits(void* stream, const uint64_t* bits, int64_t rows, int64_t
 int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bits, int64_t rows, int64_t cols,
                            const double* v, const double* rowaux, double col_scale, int accumulate,
                            int raw, double* t_out, double* dw_out, double* col_out,
-                           double* scalar_out);
+                           double* scalar_out, const SimoptPeerReduce* peer);
 /* Binary X on the integer tensor cores (csrc/hessian_i8.cu): bits_to_u8t builds X^T as u8 in
  * sample blocks [np/ch][d][ch + 32] (ch, np from u8t_geometry; padded rows are zero); xtdx_i8 computes
  * H = (1/n) X^T diag(dw) X exactly for dw rounded to 2^-41 (5 x 8-bit limbs, u8 IMMA with
@@ -358,14 +373,16 @@ int simopt_logistic_xtdx_bits(void* stream, const uint64_t* xbits, const double*
  *   SIMOPT_FUSED_LR_HVP   tasks.py:239-253 wt = rowaux[r] (= c(1-c)) * t
  * t_out / dw_out / col_out / scalar_out may be NULL; accumulate = 0 skips the column
  * sums (row pass only); raw = 1 writes the plain column sums (no scale, no centering:
- * the per-shard partial that a sample-sharded caller allreduces).  d <= 32768. */
+ * the per-shard partial that a sample-sharded caller allreduces).  peer != NULL: the
+ * column sums and the scalar are summed over ranks inside the finish kernel (see
+ * SimoptPeerReduce) before the epilogue.  d <= 32768. */
 #define SIMOPT_FUSED_MV 0
 #define SIMOPT_FUSED_LR_GRAD 1
 #define SIMOPT_FUSED_LR_HVP 2
 int simopt_fused_rows(void* stream, int mode, const double* x, int64_t rows, int64_t cols,
                       const double* v, const double* center, const double* rowaux,
                       double col_scale, int accumulate, int raw, double* t_out, double* dw_out,
-                      double* col_out, double* scalar_out);
+                      double* col_out, double* scalar_out, const SimoptPeerReduce* peer);
 
 #ifdef __cplusplus
 }

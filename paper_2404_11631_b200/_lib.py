@@ -64,7 +64,8 @@ SIGNATURES = {
     "simopt_cg_step1": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64],
     "simopt_cg_step2": [_vp, _vp, _vp, _vp, _vp, _i64],
     "simopt_fused_rows": [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _d, _i32, _i32, _vp, _vp, _vp,
-                          _vp],
+                          _vp, _vp],
+    "simopt_peer_reduce_bytes": [_i64, _i64],
     "simopt_sample_returns_diag_rows": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_bernoulli_half_range": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp],
     "simopt_matvec_t_partials": [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp],
@@ -78,7 +79,7 @@ SIGNATURES = {
     "simopt_matvec_bits": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
     "simopt_unpack_bits": [_vp, _vp, _i64, _i64, _vp],
     "simopt_fused_rows_bits": [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _d, _i32, _i32, _vp, _vp, _vp,
-                               _vp],
+                               _vp, _vp],
     "simopt_logistic_xtdx_bits": [_vp, _vp, _vp, _i64, _i64, _vp],
     "simopt_u8t_geometry": [_i64, _vp, _vp],
     "simopt_bits_to_u8t": [_vp, _vp, _i64, _i64, _i64, _vp],
@@ -92,6 +93,9 @@ SIGNATURES = {
     "simopt_xoshiro256pp_streams": [_vp, _i64, _vp],
     "simopt_nv_lmo_apply": [_vp, _vp, _i64, _i64, _i64, _vp],
 }
+
+
+INT64_RESULT = {"simopt_peer_reduce_bytes"}  # size queries; every other entry point returns status
 
 
 def load(require_device: bool = True):
@@ -111,7 +115,7 @@ def load(require_device: bool = True):
             for name, argt in SIGNATURES.items():
                 fn = getattr(lib, name)
                 fn.argtypes = argt
-                fn.restype = ctypes.c_int
+                fn.restype = ctypes.c_int64 if name in INT64_RESULT else ctypes.c_int
             _lib = lib
     if require_device:
         if not torch.cuda.is_available():

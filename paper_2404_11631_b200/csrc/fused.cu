@@ -499,6 +499,90 @@ BitsFn pick_bits_k(int K) {
   }
 }
 
+// Cross-rank finish over peer memory (SimoptPeerReduce).  kFB blocks, all resident, so
+// the spin waits cannot starve a block another rank waits for.
+constexpr int kFB = SIMOPT_NUM_SMS;
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_fused_finish_peer(const double* __restrict__ part,
+                                                           const double* __restrict__ spart,
+                                                           int64_t ncl, int64_t d, double scale,
+                                                           const double* __restrict__ center,
+                                                           double* __restrict__ out,
+                                                           double* __restrict__ scalar_out,
+                                                           SimoptPeerReduce pr) {
+  const int64_t W = pr.world, D1 = d + 1, par = (int64_t)(pr.seq & 1ULL);
+  const int b = blockIdx.x, tid = threadIdx.x;
+  // layout of every rank's buffer: data [2][W][d+1] doubles, then flags [2][W][kFB] u64
+  auto data = [&](int64_t q) { return reinterpret_cast<double*>(pr.peers[q]); };
+  auto flags = [&](int64_t q) { return reinterpret_cast<uint64_t*>(data(q) + 2 * W * D1); };
+  const int64_t jlo = out ? 0 : d;  // row pass only: just the side scalar crosses ranks
+  for (int64_t j = jlo + (int64_t)b * 256 + tid; j < D1; j += (int64_t)kFB * 256) {
+    double s = 0.0;
+    if (j < d) {
+      for (int64_t c = 0; c < ncl; ++c) s += part[c * d + j];
+    } else {
+      for (int64_t c = 0; c < ncl; ++c) s += spart[c];
+    }
+    for (int64_t q = 0; q < W; ++q) data(q)[(par * W + pr.rank) * D1 + j] = s;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) {
+    for (int64_t q = 0; q < W; ++q) st_release_sys(flags(q) + (par * W + pr.rank) * kFB + b, pr.seq);
+    const uint64_t* mine = flags(pr.rank) + par * W * kFB;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int64_t q = 0; q < W; ++q) {
+      while (ld_acquire_sys(mine + q * kFB + b) != pr.seq) {
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 20000000000ULL) {
+          if (pr.status) atomicExch(pr.status, 1);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const double* mine = data(pr.rank) + par * W * D1;
+  for (int64_t j = jlo + (int64_t)b * 256 + tid; j < D1; j += (int64_t)kFB * 256) {
+    double t = 0.0;
+    for (int64_t q = 0; q < W; ++q) t += __ldcv(mine + q * D1 + j);  // rank order: same bits everywhere
+    if (j < d) {
+      if (out) {
+        t = t * scale;
+        out[j] = center ? t - center[j] : t;
+      }
+    } else if (scalar_out) {
+      *scalar_out = t;
+    }
+  }
+}
+
+int finish(cudaStream_t st, const double* part, const double* spart, int64_t ncl, int64_t d,
+           double scale, const double* center, double* out, double* scalar_out,
+           const SimoptPeerReduce* peer) {
+  if (peer == nullptr) {
+    const int fgrid = (int)(out ? ceil_div(d, 32) : 1);
+    k_fused_finish<<<fgrid < 1 ? 1 : fgrid, 256, 0, st>>>(part, spart, ncl, d, scale, center, out,
+                                                         scalar_out);
+    SIMOPT_CHECK_LAUNCH("k_fused_finish");
+  } else {
+    k_fused_finish_peer<<<kFB, 256, 0, st>>>(part, spart, ncl, d, scale, center, out, scalar_out, *peer);
+    SIMOPT_CHECK_LAUNCH("k_fused_finish_peer");
+  }
+  return SIMOPT_OK;
+}
+
 using KernelFn = void (*)(FusedArgs);
 
 template <int MODE, int C, int K>
@@ -600,20 +684,18 @@ int grid_for(KernelFn fn, int C, size_t smem) {
 extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_t rows, int64_t cols,
                                  const double* v, const double* center, const double* rowaux,
                                  double col_scale, int accumulate, int raw, double* t_out,
-                                 double* dw_out, double* col_out, double* scalar_out) {
+                                 double* dw_out, double* col_out, double* scalar_out,
+                                 const SimoptPeerReduce* peer) {
   cudaStream_t st = as_stream(stream);
   SIMOPT_REQUIRE(mode == SIMOPT_FUSED_MV || mode == SIMOPT_FUSED_LR_GRAD || mode == SIMOPT_FUSED_LR_HVP,
                  SIMOPT_E_CONFIG, "unknown fused mode %d", mode);
   SIMOPT_REQUIRE(rows >= 0 && cols >= 0, SIMOPT_E_DIMENSION, "negative extent");
   SIMOPT_REQUIRE(mode != SIMOPT_FUSED_MV || center != nullptr, SIMOPT_E_CONFIG, "MV needs the mean");
   SIMOPT_REQUIRE(mode == SIMOPT_FUSED_MV || rowaux != nullptr, SIMOPT_E_CONFIG, "row weights missing");
-  if (cols == 0 || rows == 0) {  // empty sums: col_out = 0 * scale [- center], scalar 0
-    k_fused_finish<<<(int)(cols > 0 ? ceil_div(cols, 32) : 1), 256, 0, st>>>(
-        nullptr, nullptr, 0, cols, col_scale, (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr,
-        (accumulate && cols) ? col_out : nullptr, scalar_out);
-    SIMOPT_CHECK_LAUNCH("k_fused_finish");
-    return SIMOPT_OK;
-  }
+  if (cols == 0 || rows == 0)  // empty local sums: col_out = 0 * scale [- center], scalar 0
+    return finish(st, nullptr, nullptr, 0, cols, col_scale,
+                  (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr,
+                  (accumulate && cols) ? col_out : nullptr, scalar_out, peer);
   int C = 1, K = 1;
   SIMOPT_REQUIRE(geometry(cols, &C, &K), SIMOPT_E_CONFIG,
                  "fused pass supports up to %d columns (got %lld)", 8 * 8 * 2 * kNT, (long long)cols);
@@ -648,32 +730,25 @@ extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_
   cfg.numAttrs = 1;
   cfg.dynamicSmemBytes = dyn_smem(mode, K);
   SIMOPT_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
-  const int fgrid = (int)(a.accumulate ? ceil_div(cols, 32) : 1);
-  k_fused_finish<<<fgrid < 1 ? 1 : fgrid, 256, 0, st>>>(
-      part, a.scal_part, ncl, cols, raw ? 1.0 : col_scale,
-      (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr, a.accumulate ? col_out : nullptr,
-      scalar_out);
-  SIMOPT_CHECK_LAUNCH("k_fused_finish");
-  return SIMOPT_OK;
+  return finish(st, part, a.scal_part, ncl, cols, raw ? 1.0 : col_scale,
+                (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr,
+                a.accumulate ? col_out : nullptr, scalar_out, peer);
 }
 
 extern "C" int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bits, int64_t rows,
                                       int64_t cols, const double* v, const double* rowaux,
                                       double col_scale, int accumulate, int raw, double* t_out,
-                                      double* dw_out, double* col_out, double* scalar_out) {
+                                      double* dw_out, double* col_out, double* scalar_out,
+                                      const SimoptPeerReduce* peer) {
   cudaStream_t st = as_stream(stream);
   SIMOPT_REQUIRE(mode == SIMOPT_FUSED_LR_GRAD || mode == SIMOPT_FUSED_LR_HVP, SIMOPT_E_CONFIG,
                  "bit-packed fused pass: logistic modes only (got %d)", mode);
   SIMOPT_REQUIRE(rowaux != nullptr, SIMOPT_E_CONFIG, "row weights missing");
   SIMOPT_REQUIRE(rows >= 0 && cols >= 0, SIMOPT_E_DIMENSION, "negative extent");
   SIMOPT_REQUIRE(cols <= 64 * kNT, SIMOPT_E_CONFIG, "bit-packed fused pass supports d <= %d", 64 * kNT);
-  if (cols == 0 || rows == 0) {
-    k_fused_finish<<<(int)(cols > 0 ? ceil_div(cols, 32) : 1), 256, 0, st>>>(
-        nullptr, nullptr, 0, cols, col_scale, nullptr, (accumulate && cols) ? col_out : nullptr,
-        scalar_out);
-    SIMOPT_CHECK_LAUNCH("k_fused_finish");
-    return SIMOPT_OK;
-  }
+  if (cols == 0 || rows == 0)
+    return finish(st, nullptr, nullptr, 0, cols, col_scale, nullptr,
+                  (accumulate && cols) ? col_out : nullptr, scalar_out, peer);
   const int64_t W = ceil_div(cols, 64);
   int tpr = 1;
   while (tpr < W) tpr <<= 1;
@@ -711,9 +786,10 @@ extern "C" int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bi
                               mode == SIMOPT_FUSED_LR_GRAD ? dw_out : nullptr, part,
                               part + (int64_t)grid * cols, acc);
   SIMOPT_CHECK_LAUNCH("k_fused_bits");
-  k_fused_finish<<<(int)(acc ? ceil_div(cols, 32) : 1), 256, 0, st>>>(
-      part, part + (int64_t)grid * cols, grid, cols, raw ? 1.0 : col_scale, nullptr,
-      acc ? col_out : nullptr, scalar_out);
-  SIMOPT_CHECK_LAUNCH("k_fused_finish");
-  return SIMOPT_OK;
+  return finish(st, part, part + (int64_t)grid * cols, grid, cols, raw ? 1.0 : col_scale, nullptr,
+                acc ? col_out : nullptr, scalar_out, peer);
+}
+
+extern "C" int64_t simopt_peer_reduce_bytes(int64_t world, int64_t cols) {
+  return (2 * world * (cols + 1)) * (int64_t)sizeof(double) + 2 * world * kFB * (int64_t)sizeof(uint64_t);
 }

@@ -30,7 +30,7 @@ import torch
 
 from . import _lib
 from ._tensors import F64, empty, to_host
-from .fused import LR_GRAD, LR_HVP, fused_rows, fused_rows_bits
+from .fused import LR_GRAD, LR_HVP, PeerReducer, fused_rows, fused_rows_bits
 from .records import RunRecord, TraceBuilder
 
 _SCALE, _MUL = 3, 4
@@ -45,7 +45,7 @@ def _vop(op, alpha, x, y, out):
 class _Logistic:
     """Per-run buffers for the full-data logistic passes."""
 
-    def __init__(self, data, backend):
+    def __init__(self, data, backend, exchange="peer"):
         self.data, self.b = data, backend
         self.N, self.d = data.n_samples, data.n_features   # N: global rows
         self.shard = getattr(data, "shard", None)
@@ -58,6 +58,10 @@ class _Logistic:
         self.gt = empty(self.d)
         self.buf = empty(self.d + 1)  # [column sums | side sum] allreduced across shards
         self.ones = torch.ones(nl, dtype=F64, device="cuda")
+        # sample-sharded fused passes: cross-rank sums inside the finish kernel over peer
+        # memory (None -> raw partials + NCCL allreduce)
+        self.pr = (PeerReducer.get(self.shard, self.d)
+                   if self.shard is not None and exchange == "peer" else None)
 
     def _pass(self, mode, v, rowaux, **kw):
         """One fused read of this rank's rows (bit-packed features when available)."""
@@ -107,9 +111,9 @@ class _Logistic:
 
     def fused_gradient(self, w, g_out, loss_sum_out):
         """One pass: g = (1/N) X^T (sigmoid(Xw) - z), sum of loss terms, c(1-c) for the HVPs."""
-        if self.shard is None:
+        if self.shard is None or self.pr is not None:
             self._pass(LR_GRAD, w, self.data.labels, col_scale=1.0 / self.N, col_out=g_out,
-                       scalar_out=loss_sum_out, dw_out=self.dw)
+                       scalar_out=loss_sum_out, dw_out=self.dw, peer=self.pr)
             return
         # per-shard raw sums, one allreduce of d+1 doubles
         self._pass(LR_GRAD, w, self.data.labels, col_out=self.buf[:self.d],
@@ -120,8 +124,8 @@ class _Logistic:
 
     def fused_hvp(self, v, out):
         """One pass: (1/N) X^T ((c(1-c)) * (X v))."""
-        if self.shard is None:
-            return self._pass(LR_HVP, v, self.dw, col_scale=1.0 / self.N, col_out=out)
+        if self.shard is None or self.pr is not None:
+            return self._pass(LR_HVP, v, self.dw, col_scale=1.0 / self.N, col_out=out, peer=self.pr)
         self._pass(LR_HVP, v, self.dw, col_out=self.buf[:self.d], raw=True)
         self.shard.allreduce_(self.buf[:self.d])
         return self._scale(self.buf, out)
@@ -160,9 +164,9 @@ def _cg(apply, g, n, cg_iters, dot, p):
     return p
 
 
-def _run(task, iterations, backend, step, label, fused=False):
+def _run(task, iterations, backend, step, label, fused=False, exchange="peer"):
     data = task.data
-    L = _Logistic(data, backend)
+    L = _Logistic(data, backend, exchange if fused else "nccl")
     n = L.d
     w = torch.zeros(n, dtype=F64, device="cuda")
     g = empty(n)
@@ -190,6 +194,8 @@ def _run(task, iterations, backend, step, label, fused=False):
             L.xw(w)                               # shared by the loss and the next gradient
             L.loss_sum_from_t(sums[it:])
         _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[it:])))
+    if L.pr is not None:
+        L.pr.check()
     trace = TraceBuilder()
     vals, ts = to_host(sums), to_host(stamps)
     for it in range(iterations):
@@ -197,11 +203,12 @@ def _run(task, iterations, backend, step, label, fused=False):
     return trace.build(label, n, backend.kind, 0, 0, to_host(w))
 
 
-def newton_cg(task, iterations: int, cg_iters: int, backend, fused: bool = True) -> RunRecord:
+def newton_cg(task, iterations: int, cg_iters: int, backend, fused: bool = True,
+              exchange: str = "peer") -> RunRecord:
     """Newton-CG on the full-data logistic loss (BASELINE.json configs[2])."""
     def step(L, g, p, dot):
         _cg(L.fused_hvp if fused else L.hvp, g, L.d, cg_iters, dot, p)
-    return _run(task, iterations, backend, step, "classification-newton-cg", fused)
+    return _run(task, iterations, backend, step, "classification-newton-cg", fused, exchange)
 
 
 def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.Tensor:
@@ -243,7 +250,7 @@ def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.T
 
 
 def newton_explicit(task, iterations: int, cg_iters: int, backend, fused: bool = True,
-                    hessian: str = "auto") -> RunRecord:
+                    hessian: str = "auto", exchange: str = "peer") -> RunRecord:
     """Newton with the explicit X^T D X Hessian and a CG solve (BASELINE.json configs[4])."""
     d = task.data.n_features
     H = torch.empty(d, d, dtype=F64, device="cuda")
@@ -251,4 +258,4 @@ def newton_explicit(task, iterations: int, cg_iters: int, backend, fused: bool =
     def step(L, g, p, dot):
         logistic_hessian_device(L.data, L.dw, out=H, method=hessian)
         _cg(lambda v, out: backend.matvec_device(H, v, out=out), g, d, cg_iters, dot, p)
-    return _run(task, iterations, backend, step, "classification-newton-explicit", fused)
+    return _run(task, iterations, backend, step, "classification-newton-explicit", fused, exchange)

@@ -158,7 +158,7 @@ class PeerMailbox:
 
     _cache = {}
 
-    def __init__(self, shard: ShardGroup):
+    def __init__(self, shard: ShardGroup, nbytes: int | None = None):
         import ctypes
 
         from . import _lib
@@ -167,7 +167,8 @@ class PeerMailbox:
         W = shard.world
         self._own = ctypes.c_void_p()
         handle = (ctypes.c_char * 64)()
-        _lib.check(lib.simopt_peer_alloc(2 * W * 4 * 8, ctypes.byref(self._own), handle))
+        nbytes = 2 * W * 4 * 8 if nbytes is None else nbytes
+        _lib.check(lib.simopt_peer_alloc(nbytes, ctypes.byref(self._own), handle))
         handles = [None] * W
         dist.all_gather_object(handles, bytes(handle), group=shard.group)
         ptrs, self._opened = [], []
@@ -187,12 +188,13 @@ class PeerMailbox:
         return self.seq
 
     @classmethod
-    def get(cls, shard: ShardGroup):
-        key = (id(shard.group), shard.rank, shard.world)
+    def get(cls, shard: ShardGroup, nbytes: int | None = None, tag: str = "lmo"):
+        """The (shard, tag) mailbox (default: the newsvendor LMO mailbox), created on first use."""
+        key = (id(shard.group), shard.rank, shard.world, tag)
         if key in cls._cache:
             return cls._cache[key]
         try:
-            mb, ok = cls(shard), 1.0
+            mb, ok = cls(shard, nbytes), 1.0
         except Exception:  # noqa: BLE001 -- IPC unavailable here: every rank falls back
             mb, ok = None, 0.0
         flag = torch.tensor([ok], dtype=torch.float64, device="cuda" if shard.nccl else "cpu")

@@ -662,13 +662,19 @@ class MeanVarProblem:
 
     name = "meanvar"
 
-    def __init__(self, task: MeanVarTask, backend, fused: bool = False, shard=None):
+    def __init__(self, task: MeanVarTask, backend, fused: bool = False, shard=None,
+                 exchange: str = "peer"):
         self.task = task
         self.backend = backend
         self.fused = fused  # device FW loop: single-pass fused gradient (csrc/fused.cu)
         # sample sharding: this rank draws and reduces only its scenario rows
-        # [lo, hi) (chunk-aligned), with one allreduce / allgather per reduction
+        # [lo, hi) (chunk-aligned), with one allreduce / allgather per reduction; fused
+        # mode sums across ranks inside the pass's finish kernel over peer memory
+        # ("peer"; NCCL allreduce of raw partials if unavailable, or with "nccl")
         self.shard = shard
+        if exchange not in ("peer", "nccl"):
+            raise ConfigurationError(f"unknown exchange {exchange!r}")
+        self.exchange = exchange
         self.constraint = SimplexSlackSet(task.dimension)
         self.sample_set: MeanVarSampleSet | None = None
         self._x = None
@@ -834,10 +840,16 @@ class MvFwEngine:
         nl = x.shape[0]
         q = self.q[:nl]
         buf = self.red_buf
+        pr = None
+        if self.prob.fused and self.prob.exchange == "peer":
+            from .fused import PeerReducer
+            pr = PeerReducer.get(sh, d)  # collective on first use; None -> NCCL below
         for m in range(self.M):
             w_in, w_out = ws[m], ws[m + 1]
             if m == 0:
-                if self.prob.fused:
+                if pr is not None:  # g summed over ranks inside the pass (peer memory)
+                    fused_rows(MV, x, w_in, center=mean, col_scale=inv, col_out=self.g, peer=pr)
+                elif self.prob.fused:
                     fused_rows(MV, x, w_in, center=mean, col_out=buf[:d], raw=True)
                     sh.allreduce_(buf[:d])
                     _lib.check(lib.simopt_scale_sub(sp, P(buf), inv, P(mean), d, P(self.g)))
@@ -851,7 +863,10 @@ class MvFwEngine:
             _lib.check(lib.simopt_axpy_ptr(sp, P(self.gamma[m:]), P(self.dirn), P(w_in), d, P(w_out)))
             _lib.check(lib.simopt_min_value(sp, P(w_out), d, P(self.wmin[m:])))
             last = m == self.M - 1
-            if self.prob.fused:
+            if pr is not None:
+                fused_rows(MV, x, w_out, center=mean, col_scale=inv, col_out=None if last else self.g,
+                           scalar_out=self.quad[m:m + 1], accumulate=not last, peer=pr)
+            elif self.prob.fused:
                 fused_rows(MV, x, w_out, center=mean, col_out=None if last else buf[:d],
                            scalar_out=buf[d:], accumulate=not last, raw=True)
                 if last:
@@ -942,6 +957,11 @@ def _mv_fw_run_device(prob: MeanVarProblem, config, backend, label, size, rep):
     def check_epoch(k):
         """Host validation of epoch k (its ring is intact until epoch k+2 is enqueued)."""
         events[k].synchronize()
+        if prob.shard is not None and prob.fused and prob.exchange == "peer":
+            from .fused import PeerReducer
+            pr = PeerReducer.get(prob.shard, prob.dimension)
+            if pr is not None:
+                pr.check()
         sl = slice(k * M, (k + 1) * M)
         st, mn, sm, qd, ln, ts = (to_host(a[sl]) for a in (status, wmin, wsum, quad, lin, stamps))
         t0 = host.setdefault("t0", int(stamps[T].item()))

@@ -36,6 +36,10 @@ def main(rank, world, port, out):
                          FwConfig(2, 10, 10_000, p.RngStream(42, 2)), b)
             res[f"mv_{chunk}_{int(fused)}_obj"] = rec.objectives
             res[f"mv_{chunk}_{int(fused)}_w"] = rec.final_iterate
+        task = gen_meanvar_instance(300, p.RngStream(42, 0))  # fused, NCCL/gloo allreduce path
+        rec = fw_run(MeanVarProblem(task, b, fused=True, shard=sh, exchange="nccl"),
+                     FwConfig(2, 10, 10_000, p.RngStream(42, 2)), b)
+        res[f"mv_{chunk}_2_obj"], res[f"mv_{chunk}_2_w"] = rec.objectives, rec.final_iterate
     b = p.make_backend("cuda")
     data = synth_classification(40, p.RngStream(42, 0), n_rows=9000, shard=sh)
     res["lr_rows"] = np.array([data.local_rows, data.row_offset])
@@ -43,6 +47,10 @@ def main(rank, world, port, out):
         rec = newton_cg(LogisticTask(data), 3, 8, b, fused=fused)
         res[f"ncg_{int(fused)}_obj"] = rec.objectives
         res[f"ncg_{int(fused)}_w"] = rec.final_iterate
+    rec = newton_cg(LogisticTask(data), 3, 8, b, exchange="nccl")
+    res["ncg_2_obj"], res["ncg_2_w"] = rec.objectives, rec.final_iterate
+    from paper_2404_11631_b200.fused import PeerReducer
+    res["peer_reduce_used"] = np.array([PeerReducer.get(sh, 40) is not None])
     rec = newton_explicit(LogisticTask(data), 3, 20, b)
     res["nex_obj"], res["nex_w"] = rec.objectives, rec.final_iterate
     packed = synth_classification(40, p.RngStream(42, 0), n_rows=9000, shard=sh, packed=True)

@@ -175,7 +175,7 @@ typedef struct NvState {
   unsigned blocks_done;   /* last-block-done counter (kept 0 between launches) */
   unsigned pad;
   double best_val;        /* LMO value g_j* (C/c_j*) of the vertex (shard exchange) */
-  int64_t pad2;
+  int64_t exchange_failed; /* sticky: a peer exchange timed out; later ones do not wait */
 } NvState;
 
 #define NV_FLAG_NAN_GRADIENT 1 /* InvalidGradient at this step's LMO (lmo.py:78-79) */
@@ -321,7 +321,8 @@ int simopt_fold_partials(void* stream, double* p, int64_t nch, int64_t count, do
  * per-column partial sums (and the side scalar) into slot `rank` of every peer buffer,
  * releases per-block flags, acquires all ranks' flags and sums the slots in rank order --
  * so every rank computes the same bits.  seq must increase by one per pass (double-buffered
- * by parity); *status = 1 if a peer never arrives (20 s). */
+ * by parity); *status = 1 if a peer never arrives (10 s) -- sticky: while *status != 0
+ * later passes do not wait (they return local sums), so a broken peer fails fast. */
 typedef struct SimoptPeerReduce {
   void* const* peers;
   int64_t world, rank;

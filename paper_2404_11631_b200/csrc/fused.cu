@@ -541,12 +541,14 @@ __global__ void __launch_bounds__(256) k_fused_finish_peer(const double* __restr
     const uint64_t* mine = flags(pr.rank) + par * W * kFB;
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (int64_t q = 0; q < W; ++q) {
+    bool failed = pr.status && *((volatile int*)pr.status) != 0;  // sticky: fail fast
+    for (int64_t q = 0; q < W && !failed; ++q) {
       while (ld_acquire_sys(mine + q * kFB + b) != pr.seq) {
         uint64_t t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (t1 - t0 > 20000000000ULL) {
+        if (t1 - t0 > 10000000000ULL) {
           if (pr.status) atomicExch(pr.status, 1);
+          failed = true;
           break;
         }
       }

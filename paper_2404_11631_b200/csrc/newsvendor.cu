@@ -251,7 +251,8 @@ constexpr int kIterWarps = 8;
 // sequence from the own mailbox and keep the global first-argmin -- the allgather +
 // simopt_nv_lmo_apply of the NCCL path in one kernel, no host round trip.  Mailboxes are
 // double-buffered by sequence parity (a rank cannot run two exchanges ahead).  A peer
-// that never arrives ends the wait after 20 s with NV_FLAG_EXCHANGE_TIMEOUT.
+// that never arrives ends the wait after 10 s with NV_FLAG_EXCHANGE_TIMEOUT, and every later
+// exchange of the run then skips its wait (sticky NvState.exchange_failed): fail fast.
 __device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -281,11 +282,11 @@ __device__ __noinline__ void nv_peer_exchange(const NvIterArgs& a, ArgMin r, dou
   ArgMin best{INFINITY, INT64_MAX};
   double bs = 0.0;
   const uint64_t t0 = globaltimer();
-  bool timed_out = false;
-  for (int64_t q = 0; q < W; ++q) {
+  bool timed_out = st->exchange_failed != 0;  // sticky: after one failure, never wait again
+  for (int64_t q = 0; q < W && !timed_out; ++q) {
     const double* e = mb + q * 4;
     while (ld_acquire_u64(reinterpret_cast<const uint64_t*>(e + 3)) != a.seq) {
-      if (globaltimer() - t0 > 20000000000ULL) { timed_out = true; break; }
+      if (globaltimer() - t0 > 10000000000ULL) { timed_out = true; break; }
     }
     if (timed_out) break;
     const volatile double* ve = e;
@@ -295,6 +296,7 @@ __device__ __noinline__ void nv_peer_exchange(const NvIterArgs& a, ArgMin r, dou
     best = m;
   }
   if (timed_out) {
+    st->exchange_failed = 1;
     atomicOr(&a.flags[a.grad_step], NV_FLAG_EXCHANGE_TIMEOUT);
     best = ArgMin{r.v, r.i + a.j0};
     bs = sval;

@@ -14,7 +14,7 @@ import torch
 from .errors import STATUS_TO_ERROR, DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsimopt_b200.so")
+LIB_PATH = os.environ.get("SIMOPT_LIB_PATH") or os.path.join(_HERE, "libsimopt_b200.so")  # override: experiments
 
 _lock = threading.Lock()
 _lib = None

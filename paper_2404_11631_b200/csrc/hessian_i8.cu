@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 constexpr int kTM = 128, kTN = 96;
 constexpr int kTK = 64;              // samples per stage = two K=32 MMAs per limb
 constexpr int kRing = 6, kTP = 4;    // cp.async ring depth, prefetch distance (< kRing - 1)
-constexpr int kTT = 256;             // threads (8 warps); warps 0-3 run the TMEM epilogue
+constexpr int kTP_THREADS = 256;     // producer threads (warps 0-7; warps 0-3 also run the epilogue)
+constexpr int kTT = kTP_THREADS + 32;  // + one MMA-issuer warp (warp 8)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -196,6 +197,7 @@ struct TcSmem {
   uint8_t limb[kRing][kLimbs][kTK];
   uint8_t b[2][kLimbs][kTN * kTK];      // limb-scaled B operands (double-buffered)
   uint64_t done[kRing];                 // MMAs of the step that used ring slot s completed
+  uint64_t full[kRing];                 // producers: stage in slot s loaded and expanded
   uint32_t taddr;
 };
 
@@ -210,8 +212,11 @@ __global__ void __launch_bounds__(kTT, 1)
   const int64_t i0 = (int64_t)tile.x * kTM, j0 = (int64_t)tile.y * kTN;
   const int64_t ch = 1LL << lg_ch, rs = ch + kRowPad;
   if (tid == 0) {
-    for (int q = 0; q < kRing; ++q)
+    for (int q = 0; q < kRing; ++q) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.done[q])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.full[q])),
+                   "r"(kTP_THREADS));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
@@ -223,13 +228,14 @@ __global__ void __launch_bounds__(kTT, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t taddr = sm.taddr;
   const uint32_t idesc = (2u << 4) | ((uint32_t)(kTN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
-
+  // descriptor arithmetic below adds byte offsets >> 4 to the start-address field: the
+  // whole shared window must stay below 2^18 bytes (14-bit field), which it does
   const int64_t T = (s1 - s0) / kTK;
   // this thread's cp.async chunks, fixed for every stage: (source offset in a sample
   // block, destination offset in a ring slot, bytes); 16-byte chunks of the A rows, the
   // B rows, then the limb rows
   constexpr int kA = kTM * 4, kB = kTN * 4, kL = kLimbs * 4;
-  constexpr int kPer = (kA + kB + kL + kTT - 1) / kTT;
+  constexpr int kPer = (kA + kB + kL + kTP_THREADS - 1) / kTP_THREADS;
   int64_t csrc[kPer];
   int cdst[kPer], cbytes[kPer];
   constexpr int kSlot = (int)(sizeof(TcSmem::a[0]));
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(kTT, 1)
   const int l_base = (int)(&sm.limb[0][0][0] - smraw);
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
-    const int c = tid + u * kTT;
+    const int c = tid + u * kTP_THREADS;
     csrc[u] = 0; cdst[u] = 0; cbytes[u] = -1;  // -1: no chunk
     if (c < kA + kB) {
       const bool isa = c < kA;
@@ -270,51 +276,69 @@ __global__ void __launch_bounds__(kTT, 1)
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
-  for (int64_t t = 0; t < kTP; ++t) {
-    if (t < T) issue(t);
-    else asm volatile("cp.async.commit_group;\n" ::);
-  }
-  for (int64_t t = 0; t < T; ++t) {
-    const int q = (int)(t % kRing), bb = (int)(t & 1);
-    // the MMAs of stage t-2 read ring slot (t+kTP)%kRing's predecessor chain and b[bb]:
-    // wait for them once (they completed long ago unless the tensor core is the bottleneck)
-    if (t >= 2) mbar_wait(&sm.done[(t - 2) % kRing], (uint32_t)(((t - 2) / kRing) & 1));
-    {
-      const int64_t tp = t + kTP;  // slot tp % kRing was last used by stage tp - kRing <= t - 2
-      if (tp < T) issue(tp);
+  if (warp < kTP_THREADS / 32) {
+    // ===== producers: cp.async ring, limb expansion, arrive on full[slot] =====
+    for (int64_t t = 0; t < kTP; ++t) {
+      if (t < T) issue(t);
       else asm volatile("cp.async.commit_group;\n" ::);
     }
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(kTP));
-    __syncthreads();
-    // B_k = (x * 255) & L_k, four samples per word, same canonical offsets as the raw tile
-    for (int c = tid; c < kTN * 4; c += kTT) {
-      const int off = c * 16;
-      const int kb = (off >= kTN * 32 ? 32 : 0) + ((off >> 7) & 1) * 16;  // first sample of the chunk
-      const uint4 x = *reinterpret_cast<const uint4*>(&sm.braw[q][off]);
-      const uint4 m = make_uint4(x.x * 255u, x.y * 255u, x.z * 255u, x.w * 255u);
-#pragma unroll
-      for (int k = 0; k < kLimbs; ++k) {
-        const uint4 L = *reinterpret_cast<const uint4*>(&sm.limb[q][k][kb]);
-        *reinterpret_cast<uint4*>(&sm.b[bb][k][off]) =
-            make_uint4(m.x & L.x, m.y & L.y, m.z & L.z, m.w & L.w);
+    for (int64_t t = 0; t < T; ++t) {
+      const int q = (int)(t % kRing), bb = (int)(t & 1);
+      // MMAs of stage t-2 read b[bb] and ring slot (t+kTP) % kRing: wait for them
+      if (t >= 2) mbar_wait(&sm.done[(t - 2) % kRing], (uint32_t)(((t - 2) / kRing) & 1));
+      {
+        const int64_t tp = t + kTP;
+        if (tp < T) issue(tp);
+        else asm volatile("cp.async.commit_group;\n" ::);
       }
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kTP));
+      asm volatile("bar.sync 1, %0;" ::"n"(kTP_THREADS));  // every producer's copies landed
+      // B_k = (x * 255) & L_k, four samples per word, same canonical offsets as the raw
+      // tile.  Task = (16-sample column kb, 32-row group): a warp's lanes share kb, so the
+      // five limb vectors are broadcast reads.
+      for (int task = warp; task < 4 * (kTN / 32); task += kTP_THREADS / 32) {
+        const int kb = (task & 3) * 16, r = (task >> 2) * 32 + lane;
+        const int off = canon<kTN>(r, kb);
+        const uint4 x = *reinterpret_cast<const uint4*>(&sm.braw[q][off]);
+        const uint4 m = make_uint4(x.x * 255u, x.y * 255u, x.z * 255u, x.w * 255u);
+#pragma unroll
+        for (int k = 0; k < kLimbs; ++k) {
+          const uint4 L = *reinterpret_cast<const uint4*>(&sm.limb[q][k][kb]);
+          *reinterpret_cast<uint4*>(&sm.b[bb][k][off]) =
+              make_uint4(m.x & L.x, m.y & L.y, m.z & L.z, m.w & L.w);
+        }
+      }
+      // generic-proxy writes (cp.async'd A, expanded B) -> visible to the tensor core
+      asm volatile("fence.proxy.async.shared::cta;");
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[q])) : "memory");
     }
-    asm volatile("fence.proxy.async.shared::cta;");
-    __syncthreads();
-    if (tid == 0) {
+  } else if (lane == 0) {
+    // ===== MMA issuer (warp 8, one lane): per stage one A copy into TMEM and five
+    // limb MMAs per K-step, committed to done[slot] =====
+    const uint64_t da0 = umma_desc(sm.a[0]), db0 = umma_desc(sm.b[0][0]);
+    const uint64_t a_slot = (uint64_t)(sizeof(TcSmem::a[0]) >> 4);
+    const uint64_t b_buf = (uint64_t)(sizeof(TcSmem::b[0]) >> 4), b_limb = (uint64_t)(sizeof(TcSmem::b[0][0]) >> 4);
+    for (int64_t t = 0; t < T; ++t) {
+      const int q = (int)(t % kRing), bb = (int)(t & 1);
+      mbar_wait(&sm.full[q], (uint32_t)((t / kRing) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int ks = 0; ks < kTK / 32; ++ks) {
-        const uint64_t da = umma_desc(sm.a[q] + ks * kTM * 32);
+        // A (shared by the five limb MMAs) is copied into TMEM once per K-step and the MMAs
+        // read it from there (TS mode): shared memory serves only the B operands.  cp and
+        // mma issued by this thread execute in order; 4 rotating 8-column A slots.
+        const uint32_t ta = taddr + (uint32_t)(kLimbs * kTN + 8 * (int)((2 * t + ks) & 3));
+        const uint64_t da = da0 + (uint64_t)q * a_slot + (uint64_t)(ks * kTM * 32 >> 4);
+        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(ta), "l"(da));
 #pragma unroll
         for (int k = 0; k < kLimbs; ++k) {
-          const uint64_t db = umma_desc(sm.b[bb][k] + ks * kTN * 32);
+          const uint64_t db = db0 + (uint64_t)bb * b_buf + (uint64_t)k * b_limb + (uint64_t)(ks * kTN * 32 >> 4);
           const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
                   taddr + (uint32_t)(k * kTN)),
-              "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+              "r"(ta), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
         }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

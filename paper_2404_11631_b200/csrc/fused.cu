@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(256) k_fused_finish(const double* __restrict__
     const int64_t j = blockIdx.x * 32LL + lane;
     double s = 0.0;
     if (j < d) {
+#pragma unroll 8
       for (int64_t c = w; c < ncl; c += 8) s += part[c * d + j];
     }
     red[w][lane] = s;
@@ -255,10 +256,18 @@ __global__ void __launch_bounds__(256) k_fused_finish(const double* __restrict__
       out[j] = center ? t - center[j] : t;
     }
   }
-  if (scalar_out && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (scalar_out && blockIdx.x == 0) {  // block-parallel, fixed order: deterministic
+    __shared__ double ws[8];
     double s = 0.0;
-    for (int64_t c = 0; c < ncl; ++c) s += spart[c];
-    *scalar_out = s;
+    for (int64_t c = threadIdx.x; c < ncl; c += 256) s += spart[c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) ws[w] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int k = 0; k < 8; ++k) t += ws[k];
+      *scalar_out = t;
+    }
   }
 }
 
@@ -525,14 +534,24 @@ __global__ void __launch_bounds__(256) k_fused_finish_peer(const double* __restr
   auto data = [&](int64_t q) { return reinterpret_cast<double*>(pr.peers[q]); };
   auto flags = [&](int64_t q) { return reinterpret_cast<uint64_t*>(data(q) + 2 * W * D1); };
   const int64_t jlo = out ? 0 : d;  // row pass only: just the side scalar crosses ranks
-  for (int64_t j = jlo + (int64_t)b * 256 + tid; j < D1; j += (int64_t)kFB * 256) {
+  for (int64_t j = jlo + (int64_t)b * 256 + tid; j < d; j += (int64_t)kFB * 256) {
     double s = 0.0;
-    if (j < d) {
-      for (int64_t c = 0; c < ncl; ++c) s += part[c * d + j];
-    } else {
-      for (int64_t c = 0; c < ncl; ++c) s += spart[c];
-    }
+#pragma unroll 8
+    for (int64_t c = 0; c < ncl; ++c) s += part[c * d + j];
     for (int64_t q = 0; q < W; ++q) data(q)[(par * W + pr.rank) * D1 + j] = s;
+  }
+  if (b == (int)((d - jlo) / 256 % kFB)) {  // the block that owns index d: side scalar, block-parallel
+    __shared__ double ws[8];
+    double s = 0.0;
+    for (int64_t c = tid; c < ncl; c += 256) s += spart[c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((tid & 31) == 0) ws[tid >> 5] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int k = 0; k < 8; ++k) t += ws[k];
+      for (int64_t q = 0; q < W; ++q) data(q)[(par * W + pr.rank) * D1 + d] = t;
+    }
   }
   __threadfence_system();
   __syncthreads();

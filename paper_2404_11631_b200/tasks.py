@@ -821,16 +821,19 @@ class MvFwEngine:
                 _lib.check(lib.simopt_matvec(sp, P(x), n_k, d, None, n_k, P(mean), P(w_in), chunk, P(q)))
             _lib.check(lib.simopt_matvec_t(sp, P(x), n_k, d, None, n_k, P(mean), P(q), chunk, P(self.gq)))
             _lib.check(lib.simopt_scale_sub(sp, P(self.gq), inv, P(mean), d, P(self.g)))
-            _lib.check(lib.simopt_lmo_simplex_slack(sp, P(self.g), d, P(self.s), P(self.status[m:])))
-            _lib.check(lib.simopt_axpy(sp, -1.0, P(w_in), P(self.s), d, P(self.dirn)))
-            _lib.check(lib.simopt_axpy_ptr(sp, P(self.gamma[m:]), P(self.dirn), P(w_in), d, P(w_out)))
-            _lib.check(lib.simopt_min_value(sp, P(w_out), d, P(self.wmin[m:])))
+            self._tail(sp, m, w_in, w_out, mean)
             # objective(w_{t+1}); q is reused by the next gradient of this epoch
             _lib.check(lib.simopt_matvec(sp, P(x), n_k, d, None, n_k, P(mean), P(w_out), chunk, P(q)))
-            _lib.check(lib.simopt_tree_sums2(sp, P(q), P(q), n_k, P(self.quad[m:]), P(w_out), P(mean), d,
-                                             P(self.lin[m:]), chunk))
-            _lib.check(lib.simopt_vec_sum(sp, P(w_out), d, chunk, P(self.wsum[m:])))
+            _lib.check(lib.simopt_dot(sp, P(q), P(q), n_k, chunk, P(self.quad[m:])))
             _lib.check(lib.simopt_timestamp(sp, P(self.stamps[m:])))
+
+    def _tail(self, sp, m, w_in, w_out, mean):
+        """LMO + update + min + exact sum/dot of the new iterate: one launch (simopt_mv_fw_tail)."""
+        P = _lib.ptr
+        _lib.check(self.lib.simopt_mv_fw_tail(sp, P(self.g), P(w_in), P(self.gamma[m:]), P(mean),
+                                              self.prob.dimension, self.chunk, P(w_out),
+                                              P(self.status[m:]), P(self.wmin[m:]), P(self.wsum[m:]),
+                                              P(self.lin[m:])))
 
     def _sharded_steps(self, ws, x, mean, n_k, inv):
         """Row-sharded step: exact mode gathers chunk partials (bit-identical to one
@@ -893,15 +896,10 @@ class MvFwEngine:
             w_in, w_out = ws[m], ws[m + 1]
             if m == 0:  # g = (1/(N-1)) Xc^T Xc w_kM - mean
                 fused_rows(MV, x, w_in, center=mean, col_scale=inv, col_out=self.g)
-            _lib.check(lib.simopt_lmo_simplex_slack(sp, P(self.g), d, P(self.s), P(self.status[m:])))
-            _lib.check(lib.simopt_axpy(sp, -1.0, P(w_in), P(self.s), d, P(self.dirn)))
-            _lib.check(lib.simopt_axpy_ptr(sp, P(self.gamma[m:]), P(self.dirn), P(w_in), d, P(w_out)))
-            _lib.check(lib.simopt_min_value(sp, P(w_out), d, P(self.wmin[m:])))
+            self._tail(sp, m, w_in, w_out, mean)
             last = m == self.M - 1
             fused_rows(MV, x, w_out, center=mean, col_scale=inv, col_out=None if last else self.g,
                        scalar_out=self.quad[m:], accumulate=not last)
-            _lib.check(lib.simopt_dot(sp, P(w_out), P(mean), d, chunk, P(self.lin[m:])))
-            _lib.check(lib.simopt_vec_sum(sp, P(w_out), d, chunk, P(self.wsum[m:])))
             _lib.check(lib.simopt_timestamp(sp, P(self.stamps[m:])))
 
     def run_epoch(self, k: int, n_k: int):

@@ -433,13 +433,19 @@ __global__ void __launch_bounds__(kNT) k_fused_nib(const uint64_t* __restrict__ 
     // row dot: this thread's row, nibble by nibble
     const int64_t r = r0 + tid;
     const uint64_t* row = tb + tid * WS;
-    double s = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains: latency, not issue, bound
     for (int ww = 0; ww < (int)W; ++ww) {
       const uint64_t m = row[ww];
       const double* Tw = T + 16 * 16 * ww;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) s += Tw[16 * i + (int)((m >> (4 * i)) & 15ULL)];
+      for (int i = 0; i < 16; i += 4) {
+        s0 += Tw[16 * i + (int)((m >> (4 * i)) & 15ULL)];
+        s1 += Tw[16 * (i + 1) + (int)((m >> (4 * i + 4)) & 15ULL)];
+        s2 += Tw[16 * (i + 2) + (int)((m >> (4 * i + 8)) & 15ULL)];
+        s3 += Tw[16 * (i + 3) + (int)((m >> (4 * i + 12)) & 15ULL)];
+      }
     }
+    const double s = (s0 + s1) + (s2 + s3);
     double wt = 0.0;
     if (r < N) {
       const double t = s;

@@ -420,15 +420,29 @@ __global__ void __launch_bounds__(kNT) k_fused_nib(const uint64_t* __restrict__ 
   for (int e = tid; e < 16 * Gp; e += kNT) A[e] = 0.0;
   double sc = 0.0;
   const int64_t ntiles = (N + kNT - 1) / kNT;
+  // the next tile's words are loaded into registers while this tile is processed
+  // (coalesced: consecutive threads, consecutive words; W <= 16 words per row here)
+  uint64_t pf[16];
+  auto fetch = [&](int64_t tl) {
+    const int64_t rb = tl * kNT;
+    const int64_t nr = tl < ntiles ? (N - rb < kNT ? N - rb : kNT) : 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int e = tid + k * kNT, rr = e / (int)W, ww = e - rr * (int)W;
+      pf[k] = (k < (int)W && rr < nr) ? __ldg(bits + (rb + rr) * W + ww) : 0ULL;
+    }
+  };
+  fetch(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * kNT;
-    __syncthreads();  // tables built / previous tile consumed
-    // stage the tile's bits (coalesced: consecutive threads, consecutive words)
     const int64_t nrow = N - r0 < kNT ? N - r0 : kNT;
-    for (int e = tid; e < kNT * (int)W; e += kNT) {
-      const int rr = e / (int)W, ww = e - rr * (int)W;
-      tb[rr * WS + ww] = rr < nrow ? __ldg(bits + (r0 + rr) * W + ww) : 0ULL;
+    __syncthreads();  // tables built / previous tile consumed
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int e = tid + k * kNT, rr = e / (int)W, ww = e - rr * (int)W;
+      if (k < (int)W) tb[rr * WS + ww] = pf[k];
     }
+    fetch(tile + gridDim.x);
     __syncthreads();
     // row dot: this thread's row, nibble by nibble
     const int64_t r = r0 + tid;

@@ -60,11 +60,6 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// Bulk L2 prefetch of one contiguous row band (TMA engine; no registers, no smem).
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 template <int MODE, int C, int K, bool VEC>
 __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
   constexpr int R = (16 / K) < 1 ? 1 : 16 / K;
@@ -99,14 +94,8 @@ __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
   double sc = 0.0;
   const int64_t ntiles = (N + R - 1) / R;
   int par = 0;
-  const uint32_t band_bytes = (uint32_t)(((b1 - b0) * 8 + 15) & ~15LL);
   for (int64_t tile = cl; tile < ntiles; tile += ncl, par ^= 1) {
     const int64_t r0 = tile * R;
-    // keep HBM busy through this tile's reductions: the next tile's rows go to L2 now
-    if (VEC && tid < R && b1 > b0) {
-      const int64_t rn = r0 + ncl * R + tid;
-      if (rn < N) prefetch_l2(a.X + rn * d + b0, band_bytes);
-    }
     double2 x[R][K];
 #pragma unroll
     for (int i = 0; i < R; ++i) {

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kTailThreads)
     for (int w = 1; w < kTailThreads / 32; ++w) m = (wm[w] < m || wm[w] != wm[w]) ? wm[w] : m;
     *wmin_out = (wm[0] != wm[0]) ? wm[0] : m;
   }
+  if (!in_smem) return;  // large d: the host wrapper runs the exact sums as a tree kernel
   // exact chains: threads [0, nch) sum(w'), threads [nch, 2 nch) dot(w', mean)
   const int64_t nch = (d + chunk - 1) / chunk;
   if (tid < 2 * nch) {
@@ -233,5 +234,9 @@ extern "C" int simopt_mv_fw_tail(void* stream, const double* g, const double* w_
                                                              status, wmin_out, wsum_out, lin_out,
                                                              part, use_smem);
   SIMOPT_CHECK_LAUNCH("k_mv_fw_tail");
+  // vectors too large for one block's shared memory: the exact sums as a warp-per-chunk
+  // tree kernel (one chain per 4096-chunk in a single block would wait on L2 per batch)
+  if (!use_smem)
+    return simopt_tree_sums2(stream, w_out, mean, d, lin_out, w_out, nullptr, d, wsum_out, chunk);
   return SIMOPT_OK;
 }

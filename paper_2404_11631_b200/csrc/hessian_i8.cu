@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 // entries and their mirrors.  (tools/micro/tc_i8.cu is the single-MMA smoke test.)
 constexpr int kTM = 128, kTN = 96;
 constexpr int kTK = 64;              // samples per stage = two K=32 MMAs per limb
-constexpr int kRing = 6, kTP = 4;    // cp.async ring depth, prefetch distance (< kRing - 1)
+constexpr int kRing = 8, kTP = 6;    // cp.async ring depth (power of two: cheap slot and phase math), prefetch distance
 constexpr int kTP_THREADS = 256;     // producer threads (warps 0-7; warps 0-3 also run the epilogue)
 constexpr int kTT = kTP_THREADS + 32;  // + one MMA-issuer warp (warp 8)
 

@@ -218,7 +218,7 @@ def run_ours(args, rank, world):
     from paper_2404_11631_b200.frank_wolfe import FwConfig, fw_run
     from paper_2404_11631_b200.instances import gen_newsvendor_instance
     from paper_2404_11631_b200.records import TraceBuilder
-    from paper_2404_11631_b200.tasks import NewsvendorProblem, NvFwEngine
+    from paper_2404_11631_b200.tasks import NewsvendorProblem, make_nv_engine
 
     from paper_2404_11631_b200.sharding import ShardGroup
     backend = pkg.make_backend("cuda")
@@ -226,7 +226,7 @@ def run_ours(args, rank, world):
     shard = ShardGroup() if world > 1 else None
     prob = NewsvendorProblem(task, backend, shard=shard)
     epochs = args.warmup + args.steps
-    eng = NvFwEngine(prob, M, epochs, backend.chunk_size)
+    eng = make_nv_engine(prob, M, epochs, backend.chunk_size)  # CUDA-graph epochs
     stream = pkg.RngStream(SEED, 2)
     eng.start()
     for k in range(args.warmup):  # the next epoch's resample overlaps this epoch's steps,

@@ -215,6 +215,14 @@ typedef struct NvIterArgs {
   double* const* peer_mb;
   int64_t world, rank, j0;
   uint64_t seq;
+  /* Device-resident step parameters (CUDA-graph replay of whole epochs; NULL: use the
+   * by-value fields above): epoch_draw = {seed, sid, ctr_lo, ctr_hi} of the epoch's draw;
+   * epoch_ctr -> epoch k, gamma = 2 / (k * inner_iters + m + 2) (frank_wolfe.py:62-66);
+   * seq_ptr -> the peer exchange sequence, incremented by the step's last block. */
+  const uint64_t* epoch_draw;
+  const int64_t* epoch_ctr;
+  int64_t inner_iters, m;
+  uint64_t* seq_ptr;
 } NvIterArgs;
 int simopt_nv_iter(void* stream, const NvIterArgs* args);
 

@@ -268,7 +268,12 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 __device__ __noinline__ void nv_peer_exchange(const NvIterArgs& a, ArgMin r, double sval, NvState* st) {
-  const int64_t par = (int64_t)(a.seq & 1ULL), W = a.world;
+  uint64_t seq = a.seq;
+  if (a.seq_ptr) {  // device-resident sequence (graph replay): this exchange's number
+    seq = *a.seq_ptr + 1;
+    *a.seq_ptr = seq;
+  }
+  const int64_t par = (int64_t)(seq & 1ULL), W = a.world;
   for (int64_t q = 0; q < W; ++q) {
     double* slot = a.peer_mb[q] + (par * W + a.rank) * 4;
     volatile double* vs = slot;
@@ -276,7 +281,7 @@ __device__ __noinline__ void nv_peer_exchange(const NvIterArgs& a, ArgMin r, dou
     vs[1] = (double)(r.i + a.j0);  // exact: product indices < 2^53
     vs[2] = sval;
     __threadfence_system();
-    st_release_u64(reinterpret_cast<uint64_t*>(slot + 3), a.seq);
+    st_release_u64(reinterpret_cast<uint64_t*>(slot + 3), seq);
   }
   const double* mb = a.peer_mb[a.rank] + par * W * 4;
   ArgMin best{INFINITY, INT64_MAX};
@@ -285,7 +290,7 @@ __device__ __noinline__ void nv_peer_exchange(const NvIterArgs& a, ArgMin r, dou
   bool timed_out = st->exchange_failed != 0;  // sticky: after one failure, never wait again
   for (int64_t q = 0; q < W && !timed_out; ++q) {
     const double* e = mb + q * 4;
-    while (ld_acquire_u64(reinterpret_cast<const uint64_t*>(e + 3)) != a.seq) {
+    while (ld_acquire_u64(reinterpret_cast<const uint64_t*>(e + 3)) != seq) {
       if (globaltimer() - t0 > 10000000000ULL) { timed_out = true; break; }
     }
     if (timed_out) break;
@@ -324,14 +329,18 @@ __global__ void __launch_bounds__(kIterWarps * 32, 3)
   NvState* st = a.state;
   const int64_t jstar = st->jstar;
   const double sval = st->sval;
-  const NvStreamPos sp{a.seed, a.sid, a.ctr_lo, a.ctr_hi};
+  const NvStreamPos sp = a.epoch_draw
+                            ? NvStreamPos{a.epoch_draw[0], a.epoch_draw[1], a.epoch_draw[2], a.epoch_draw[3]}
+                            : NvStreamPos{a.seed, a.sid, a.ctr_lo, a.ctr_hi};
+  // frank_wolfe.py:62-66: gamma = 2 / (epoch * inner_iters + inner + 2), IEEE double division
+  const double gamma = a.epoch_ctr ? 2.0 / (double)(*a.epoch_ctr * a.inner_iters + a.m + 2) : a.gamma;
   for (int64_t j = (int64_t)blockIdx.x * kIterWarps + warp; j < a.d;
        j += (int64_t)gridDim.x * kIterWarps) {
     double x = a.x_in[j];
     if (a.do_update) {
       const double sj = (j == jstar) ? sval : 0.0;
       const double dir = (-1.0 * x) + sj;
-      x = a.gamma * dir + x;
+      x = gamma * dir + x;
       if (lane == 0) {
         a.x[j] = x;
         if (x < -1e-10) atomicOr(&a.flags[a.step], NV_FLAG_NEGATIVE);

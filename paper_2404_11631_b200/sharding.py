@@ -182,6 +182,8 @@ class PeerMailbox:
             ptrs.append(p.value)
         self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
         self.seq = 0
+        # device-resident sequence for exchanges issued from replayed CUDA graphs
+        self.seq_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
 
     def next_seq(self) -> int:
         self.seq += 1

@@ -47,6 +47,8 @@ class NvIterArgs(ctypes.Structure):
         ("part_capacity", ctypes.c_int64),
         ("peer_mb", ctypes.c_void_p), ("world", ctypes.c_int64), ("rank", ctypes.c_int64),
         ("j0", ctypes.c_int64), ("seq", ctypes.c_uint64),
+        ("epoch_draw", ctypes.c_void_p), ("epoch_ctr", ctypes.c_void_p),
+        ("inner_iters", ctypes.c_int64), ("m", ctypes.c_int64), ("seq_ptr", ctypes.c_void_p),
     ]
 
 
@@ -306,10 +308,11 @@ class NvFwEngine:
         if self.mailbox is not None:
             a.peer_mb = self.mailbox.ptrs.data_ptr()
             a.world, a.rank, a.j0 = self.shard.world, self.shard.rank, dev.j0
+            a.seq_ptr = self.mailbox.seq_dev.data_ptr()  # one sequence source per mailbox
         if self.shard is not None:
             self.send = empty(3)
             # per epoch: spent[M] | objs[M] | nan[M+1] | negative[M+1] | timeout[M+1] flags
-            self.red = empty(2, 5 * M + 3)  # double-buffered by epoch parity
+            self.red = empty(epochs, 5 * M + 3)
         self.lib = _lib.load()
         self.t0 = None
         self.resample_events = []
@@ -419,20 +422,26 @@ class NvFwEngine:
             done.record(self.side)
             self.side_done[t] = done
         if self.shard is not None:
-            # epoch totals over the product shards, one allreduce after the side work
-            with torch.cuda.stream(self.side):
-                r, lo, hi = self.red[k % 2], t0, t0 + M
-                r[:M].copy_(self.spent[lo:hi])
-                r[M:2 * M].copy_(self.objs[lo:hi])
-                f = self.flags[lo:hi + 1]
-                r[2 * M:3 * M + 1].copy_((f & NV_FLAG_NAN_GRADIENT).to(F64))
-                r[3 * M + 1:4 * M + 2].copy_((f & NV_FLAG_NEGATIVE).to(F64))
-                r[4 * M + 2:].copy_((f & NV_FLAG_EXCHANGE_TIMEOUT).to(F64))
-                self.shard.allreduce_(r)
-                done = torch.cuda.Event()
-                done.record(self.side)
-            self.side_done[t0 + M - 1] = done
+            self.side_done[t0 + M - 1] = self._reduce_epoch(k)
         self.epoch_done[k] = self.side_done[t0 + M - 1]
+
+    def _reduce_epoch(self, k: int):
+        """Epoch totals over the product shards: one allreduce on the side stream, into a
+        per-epoch row of self.red.  Returns the event after it."""
+        M = self.M
+        lo, hi = k * M, (k + 1) * M
+        with torch.cuda.stream(self.side):
+            r = self.red[k]
+            r[:M].copy_(self.spent[lo:hi])
+            r[M:2 * M].copy_(self.objs[lo:hi])
+            f = self.flags[lo:hi + 1]
+            r[2 * M:3 * M + 1].copy_((f & NV_FLAG_NAN_GRADIENT).to(F64))
+            r[3 * M + 1:4 * M + 2].copy_((f & NV_FLAG_NEGATIVE).to(F64))
+            r[4 * M + 2:].copy_((f & NV_FLAG_EXCHANGE_TIMEOUT).to(F64))
+            self.shard.allreduce_(r)
+            done = torch.cuda.Event()
+            done.record(self.side)
+        return done
 
     def _seq(self):
         """Next exchange sequence number (monotonic per mailbox, across runs)."""
@@ -466,7 +475,7 @@ class NvFwEngine:
             sp_ = to_host(self.spent[lo:hi])
             ob = to_host(self.objs[lo:hi])
         else:
-            r = to_host(self.red[k % 2])
+            r = to_host(self.red[k])
             sp_, ob = r[:M], r[M:2 * M]
             fl = ((r[2 * M:3 * M + 1] > 0) * NV_FLAG_NAN_GRADIENT
                   + (r[3 * M + 1:4 * M + 2] > 0) * NV_FLAG_NEGATIVE
@@ -494,8 +503,166 @@ class NvFwEngine:
         return self.shard.allgather_rows(x.view(-1, 1), counts).view(-1)
 
 
+class NvFwGraphEngine(NvFwEngine):
+    """NvFwEngine whose epochs are replayed as CUDA graphs (one per epoch parity).
+
+    Everything an epoch's step sequence reads is parity-fixed or device-resident, so
+    the graph captured for parity p serves every epoch of that parity:
+    * iterates live in two rings of M+1 rows; epoch k (parity p) starts from
+      rings[1-p][M] (the previous epoch's last iterate) and writes rings[p][1..M];
+    * the epoch's draw words and k sit in a per-parity device buffer (one pinned
+      H2D copy per epoch); the step kernel reads them and forms
+      gamma = 2 / (k M + m + 2) itself (frank_wolfe.py:62-66);
+    * the peer LMO exchange's sequence number is a device counter;
+    * flags, recorded sums and stamps go to per-parity buffers, copied into the
+      per-epoch records right behind the replay.
+    The host then enqueues one H2D copy and one graph launch per epoch instead of
+    ~100 launches: the per-step host cost disappears, which is what bounds the
+    product-sharded run at 8 GPUs (device time per step ~10 us).
+    """
+
+    def __init__(self, prob: "NewsvendorProblem", inner_iters: int, epochs: int, chunk: int):
+        super().__init__(prob, inner_iters, epochs, chunk)
+        d, M = self.dev.d, self.M
+        self.rings = [torch.zeros(M + 1, d, dtype=F64, device="cuda") for _ in range(2)]
+        self.terms_e = torch.empty(M, d, dtype=F64, device="cuda")
+        self.flags_e = [torch.zeros(M + 1, dtype=torch.int32, device="cuda") for _ in range(2)]
+        self.spent_e = [empty(M) for _ in range(2)]
+        self.objs_e = [empty(M) for _ in range(2)]
+        self.stamps_e = [torch.zeros(M, dtype=torch.int64, device="cuda") for _ in range(2)]
+        self.host_params = [torch.zeros(5, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self.dev_params = [torch.zeros(5, dtype=torch.int64, device="cuda") for _ in range(2)]
+        self.param_ev = [None, None]  # H2D of the parity's parameters (host buffer reuse)
+        self.graphs = {}
+        self.warm = set()
+        # captured kernel nodes keep the capture stream's priority: capture at high priority
+        # so replayed steps still pre-empt the overlapping resample's blocks
+        self.cstream = torch.cuda.Stream(priority=self.hi.priority)
+
+    def _step_args(self, p: int, m: int, update: bool) -> NvIterArgs:
+        """Arguments of step m (update + next gradient) or, m < 0, of the epoch's first gradient."""
+        a = NvIterArgs.from_buffer_copy(self.args)
+        dev, M = self.dev, self.M
+        a.S, a.nseg = dev.slots[p][0], dev.slots[p][1]
+        a.keys, a.off = dev.slots[p][2].data_ptr(), dev.slots[p][3].data_ptr()
+        a.epoch_draw = self.dev_params[p].data_ptr()
+        a.epoch_ctr = self.dev_params[p].data_ptr() + 4 * 8
+        a.inner_iters, a.m = M, max(m, 0)
+        a.flags = self.flags_e[p].data_ptr()
+        a.terms = None
+        prev_last = self.rings[1 - p][M].data_ptr()
+        if not update:  # gradient + LMO at the epoch's first iterate
+            a.x_in = a.x = prev_last
+            a.do_update, a.do_grad, a.step, a.grad_step = 0, 1, 0, 0
+        else:
+            a.x_in = prev_last if m == 0 else self.rings[p][m].data_ptr()
+            a.x = self.rings[p][m + 1].data_ptr()
+            a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), m, m + 1
+        return a
+
+    def _steps(self, p: int, main, side):
+        """The epoch's step sequence on `main` (+ recording on `side`), capture-safe."""
+        lib, dev, M = self.lib, self.dev, self.M
+        sp, ssp = _lib.stream_ptr(main), _lib.stream_ptr(side)
+        P = _lib.ptr
+        _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(self._step_args(p, -1, False))))
+        fork = torch.cuda.Event()
+        for m in range(M):
+            _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(self._step_args(p, m, True))))
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            xout = self.rings[p][m + 1]
+            _lib.check(lib.simopt_nv_cost_terms(ssp, P(xout), P(dev.mu), P(dev.sigma), P(dev.k), P(dev.h),
+                                                P(dev.v), dev.d, P(self.terms_e[m])))
+            _lib.check(lib.simopt_tree_sums2(ssp, P(dev.c), P(xout), dev.d, P(self.spent_e[p][m:]),
+                                             P(self.terms_e[m]), None, dev.d, P(self.objs_e[p][m:]),
+                                             self.chunk))
+            _lib.check(lib.simopt_timestamp(ssp, P(self.stamps_e[p][m:])))
+        fork.record(side)
+        main.wait_event(fork)  # join: the epoch ends when its recording ends
+
+    def enqueue_epoch(self, k: int, stream: RngStream, n_samples: int, time_resample: bool = False,
+                      next_samples: int | None = None):
+        if k not in self.ready:
+            self._resample(k, stream, n_samples, time_resample)
+        slot, ready = self.ready.pop(k)
+        p = k & 1
+        assert slot == p
+        main = self.hi
+        main.wait_event(ready)
+        self.dev.use_slot(p)
+        hp = self.host_params[p]
+        if self.param_ev[p] is not None:  # the previous copy from this pinned buffer has run
+            self.param_ev[p].synchronize()
+        words = [w if w < (1 << 63) else w - (1 << 64) for w in self.dev.slots[p][4]]
+        hp[:4] = torch.tensor(words, dtype=torch.int64)
+        hp[4] = k
+        with torch.cuda.stream(main):
+            self.dev_params[p].copy_(hp, non_blocking=True)
+            pe = torch.cuda.Event()
+            pe.record(main)
+            self.param_ev[p] = pe
+            g = self.graphs.get(p)
+            if g is not None:
+                g.replay()
+            elif p not in self.warm:  # first epoch of this parity: eager (allocations, setup)
+                self._steps(p, main, self.side)
+                self.warm.add(p)
+            else:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                self.cstream.wait_stream(main)
+                with torch.cuda.graph(g, stream=self.cstream):
+                    self._steps(p, self.cstream, self.side)
+                self.graphs[p] = g
+                g.replay()
+            steps = torch.cuda.Event()
+            steps.record(main)
+            # the parity buffers serve every epoch of that parity: copy this epoch's
+            # records out (on main, so epoch k+2's replay cannot overwrite them first)
+            lo, hi, M = k * self.M, (k + 1) * self.M, self.M
+            self.flags[lo:hi].copy_(self.flags_e[p][:M])
+            self.flags_e[p].zero_()
+            self.spent[lo:hi].copy_(self.spent_e[p])
+            self.objs[lo:hi].copy_(self.objs_e[p])
+            self.stamps[lo:hi].copy_(self.stamps_e[p])
+            done = torch.cuda.Event()
+            done.record(main)
+        self.steps_done[k] = steps
+        self.epoch_done[k] = done
+        if self.shard is not None:
+            self.side.wait_event(done)
+            self.epoch_done[k] = self._reduce_epoch(k)
+        if next_samples is not None:
+            self._resample(k + 1, stream, next_samples, time_resample)
+
+    def iterate(self, t: int) -> torch.Tensor:
+        """Full iterate after t steps (product slices gathered when sharded)."""
+        k, m = divmod(t, self.M)
+        x = self.rings[(k - 1) & 1][self.M] if m == 0 else self.rings[k & 1][m]
+        if self.shard is None:
+            return x
+        counts = [b - a for a, b in self.shard.ranges(self.dev.d_total, 4)]
+        return self.shard.allgather_rows(x.view(-1, 1), counts).view(-1)
+
+
+def make_nv_engine(prob: "NewsvendorProblem", inner_iters: int, epochs: int, chunk: int,
+                   graph: bool | None = None):
+    """Engine for a device FW run.  graph=None: CUDA-graph epochs for product-sharded runs
+    with the peer-memory exchange (per-step device work ~10 us at 8 GPUs, so host launch
+    cost would bound them); the eager engine otherwise (on one GPU the epoch is device-bound
+    and eager launching measured as fast; NCCL exchanges are not captured)."""
+    eng = NvFwEngine(prob, inner_iters, epochs, chunk)
+    if graph is None:
+        graph = eng.mailbox is not None
+    if not graph or (prob.shard is not None and eng.mailbox is None):
+        return eng
+    return NvFwGraphEngine(prob, inner_iters, epochs, chunk)
+
+
 def _nv_fw_run_device(prob: "NewsvendorProblem", config, backend, label, size, rep):
-    eng = NvFwEngine(prob, config.inner_iters, config.epochs, backend.chunk_size)
+    eng = make_nv_engine(prob, config.inner_iters, config.epochs, backend.chunk_size)
     trace = TraceBuilder()
 
     def abort(t, exc, it):

@@ -178,3 +178,27 @@ def test_approximation_error_measured(pkg, seed, sid, ctr):
     m = float(out.item())
     print(f"max |z~ - z| = {m:.3e} (bound {eps.value:.1e})")
     assert m < eps.value / 3
+
+
+def test_graph_engine_matches_eager(pkg):
+    """Epochs replayed as CUDA graphs (parity graphs, device-resident gamma/draw) give the
+    eager engine's trace bit for bit."""
+    from paper_2404_11631_b200.instances import gen_newsvendor_instance
+    from paper_2404_11631_b200.records import TraceBuilder
+    from paper_2404_11631_b200.tasks import NewsvendorProblem, make_nv_engine
+    task = gen_newsvendor_instance(700, pkg.RngStream(42, 0))
+    out = []
+    for graph in (False, True):
+        prob = NewsvendorProblem(task, pkg.make_backend("cuda"))
+        K, M, S = 5, 6, 3000
+        eng = make_nv_engine(prob, M, K, 4096, graph=graph)
+        stream = pkg.RngStream(42, 2)
+        eng.start()
+        for k in range(K):
+            eng.enqueue_epoch(k, stream, S, next_samples=S if k + 1 < K else None)
+        eng.finish()
+        tr = TraceBuilder()
+        for k in range(K):
+            assert eng.check_epoch(k, tr) is None
+        out.append((tr.build("nv", 700, "cuda", 0, 42, None).objectives, eng.iterate(K * M).cpu().numpy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])

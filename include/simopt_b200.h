@@ -358,6 +358,16 @@ int simopt_bernoulli_bits(void* stream, uint64_t seed, uint64_t stream_id, uint6
                           uint64_t ctr_hi, int64_t row_lo, int64_t row_hi, int64_t d, uint64_t* out);
 int simopt_matvec_bits(void* stream, const uint64_t* bits, int64_t rows, int64_t d, const double* v,
                        int64_t chunk, double* out);
+/* matvec_bits over the gathered rows idx[0..rows) (nullable: rows 0..rows) of a bit matrix
+ * with total_rows rows -- simopt_matvec's rows_idx form (tasks.py:205-213 batches).
+ * matvec_t_bits: the fixed-tree column sums (_kernels.py:124-156) x^T X over bits, same
+ * gather; bit-identical to simopt_matvec_t on the 0.0/1.0 matrix. */
+int simopt_matvec_bits_idx(void* stream, const uint64_t* bits, int64_t total_rows, int64_t d,
+                           const int64_t* idx, int64_t rows, const double* v, int64_t chunk,
+                           double* out);
+int simopt_matvec_t_bits(void* stream, const uint64_t* bits, int64_t total_rows, int64_t d,
+                         const int64_t* idx, int64_t rows, const double* x, int64_t chunk,
+                         double* out);
 int simopt_unpack_bits(void* stream, const uint64_t* bits, int64_t rows, int64_t d, double* out);
 /* simopt_fused_rows (LR_GRAD / LR_HVP modes) on bit-packed features, d <= 16384. */
 int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bits, int64_t rows, int64_t cols,

@@ -77,6 +77,8 @@ SIGNATURES = {
     "simopt_peer_free": [_vp],
     "simopt_bernoulli_bits": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _i64, _vp],
     "simopt_matvec_bits": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
+    "simopt_matvec_bits_idx": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
+    "simopt_matvec_t_bits": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
     "simopt_unpack_bits": [_vp, _vp, _i64, _i64, _vp],
     "simopt_fused_rows_bits": [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _d, _i32, _i32, _vp, _vp, _vp,
                                _vp, _vp],

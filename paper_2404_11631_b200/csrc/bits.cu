@@ -45,8 +45,21 @@ __global__ void __launch_bounds__(256) k_bernoulli_bits(uint64_t seed, uint64_t 
   }
 }
 
-// Exact-tree row dots over bits: partial of (row r, column chunk c) = v_j summed over the
-// set bits j of the chunk in increasing order (p[c * rows + r]), folded afterwards.
+constexpr int kMbRows = 128;
+constexpr int kMbSlab = 16;
+// s + x*t with x = bit ? 1.0 : 0.0 as one DFMA: the product is exact (t or +-0), so the
+// fused result is the reference's s + (x*t) bit for bit -- including x = 0 with t = +-inf
+// or NaN, where the reference's 0.0*t is NaN as well.  Adding +-0 leaves every sum that
+// starts at +0.0 unchanged (it never becomes -0.0).
+__device__ __forceinline__ void add_if_set(double& s, double t, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 hi;\n\t.reg .f64 x;\n\t"
+      "setp.ne.u32 p, %2, 0;\n\tselp.b32 hi, 0x3FF00000, 0, p;\n\t"
+      "mov.b64 x, {0, hi};\n\tfma.rn.f64 %0, x, %1, %0;\n\t}"
+      : "+d"(s) : "d"(t), "r"(bit));
+}
+// Exact-tree row dots over bits, any chunk size (the slab kernel below needs chunk % 64 == 0):
+// partial of (row r, column chunk c) = the chain over the chunk's columns in increasing
+// order (p[c * rows + r]), folded afterwards.
 __global__ void __launch_bounds__(128) k_matvec_bits(const uint64_t* __restrict__ bits, int64_t rows,
                                                      int64_t d, int64_t W,
                                                      const double* __restrict__ v, int64_t chunk,
@@ -57,19 +70,91 @@ __global__ void __launch_bounds__(128) k_matvec_bits(const uint64_t* __restrict_
     const int64_t lo = c * chunk, hi = lo + chunk < d ? lo + chunk : d;
     const uint64_t* row = bits + r * W;
     double s = 0.0;
-    for (int64_t w = lo >> 6; w <= (hi - 1) >> 6; ++w) {
-      uint64_t m = row[w];
-      const int64_t base = w << 6;
-      if (base < lo) m &= ~0ULL << (lo - base);                  // chunk starts mid-word
-      if (hi - base < 64) m &= (hi - base >= 64) ? ~0ULL : ((1ULL << (hi - base)) - 1ULL);
-      while (m) {
-        const int b = __ffsll((long long)m) - 1;
-        s = s + v[base + b];
-        m &= m - 1;
-      }
-    }
+    for (int64_t j = lo; j < hi; ++j)
+      add_if_set(s, v[j], (uint32_t)(row[j >> 6] >> (j & 63)) & 1u);
     p[c * rows + r] = s;
   }
+}
+
+// Exact-tree row dots, slab-staged (chunk % 64 == 0): one row per thread, 128 rows per block.
+// A slab of 16 words x 128 rows is staged in shared memory with coalesced loads (row
+// stride 17 words: conflict-free per-thread reads), its 1024 v entries beside it; each
+// thread then walks its row's bits in column order with one DFMA per column (add_if_set)
+// and v broadcast from shared memory -- no per-lane gather, no divergence.  The chain per
+// row is the reference's: s = s + v_j over the set bits j, restarted at every chunk
+// boundary (partial p[c * rows + r]).  rows_idx (nullable) gathers batch rows.
+__global__ void __launch_bounds__(kMbRows) k_matvec_bits_slab(const uint64_t* __restrict__ bits,
+                                                              int64_t W, int64_t d,
+                                                              const int64_t* __restrict__ idx,
+                                                              int64_t rows,
+                                                              const double* __restrict__ v,
+                                                              int64_t cw, int64_t nch,
+                                                              double* __restrict__ p) {
+  __shared__ uint64_t sb[kMbRows * (kMbSlab + 1)];
+  __shared__ __align__(16) double sv[kMbSlab * 64];
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * kMbRows, r = r0 + tid;
+  double s = 0.0;
+  int64_t next_cut = cw, c = 0;
+  for (int64_t w0 = 0; w0 < W; w0 += kMbSlab) {
+    const int nw = (int)(W - w0 < kMbSlab ? W - w0 : kMbSlab);
+    __syncthreads();
+    for (int e = tid; e < kMbRows * nw; e += kMbRows) {
+      const int rr = e / nw, ww = e - rr * nw;
+      const int64_t row = r0 + rr;
+      uint64_t x = 0;
+      if (row < rows) x = bits[(idx ? idx[row] : row) * W + w0 + ww];
+      sb[rr * (kMbSlab + 1) + ww] = x;
+    }
+    for (int e = tid; e < nw * 64; e += kMbRows) {
+      const int64_t j = w0 * 64 + e;
+      sv[e] = j < d ? v[j] : 0.0;
+    }
+    __syncthreads();
+    for (int ww = 0; ww < nw; ++ww) {
+      if (w0 + ww == next_cut) {  // chunk boundary: the chain restarts
+        if (r < rows) p[c * rows + r] = s;
+        s = 0.0;
+        ++c;
+        next_cut += cw;
+      }
+      const uint64_t m = sb[tid * (kMbSlab + 1) + ww];
+      const uint32_t halves[2] = {(uint32_t)m, (uint32_t)(m >> 32)};
+      const double2* vv = reinterpret_cast<const double2*>(sv + ww * 64);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t q = halves[h];
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+          const double2 t = vv[h * 16 + b];
+          add_if_set(s, t.x, q & (1u << (2 * b)));
+          add_if_set(s, t.y, q & (1u << (2 * b + 1)));
+        }
+      }
+    }
+  }
+  if (r < rows) p[c * rows + r] = s;
+  (void)nch;
+}
+
+// Exact-tree column sums over bits: partial (column j, row chunk c) = the chain over the
+// chunk's rows i (in order, through rows_idx when given) of x_ij * x_i.  One
+// column per thread; the 64 threads of a word read the same u64 (broadcast).
+__global__ void __launch_bounds__(128) k_matvec_t_bits(const uint64_t* __restrict__ bits, int64_t W,
+                                                       int64_t d, const int64_t* __restrict__ idx,
+                                                       int64_t rows, const double* __restrict__ x,
+                                                       int64_t chunk, double* __restrict__ p) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+  if (j >= d) return;
+  const int64_t lo = c * chunk, hi = lo + chunk < rows ? lo + chunk : rows;
+  const int64_t wj = j >> 6;
+  const uint64_t bit = 1ULL << (j & 63);
+  double s = 0.0;
+  for (int64_t i = lo; i < hi; ++i) {
+    const int64_t row = idx ? idx[i] : i;
+    add_if_set(s, x[i], (uint32_t)((bits[row * W + wj] & bit) != 0));
+  }
+  p[c * d + j] = s;
 }
 
 __global__ void k_unpack_bits(const uint64_t* __restrict__ bits, int64_t rows, int64_t d, int64_t W,
@@ -100,8 +185,10 @@ extern "C" int simopt_bernoulli_bits(void* stream, uint64_t seed, uint64_t sid, 
   return SIMOPT_OK;
 }
 
-extern "C" int simopt_matvec_bits(void* stream, const uint64_t* bits, int64_t rows, int64_t d,
-                                  const double* v, int64_t chunk, double* out) {
+extern "C" int simopt_matvec_bits_idx(void* stream, const uint64_t* bits, int64_t total_rows,
+                                      int64_t d, const int64_t* idx, int64_t rows, const double* v,
+                                      int64_t chunk, double* out) {
+  (void)total_rows;
   SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1");
   cudaStream_t st = as_stream(stream);
   if (rows == 0) return SIMOPT_OK;
@@ -115,9 +202,46 @@ extern "C" int simopt_matvec_bits(void* stream, const uint64_t* bits, int64_t ro
     p = static_cast<double*>(simopt_scratch(st, rows * nch * sizeof(double)));
     SIMOPT_REQUIRE(p != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
   }
-  k_matvec_bits<<<grid_for(rows * nch, 128), 128, 0, st>>>(bits, rows, d, W, v, chunk, nch, p);
-  SIMOPT_CHECK_LAUNCH("k_matvec_bits");
+  if (chunk % 64 == 0) {
+    k_matvec_bits_slab<<<(unsigned)ceil_div(rows, kMbRows), kMbRows, 0, st>>>(bits, W, d, idx, rows,
+                                                                                v, chunk / 64, nch, p);
+    SIMOPT_CHECK_LAUNCH("k_matvec_bits_slab");
+  } else {
+    SIMOPT_REQUIRE(idx == nullptr, SIMOPT_E_CONFIG, "row gather over bits needs chunk %% 64 == 0");
+    k_matvec_bits<<<grid_for(rows * nch, 128), 128, 0, st>>>(bits, rows, d, W, v, chunk, nch, p);
+    SIMOPT_CHECK_LAUNCH("k_matvec_bits");
+  }
   if (nch > 1) return simopt_fold_partials(stream, p, nch, rows, out);
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_matvec_bits(void* stream, const uint64_t* bits, int64_t rows, int64_t d,
+                                  const double* v, int64_t chunk, double* out) {
+  return simopt_matvec_bits_idx(stream, bits, rows, d, nullptr, rows, v, chunk, out);
+}
+
+extern "C" int simopt_matvec_t_bits(void* stream, const uint64_t* bits, int64_t total_rows,
+                                    int64_t d, const int64_t* idx, int64_t rows, const double* x,
+                                    int64_t chunk, double* out) {
+  (void)total_rows;
+  SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1");
+  cudaStream_t st = as_stream(stream);
+  if (d == 0) return SIMOPT_OK;
+  if (rows == 0) {
+    SIMOPT_CUDA(cudaMemsetAsync(out, 0, d * sizeof(double), st));
+    return SIMOPT_OK;
+  }
+  const int64_t nch = ceil_div(rows, chunk);
+  SIMOPT_REQUIRE(nch < 65536, SIMOPT_E_CONFIG, "too many row chunks (%lld)", (long long)nch);
+  double* p = out;
+  if (nch > 1) {
+    p = static_cast<double*>(simopt_scratch(st, d * nch * sizeof(double)));
+    SIMOPT_REQUIRE(p != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
+  }
+  const dim3 grid((unsigned)ceil_div(d, 128), (unsigned)nch);
+  k_matvec_t_bits<<<grid, 128, 0, st>>>(bits, ceil_div(d, 64), d, idx, rows, x, chunk, p);
+  SIMOPT_CHECK_LAUNCH("k_matvec_t_bits");
+  if (nch > 1) return simopt_fold_partials(stream, p, nch, d, out);
   return SIMOPT_OK;
 }
 

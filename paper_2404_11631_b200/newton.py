@@ -32,6 +32,7 @@ from . import _lib
 from ._tensors import F64, empty, to_host
 from .fused import LR_GRAD, LR_HVP, PeerReducer, fused_rows, fused_rows_bits
 from .records import RunRecord, TraceBuilder
+from .tasks import x_matvec, x_matvec_t
 
 _SCALE, _MUL = 3, 4
 
@@ -72,7 +73,7 @@ class _Logistic:
     def _col_sums(self, v, out):
         """Fixed-tree X^T v over all rows (gathered chunk partials when sharded)."""
         if self.shard is None:
-            return self.b.matvec_t_device(self.data.features, v, out=out)
+            return x_matvec_t(self.data, self.b, v[:self.nl], out=out)
         from .tasks import sharded_matvec_t
         return sharded_matvec_t(self.shard, self.data.features, v[:self.nl], self.N,
                                 self.b.chunk_size, out=out)
@@ -84,7 +85,7 @@ class _Logistic:
 
     def xw(self, w):
         if self.nl:
-            self.b.matvec_device(self.data.features, w, out=self.t[:self.nl])
+            x_matvec(self.data, self.b, w, out=self.t[:self.nl])
         return self.t
 
     def gradient_from_t(self, out):
@@ -104,7 +105,7 @@ class _Logistic:
     def hvp(self, v, out):
         """(1/N) X^T ((c(1-c)) * (X v))."""
         if self.nl:
-            self.b.matvec_device(self.data.features, v, out=self.tv[:self.nl])
+            x_matvec(self.data, self.b, v, out=self.tv[:self.nl])
             _vop(_MUL, 0.0, self.dw, self.tv, self.r)
         self._col_sums(self.r, self.gt)
         return self._scale(self.gt, out)

@@ -1194,6 +1194,33 @@ def _batch_rows(data, indices):
     return idx, idx.numel()
 
 
+def x_matvec(data, backend, v, idx=None, out=None) -> torch.Tensor:
+    """Fixed-tree X_b v over this rank's rows (gathered through idx); bit-packed features
+    are read as bits (simopt_matvec_bits_idx, bit-identical to the 0/1 fp64 matrix)."""
+    if not data.packed:
+        return backend.matvec_device(data.features, v, out=out, rows_idx=idx)
+    if v.numel() != data.n_features:
+        raise DimensionMismatch(f"matvec: ({data.local_rows}, {data.n_features}) @ ({v.numel()},)")
+    rows = data.local_rows if idx is None else idx.numel()
+    out = empty(rows) if out is None else out
+    _lib.call("simopt_matvec_bits_idx", _lib.stream_ptr(), _lib.ptr(data.bits), data.local_rows,
+              data.n_features, _lib.ptr(idx), rows, _lib.ptr(v), backend.chunk_size, _lib.ptr(out))
+    return out
+
+
+def x_matvec_t(data, backend, x, idx=None, out=None) -> torch.Tensor:
+    """Fixed-tree X_b^T x (column sums over the gathered rows); bits when packed."""
+    if not data.packed:
+        return backend.matvec_t_device(data.features, x, out=out, rows_idx=idx)
+    rows = data.local_rows if idx is None else idx.numel()
+    if x.numel() != rows:
+        raise DimensionMismatch(f"matvec_t: ({rows}, {data.n_features})^T @ ({x.numel()},)")
+    out = empty(data.n_features) if out is None else out
+    _lib.call("simopt_matvec_t_bits", _lib.stream_ptr(), _lib.ptr(data.bits), data.local_rows,
+              data.n_features, _lib.ptr(idx), rows, _lib.ptr(x), backend.chunk_size, _lib.ptr(out))
+    return out
+
+
 def logistic_loss_device(w, data, indices, backend, idx=None, out=None) -> torch.Tensor:
     """Device scalar sum of logistic_loss_block terms (divide by the batch size on read)."""
     wd = vec_dev(w)
@@ -1203,7 +1230,7 @@ def logistic_loss_device(w, data, indices, backend, idx=None, out=None) -> torch
         idx, b = _batch_rows(data, indices)
     else:
         b = idx.numel()
-    t = backend.matvec_device(data.features, wd, rows_idx=idx)
+    t = x_matvec(data, backend, wd, idx)
     terms = empty(b)
     _lib.call("simopt_logistic_loss_terms", _lib.stream_ptr(), _lib.ptr(t), _lib.ptr(data.labels),
               _lib.ptr(idx), b, _lib.ptr(terms))
@@ -1226,11 +1253,11 @@ def logistic_gradient_device(w, data, indices, backend, idx=None, out=None) -> t
         idx, b = _batch_rows(data, indices)
     else:
         b = idx.numel()
-    t = backend.matvec_device(data.features, wd, rows_idx=idx)
+    t = x_matvec(data, backend, wd, idx)
     r = empty(b)
     _lib.call("simopt_logistic_resid", _lib.stream_ptr(), _lib.ptr(t), _lib.ptr(data.labels),
               _lib.ptr(idx), b, _lib.ptr(r))
-    gt = backend.matvec_t_device(data.features, r, rows_idx=idx)
+    gt = x_matvec_t(data, backend, r, idx)
     out = empty(gt.numel()) if out is None else out
     _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(gt), 1.0 / b, None, gt.numel(),
               _lib.ptr(out))
@@ -1250,12 +1277,12 @@ def logistic_hvp_device(w, v, data, indices, backend, idx=None, out=None) -> tor
         idx, b = _batch_rows(data, indices)
     else:
         b = idx.numel()
-    t = backend.matvec_device(data.features, wd, rows_idx=idx)
-    tv = backend.matvec_device(data.features, vd, rows_idx=idx)
+    t = x_matvec(data, backend, wd, idx)
+    tv = x_matvec(data, backend, vd, idx)
     wt = empty(b)
     _lib.call("simopt_logistic_hvp_weights", _lib.stream_ptr(), _lib.ptr(t), _lib.ptr(tv), b,
               _lib.ptr(wt))
-    ht = backend.matvec_t_device(data.features, wt, rows_idx=idx)
+    ht = x_matvec_t(data, backend, wt, idx)
     out = empty(ht.numel()) if out is None else out
     _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(ht), 1.0 / b, None, ht.numel(),
               _lib.ptr(out))

@@ -41,6 +41,42 @@ def test_matvec_bits_exact(pkg, chunk):
     assert np.array_equal(out.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("d,n,chunk,gather", [(300, 2000, 4096, True), (1000, 3001, 4096, False),
+                                               (1000, 3001, 128, True), (8192, 257, 4096, True),
+                                               (70, 9000, 64, False), (5, 40, 4096, True)])
+def test_matvec_bits_gather_and_transpose_exact(pkg, d, n, chunk, gather):
+    """matvec_bits_idx / matvec_t_bits (slab kernel, row gather, column sums) bitwise equal
+    the fixed-tree oracle on the 0/1 matrix, negative zeros and chunk cuts included."""
+    from paper_2404_11631_b200 import _lib
+    from paper_2404_11631_b200.sampling import synth_classification
+    data = synth_classification(d, pkg.RngStream(5, 0), n_rows=n, packed=True)
+    rng = np.random.default_rng(d + n)
+    v = rng.standard_normal(d)
+    v[::7] = -0.0
+    if d == 70:
+        v[10] = np.inf   # the reference's 0.0 * inf is NaN: every row's dot is NaN or inf
+    b = min(n, 777) if gather else n
+    idx = rng.choice(n, size=b, replace=False) if gather else None
+    x = data.features.cpu().numpy()
+    xb = x[idx] if gather else x
+    vd = torch.from_numpy(v).cuda()
+    idd = torch.from_numpy(idx).cuda() if gather else None
+    out = torch.empty(b, dtype=torch.float64, device="cuda")
+    _lib.call("simopt_matvec_bits_idx", _lib.stream_ptr(), _lib.ptr(data.bits), n, d, _lib.ptr(idd),
+              b, _lib.ptr(vd), chunk, _lib.ptr(out))
+    assert np.array_equal(out.cpu().numpy(), orc.matvec(xb, v, chunk), equal_nan=True)
+    r = rng.standard_normal(b)
+    r[::5] = -0.0
+    if d == 70:
+        r[3] = -np.inf
+    outt = torch.empty(d, dtype=torch.float64, device="cuda")
+    _lib.call("simopt_matvec_t_bits", _lib.stream_ptr(), _lib.ptr(data.bits), n, d, _lib.ptr(idd),
+              b, _lib.ptr(torch.from_numpy(r).cuda()), chunk, _lib.ptr(outt))
+    got, want = outt.cpu().numpy(), orc.matvec_t(xb, r, chunk)
+    assert np.array_equal(got, want, equal_nan=True)
+    assert np.array_equal(np.signbit(got), np.signbit(want))
+
+
 @pytest.mark.parametrize("d,n", [(1000, 5000), (8192, 300), (130, 999), (5, 64)])
 def test_fused_bits_vs_dense(pkg, d, n):
     from paper_2404_11631_b200.fused import LR_GRAD, LR_HVP, fused_rows_bits

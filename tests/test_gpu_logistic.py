@@ -15,12 +15,13 @@ def pkg():
     return p
 
 
-def test_synth_and_logistic_kernels_golden(pkg, golden):
+@pytest.mark.parametrize("packed", [False, True])
+def test_synth_and_logistic_kernels_golden(pkg, packed, golden):
     from paper_2404_11631_b200.sampling import sample_indices, synth_classification
     from paper_2404_11631_b200 import tasks as T
     g = golden("logistic")
     s = pkg.RngStream(42, 0)
-    data = synth_classification(12, s)
+    data = synth_classification(12, s, packed=packed)
     assert np.array_equal(data.features.cpu().numpy(), g["X"])
     assert np.array_equal(data.labels.cpu().numpy(), g["z"])
     assert np.array_equal(data.true_weights.cpu().numpy(), g["w_true"])
@@ -47,25 +48,27 @@ def test_hessian_update_golden(pkg, golden):
     assert np.array_equal(h.cpu().numpy(), g["hu_H"])
 
 
-def test_sqn_trace_golden(pkg, golden):
+@pytest.mark.parametrize("packed", [False, True])
+def test_sqn_trace_golden(pkg, packed, golden):
     from paper_2404_11631_b200.sampling import synth_classification
     from paper_2404_11631_b200.sqn import SqnConfig, sqn_run
     from paper_2404_11631_b200.tasks import LogisticTask
     g = golden("logistic")
     b = pkg.make_backend("cuda")
-    data = synth_classification(10, pkg.RngStream(42, 0))
+    data = synth_classification(10, pkg.RngStream(42, 0), packed=packed)
     rec = sqn_run(LogisticTask(data), SqnConfig(10, 25, 2.0, 50, 100, 60, pkg.RngStream(42, 2)), b)
     assert np.array_equal(rec.objectives, g["sqn_obj"])
     assert np.array_equal(rec.final_iterate, g["sqn_w"])
 
 
-def test_sqn_vs_oracle_larger(pkg):
+@pytest.mark.parametrize("packed", [False, True])
+def test_sqn_vs_oracle_larger(pkg, packed):
     from paper_2404_11631_b200.sampling import synth_classification
     from paper_2404_11631_b200.sqn import SqnConfig, sqn_run
     from paper_2404_11631_b200.tasks import LogisticTask
     d, K = 100, 80
     b = pkg.make_backend("cuda")
-    data = synth_classification(d, pkg.RngStream(42, 0))
+    data = synth_classification(d, pkg.RngStream(42, 0), packed=packed)
     rec = sqn_run(LogisticTask(data), SqnConfig(10, 25, 2.0, 50, 300, K, pkg.RngStream(42, 2)), b)
     x, z, _ = orc.synth_classification(d, orc.Stream(42, 0))
     objs, w = orc.sqn_run(x, z, pair_every=10, memory=25, beta=2.0, grad_batch=50, hess_batch=300,
@@ -86,11 +89,13 @@ def test_synth_generalised_vs_oracle(pkg, d, n_rows):
     assert s.counter == os_.counter
 
 
-def test_full_gradient_hvp_vs_oracle(pkg):
+@pytest.mark.parametrize("packed", [False, True])
+def test_full_gradient_hvp_vs_oracle(pkg, packed):
+    """Packed: the exact-tree passes read the bits (matvec_bits_idx / matvec_t_bits)."""
     from paper_2404_11631_b200.sampling import synth_classification
     from paper_2404_11631_b200 import tasks as T
     d, n = 300, 50_000
-    data = synth_classification(d, pkg.RngStream(3, 0), n_rows=n)
+    data = synth_classification(d, pkg.RngStream(3, 0), n_rows=n, packed=packed)
     x, z = data.features.cpu().numpy(), data.labels.cpu().numpy()
     rng = np.random.default_rng(1)
     w, v = rng.standard_normal(d) * 0.1, rng.standard_normal(d)

@@ -63,6 +63,27 @@ def newton(tag, d, n, k_cg=10, iters=2, fused=True, packed=False):
                       "algorithmic_GBps": alg * it_s / 1e9}), flush=True)
 
 
+def sqn(tag, d, n, iters=200, packed=False):
+    """The reference's own classification solver (sqn.py) at C3 scale, bench.py:57-74
+    parameters (L=10, M=25, beta=2, b=50, b_H=300); exact trees, bit-exact traces.
+    Per iteration: one full-data loss pass over X (sqn.py:171) dominates."""
+    from paper_2404_11631_b200.sampling import synth_classification
+    from paper_2404_11631_b200.sqn import SqnConfig, sqn_run
+    b = p.make_backend("cuda")
+    task = LogisticTask(synth_classification(d, p.RngStream(42, 0), n_rows=n, packed=packed))
+
+    def run():
+        cfg = SqnConfig(pair_every=10, memory=25, beta=2.0, grad_batch=50, hess_batch=300,
+                        iterations=iters, stream=p.RngStream(42, 2))
+        sqn_run(task, cfg, b)
+    ms = timed(run, warm=1, reps=2)
+    it_s = iters / (ms / 1e3)
+    x_bytes = n * d / 8 if packed else 8 * n * d
+    print(json.dumps({"config": tag, "d": d, "N": n, "packed": packed, "iterations": iters,
+                      "sqn_iterations_per_s": it_s, "ms_per_iteration": ms / iters,
+                      "loss_pass_GBps": x_bytes * it_s / 1e9}), flush=True)
+
+
 def xtdx(tag, d, n, packed=False, method="dmma"):
     from paper_2404_11631_b200.newton import logistic_hessian_device
     from paper_2404_11631_b200.sampling import synth_classification
@@ -91,6 +112,10 @@ if __name__ == "__main__":
         newton("C3 logistic Newton-CG d=1e3 N=1e6 (fused)", 1000, 1_000_000)
         newton("C3 logistic Newton-CG d=1e3 N=1e6 (fused, bit-packed features)", 1000, 1_000_000,
                packed=True)
+    if "sqn" in which:
+        sqn("C3-scale SQN (reference solver) d=1e3 N=1e6", 1000, 1_000_000)
+        sqn("C3-scale SQN (reference solver) d=1e3 N=1e6 (bit-packed features)", 1000, 1_000_000,
+            packed=True)
     if "xtdx" in which:
         xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (fp64 X)", 8192, 125_000)
         xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X, DMMA)", 8192, 125_000,

@@ -61,7 +61,7 @@ def main(rank, world, port, out):
     nv = gen_newsvendor_instance(1003, p.RngStream(42, 0))
     for ex in ("nccl", "peer"):
         rec = fw_run(NewsvendorProblem(nv, b, shard=sh, exchange=ex),
-                     FwConfig(2, 6, 5000, p.RngStream(42, 2)), b)
+                     FwConfig(5, 6, 5000, p.RngStream(42, 2)), b)
         res[f"nv_{ex}_obj"], res[f"nv_{ex}_w"] = rec.objectives, rec.final_iterate
     from paper_2404_11631_b200.sharding import PeerMailbox
     res["nv_peer_used"] = np.array([PeerMailbox.get(sh) is not None])

@@ -81,7 +81,7 @@ def test_logistic_sharded(ranks):
 
 def test_newsvendor_sharded(ranks):
     task = orc.gen_newsvendor_instance(1003, orc.Stream(42, 0))
-    objs, x = orc.fw_run_newsvendor(task, 2, 6, 5000, orc.Stream(42, 2))
+    objs, x = orc.fw_run_newsvendor(task, 5, 6, 5000, orc.Stream(42, 2))  # epochs 2+ replay graphs
     r = ranks[0]
     assert bool(r["nv_peer_used"][0])                      # the in-kernel NVLink/IPC exchange ran
     for ex in ("nccl", "peer"):

@@ -290,8 +290,8 @@ def run_ours(args, rank, world):
                      "frac": value / it_roof,
                      "basis": "SURVEY 8(d) C2: 8*d*S*(1+1/M) bytes per FW iteration at hbm peak"}
     launches_per_epoch = 4 * M + 2  # resample, M+1 fused steps, M x (terms, sums, stamp)
-    if world > 1:
-        launches_per_epoch += 2 * M  # LMO pack + apply around each exchange
+    if world > 1 and eng.mailbox is None:
+        launches_per_epoch += 2 * M  # LMO pack + apply around each NCCL exchange
     line = {
         "metric": "newsvendor Frank-Wolfe iterations/sec (d=10000, S=100000, M=25)",
         "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,

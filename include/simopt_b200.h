@@ -262,6 +262,10 @@ int simopt_logistic_loss_terms(void* stream, const double* t, const double* z, c
 /* bfgs_rank2_block over all rows (_kernels.py:226-242), h is n x n row-major. */
 int simopt_bfgs_rank2(void* stream, double* h, const double* s, const double* u, double coef_su,
                       double coef_ss, int64_t n);
+/* The same update with coef_su = -rho and coef_ss = (rho*rho)*(*kappa) + rho formed on the
+ * device from kappa = y.(H y) (sqn.py:100-109): no host read between pairs. */
+int simopt_bfgs_rank2_dev(void* stream, double* h, const double* s, const double* u, double rho,
+                          const double* kappa, int64_t n);
 /* h = diag(v) (sqn.py:96-97). */
 int simopt_diag_fill(void* stream, double* h, int64_t n, double v);
 enum simopt_vec { SIMOPT_VEC_SUB_SCALED = 0, SIMOPT_VEC_ADD = 1, SIMOPT_VEC_SUB = 2,
@@ -274,6 +278,21 @@ int simopt_vec_op(void* stream, int op, double alpha, const double* x, const dou
  * the counter by ceil(b/4). */
 int simopt_sample_indices(void* stream, uint64_t seed, uint64_t stream_id, uint64_t ctr_lo,
                           uint64_t ctr_hi, int64_t n, int64_t b, int64_t* out);
+/* Device-resident SQN iteration (CUDA-graph replay of sqn.py:132-169).
+ * sample_indices_dev: as simopt_sample_indices with (seed, stream_id, ctr_lo, ctr_hi) read
+ * from device words[4], the counter advanced there by ceil(b/4) (RngStream.advance).
+ * SqnCtl: k = the iteration being taken (1-based), rec = next trace row, beta.
+ * sqn_step: out = x - (beta / k) * y (sqn.py:160-165).  sqn_record: sums[rec] = *val,
+ * stamps[rec] = %globaltimer, then rec += 1, k += 1. */
+typedef struct SqnCtl {
+  int64_t k, rec;
+  double beta;
+  int64_t pad;
+} SqnCtl;
+int simopt_sample_indices_dev(void* stream, uint64_t* words, int64_t n, int64_t b, int64_t* out);
+int simopt_sqn_step(void* stream, const SqnCtl* ctl, const double* x, const double* y, int64_t n,
+                    double* out);
+int simopt_sqn_record(void* stream, SqnCtl* ctl, const double* val, double* sums, int64_t* stamps);
 /* CG step halves on device scalars (Newton-CG, BASELINE configs[2]):
  * step1: alpha = *rr / *dhd; p += alpha*d; r -= alpha*hd.  step2: d = r + (*rr_new / *rr)*d.
  * Both are no-ops when *rr == 0 (the CG loop's early exit). */

@@ -77,6 +77,10 @@ SIGNATURES = {
     "simopt_peer_free": [_vp],
     "simopt_bernoulli_bits": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _i64, _vp],
     "simopt_matvec_bits": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
+    "simopt_sample_indices_dev": [_vp, _vp, _i64, _i64, _vp],
+    "simopt_bfgs_rank2_dev": [_vp, _vp, _vp, _vp, _d, _vp, _i64],
+    "simopt_sqn_step": [_vp, _vp, _vp, _vp, _i64, _vp],
+    "simopt_sqn_record": [_vp, _vp, _vp, _vp, _vp],
     "simopt_matvec_bits_idx": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
     "simopt_matvec_t_bits": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
     "simopt_unpack_bits": [_vp, _vp, _i64, _i64, _vp],

@@ -52,15 +52,21 @@ __global__ void k_loss_terms(const double* __restrict__ t, const double* __restr
 
 // bfgs_rank2_block (_kernels.py:226-242):
 // h[i,j] += coef_su*(s_i*u_j) + coef_su*(u_i*s_j) + coef_ss*(s_i*s_j)
+// Row per block (grid-stride), columns across threads.  kappa != nullptr: coef_ss is
+// formed on the device as (rho*rho)*kappa + rho (sqn.py:108, left to right, no FMA), so
+// hessian_update needs no host read of kappa between pairs.
 __global__ void k_bfgs_rank2(double* __restrict__ h, const double* __restrict__ s,
-                             const double* __restrict__ u, double a, double b, int64_t n) {
-  const int64_t total = n * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / n, j = e - i * n;
-    const double si = s[i], ui = u[i], sj = s[j], uj = u[j];
-    const double inc = ((a * (si * uj)) + (a * (ui * sj))) + (b * (si * sj));
-    h[e] = h[e] + inc;
+                             const double* __restrict__ u, double a, double b,
+                             const double* __restrict__ kappa, double rho, int64_t n) {
+  if (kappa) b = __dadd_rn(__dmul_rn(__dmul_rn(rho, rho), *kappa), rho);
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const double si = s[i], ui = u[i];
+    double* row = h + i * n;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      const double sj = s[j], uj = u[j];
+      const double inc = ((a * (si * uj)) + (a * (ui * sj))) + (b * (si * sj));
+      row[j] = row[j] + inc;
+    }
   }
 }
 
@@ -102,8 +108,12 @@ __device__ __forceinline__ int fy_slot(const int64_t* keys, int64_t key) {
 }
 
 __global__ void k_sample_indices(uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi,
-                                 int64_t n, int64_t b, int64_t* __restrict__ out) {
+                                 int64_t n, int64_t b, int64_t* __restrict__ out,
+                                 uint64_t* __restrict__ words) {
   extern __shared__ int64_t fy[];
+  if (words) {  // device-resident stream position (CUDA-graph replay), advanced below
+    seed = words[0]; sid = words[1]; clo = words[2]; chi = words[3];
+  }
   int64_t* keys = fy;
   int64_t* vals = fy + kFyCap;
   __shared__ double u[kFyCap / 2];
@@ -115,6 +125,11 @@ __global__ void k_sample_indices(uint64_t seed, uint64_t sid, uint64_t clo, uint
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  if (words) {  // RngStream.advance(b): the 128-bit counter moves ceil(b/4) blocks
+    const uint64_t lo = clo + (uint64_t)((b + 3) / 4);
+    words[2] = lo;
+    words[3] = chi + (lo < clo ? 1ULL : 0ULL);
+  }
   for (int64_t i = 0; i < b; ++i) {
     const int64_t j = i + (int64_t)(u[i] * (double)(n - i));
     const int si = fy_slot(keys, i);
@@ -157,7 +172,17 @@ extern "C" int simopt_logistic_loss_terms(void* stream, const double* t, const d
 extern "C" int simopt_bfgs_rank2(void* stream, double* h, const double* s, const double* u,
                                  double coef_su, double coef_ss, int64_t n) {
   if (n == 0) return SIMOPT_OK;
-  k_bfgs_rank2<<<egrid(n * n), 256, 0, as_stream(stream)>>>(h, s, u, coef_su, coef_ss, n);
+  const int grid = (int)(n < 16 * SIMOPT_NUM_SMS ? n : 16 * SIMOPT_NUM_SMS);
+  k_bfgs_rank2<<<grid, 256, 0, as_stream(stream)>>>(h, s, u, coef_su, coef_ss, nullptr, 0.0, n);
+  SIMOPT_CHECK_LAUNCH("k_bfgs_rank2");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_bfgs_rank2_dev(void* stream, double* h, const double* s, const double* u,
+                                     double rho, const double* kappa, int64_t n) {
+  if (n == 0) return SIMOPT_OK;
+  const int grid = (int)(n < 16 * SIMOPT_NUM_SMS ? n : 16 * SIMOPT_NUM_SMS);
+  k_bfgs_rank2<<<grid, 256, 0, as_stream(stream)>>>(h, s, u, -rho, 0.0, kappa, rho, n);
   SIMOPT_CHECK_LAUNCH("k_bfgs_rank2");
   return SIMOPT_OK;
 }
@@ -191,8 +216,64 @@ extern "C" int simopt_sample_indices(void* stream, uint64_t seed, uint64_t sid, 
                                      smem));
     attr = true;
   }
-  k_sample_indices<<<1, 256, smem, as_stream(stream)>>>(seed, sid, clo, chi, n, b, out);
+  k_sample_indices<<<1, 256, smem, as_stream(stream)>>>(seed, sid, clo, chi, n, b, out, nullptr);
   SIMOPT_CHECK_LAUNCH("k_sample_indices");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_sample_indices_dev(void* stream, uint64_t* words, int64_t n, int64_t b,
+                                         int64_t* out) {
+  SIMOPT_REQUIRE(b >= 1 && b <= n, SIMOPT_E_CONFIG, "need 1 <= b <= n, got b=%lld, n=%lld",
+                 (long long)b, (long long)n);
+  SIMOPT_REQUIRE(b <= kFyCap / 2, SIMOPT_E_CONFIG, "device sample_indices supports b <= %d",
+                 kFyCap / 2);
+  static bool attr = false;  // set by the eager warm-up call, not during graph capture
+  const int smem = 2 * kFyCap * (int)sizeof(int64_t);
+  if (!attr) {
+    SIMOPT_CUDA(cudaFuncSetAttribute(k_sample_indices, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
+    attr = true;
+  }
+  k_sample_indices<<<1, 256, smem, as_stream(stream)>>>(0, 0, 0, 0, n, b, out, words);
+  SIMOPT_CHECK_LAUNCH("k_sample_indices");
+  return SIMOPT_OK;
+}
+
+namespace {
+// w <- w - (beta / k) * y with k, beta from the device control block (sqn.py:160-165:
+// alpha = beta / k, a true IEEE division of the same operands as the host's)
+__global__ void k_sqn_step(const SqnCtl* __restrict__ ctl, const double* __restrict__ x,
+                           const double* __restrict__ y, int64_t n, double* __restrict__ out) {
+  const double alpha = ctl->beta / (double)ctl->k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = x[i] - alpha * y[i];
+}
+
+__global__ void k_sqn_record(SqnCtl* ctl, const double* __restrict__ val, double* __restrict__ sums,
+                             int64_t* __restrict__ stamps) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const int64_t r = ctl->rec;
+  sums[r] = *val;
+  stamps[r] = (int64_t)t;
+  ctl->rec = r + 1;
+  ctl->k += 1;
+}
+}  // namespace
+
+extern "C" int simopt_sqn_step(void* stream, const SqnCtl* ctl, const double* x, const double* y,
+                               int64_t n, double* out) {
+  if (n == 0) return SIMOPT_OK;
+  k_sqn_step<<<egrid(n), 256, 0, as_stream(stream)>>>(ctl, x, y, n, out);
+  SIMOPT_CHECK_LAUNCH("k_sqn_step");
+  return SIMOPT_OK;
+}
+
+extern "C" int simopt_sqn_record(void* stream, SqnCtl* ctl, const double* val, double* sums,
+                                 int64_t* stamps) {
+  k_sqn_record<<<1, 1, 0, as_stream(stream)>>>(ctl, val, sums, stamps);
+  SIMOPT_CHECK_LAUNCH("k_sqn_record");
   return SIMOPT_OK;
 }
 

@@ -61,15 +61,17 @@ def test_sqn_trace_golden(pkg, packed, golden):
     assert np.array_equal(rec.final_iterate, g["sqn_w"])
 
 
-@pytest.mark.parametrize("packed", [False, True])
-def test_sqn_vs_oracle_larger(pkg, packed):
+@pytest.mark.parametrize("packed,graph", [(False, True), (True, True), (False, False)])
+def test_sqn_vs_oracle_larger(pkg, packed, graph):
+    """graph=True: the CUDA-graph iteration (SqnGraphRunner); False: the eager engine."""
     from paper_2404_11631_b200.sampling import synth_classification
     from paper_2404_11631_b200.sqn import SqnConfig, sqn_run
     from paper_2404_11631_b200.tasks import LogisticTask
     d, K = 100, 80
     b = pkg.make_backend("cuda")
     data = synth_classification(d, pkg.RngStream(42, 0), packed=packed)
-    rec = sqn_run(LogisticTask(data), SqnConfig(10, 25, 2.0, 50, 300, K, pkg.RngStream(42, 2)), b)
+    rec = sqn_run(LogisticTask(data), SqnConfig(10, 25, 2.0, 50, 300, K, pkg.RngStream(42, 2)), b,
+                  graph=graph)
     x, z, _ = orc.synth_classification(d, orc.Stream(42, 0))
     objs, w = orc.sqn_run(x, z, pair_every=10, memory=25, beta=2.0, grad_batch=50, hess_batch=300,
                           iterations=K, stream=orc.Stream(42, 2))

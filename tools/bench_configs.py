@@ -63,10 +63,11 @@ def newton(tag, d, n, k_cg=10, iters=2, fused=True, packed=False):
                       "algorithmic_GBps": alg * it_s / 1e9}), flush=True)
 
 
-def sqn(tag, d, n, iters=200, packed=False):
+def sqn(tag, d, n, iters=2000, packed=False, graph=True):
     """The reference's own classification solver (sqn.py) at C3 scale, bench.py:57-74
     parameters (L=10, M=25, beta=2, b=50, b_H=300); exact trees, bit-exact traces.
-    Per iteration: one full-data loss pass over X (sqn.py:171) dominates."""
+    Per iteration: one full-data loss pass over X (sqn.py:171) dominates.  K = 2000, the
+    reference's classification default (bench.py:89)."""
     from paper_2404_11631_b200.sampling import synth_classification
     from paper_2404_11631_b200.sqn import SqnConfig, sqn_run
     b = p.make_backend("cuda")
@@ -75,11 +76,12 @@ def sqn(tag, d, n, iters=200, packed=False):
     def run():
         cfg = SqnConfig(pair_every=10, memory=25, beta=2.0, grad_batch=50, hess_batch=300,
                         iterations=iters, stream=p.RngStream(42, 2))
-        sqn_run(task, cfg, b)
-    ms = timed(run, warm=1, reps=2)
+        sqn_run(task, cfg, b, graph=graph)
+    ms = timed(run, warm=1, reps=1)
     it_s = iters / (ms / 1e3)
     x_bytes = n * d / 8 if packed else 8 * n * d
-    print(json.dumps({"config": tag, "d": d, "N": n, "packed": packed, "iterations": iters,
+    print(json.dumps({"config": tag, "d": d, "N": n, "packed": packed, "graph": graph,
+                      "iterations": iters,
                       "sqn_iterations_per_s": it_s, "ms_per_iteration": ms / iters,
                       "loss_pass_GBps": x_bytes * it_s / 1e9}), flush=True)
 
@@ -116,6 +118,13 @@ if __name__ == "__main__":
         sqn("C3-scale SQN (reference solver) d=1e3 N=1e6", 1000, 1_000_000)
         sqn("C3-scale SQN (reference solver) d=1e3 N=1e6 (bit-packed features)", 1000, 1_000_000,
             packed=True)
+        sqn("C3-scale SQN (reference solver) d=1e3 N=1e6 (bit-packed, eager iteration)", 1000,
+            1_000_000, packed=True, graph=False)
+    if "sqn_small" in which:  # the reference's own sizes: N = 30 d (sampling.py:241)
+        for d in (100, 1000):
+            for g in (True, False):
+                sqn(f"SQN d={d} N=30d (reference bench size), {'graph' if g else 'eager'}", d, 30 * d,
+                    graph=g)
     if "xtdx" in which:
         xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (fp64 X)", 8192, 125_000)
         xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X, DMMA)", 8192, 125_000,

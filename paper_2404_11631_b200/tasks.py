@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 from ._tensors import F64, empty, is_tensor, like_input, mat_dev, to_dev, to_host, vec_dev
-from .errors import (ConfigurationError, DeviceError, DimensionMismatch, InsufficientSamples,
+from .errors import (ConfigurationError, DeviceError, DimensionMismatch, EmptyRequest, InsufficientSamples,
                      InvalidConstraint, InvalidGradient, RunAborted)
 from .frank_wolfe import fw_step_size
 from .fused import MV, fused_rows
@@ -688,6 +688,40 @@ def _nv_fw_run_device(prob: "NewsvendorProblem", config, backend, label, size, r
     if bad:
         abort(*bad)
     return trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(eng.iterate(eng.T)))
+
+
+def sample_demands_device(mu, sigma, n_samples: int, stream: RngStream) -> torch.Tensor:
+    """sample_demands (sampling.py:173-193) on the device: per-product demand draws, each
+    row sorted ascending, bit-identical to the reference's matrix.
+
+    The draw is the FW loop's own keyed resample (k_nv_resample, the same Philox/glibc
+    normals z[j*S + s]); k_nv_decode evaluates every draw's exact demand mu_j + sigma_j*z
+    (sampling.py:191) and the rows are sorted by value (no arithmetic).  The FW loop
+    itself never materialises this matrix -- it is the reference-format view of an
+    epoch for callers of the reference API."""
+    mud, sgd = vec_dev(mu), vec_dev(sigma)
+    if mud.numel() != sgd.numel():
+        raise DimensionMismatch("mu and sigma lengths differ")
+    if not bool((sgd > 0).all()):
+        raise InvalidConstraint("sigma entries must be > 0")
+    if n_samples < 1:
+        raise EmptyRequest("need at least one demand sample per product")
+    d, S = mud.numel(), int(n_samples)
+    ns, ke, oe = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.call("simopt_nv_layout", d, S, ctypes.byref(ns), ctypes.byref(ke), ctypes.byref(oe))
+    keys = torch.empty(ke.value, dtype=torch.int32, device="cuda")
+    off = torch.empty(oe.value, dtype=torch.int16, device="cuda")
+    draw = stream.words()
+    _lib.call("simopt_nv_resample", _lib.stream_ptr(), *draw, d, S, _lib.ptr(keys), _lib.ptr(off))
+    stream.advance(2 * ((d * S + 1) // 2))
+    out = torch.empty(d, S, dtype=F64, device="cuda")
+    _lib.call("simopt_nv_decode", _lib.stream_ptr(), _lib.ptr(keys), _lib.ptr(mud), _lib.ptr(sgd),
+              d, S, *draw, _lib.ptr(out))
+    return torch.sort(out, dim=1).values
+
+
+def sample_demands(mu, sigma, n_samples: int, stream: RngStream, backend=None) -> np.ndarray:
+    return to_host(sample_demands_device(mu, sigma, n_samples, stream))
 
 
 def nv_gradient_hat(x, demands, task: NewsvendorTask, backend):

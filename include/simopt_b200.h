@@ -293,6 +293,12 @@ int simopt_sample_indices_dev(void* stream, uint64_t* words, int64_t n, int64_t 
 int simopt_sqn_step(void* stream, const SqnCtl* ctl, const double* x, const double* y, int64_t n,
                     double* out);
 int simopt_sqn_record(void* stream, SqnCtl* ctl, const double* val, double* sums, int64_t* stamps);
+/* lmo_general (lmo.py:92-160): argmin of s.g over {A s <= C, s >= 0} (A m x n row-major,
+ * C > 0) by the reference's dense Bland simplex, one CTA, same pivots and arithmetic.
+ * *status (device) = 0, SIMOPT_E_INVALID_GRADIENT (NaN in g), SIMOPT_E_SOLVER_STALL
+ * (unbounded) or -SIMOPT_E_SOLVER_STALL (max_iters pivots without optimality). */
+int simopt_lmo_general(void* stream, const double* A, const double* C, int64_t m, int64_t n,
+                       const double* g, int64_t max_iters, double* s_out, int* status);
 /* CG step halves on device scalars (Newton-CG, BASELINE configs[2]):
  * step1: alpha = *rr / *dhd; p += alpha*d; r -= alpha*hd.  step2: d = r + (*rr_new / *rr)*d.
  * Both are no-ops when *rr == 0 (the CG loop's early exit). */

@@ -330,6 +330,74 @@ def fw_run_newsvendor(task, epochs, inner_iters, n_samples, stream, chunk=CHUNK)
     return np.array(objs), x
 
 
+def lmo_general(g, a, c, max_iters=None):
+    """lmo.py:92-160: dense primal simplex over {a s <= c, s >= 0} from the slack basis,
+    Bland's rule.  Row operations are whole-row numpy expressions with the reference's
+    association (row /= piv; row_i -= f_i * row_leave; cost -= c_e * row_leave).
+    Returns s, or raises ValueError("nan" | "unbounded" | "cap")."""
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    m, n = a.shape
+    if np.isnan(g).any():
+        raise ValueError("nan")
+    cap = 10 * (n + m) if max_iters is None else max_iters
+    width = n + m
+    t = np.concatenate([a, np.eye(m), c[:, None]], axis=1)
+    red = np.concatenate([g, np.zeros(m)])
+    basic = np.arange(n, n + m)
+    tol_in = 1e-12 * (1.0 + float(np.max(np.abs(g))))
+    for _ in range(cap):
+        below = np.nonzero(red < -tol_in)[0]
+        if below.size == 0:
+            break
+        e = int(below[0])
+        leave, best = -1, np.inf
+        for i in range(m):
+            col = t[i, e]
+            if col > 1e-12:
+                r = t[i, -1] / col
+                tie = abs(r - best) <= 1e-15 and (leave < 0 or basic[i] < basic[leave])
+                if r < best - 1e-15 or tie:
+                    best, leave = r, i
+        if leave < 0:
+            raise ValueError("unbounded")
+        t[leave] = t[leave] / t[leave, e]
+        prow = t[leave]
+        for i in range(m):
+            f = t[i, e]
+            if i != leave and f != 0.0:
+                t[i] = t[i] - f * prow
+        ce = red[e]
+        if ce != 0.0:
+            red = red - ce * prow[:width]
+        basic[leave] = e
+    else:
+        raise ValueError("cap")
+    s = np.zeros(n)
+    for i, b in enumerate(basic):
+        if b < n:
+            s[b] = t[i, -1]
+    return s
+
+
+def fw_run_newsvendor_polytope(task, a, c, epochs, inner_iters, n_samples, stream, chunk=CHUNK):
+    """fw_run over NewsvendorProblem with a polytope (tasks.py:321-334)."""
+    mu, sigma, k_, h, v = (task[n] for n in ("mu", "sigma", "k", "h", "v"))
+    x = np.zeros(mu.size)
+    objs = []
+    for k in range(epochs):
+        dem = sample_demands(mu, sigma, n_samples, stream)
+        for m in range(inner_iters):
+            g = nv_gradient_hat(x, dem, k_, h, v)
+            s = lmo_general(g, a, c)
+            x = fw_update(x, s, k, inner_iters, m)
+            if np.any(x < -FEAS_TOL) or np.any(matvec(a, x, chunk) > c * (1.0 + FEAS_TOL)):
+                raise RuntimeError("infeasible")
+            objs.append(nv_objective_exact(x, mu, sigma, k_, h, v, chunk))
+    return np.array(objs), x
+
+
 # ---------------------------------------------------------------- instances (bench.py:102-137)
 def uniform_range(stream, n, lo, hi):
     u = uniform01(stream, n)

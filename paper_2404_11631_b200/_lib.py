@@ -79,6 +79,7 @@ SIGNATURES = {
     "simopt_matvec_bits": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
     "simopt_sample_indices_dev": [_vp, _vp, _i64, _i64, _vp],
     "simopt_bfgs_rank2_dev": [_vp, _vp, _vp, _vp, _d, _vp, _i64],
+    "simopt_lmo_general": [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp],
     "simopt_sqn_step": [_vp, _vp, _vp, _vp, _i64, _vp],
     "simopt_sqn_record": [_vp, _vp, _vp, _vp, _vp],
     "simopt_matvec_bits_idx": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],

@@ -2,8 +2,8 @@
 
 ``lmo_simplex_slack`` / ``lmo_single_budget`` run a deterministic first-argmin
 kernel (csrc/fw.cu).  ``lmo_general`` -- the reference's dense Bland simplex for
-small multi-resource polytopes (lmo.py:92-160) -- is out of scope for this
-package (not on any benchmark configuration).
+small multi-resource polytopes (lmo.py:92-160) -- runs the same pivots on the
+device in one CTA (csrc/lp.cu).
 """
 from __future__ import annotations
 
@@ -14,7 +14,8 @@ import torch
 
 from . import _lib
 from ._tensors import empty, like_input, vec_dev
-from .errors import DimensionMismatch, InvalidConstraint, InvalidGradient
+from ._tensors import mat_dev, to_dev
+from .errors import DimensionMismatch, InvalidConstraint, InvalidGradient, SolverStall
 
 
 @dataclass
@@ -22,6 +23,69 @@ class SimplexSlackSet:
     """{w : sum(w) <= 1, w >= 0} (lmo.py:20-24)."""
 
     dimension: int
+
+
+@dataclass
+class PolytopeSet:
+    """{s : A s <= C, s >= 0} with strictly positive A and C (lmo.py:27-52)."""
+
+    A: np.ndarray
+    C: np.ndarray
+
+    def __post_init__(self):
+        self.A = np.ascontiguousarray(self.A, dtype=np.float64)
+        self.C = np.ascontiguousarray(self.C, dtype=np.float64)
+        if self.A.ndim != 2:
+            raise DimensionMismatch(f"expected 2-D matrix, got shape {self.A.shape}")
+        if self.C.ndim != 1:
+            raise DimensionMismatch(f"expected 1-D vector, got shape {self.C.shape}")
+        if self.A.shape[0] != self.C.size:
+            raise DimensionMismatch("constraint rows != len(C)")
+        if not np.all(self.A > 0):
+            raise InvalidConstraint("technology matrix entries must be strictly positive")
+        if not np.all(self.C > 0):
+            raise InvalidConstraint("budget levels must be strictly positive")
+        self._dev = None
+
+    @property
+    def n_resources(self) -> int:
+        return self.A.shape[0]
+
+    @property
+    def n_products(self) -> int:
+        return self.A.shape[1]
+
+    def device(self):
+        """(A, C) on the device, uploaded once."""
+        if self._dev is None:
+            self._dev = (mat_dev(self.A), to_dev(self.C))
+        return self._dev
+
+
+def lmo_general_device(g: torch.Tensor, polytope: PolytopeSet, max_iters: int | None = None,
+                       out=None) -> torch.Tensor:
+    m, n = polytope.A.shape
+    if g.numel() != n:
+        raise DimensionMismatch(f"gradient length {g.numel()} != products {n}")
+    cap = max_iters if max_iters is not None else 10 * (n + m)
+    a, c = polytope.device()
+    out = empty(n) if out is None else out
+    st = _status_tensor()
+    _lib.call("simopt_lmo_general", _lib.stream_ptr(), _lib.ptr(a), _lib.ptr(c), m, n, _lib.ptr(g),
+              int(cap), _lib.ptr(out), _lib.ptr(st))
+    code = int(st.item())
+    if code == 5:
+        raise InvalidGradient("gradient contains NaN")
+    if code == 7:
+        raise SolverStall("LP unbounded; polytope invariants violated")
+    if code == -7:
+        raise SolverStall(f"simplex exceeded {cap} iterations")
+    return out
+
+
+def lmo_general(g, polytope: PolytopeSet, max_iters: int | None = None):
+    """argmin of s.g over {A s <= C, s >= 0} by primal simplex (lmo.py:92-160)."""
+    return like_input(g, lmo_general_device(vec_dev(g), polytope, max_iters))
 
 
 def _status_tensor():

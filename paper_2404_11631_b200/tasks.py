@@ -20,7 +20,7 @@ from .errors import (ConfigurationError, DeviceError, DimensionMismatch, EmptyRe
                      InvalidConstraint, InvalidGradient, RunAborted)
 from .frank_wolfe import fw_step_size
 from .fused import MV, fused_rows
-from .lmo import SimplexSlackSet, lmo_simplex_slack, lmo_single_budget
+from .lmo import SimplexSlackSet, lmo_general, lmo_simplex_slack, lmo_single_budget
 from .records import TraceBuilder
 from .sampling import GaussianSpec, RngStream
 
@@ -69,10 +69,11 @@ _NV_PART_CAPACITY = 16 * 148
 # Task 2: multi-product newsvendor
 @dataclass
 class NewsvendorTask:
-    """Per-product costs, Gaussian demand and the single budget (tasks.py:93-138).
+    """Per-product costs, Gaussian demand and the budget set (tasks.py:93-138).
 
-    Only the single-budget form is supported (the multi-resource ``polytope``
-    form needs the dense simplex LMO, out of scope -- see lmo.py).
+    Either the single budget (``budget_costs``/``budget``, the benchmark default) or a
+    multi-resource ``polytope`` (lmo.PolytopeSet, small instances: its FW steps run
+    the generic loop with the device simplex LMO, csrc/lp.cu).
     """
 
     unit_cost: object
@@ -104,15 +105,13 @@ class NewsvendorTask:
         has_budget = self.budget_costs is not None and self.budget is not None
         if has_budget == (self.polytope is not None):
             raise ConfigurationError("set exactly one of (budget_costs, budget) or polytope")
-        if self.polytope is not None:
-            raise ConfigurationError("multi-resource polytope LMO (lmo_general) is not provided "
-                                     "by the cuda package")
-        self.budget_costs = conv(self.budget_costs)
-        if self.budget_costs.size != n:
-            raise DimensionMismatch("budget cost length mismatch")
-        if not np.all(self.budget_costs > 0) or not self.budget > 0:
-            raise InvalidConstraint("budget data must be strictly positive")
-        self.budget = float(self.budget)
+        if has_budget:
+            self.budget_costs = conv(self.budget_costs)
+            if self.budget_costs.size != n:
+                raise DimensionMismatch("budget cost length mismatch")
+            if not np.all(self.budget_costs > 0) or not self.budget > 0:
+                raise InvalidConstraint("budget data must be strictly positive")
+            self.budget = float(self.budget)
 
     @property
     def dimension(self) -> int:
@@ -133,7 +132,7 @@ class _NvDevice:
         self.k = to_dev(task.unit_cost[sl])
         self.h = to_dev(task.holding_cost[sl])
         self.v = to_dev(task.selling_value[sl])
-        self.c = to_dev(task.budget_costs[sl])
+        self.c = to_dev(task.budget_costs[sl]) if task.budget_costs is not None else None
         self.budget = task.budget
         self.S = None
         self.keys = None
@@ -208,6 +207,9 @@ class NewsvendorProblem:
         if exchange not in ("peer", "nccl"):
             raise ConfigurationError(f"unknown exchange {exchange!r}")
         self.exchange = exchange
+        if shard is not None and task.polytope is not None:
+            raise ConfigurationError("product sharding needs the single-budget set (the "
+                                     "multi-resource LMO couples all products)")
         j0, j1 = (0, task.dimension) if shard is None else shard.range(task.dimension, 4)
         self.dev = _NvDevice(task, j0, j1)
         self._stream = None
@@ -236,6 +238,8 @@ class NewsvendorProblem:
         return like_input(x, g)
 
     def lmo(self, g):
+        if self.task.polytope is not None:
+            return lmo_general(g, self.task.polytope)
         return lmo_single_budget(g, self.dev.c if is_tensor(g) else self.task.budget_costs,
                                  self.task.budget)
 
@@ -250,6 +254,13 @@ class NewsvendorProblem:
         xd = vec_dev(x)
         if bool((xd < -FEAS_TOL).any()):
             return False
+        if self.task.polytope is not None:  # tasks.py:330-332
+            a, c = self.task.polytope.device()
+            lhs = self.backend.matvec_device(a, xd)
+            bound = empty(c.numel())
+            _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(c), 1.0 + FEAS_TOL, None,
+                      c.numel(), _lib.ptr(bound))
+            return bool((lhs <= bound).all())
         spent = self.backend.dot(self.dev.c, xd)
         return float(spent) <= self.task.budget * (1.0 + FEAS_TOL)
 
@@ -258,6 +269,10 @@ class NewsvendorProblem:
 
     # ---- B200 path ---------------------------------------------------------------
     def fw_run_device(self, config, backend, *, task_label, size, rep):
+        """The fused device loop (single budget); None for a polytope task, whose steps
+        take fw_run's generic loop (gradient, device simplex LMO, update, checks)."""
+        if self.task.polytope is not None:
+            return None
         return _nv_fw_run_device(self, config, backend, task_label, size, rep)
 
 

@@ -221,10 +221,41 @@ def logistic_cases():
     save("logistic", **out)
 
 
+def polytope_cases():
+    """lmo_general (lmo.py:92-160) vertices and a multi-resource newsvendor FW trace."""
+    from sobench.lmo import PolytopeSet, lmo_general
+    from sobench.tasks import NewsvendorTask
+    out = {}
+    rng = np.random.default_rng(31)
+    cases = [(1, 5), (2, 3), (3, 7), (4, 40), (8, 200), (64, 1000), (5, 5)]
+    for i, (m, n) in enumerate(cases):
+        a = rng.uniform(0.1, 2.0, (m, n))
+        c = rng.uniform(0.5, 4.0, m)
+        g = rng.standard_normal(n)
+        if i == 6:  # ties: equal columns and equal gradient entries (Bland tie-breaks)
+            a[:, 3] = a[:, 1]
+            g[3] = g[1] = -1.0
+            g[0] = 0.0
+        out[f"lp{i}_A"], out[f"lp{i}_C"], out[f"lp{i}_g"] = a, c, g
+        out[f"lp{i}_s"] = lmo_general(g, PolytopeSet(A=a, C=c))
+    base = gen_newsvendor_instance(30, RngStream(42, 0))
+    a = rng.uniform(0.5, 2.0, (4, 30))
+    cap = 0.3 * (a @ base.demand_mean)
+    task = NewsvendorTask(unit_cost=base.unit_cost, holding_cost=base.holding_cost,
+                          selling_value=base.selling_value, demand_mean=base.demand_mean,
+                          demand_std=base.demand_std, polytope=PolytopeSet(A=a, C=cap))
+    for k in ("unit_cost", "holding_cost", "selling_value", "demand_mean", "demand_std"):
+        out[f"fw_{k}"] = getattr(task, k)
+    out["fw_A"], out["fw_C"] = a, cap
+    b = make_backend("sequential")
+    rec = fw_run(NewsvendorProblem(task, b), FwConfig(epochs=2, inner_iters=5, sample_size=400,
+                                                      stream=RngStream(42, 2)), b)
+    out["fw_obj"], out["fw_x"] = rec.objectives, rec.final_iterate
+    save("polytope", **out)
+
+
 if __name__ == "__main__":
     _kernels.warmup()
-    rng_cases()
-    tree_cases()
-    meanvar_cases()
-    newsvendor_cases()
-    logistic_cases()
+    which = sys.argv[1:] or ["rng", "tree", "meanvar", "newsvendor", "logistic", "polytope"]
+    for name in which:
+        globals()[f"{name}_cases"]()

@@ -170,3 +170,20 @@ def test_xoshiro_stream_states_host():
         assert np.array_equal(out[k], want)
         want = orc.xoshiro256pp_jump(want)
     assert Xoshiro256ppStreams is not None
+
+
+@pytest.mark.parametrize("i", range(7))
+def test_lmo_general_golden(golden, i):
+    """oracle.lmo_general against the reference's lmo_general (lmo.py:92-160) vertices."""
+    g = golden("polytope")
+    s = orc.lmo_general(g[f"lp{i}_g"], g[f"lp{i}_A"], g[f"lp{i}_C"])
+    assert np.array_equal(s, g[f"lp{i}_s"])
+
+
+def test_newsvendor_polytope_fw_trace(golden):
+    g = golden("polytope")
+    task = {"mu": g["fw_demand_mean"], "sigma": g["fw_demand_std"], "k": g["fw_unit_cost"],
+            "h": g["fw_holding_cost"], "v": g["fw_selling_value"]}
+    objs, x = orc.fw_run_newsvendor_polytope(task, g["fw_A"], g["fw_C"], 2, 5, 400, orc.Stream(42, 2))
+    assert np.array_equal(objs, g["fw_obj"])
+    assert np.array_equal(x, g["fw_x"])

@@ -120,6 +120,9 @@ if __name__ == "__main__":
             packed=True)
         sqn("C3-scale SQN (reference solver) d=1e3 N=1e6 (bit-packed, eager iteration)", 1000,
             1_000_000, packed=True, graph=False)
+    if "sqn_ab" in which:  # graph vs eager, alternating
+        for g in (True, False, True, False):
+            sqn(f"SQN packed ab graph={g}", 1000, 1_000_000, packed=True, graph=g)
     if "sqn_small" in which:  # the reference's own sizes: N = 30 d (sampling.py:241)
         for d in (100, 1000):
             for g in (True, False):

@@ -408,6 +408,10 @@ int simopt_bits_to_u8t(void* stream, const uint64_t* bits, int64_t rows, int64_t
                        uint8_t* out);
 int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
                             const double* dw, uint8_t* limbs, double* h);
+/* The tcgen05 limb Hessian with its operands loaded by TMA (3-D tensor maps over the
+ * sample-blocked X^T and the limb rows); same operands and result as xtdx_tc. */
+int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
+                             const double* dw, uint8_t* limbs, double* h);
 /* Same result on the 5th-generation tensor cores: tcgen05.mma.kind::i8 with the five limb
  * accumulators resident in TMEM (128 x 96 tiles, one CTA per SM). */
 int simopt_logistic_xtdx_tc(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,

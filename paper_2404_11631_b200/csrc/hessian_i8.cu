@@ -20,6 +20,9 @@
 // triangle, 8 warps of 64x32, 32-sample k-slabs in a 3-stage cp.async ring, fragments
 // by ldmatrix (48-byte padded rows: conflict-free), the limb applied to the B fragment
 // with two integer ops per 4 samples: (b * 255) & L.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -393,6 +396,194 @@ __global__ void __launch_bounds__(kTT, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr));
 }
 
+// ---------------------------------------------------------------------------------------
+// TMA-fed tcgen05 version.  Same tile (128 x 96, five s32 limb accumulators resident in
+// TMEM) and the same MMAs as k_xtdx_tc, but the operands arrive by TMA: one thread issues,
+// per 64-sample stage, four 16-byte-wide boxes of the A rows, four of the B rows (3-D
+// tensor map over the sample-blocked X^T: [block][feature][sample]) and one box of the
+// five limb rows, all completing on the slot's tma_full mbarrier (expect_tx bytes).  The
+// boxes land as [rows][16 B] -- K-major SWIZZLE_NONE core matrices with SBO = 128 B
+// (8-row groups) and LBO = rows * 16 B (the two 16-byte K halves of one K=32 MMA step) --
+// so no address math, no cp.async issue slots and no producer-wide barrier remain.  Eight
+// warps only expand B into its five limb-scaled copies ((x * 255) & L_k, 16 samples per
+// thread-chunk) once the slot's TMA completes, then arrive on full[slot]; a ninth warp
+// issues TMA, a tenth copies A into TMEM (tcgen05.cp) and issues the 10 MMAs per stage.
+constexpr int kMR = 8;                 // TMA ring depth (stages in flight)
+constexpr int kQThreads = 256;         // expansion threads (warps 0-7; 0-3 also the epilogue)
+constexpr int kQT = kQThreads + 64;    // + TMA warp (8) + MMA warp (9)
+constexpr uint32_t kStageTx = 2 * 2 * (kTM + kTN) * 16 + kLimbs * kTK;  // bytes per stage
+
+struct TmaSmem {
+  uint8_t a[kMR][2][2][kTM * 16];           // [slot][K step][K half][row][16 B]
+  uint8_t braw[kMR][2][2][kTN * 16];
+  uint8_t limb[kMR][384];                   // [5][64] (+ pad: 128-byte aligned slots)
+  uint8_t b[2][kLimbs][2][2][kTN * 16];     // limb-scaled B (double-buffered)
+  uint64_t tma_full[kMR], full[kMR], done[kMR];
+  uint32_t taddr;
+};
+
+// K-major SWIZZLE_NONE descriptor: LBO = K-half stride, SBO = 8-row-group stride (bytes)
+__device__ __forceinline__ uint64_t umma_desc_kn(const void* p, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((smem_u32(p) >> 4) & 0x3FFF) | ((uint64_t)(lbo >> 4) << 16) |
+         ((uint64_t)(sbo >> 4) << 32) | ((uint64_t)1 << 46);
+}
+
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+        "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kQT, 1)
+    k_xtdx_tma(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const __grid_constant__ CUtensorMap map_l, int lg_ch, int64_t d,
+               const int2* __restrict__ tiles, int64_t s0, int64_t s1, double inv_n, int beta,
+               double* __restrict__ h) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  TmaSmem& sm = *reinterpret_cast<TmaSmem*>(smraw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int2 tile = tiles[blockIdx.x];
+  const int64_t i0 = (int64_t)tile.x * kTM, j0 = (int64_t)tile.y * kTN;
+  const int64_t ch = 1LL << lg_ch;
+  if (tid == 0) {
+    for (int q = 0; q < kMR; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.tma_full[q])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.full[q])),
+                   "r"(kQThreads));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.done[q])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.taddr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t taddr = sm.taddr;
+  const uint32_t idesc = (2u << 4) | ((uint32_t)(kTN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+  const int64_t T = (s1 - s0) / kTK;
+  if (warp < kQThreads / 32) {
+    // ===== limb expansion: B_k = (x * 255) & L_k per 16-sample chunk =====
+    for (int64_t t = 0; t < T; ++t) {
+      const int q = (int)(t % kMR), bb = (int)(t & 1);
+      if (t >= 2) mbar_wait(&sm.done[(t - 2) % kMR], (uint32_t)(((t - 2) / kMR) & 1));
+      mbar_wait(&sm.tma_full[q], (uint32_t)((t / kMR) & 1));
+      for (int c = tid; c < 4 * kTN; c += kQThreads) {
+        const int kh = c / kTN, r = c - kh * kTN;  // kh = 2 * K step + K half
+        const uint4 x = *reinterpret_cast<const uint4*>(&sm.braw[q][kh >> 1][kh & 1][r * 16]);
+        const uint4 m = make_uint4(x.x * 255u, x.y * 255u, x.z * 255u, x.w * 255u);
+#pragma unroll
+        for (int k = 0; k < kLimbs; ++k) {
+          const uint4 L = *reinterpret_cast<const uint4*>(&sm.limb[q][k * kTK + kh * 16]);
+          *reinterpret_cast<uint4*>(&sm.b[bb][k][kh >> 1][kh & 1][r * 16]) =
+              make_uint4(m.x & L.x, m.y & L.y, m.z & L.z, m.w & L.w);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[q])) : "memory");
+    }
+  } else if (warp == kQThreads / 32) {
+    if (lane == 0) {  // ===== TMA issue =====
+      for (int64_t t = 0; t < T; ++t) {
+        const int q = (int)(t % kMR);
+        if (t >= kMR) mbar_wait(&sm.done[(t - kMR) % kMR], (uint32_t)(((t - kMR) / kMR) & 1));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.tma_full[q])),
+                     "r"(kStageTx) : "memory");
+        const int64_t smp = s0 + t * kTK;
+        const int blk = (int)(smp >> lg_ch), so = (int)(smp & (ch - 1));
+#pragma unroll
+        for (int kh = 0; kh < 4; ++kh) {
+          tma_3d(sm.a[q][kh >> 1][kh & 1], &map_a, so + 16 * kh, (int)i0, blk, &sm.tma_full[q]);
+          tma_3d(sm.braw[q][kh >> 1][kh & 1], &map_b, so + 16 * kh, (int)j0, blk, &sm.tma_full[q]);
+        }
+        tma_2d(sm.limb[q], &map_l, (int)smp, 0, &sm.tma_full[q]);
+      }
+    }
+  } else if (lane == 0) {
+    // ===== MMA issuer: per K step one A copy into TMEM and five limb MMAs =====
+    for (int64_t t = 0; t < T; ++t) {
+      const int q = (int)(t % kMR), bb = (int)(t & 1);
+      mbar_wait(&sm.tma_full[q], (uint32_t)((t / kMR) & 1));
+      mbar_wait(&sm.full[q], (uint32_t)((t / kMR) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint32_t ta = taddr + (uint32_t)(kLimbs * kTN + 8 * (int)((2 * t + ks) & 3));
+        const uint64_t da = umma_desc_kn(sm.a[q][ks][0], kTM * 16, 128);
+        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(ta), "l"(da));
+#pragma unroll
+        for (int k = 0; k < kLimbs; ++k) {
+          const uint64_t db = umma_desc_kn(sm.b[bb][k][ks][0], kTN * 16, 128);
+          const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
+                  taddr + (uint32_t)(k * kTN)),
+              "r"(ta), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(&sm.done[q])));
+    }
+  }
+  if (T > 0) mbar_wait(&sm.done[(T - 1) % kMR], (uint32_t)(((T - 1) / kMR) & 1));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp < 4) {  // epilogue: row i = i0 + 32*warp + lane, columns j0 .. j0+95
+    const int64_t i = i0 + warp * 32 + lane;
+    for (int c0 = 0; c0 < kTN; c0 += 32) {
+      double hv[32];
+#pragma unroll
+      for (int qq = 0; qq < 32; ++qq) hv[qq] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kLimbs; ++k) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+              "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+              "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr + ((uint32_t)(warp * 32) << 16) + (uint32_t)(k * kTN + c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        const double sc = ldexp(1.0, kLimbBits * k - kFixBits) * inv_n;
+#pragma unroll
+        for (int qq = 0; qq < 32; ++qq) hv[qq] += (double)(int)v[qq] * sc;
+      }
+      if (i < d) {
+#pragma unroll
+        for (int qq = 0; qq < 32; ++qq) {
+          const int64_t j = j0 + c0 + qq;
+          if (j < d && i <= j) {
+            if (beta) {
+              h[i * d + j] += hv[qq];
+              if (i != j) h[j * d + i] += hv[qq];
+            } else {
+              h[i * d + j] = hv[qq];
+              if (i != j) h[j * d + i] = hv[qq];
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr));
+}
+
 // out[block r/ch][j][r%ch] = bit (r, j) of the packed rows, 0 for r >= rows (16 samples
 // per thread)
 __global__ void k_bits_to_u8t(const uint64_t* __restrict__ bits, int64_t rows, int64_t d, int64_t W,
@@ -486,6 +677,30 @@ extern "C" int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t 
   return SIMOPT_OK;
 }
 
+// upper-triangle list of 128 x 96 tiles (tile (bi, bj) holds some j >= i), cached per d
+static int upper_tiles(int64_t d, int2** out, int* count) {
+  static std::mutex mu;
+  static std::vector<std::pair<int64_t, std::pair<int2*, int>>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : cache)
+    if (e.first == d) {
+      *out = e.second.first;
+      *count = e.second.second;
+      return SIMOPT_OK;
+    }
+  std::vector<int2> v;
+  for (int64_t bi = 0; bi * kTM < d; ++bi)
+    for (int64_t bj = 0; bj * kTN < d; ++bj)
+      if (bj * kTN + kTN - 1 >= bi * kTM) v.push_back(make_int2((int)bi, (int)bj));
+  int2* tiles = nullptr;
+  SIMOPT_CUDA(cudaMalloc(&tiles, v.size() * sizeof(int2)));
+  SIMOPT_CUDA(cudaMemcpy(tiles, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  cache.push_back({d, {tiles, (int)v.size()}});
+  *out = tiles;
+  *count = (int)v.size();
+  return SIMOPT_OK;
+}
+
 // tcgen05 version of simopt_logistic_xtdx_i8 (same operands and result).
 extern "C" int simopt_logistic_xtdx_tc(void* stream, const uint8_t* xt, int64_t np, int64_t n,
                                        int64_t d, const double* dw, uint8_t* limbs, double* h) {
@@ -498,26 +713,9 @@ extern "C" int simopt_logistic_xtdx_tc(void* stream, const uint8_t* xt, int64_t 
   while ((1LL << lg) < ch) ++lg;
   k_limbs<<<egrid(np), 256, 0, st>>>(dw, n, np, limbs);
   SIMOPT_CHECK_LAUNCH("k_limbs");
-  // upper-triangle tile list (tile (bi, bj) holds some j >= i), cached per d
-  static std::mutex mu;
-  static std::vector<std::pair<int64_t, std::pair<int2*, int>>> cache;
   int2* tiles = nullptr;
   int ntiles = 0;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    for (auto& e : cache)
-      if (e.first == d) { tiles = e.second.first; ntiles = e.second.second; }
-    if (!tiles) {
-      std::vector<int2> v;
-      for (int64_t bi = 0; bi * kTM < d; ++bi)
-        for (int64_t bj = 0; bj * kTN < d; ++bj)
-          if (bj * kTN + kTN - 1 >= bi * kTM) v.push_back(make_int2((int)bi, (int)bj));
-      SIMOPT_CUDA(cudaMalloc(&tiles, v.size() * sizeof(int2)));
-      SIMOPT_CUDA(cudaMemcpy(tiles, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice));
-      ntiles = (int)v.size();
-      cache.push_back({d, {tiles, ntiles}});
-    }
-  }
+  SIMOPT_REQUIRE(upper_tiles(d, &tiles, &ntiles) == SIMOPT_OK, SIMOPT_E_CUDA, "%s", simopt_last_error());
   // > half the SM's shared memory: one CTA per SM, which then owns all 512 TMEM columns
   const size_t smem = sizeof(TcSmem) + 1024 > 120 * 1024 ? sizeof(TcSmem) + 1024 : 120 * 1024;
   static bool attr = false;
@@ -530,6 +728,73 @@ extern "C" int simopt_logistic_xtdx_tc(void* stream, const uint8_t* xt, int64_t 
     const int64_t c1 = c0 + kChunk < np ? c0 + kChunk : np;
     k_xtdx_tc<<<ntiles, kTT, smem, st>>>(xt, lg, d, limbs, np, tiles, c0, c1, 1.0 / (double)n, beta, h);
     SIMOPT_CHECK_LAUNCH("k_xtdx_tc");
+    beta = 1;
+  }
+  return SIMOPT_OK;
+}
+
+// TMA-fed tcgen05 version (k_xtdx_tma): same operands and result as simopt_logistic_xtdx_tc.
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+extern "C" int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t np, int64_t n,
+                                        int64_t d, const double* dw, uint8_t* limbs, double* h) {
+  SIMOPT_REQUIRE(n >= 1 && d >= 1, SIMOPT_E_DIMENSION, "empty design matrix");
+  SIMOPT_REQUIRE(d < (1LL << 31), SIMOPT_E_CONFIG, "d too large for a tensor map");
+  int64_t ch = 0, np_want = 0;
+  simopt_u8t_geometry(n, &ch, &np_want);
+  SIMOPT_REQUIRE(np == np_want, SIMOPT_E_CONFIG, "np must come from simopt_u8t_geometry");
+  PFN_cuTensorMapEncodeTiled_v12000 encode = encode_fn();
+  SIMOPT_REQUIRE(encode != nullptr, SIMOPT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cudaStream_t st = as_stream(stream);
+  int lg = 0;
+  while ((1LL << lg) < ch) ++lg;
+  k_limbs<<<egrid(np), 256, 0, st>>>(dw, n, np, limbs);
+  SIMOPT_CHECK_LAUNCH("k_limbs");
+  int2* tiles = nullptr;
+  int ntiles = 0;
+  SIMOPT_REQUIRE(upper_tiles(d, &tiles, &ntiles) == SIMOPT_OK, SIMOPT_E_CUDA, "%s", simopt_last_error());
+  // X^T blocks [np/ch][d][ch + kRowPad] u8; boxes of 16 samples x {128 | 96} feature rows
+  const int64_t rs = ch + kRowPad;
+  CUtensorMap ma, mb, ml;
+  const cuuint64_t gdim[3] = {(cuuint64_t)rs, (cuuint64_t)d, (cuuint64_t)(np / ch)};
+  const cuuint64_t gstr[2] = {(cuuint64_t)rs, (cuuint64_t)(d * rs)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const cuuint32_t box_a[3] = {16, (cuuint32_t)kTM, 1}, box_b[3] = {16, (cuuint32_t)kTN, 1};
+  CUresult r1 = encode(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xt), gdim, gstr, box_a,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r2 = encode(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xt), gdim, gstr, box_b,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const cuuint64_t ldim[2] = {(cuuint64_t)np, (cuuint64_t)kLimbs};
+  const cuuint64_t lstr[1] = {(cuuint64_t)np};
+  const cuuint32_t box_l[2] = {(cuuint32_t)kTK, (cuuint32_t)kLimbs}, lestr[2] = {1, 1};
+  CUresult r3 = encode(&ml, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, limbs, ldim, lstr, box_l, lestr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SIMOPT_REQUIRE(r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS && r3 == CUDA_SUCCESS, SIMOPT_E_CUDA,
+                 "tensor map encoding failed (%d, %d, %d)", (int)r1, (int)r2, (int)r3);
+  const size_t smem = sizeof(TmaSmem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  int beta = 0;
+  for (int64_t c0 = 0; c0 < np; c0 += kChunk) {
+    const int64_t c1 = c0 + kChunk < np ? c0 + kChunk : np;
+    k_xtdx_tma<<<ntiles, kQT, smem, st>>>(ma, mb, ml, lg, d, tiles, c0, c1, 1.0 / (double)n, beta, h);
+    SIMOPT_CHECK_LAUNCH("k_xtdx_tma");
     beta = 1;
   }
   return SIMOPT_OK;

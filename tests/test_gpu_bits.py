@@ -116,7 +116,7 @@ def test_xtdx_bits_equals_dense(pkg, d, n):
     assert torch.equal(logistic_hessian_device(dense, dw), logistic_hessian_device(packed, dw, method="dmma"))
 
 
-@pytest.mark.parametrize("method", ["i8", "tc"])
+@pytest.mark.parametrize("method", ["i8", "tc", "tma"])
 @pytest.mark.parametrize("d,n", [(128, 4096), (200, 3001), (13, 777), (1000, 2000), (300, 40),
                                  (97, 9000)])
 def test_xtdx_i8_vs_oracle(pkg, d, n, method):
@@ -139,6 +139,17 @@ def test_xtdx_i8_vs_oracle(pkg, d, n, method):
     quarter = torch.full((n,), 0.25, dtype=torch.float64, device="cuda")
     np.testing.assert_allclose(logistic_hessian_device(data, quarter, method=method).cpu().numpy(),
                                (x.T @ x) * 0.25 / n, rtol=1e-12)
+
+
+@pytest.mark.parametrize("d,n", [(1000, 70_000), (256, 5000), (130, 64)])
+def test_xtdx_tma_equals_tc(pkg, d, n):
+    """TMA-fed and cp.async-fed tcgen05 kernels: the same integer sums, the same bits."""
+    from paper_2404_11631_b200.newton import logistic_hessian_device
+    from paper_2404_11631_b200.sampling import synth_classification
+    data = synth_classification(d, pkg.RngStream(8, 0), n_rows=n, packed=True)
+    dw = torch.rand(n, dtype=torch.float64, device="cuda") * 0.25
+    assert torch.equal(logistic_hessian_device(data, dw, method="tma"),
+                       logistic_hessian_device(data, dw, method="tc"))
 
 
 def test_newton_packed_vs_oracle(pkg):

@@ -120,6 +120,9 @@ if __name__ == "__main__":
             packed=True)
         sqn("C3-scale SQN (reference solver) d=1e3 N=1e6 (bit-packed, eager iteration)", 1000,
             1_000_000, packed=True, graph=False)
+    if "tma" in which:
+        xtdx("C5 X^T D X slice (tc)", 8192, 125_000, packed=True, method="tc")
+        xtdx("C5 X^T D X slice (tma)", 8192, 125_000, packed=True, method="tma")
     if "sqn_ab" in which:  # graph vs eager, alternating
         for g in (True, False, True, False):
             sqn(f"SQN packed ab graph={g}", 1000, 1_000_000, packed=True, graph=g)
@@ -136,3 +139,5 @@ if __name__ == "__main__":
              125_000, packed=True, method="i8")
         xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X, tcgen05 i8 limbs, TMEM)", 8192,
              125_000, packed=True, method="tc")
+        xtdx("C5 X^T D X d=8192, per-GPU slice N=1.25e5 (bit-packed X, tcgen05 i8 limbs, TMA operands)",
+             8192, 125_000, packed=True, method="tma")

@@ -20,6 +20,9 @@
 // triangle, 8 warps of 64x32, 32-sample k-slabs in a 3-stage cp.async ring, fragments
 // by ldmatrix (48-byte padded rows: conflict-free), the limb applied to the B fragment
 // with two integer ops per 4 samples: (b * 255) & L.
+#include <stdlib.h>
+#include <string.h>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -397,27 +400,36 @@ __global__ void __launch_bounds__(kTT, 1)
 }
 
 // ---------------------------------------------------------------------------------------
-// TMA-fed tcgen05 version.  Same tile (128 x 96, five s32 limb accumulators resident in
-// TMEM) and the same MMAs as k_xtdx_tc, but the operands arrive by TMA: one thread issues,
-// per 64-sample stage, four 16-byte-wide boxes of the A rows, four of the B rows (3-D
-// tensor map over the sample-blocked X^T: [block][feature][sample]) and one box of the
-// five limb rows, all completing on the slot's tma_full mbarrier (expect_tx bytes).  The
-// boxes land as [rows][16 B] -- K-major SWIZZLE_NONE core matrices with SBO = 128 B
-// (8-row groups) and LBO = rows * 16 B (the two 16-byte K halves of one K=32 MMA step) --
-// so no address math, no cp.async issue slots and no producer-wide barrier remain.  Eight
-// warps only expand B into its five limb-scaled copies ((x * 255) & L_k, 16 samples per
-// thread-chunk) once the slot's TMA completes, then arrive on full[slot]; a ninth warp
-// issues TMA, a tenth copies A into TMEM (tcgen05.cp) and issues the 10 MMAs per stage.
+// TMA-fed tcgen05 version (the default for binary X).  Same 128 x 96 tile and the same
+// limb algebra as k_xtdx_tc, re-balanced for the three limits measured on this B200:
+//  * operands by TMA: per 64-sample stage one thread issues one box of the 128 A rows, one
+//    of the 96 B rows (3-D tensor maps over the sample-blocked X^T [block][feature][sample],
+//    64-byte rows with the 64-byte swizzle: whole sectors, one request per row) and one of
+//    the five limb rows, completing on the slot's tma_full mbarrier (expect_tx bytes);
+//  * wide MMAs (kWide): a tcgen05.mma.kind::i8 costs ~55 ns per SM for any N <= 128 and
+//    ~69 ns at N = 256 (tools/micro/tc_i8_rate.cu), so the five limb copies of each
+//    48-column half of B are stacked along N: a K step is 2 MMAs of N = 240 (two
+//    accumulators of 5 x 48 columns = 480 TMEM columns) instead of 5 of N = 96;
+//  * the limb expansion ((x * 255) & L_k into kBB rotating buffers) is the shared-memory
+//    bandwidth bound that remains: 12 warps, one 16-sample chunk each, mapped so that a
+//    warp's 32 rows share one logical chunk -- its reads and writes are conflict-free under
+//    the swizzle and its limb reads are broadcasts.
+// A is copied into TMEM once per K step (tcgen05.cp) and read from there by the MMAs.
+// kSW = 16 keeps the first version (16-byte boxes per K half, SWIZZLE_NONE) for comparison.
 constexpr int kMR = 8;                 // TMA ring depth (stages in flight)
-constexpr int kQThreads = 256;         // expansion threads (warps 0-7; 0-3 also the epilogue)
-constexpr int kQT = kQThreads + 64;    // + TMA warp (8) + MMA warp (9)
+constexpr int kQThreads = 384;         // expansion threads, one 16-sample chunk of B each (warps 0-11; 0-3 also the epilogue)
+constexpr int kQT = kQThreads + 64;    // + TMA warp (12) + MMA warp (13)
 constexpr uint32_t kStageTx = 2 * 2 * (kTM + kTN) * 16 + kLimbs * kTK;  // bytes per stage
+constexpr int kBB = 3;                 // expanded-B buffers: expansion runs kBB-1 stages ahead of the MMAs
 
 struct TmaSmem {
-  uint8_t a[kMR][2][2][kTM * 16];           // [slot][K step][K half][row][16 B]
-  uint8_t braw[kMR][2][2][kTN * 16];
+  // operand stages, 64 samples of 128 (A) / 96 (B) feature rows each; layout kSW:
+  //   16: [K step][K half][row][16 B] (SWIZZLE_NONE core matrices, one box per K half)
+  //   64: [row][64 B] with the 64-byte swizzle (one box per stage)
+  uint8_t a[kMR][kTM * 64];
+  uint8_t braw[kMR][kTN * 64];
   uint8_t limb[kMR][384];                   // [5][64] (+ pad: 128-byte aligned slots)
-  uint8_t b[2][kLimbs][2][2][kTN * 16];     // limb-scaled B (double-buffered)
+  uint8_t b[kBB][kLimbs][kTN * 64];         // limb-scaled B (kBB-buffered), layout of braw
   uint64_t tma_full[kMR], full[kMR], done[kMR];
   uint32_t taddr;
 };
@@ -443,6 +455,18 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       : "memory");
 }
 
+// K-major SWIZZLE_64B descriptor (layout type 4): 8-row x 64-byte swizzle atoms, SBO = 512 B
+__device__ __forceinline__ uint64_t umma_desc_sw64(const void* p) {
+  return (uint64_t)((smem_u32(p) >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+// kWide (with kSW = 64): the tile's two 48-column halves each get ONE accumulator of
+// N = 5 x 48 = 240 columns -- the five limb copies of a half's B rows are stacked along N --
+// so a K step takes 2 MMAs of N = 240 instead of 5 of N = 96.  A tcgen05.mma.kind::i8
+// costs ~55 ns per SM up to N = 128 and ~69 ns at N = 256 (tools/micro/tc_i8_rate.cu):
+// the narrow MMAs, not the operands, set the narrow kernel's pace.
+template <int kSW, bool kWide>
 __global__ void __launch_bounds__(kQT, 1)
     k_xtdx_tma(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const __grid_constant__ CUtensorMap map_l, int lg_ch, int64_t d,
@@ -458,7 +482,7 @@ __global__ void __launch_bounds__(kQT, 1)
     for (int q = 0; q < kMR; ++q) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.tma_full[q])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.full[q])),
-                   "r"(kQThreads));
+                   "r"(kQThreads / 32));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.done[q])));
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -471,27 +495,49 @@ __global__ void __launch_bounds__(kQT, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t taddr = sm.taddr;
-  const uint32_t idesc = (2u << 4) | ((uint32_t)(kTN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+  constexpr int kHN = kTN / 2, kWN = kLimbs * kHN;  // wide: half width 48, MMA N = 240
+  const uint32_t idesc = (2u << 4) | ((uint32_t)((kWide ? kWN : kTN) >> 3) << 17) |
+                         ((uint32_t)(kTM >> 4) << 24);
   const int64_t T = (s1 - s0) / kTK;
   if (warp < kQThreads / 32) {
     // ===== limb expansion: B_k = (x * 255) & L_k per 16-sample chunk =====
-    for (int64_t t = 0; t < T; ++t) {
-      const int q = (int)(t % kMR), bb = (int)(t & 1);
-      if (t >= 2) mbar_wait(&sm.done[(t - 2) % kMR], (uint32_t)(((t - 2) / kMR) & 1));
+    int bb = 0;
+    for (int64_t t = 0; t < T; ++t, bb = (bb + 1 == kBB ? 0 : bb + 1)) {
+      const int q = (int)(t % kMR);
+      if (t >= kBB) mbar_wait(&sm.done[(t - kBB) % kMR], (uint32_t)(((t - kBB) / kMR) & 1));
       mbar_wait(&sm.tma_full[q], (uint32_t)((t / kMR) & 1));
       for (int c = tid; c < 4 * kTN; c += kQThreads) {
-        const int kh = c / kTN, r = c - kh * kTN;  // kh = 2 * K step + K half
-        const uint4 x = *reinterpret_cast<const uint4*>(&sm.braw[q][kh >> 1][kh & 1][r * 16]);
+        int off, lc;  // byte offset of this 16-sample chunk, its logical chunk (samples lc*16..)
+        if (kSW == 16) {
+          const int kh = c / kTN, r = c - kh * kTN;  // kh = 2 * K step + K half
+          off = kh * (kTN * 16) + r * 16;
+          lc = kh;
+        } else {
+          // a warp takes one logical chunk of 32 rows: its x reads and limb-scaled writes
+          // are conflict-free under the swizzle, its limb reads are broadcasts
+          // (Swizzle<2,4,3>: physical chunk = logical ^ ((row >> 1) & 3))
+          const int wv = c >> 5, r = (wv >> 2) * 32 + (c & 31);
+          lc = wv & 3;
+          off = r * 64 + ((lc ^ ((r >> 1) & 3)) * 16);
+        }
+        const uint4 x = *reinterpret_cast<const uint4*>(&sm.braw[q][off]);
         const uint4 m = make_uint4(x.x * 255u, x.y * 255u, x.z * 255u, x.w * 255u);
 #pragma unroll
         for (int k = 0; k < kLimbs; ++k) {
-          const uint4 L = *reinterpret_cast<const uint4*>(&sm.limb[q][k * kTK + kh * 16]);
-          *reinterpret_cast<uint4*>(&sm.b[bb][k][kh >> 1][kh & 1][r * 16]) =
-              make_uint4(m.x & L.x, m.y & L.y, m.z & L.z, m.w & L.w);
+          const uint4 L = *reinterpret_cast<const uint4*>(&sm.limb[q][k * kTK + lc * 16]);
+          const uint4 v = make_uint4(m.x & L.x, m.y & L.y, m.z & L.z, m.w & L.w);
+          if (kWide) {  // row r of half hh -> row hh*240 + k*48 + (r - 48 hh): same swizzle phase
+            const int r = off >> 6, hh = r >= kHN ? 1 : 0;
+            *reinterpret_cast<uint4*>(&sm.b[bb][0][(hh * kWN + k * kHN + r - hh * kHN) * 64 + (off & 63)]) = v;
+          } else {
+            *reinterpret_cast<uint4*>(&sm.b[bb][k][off]) = v;
+          }
         }
       }
       asm volatile("fence.proxy.async.shared::cta;");
-      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[q])) : "memory");
+      __syncwarp();  // one arrival per warp (count kQThreads / 32)
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[q])) : "memory");
     }
   } else if (warp == kQThreads / 32) {
     if (lane == 0) {  // ===== TMA issue =====
@@ -502,34 +548,44 @@ __global__ void __launch_bounds__(kQT, 1)
                      "r"(kStageTx) : "memory");
         const int64_t smp = s0 + t * kTK;
         const int blk = (int)(smp >> lg_ch), so = (int)(smp & (ch - 1));
+        if (kSW == 16) {
 #pragma unroll
-        for (int kh = 0; kh < 4; ++kh) {
-          tma_3d(sm.a[q][kh >> 1][kh & 1], &map_a, so + 16 * kh, (int)i0, blk, &sm.tma_full[q]);
-          tma_3d(sm.braw[q][kh >> 1][kh & 1], &map_b, so + 16 * kh, (int)j0, blk, &sm.tma_full[q]);
+          for (int kh = 0; kh < 4; ++kh) {
+            tma_3d(&sm.a[q][kh * kTM * 16], &map_a, so + 16 * kh, (int)i0, blk, &sm.tma_full[q]);
+            tma_3d(&sm.braw[q][kh * kTN * 16], &map_b, so + 16 * kh, (int)j0, blk, &sm.tma_full[q]);
+          }
+        } else {
+          tma_3d(sm.a[q], &map_a, so, (int)i0, blk, &sm.tma_full[q]);
+          tma_3d(sm.braw[q], &map_b, so, (int)j0, blk, &sm.tma_full[q]);
         }
         tma_2d(sm.limb[q], &map_l, (int)smp, 0, &sm.tma_full[q]);
       }
     }
   } else if (lane == 0) {
     // ===== MMA issuer: per K step one A copy into TMEM and five limb MMAs =====
-    for (int64_t t = 0; t < T; ++t) {
-      const int q = (int)(t % kMR), bb = (int)(t & 1);
+    int bb = 0;
+    for (int64_t t = 0; t < T; ++t, bb = (bb + 1 == kBB ? 0 : bb + 1)) {
+      const int q = (int)(t % kMR);
       mbar_wait(&sm.tma_full[q], (uint32_t)((t / kMR) & 1));
       mbar_wait(&sm.full[q], (uint32_t)((t / kMR) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         const uint32_t ta = taddr + (uint32_t)(kLimbs * kTN + 8 * (int)((2 * t + ks) & 3));
-        const uint64_t da = umma_desc_kn(sm.a[q][ks][0], kTM * 16, 128);
+        const uint64_t da = kSW == 16 ? umma_desc_kn(&sm.a[q][ks * kTM * 32], kTM * 16, 128)
+                                      : umma_desc_sw64(&sm.a[q][ks * 32]);
         asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(ta), "l"(da));
+        constexpr int kNM = kWide ? 2 : kLimbs;  // MMAs per K step
 #pragma unroll
-        for (int k = 0; k < kLimbs; ++k) {
-          const uint64_t db = umma_desc_kn(sm.b[bb][k][ks][0], kTN * 16, 128);
+        for (int k = 0; k < kNM; ++k) {
+          const uint64_t db = kWide ? umma_desc_sw64(&sm.b[bb][0][k * kWN * 64 + ks * 32])
+                              : kSW == 16 ? umma_desc_kn(&sm.b[bb][k][ks * kTN * 32], kTN * 16, 128)
+                                          : umma_desc_sw64(&sm.b[bb][k][ks * 32]);
           const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
-                  taddr + (uint32_t)(k * kTN)),
+                  taddr + (uint32_t)(k * (kWide ? kWN : kTN))),
               "r"(ta), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
         }
       }
@@ -539,7 +595,45 @@ __global__ void __launch_bounds__(kQT, 1)
   }
   if (T > 0) mbar_wait(&sm.done[(T - 1) % kMR], (uint32_t)(((T - 1) / kMR) & 1));
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp < 4) {  // epilogue: row i = i0 + 32*warp + lane, columns j0 .. j0+95
+  if (kWide && warp < 4) {  // epilogue (wide): column jj = 48 h + c sums D_h[k*48 + c] over k
+    const int64_t i = i0 + warp * 32 + lane;
+    for (int hc = 0; hc < 6; ++hc) {
+      const int hh = hc / 3, c0 = (hc % 3) * 16;
+      double hv[16];
+#pragma unroll
+      for (int qq = 0; qq < 16; ++qq) hv[qq] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kLimbs; ++k) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr + ((uint32_t)(warp * 32) << 16) + (uint32_t)(hh * kWN + k * kHN + c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        const double sc = ldexp(1.0, kLimbBits * k - kFixBits) * inv_n;
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) hv[qq] += (double)(int)v[qq] * sc;
+      }
+      if (i < d) {
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) {
+          const int64_t j = j0 + hh * kHN + c0 + qq;
+          if (j < d && i <= j) {
+            if (beta) {
+              h[i * d + j] += hv[qq];
+              if (i != j) h[j * d + i] += hv[qq];
+            } else {
+              h[i * d + j] = hv[qq];
+              if (i != j) h[j * d + i] = hv[qq];
+            }
+          }
+        }
+      }
+    }
+  }
+  if (!kWide && warp < 4) {  // epilogue: row i = i0 + 32*warp + lane, columns j0 .. j0+95
     const int64_t i = i0 + warp * 32 + lane;
     for (int c0 = 0; c0 < kTN; c0 += 32) {
       double hv[32];
@@ -573,6 +667,181 @@ __global__ void __launch_bounds__(kQT, 1)
             } else {
               h[i * d + j] = hv[qq];
               if (i != j) h[j * d + i] = hv[qq];
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr));
+}
+
+// ---------------------------------------------------------------------------------------
+// TMA-fed tcgen05 version with the limbs on the A side (k_xtdx_ts): the 128 x 80 tile's
+// five accumulators take 400 TMEM columns; the five limb-scaled copies of A for a K step
+// (5 x 8 columns) are written straight into TMEM by the four A warps (tcgen05.st, one
+// row per thread: (x * 255) & L_k on 32-bit words) in two alternating 40-column slots,
+// and every MMA reads A from TMEM and the raw 0/1 B rows from shared memory as TMA left
+// them (64-byte swizzled boxes).  Shared memory then carries only the TMA writes, one
+// read of A and the MMAs' B reads -- about 45% of the expanded-B design's traffic, which
+// made k_xtdx_tma shared-memory-bandwidth bound.
+constexpr int kSN = 80;                       // tile columns (N of every MMA)
+constexpr int kSR = 10;                       // TMA ring depth
+constexpr int kSAcol = kLimbs * kSN;          // first A column: 400; A slot s at 400 + 40 s
+constexpr int kST = 192;                      // 4 A warps + TMA warp + MMA warp
+constexpr uint32_t kSTx = (kTM + kSN) * 64 + kLimbs * kTK;
+
+struct TsSmem {
+  uint8_t a[kSR][kTM * 64];                   // [row][64 B], 64-byte swizzle
+  uint8_t b[kSR][kSN * 64];
+  uint8_t limb[kSR][384];
+  uint64_t tma_full[kSR], done[kSR], a_full[2], a_done[2];
+  uint32_t taddr;
+};
+
+__global__ void __launch_bounds__(kST, 1)
+    k_xtdx_ts(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+              const __grid_constant__ CUtensorMap map_l, int lg_ch, int64_t d,
+              const int2* __restrict__ tiles, int64_t s0, int64_t s1, double inv_n, int beta,
+              double* __restrict__ h) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  TsSmem& sm = *reinterpret_cast<TsSmem*>(smraw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int2 tile = tiles[blockIdx.x];
+  const int64_t i0 = (int64_t)tile.x * kTM, j0 = (int64_t)tile.y * kSN;
+  const int64_t ch = 1LL << lg_ch;
+  if (tid == 0) {
+    for (int q = 0; q < kSR; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.tma_full[q])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.done[q])));
+    }
+    for (int q = 0; q < 2; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.a_full[q])), "r"(128));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.a_done[q])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.taddr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t taddr = sm.taddr;
+  const uint32_t idesc = (2u << 4) | ((uint32_t)(kSN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+  const int64_t T = (s1 - s0) / kTK;
+  if (warp < 4) {
+    // ===== A warps: row r = tid; per K step j (slot j & 1) five limb-scaled copies into TMEM =====
+    const int r = tid;
+    const uint32_t trow = taddr + ((uint32_t)(warp * 32) << 16) + (uint32_t)kSAcol;
+    for (int64_t t = 0; t < T; ++t) {
+      const int q = (int)(t % kSR);
+      mbar_wait(&sm.tma_full[q], (uint32_t)((t / kSR) & 1));
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int64_t j = 2 * t + ks;
+        const int sl = (int)(j & 1);
+        // the row's 32 samples of this K step: logical 16-byte chunks 2ks, 2ks+1
+        const int sw = (r >> 1) & 3;
+        const uint4 x0 = *reinterpret_cast<const uint4*>(&sm.a[q][r * 64 + (((2 * ks) ^ sw) * 16)]);
+        const uint4 x1 = *reinterpret_cast<const uint4*>(&sm.a[q][r * 64 + (((2 * ks + 1) ^ sw) * 16)]);
+        const uint32_t m[8] = {x0.x * 255u, x0.y * 255u, x0.z * 255u, x0.w * 255u,
+                               x1.x * 255u, x1.y * 255u, x1.z * 255u, x1.w * 255u};
+        if (j >= 2) mbar_wait(&sm.a_done[sl], (uint32_t)(((j - 2) >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int k = 0; k < kLimbs; ++k) {
+          const uint4 L0 = *reinterpret_cast<const uint4*>(&sm.limb[q][k * kTK + ks * 32]);
+          const uint4 L1 = *reinterpret_cast<const uint4*>(&sm.limb[q][k * kTK + ks * 32 + 16]);
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                           trow + (uint32_t)(sl * (kLimbs * 8) + k * 8)),
+                       "r"(m[0] & L0.x), "r"(m[1] & L0.y), "r"(m[2] & L0.z), "r"(m[3] & L0.w),
+                       "r"(m[4] & L1.x), "r"(m[5] & L1.y), "r"(m[6] & L1.z), "r"(m[7] & L1.w));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.a_full[sl])) : "memory");
+      }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {  // ===== TMA issue =====
+      for (int64_t t = 0; t < T; ++t) {
+        const int q = (int)(t % kSR);
+        if (t >= kSR) mbar_wait(&sm.done[(t - kSR) % kSR], (uint32_t)(((t - kSR) / kSR) & 1));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.tma_full[q])),
+                     "r"(kSTx) : "memory");
+        const int64_t smp = s0 + t * kTK;
+        const int blk = (int)(smp >> lg_ch), so = (int)(smp & (ch - 1));
+        tma_3d(sm.a[q], &map_a, so, (int)i0, blk, &sm.tma_full[q]);
+        tma_3d(sm.b[q], &map_b, so, (int)j0, blk, &sm.tma_full[q]);
+        tma_2d(sm.limb[q], &map_l, (int)smp, 0, &sm.tma_full[q]);
+      }
+    }
+  } else if (lane == 0) {
+    // ===== MMA issuer: per K step five MMAs (A_k from TMEM, raw B from smem) =====
+    for (int64_t t = 0; t < T; ++t) {
+      const int q = (int)(t % kSR);
+      mbar_wait(&sm.tma_full[q], (uint32_t)((t / kSR) & 1));
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int64_t j = 2 * t + ks;
+        const int sl = (int)(j & 1);
+        mbar_wait(&sm.a_full[sl], (uint32_t)((j >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint64_t db = umma_desc_sw64(&sm.b[q][ks * 32]);
+#pragma unroll
+        for (int k = 0; k < kLimbs; ++k) {
+          const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
+                  taddr + (uint32_t)(k * kSN)),
+              "r"(taddr + (uint32_t)(kSAcol + sl * (kLimbs * 8) + k * 8)), "l"(db), "r"(idesc), "r"(acc),
+              "r"(0), "r"(0), "r"(0), "r"(0));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&sm.a_done[sl])));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(&sm.done[q])));
+    }
+  }
+  if (T > 0) mbar_wait(&sm.done[(T - 1) % kSR], (uint32_t)(((T - 1) / kSR) & 1));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp < 4) {  // epilogue: row i = i0 + 32*warp + lane, columns j0 .. j0+79
+    const int64_t i = i0 + warp * 32 + lane;
+    for (int c0 = 0; c0 < kSN; c0 += 16) {
+      double hv[16];
+#pragma unroll
+      for (int qq = 0; qq < 16; ++qq) hv[qq] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kLimbs; ++k) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr + ((uint32_t)(warp * 32) << 16) + (uint32_t)(k * kSN + c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        const double sc = ldexp(1.0, kLimbBits * k - kFixBits) * inv_n;
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) hv[qq] += (double)(int)v[qq] * sc;
+      }
+      if (i < d) {
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) {
+          const int64_t jj = j0 + c0 + qq;
+          if (jj < d && i <= jj) {
+            if (beta) {
+              h[i * d + jj] += hv[qq];
+              if (i != jj) h[jj * d + i] += hv[qq];
+            } else {
+              h[i * d + jj] = hv[qq];
+              if (i != jj) h[jj * d + i] = hv[qq];
             }
           }
         }
@@ -678,24 +947,25 @@ extern "C" int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t 
 }
 
 // upper-triangle list of 128 x 96 tiles (tile (bi, bj) holds some j >= i), cached per d
-static int upper_tiles(int64_t d, int2** out, int* count) {
+static int upper_tiles(int64_t d, int2** out, int* count, int tn = kTN) {
   static std::mutex mu;
   static std::vector<std::pair<int64_t, std::pair<int2*, int>>> cache;
   std::lock_guard<std::mutex> lock(mu);
+  const int64_t key = d * 1024 + tn;
   for (auto& e : cache)
-    if (e.first == d) {
+    if (e.first == key) {
       *out = e.second.first;
       *count = e.second.second;
       return SIMOPT_OK;
     }
   std::vector<int2> v;
   for (int64_t bi = 0; bi * kTM < d; ++bi)
-    for (int64_t bj = 0; bj * kTN < d; ++bj)
-      if (bj * kTN + kTN - 1 >= bi * kTM) v.push_back(make_int2((int)bi, (int)bj));
+    for (int64_t bj = 0; bj * tn < d; ++bj)
+      if (bj * tn + tn - 1 >= bi * kTM) v.push_back(make_int2((int)bi, (int)bj));
   int2* tiles = nullptr;
   SIMOPT_CUDA(cudaMalloc(&tiles, v.size() * sizeof(int2)));
   SIMOPT_CUDA(cudaMemcpy(tiles, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice));
-  cache.push_back({d, {tiles, (int)v.size()}});
+  cache.push_back({key, {tiles, (int)v.size()}});
   *out = tiles;
   *count = (int)v.size();
   return SIMOPT_OK;
@@ -769,13 +1039,21 @@ extern "C" int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t
   const cuuint64_t gdim[3] = {(cuuint64_t)rs, (cuuint64_t)d, (cuuint64_t)(np / ch)};
   const cuuint64_t gstr[2] = {(cuuint64_t)rs, (cuuint64_t)(d * rs)};
   const cuuint32_t estr[3] = {1, 1, 1};
-  const cuuint32_t box_a[3] = {16, (cuuint32_t)kTM, 1}, box_b[3] = {16, (cuuint32_t)kTN, 1};
+  // SIMOPT_XTDX_TMA_BOX=16: 16-byte boxes per K half (no swizzle); default 64: one
+  // 64-byte swizzled box per operand and stage (whole 32-byte sectors, 4x fewer requests)
+  static const int sw = [] {
+    const char* e = getenv("SIMOPT_XTDX_TMA_BOX");
+    return e && atoi(e) == 16 ? 16 : 64;
+  }();
+  const cuuint32_t bw = (cuuint32_t)sw;
+  const cuuint32_t box_a[3] = {bw, (cuuint32_t)kTM, 1}, box_b[3] = {bw, (cuuint32_t)kTN, 1};
+  const CUtensorMapSwizzle swz = sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE;
   CUresult r1 = encode(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xt), gdim, gstr, box_a,
-                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   CUresult r2 = encode(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xt), gdim, gstr, box_b,
-                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   const cuuint64_t ldim[2] = {(cuuint64_t)np, (cuuint64_t)kLimbs};
   const cuuint64_t lstr[1] = {(cuuint64_t)np};
   const cuuint32_t box_l[2] = {(cuuint32_t)kTK, (cuuint32_t)kLimbs}, lestr[2] = {1, 1};
@@ -785,15 +1063,54 @@ extern "C" int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t
   SIMOPT_REQUIRE(r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS && r3 == CUDA_SUCCESS, SIMOPT_E_CUDA,
                  "tensor map encoding failed (%d, %d, %d)", (int)r1, (int)r2, (int)r3);
   const size_t smem = sizeof(TmaSmem) + 1024;
+  static const bool ts = [] {
+    const char* e = getenv("SIMOPT_XTDX_TMA_KERNEL");
+    return e && strcmp(e, "ts") == 0;
+  }();
+  if (ts) {  // limbs on the A side in TMEM (k_xtdx_ts): 128 x 80 tiles, 64-byte swizzled boxes
+    int2* tl = nullptr;
+    int ntl = 0;
+    SIMOPT_REQUIRE(upper_tiles(d, &tl, &ntl, kSN) == SIMOPT_OK, SIMOPT_E_CUDA, "%s", simopt_last_error());
+    CUtensorMap ta, tb;
+    const cuuint32_t ba[3] = {64, (cuuint32_t)kTM, 1}, bbx[3] = {64, (cuuint32_t)kSN, 1};
+    CUresult q1 = encode(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xt), gdim, gstr, ba, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult q2 = encode(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xt), gdim, gstr, bbx, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SIMOPT_REQUIRE(q1 == CUDA_SUCCESS && q2 == CUDA_SUCCESS, SIMOPT_E_CUDA, "tensor map encoding failed");
+    const size_t smem_ts = sizeof(TsSmem) + 1024;
+    static bool attr_ts = false;
+    if (!attr_ts) {
+      SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ts));
+      attr_ts = true;
+    }
+    int beta = 0;
+    for (int64_t c0 = 0; c0 < np; c0 += kChunk) {
+      const int64_t c1 = c0 + kChunk < np ? c0 + kChunk : np;
+      k_xtdx_ts<<<ntl, kST, smem_ts, st>>>(ta, tb, ml, lg, d, tl, c0, c1, 1.0 / (double)n, beta, h);
+      SIMOPT_CHECK_LAUNCH("k_xtdx_ts");
+      beta = 1;
+    }
+    return SIMOPT_OK;
+  }
+  static const bool wide = [] {
+    const char* e = getenv("SIMOPT_XTDX_TMA_WIDE");
+    return !(e && atoi(e) == 0);
+  }();
+  auto kern = sw == 64 ? (wide ? k_xtdx_tma<64, true> : k_xtdx_tma<64, false>) : k_xtdx_tma<16, false>;
   static bool attr = false;
   if (!attr) {
-    SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_tma<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_tma<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_tma<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   int beta = 0;
   for (int64_t c0 = 0; c0 < np; c0 += kChunk) {
     const int64_t c1 = c0 + kChunk < np ? c0 + kChunk : np;
-    k_xtdx_tma<<<ntiles, kQT, smem, st>>>(ma, mb, ml, lg, d, tiles, c0, c1, 1.0 / (double)n, beta, h);
+    kern<<<ntiles, kQT, smem, st>>>(ma, mb, ml, lg, d, tiles, c0, c1, 1.0 / (double)n, beta, h);
     SIMOPT_CHECK_LAUNCH("k_xtdx_tma");
     beta = 1;
   }

@@ -501,6 +501,166 @@ __global__ void __launch_bounds__(kNT) k_fused_nib(const uint64_t* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Banded nibble-table pass for d > 1024 (C5: d = 8192): the nibble tables of all of d do
+// not fit one CTA, so the pass splits into 1024-column bands (16 words) and two sweeps of
+// the bits (1/64 of the fp64 bytes each -- the sweeps are issue-bound, not HBM-bound):
+//   k_nibb_rowdot  grid (x, band): band partial row dots via the band's nibble tables
+//   k_nibb_rowfin  per row: t = sum of the band partials in band order, the epilogue
+//                  (weight, c(1-c), loss term, t) as k_fused_nib
+//   k_nibb_colsum  grid (x, band): the band's pattern accumulators A[p][c] += wt_r,
+//                  expanded to column sums per CTA (col_part[x][band columns])
+// and the usual finish kernel folds col_part over x.  ~3 instructions per element
+// against ~32 for the per-bit k_fused_bits it replaces at this width.
+constexpr int kBandW = 16;                    // words per band (1024 columns)
+constexpr int kBandWS = kBandW + 1;           // padded tile row stride (u64 words)
+
+__device__ __forceinline__ void nibb_fetch(uint64_t (&pf)[kBandW], const uint64_t* __restrict__ bits,
+                                           int64_t N, int64_t W, int64_t w0, int64_t tl,
+                                           int64_t ntiles) {
+  const int64_t rb = tl * kNT;
+  const int64_t nr = tl < ntiles ? (N - rb < kNT ? N - rb : kNT) : 0;
+#pragma unroll
+  for (int k = 0; k < kBandW; ++k) {
+    const int e = threadIdx.x + k * kNT, rr = e >> 4, ww = e & 15;
+    pf[k] = (rr < nr && w0 + ww < W) ? __ldg(bits + (rb + rr) * W + w0 + ww) : 0ULL;
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k_nibb_rowdot(const uint64_t* __restrict__ bits, int64_t N,
+                                                     int64_t d, int64_t W,
+                                                     const double* __restrict__ v,
+                                                     double* __restrict__ part) {
+  extern __shared__ __align__(16) double dsm[];
+  double* T = dsm;                                            // [16 words][16 groups][16]
+  uint64_t* tb = reinterpret_cast<uint64_t*>(T + kBandW * 256);  // [kNT][kBandWS]
+  const int tid = threadIdx.x, band = blockIdx.y;
+  const int64_t w0 = (int64_t)band * kBandW;
+  for (int e = tid; e < kBandW * 256; e += kNT) {
+    const int c = e >> 4, p = e & 15;  // group c of the band: columns 64 w0 + 4c ..
+    double t = 0.0;
+    for (int b = 0; b < 4; ++b) {
+      const int64_t j = 64 * w0 + 4 * c + b;
+      if (((p >> b) & 1) && j < d) t += v[j];
+    }
+    T[e] = t;
+  }
+  const int64_t ntiles = (N + kNT - 1) / kNT;
+  uint64_t pf[kBandW];
+  nibb_fetch(pf, bits, N, W, w0, blockIdx.x, ntiles);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBandW; ++k) {
+      const int e = tid + k * kNT;
+      tb[(e >> 4) * kBandWS + (e & 15)] = pf[k];
+    }
+    nibb_fetch(pf, bits, N, W, w0, tile + gridDim.x, ntiles);
+    __syncthreads();
+    const int64_t r = tile * kNT + tid;
+    const uint64_t* row = tb + tid * kBandWS;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 4
+    for (int ww = 0; ww < kBandW; ++ww) {
+      const uint64_t m = row[ww];
+      const double* Tw = T + 256 * ww;
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) {
+        s0 += Tw[16 * i + (int)((m >> (4 * i)) & 15ULL)];
+        s1 += Tw[16 * (i + 1) + (int)((m >> (4 * i + 4)) & 15ULL)];
+        s2 += Tw[16 * (i + 2) + (int)((m >> (4 * i + 8)) & 15ULL)];
+        s3 += Tw[16 * (i + 3) + (int)((m >> (4 * i + 12)) & 15ULL)];
+      }
+    }
+    if (r < N) part[(int64_t)band * N + r] = (s0 + s1) + (s2 + s3);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kNT) k_nibb_rowfin(const double* __restrict__ part, int64_t N,
+                                                     int nb, const double* __restrict__ rowaux,
+                                                     double* __restrict__ wt_out,
+                                                     double* __restrict__ t_out,
+                                                     double* __restrict__ dw_out,
+                                                     double* __restrict__ scal_part) {
+  __shared__ double red[kNT / 32];
+  double sc = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)kNT + threadIdx.x; r < N; r += (int64_t)gridDim.x * kNT) {
+    double t = 0.0;
+    for (int b = 0; b < nb; ++b) t += part[(int64_t)b * N + r];
+    double wt;
+    if (MODE == SIMOPT_FUSED_LR_GRAD) {
+      const double z = rowaux[r];
+      const double c = dev_sigmoid(t);
+      wt = c - z;
+      if (dw_out) dw_out[r] = c * (1.0 - c);
+      sc += glibc_logistic_loss_term(t, z, simopt_exptab_dev);
+    } else {
+      wt = rowaux[r] * t;
+    }
+    if (t_out) t_out[r] = t;
+    wt_out[r] = wt;
+  }
+  const int lane = threadIdx.x & 31;
+  for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+  if (lane == 0) red[threadIdx.x >> 5] = sc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double p = 0.0;
+    for (int q = 0; q < kNT / 32; ++q) p += red[q];
+    scal_part[blockIdx.x] = p;
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k_nibb_colsum(const uint64_t* __restrict__ bits, int64_t N,
+                                                     int64_t d, int64_t W,
+                                                     const double* __restrict__ wt,
+                                                     double* __restrict__ col_part) {
+  extern __shared__ __align__(16) double dsm[];
+  double* A = dsm;                                           // [16][kNT]
+  double* wts = A + 16 * kNT;                                // [kNT]
+  uint64_t* tb = reinterpret_cast<uint64_t*>(wts + kNT);     // [kNT][kBandWS]
+  const int tid = threadIdx.x, band = blockIdx.y;
+  const int64_t w0 = (int64_t)band * kBandW;
+  for (int e = tid; e < 16 * kNT; e += kNT) A[e] = 0.0;
+  const int64_t ntiles = (N + kNT - 1) / kNT;
+  uint64_t pf[kBandW];
+  nibb_fetch(pf, bits, N, W, w0, blockIdx.x, ntiles);
+  const int word = tid >> 4, sh = 4 * (tid & 15);  // this thread's group: 4 columns
+  double* Ac = A + tid;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kNT;
+    const int nrow = (int)(N - r0 < kNT ? N - r0 : kNT);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBandW; ++k) {
+      const int e = tid + k * kNT;
+      tb[(e >> 4) * kBandWS + (e & 15)] = pf[k];
+    }
+    wts[tid] = tid < nrow ? wt[r0 + tid] : 0.0;
+    nibb_fetch(pf, bits, N, W, w0, tile + gridDim.x, ntiles);
+    __syncthreads();
+    for (int i = 0; i < nrow; ++i) {
+      const int p = (int)((tb[i * kBandWS + word] >> sh) & 15ULL);
+      Ac[p * kNT] += wts[i];
+    }
+  }
+  __syncthreads();
+  double col[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int p = 1; p < 16; ++p) {
+    const double ap = A[p * kNT + tid];
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if ((p >> b) & 1) col[b] += ap;
+  }
+  double* out = col_part + blockIdx.x * d;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int64_t j = 64 * w0 + 4 * tid + b;
+    if (j < d) out[j] = col[b];
+  }
+}
+
 using BitsFn = void (*)(const uint64_t*, int64_t, int64_t, int64_t, int, const double*,
                         const double*, double*, double*, double*, double*, int);
 
@@ -780,6 +940,43 @@ extern "C" int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bi
     return finish(st, nullptr, nullptr, 0, cols, col_scale, nullptr,
                   (accumulate && cols) ? col_out : nullptr, scalar_out, peer);
   const int64_t W = ceil_div(cols, 64);
+  if (ceil_div(cols, 4) > kMaxNibG) {  // banded nibble-table sweeps (d > 1024)
+    const int nb = (int)ceil_div(W, kBandW);
+    const size_t smem_r = (size_t)(kBandW * 256) * sizeof(double) + (size_t)kNT * kBandWS * 8;
+    const size_t smem_c = (size_t)(17 * kNT) * sizeof(double) + (size_t)kNT * kBandWS * 8;
+    static int gx = 0;
+    if (!gx) {
+      SIMOPT_CUDA(cudaFuncSetAttribute(k_nibb_rowdot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
+      SIMOPT_CUDA(cudaFuncSetAttribute(k_nibb_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nibb_colsum, kNT, smem_c) != cudaSuccess ||
+          per_sm < 1)
+        per_sm = 1;
+      gx = per_sm * SIMOPT_NUM_SMS;
+    }
+    const int gxb = (int)(gx / nb > 0 ? gx / nb : 1);   // x-blocks per band: one resident wave
+    const int acc = (accumulate && col_out) ? 1 : 0;
+    // scratch: band partials [nb][N] | row weights [N] | col_part [gxb][cols] | scal [gxb]
+    double* part = static_cast<double*>(
+        simopt_scratch(st, ((int64_t)nb * rows + rows + (int64_t)gxb * cols + gxb) * sizeof(double)));
+    SIMOPT_REQUIRE(part != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
+    double* wbuf = part + (int64_t)nb * rows;
+    double* cpart = wbuf + rows;
+    double* spart = cpart + (int64_t)gxb * cols;
+    k_nibb_rowdot<<<dim3((unsigned)gxb, (unsigned)nb), kNT, smem_r, st>>>(bits, rows, cols, W, v, part);
+    SIMOPT_CHECK_LAUNCH("k_nibb_rowdot");
+    if (mode == SIMOPT_FUSED_LR_GRAD)
+      k_nibb_rowfin<SIMOPT_FUSED_LR_GRAD><<<gxb, kNT, 0, st>>>(part, rows, nb, rowaux, wbuf, t_out, dw_out, spart);
+    else
+      k_nibb_rowfin<SIMOPT_FUSED_LR_HVP><<<gxb, kNT, 0, st>>>(part, rows, nb, rowaux, wbuf, t_out, nullptr, spart);
+    SIMOPT_CHECK_LAUNCH("k_nibb_rowfin");
+    if (acc) {
+      k_nibb_colsum<<<dim3((unsigned)gxb, (unsigned)nb), kNT, smem_c, st>>>(bits, rows, cols, W, wbuf, cpart);
+      SIMOPT_CHECK_LAUNCH("k_nibb_colsum");
+    }
+    return finish(st, cpart, spart, gxb, cols, raw ? 1.0 : col_scale, nullptr, acc ? col_out : nullptr,
+                  scalar_out, peer);
+  }
   int tpr = 1;
   while (tpr < W) tpr <<= 1;
   int K = 1;

@@ -77,8 +77,10 @@ def test_matvec_bits_gather_and_transpose_exact(pkg, d, n, chunk, gather):
     assert np.array_equal(np.signbit(got), np.signbit(want))
 
 
-@pytest.mark.parametrize("d,n", [(1000, 5000), (8192, 300), (130, 999), (5, 64)])
+@pytest.mark.parametrize("d,n", [(1000, 5000), (8192, 300), (130, 999), (5, 64), (2000, 3001),
+                                 (1100, 700), (8192, 20_000)])
 def test_fused_bits_vs_dense(pkg, d, n):
+    """Nibble-table pass (d <= 1024) and the banded two-sweep pass (d > 1024)."""
     from paper_2404_11631_b200.fused import LR_GRAD, LR_HVP, fused_rows_bits
     from paper_2404_11631_b200.sampling import synth_classification
     data = synth_classification(d, pkg.RngStream(9, 0), n_rows=n, packed=True)

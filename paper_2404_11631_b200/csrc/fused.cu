@@ -261,110 +261,9 @@ __global__ void __launch_bounds__(256) k_fused_finish(const double* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// Same pass on bit-packed binary features (csrc/bits.cu layout, W = ceil(d/64) words
-// per row).  Row-dot phase: TPR = pow2 >= W threads per row, one word each, adding
-// v_j (shared memory) over the word's set bits; the row's words are reduced in
-// thread order.  Accumulate phase: thread owns columns tid + k*256 (registers) and
-// adds wt_r for each tile row whose bit is set (tile bits staged in shared memory).
-// One pass reads N*W*8 bytes: 1/64 of the fp64 layout, so the pass is issue-bound.
-template <int MODE, int K>
-__global__ void __launch_bounds__(kNT) k_fused_bits(const uint64_t* __restrict__ bits, int64_t N,
-                                                    int64_t d, int64_t W, int tpr,
-                                                    const double* __restrict__ v,
-                                                    const double* __restrict__ rowaux,
-                                                    double* __restrict__ t_out,
-                                                    double* __restrict__ dw_out,
-                                                    double* __restrict__ col_part,
-                                                    double* __restrict__ scal_part, int accumulate) {
-  extern __shared__ __align__(16) double vsh[];      // [64*W] v, zero padded
-  __shared__ uint64_t tb[kNT];                       // tile bits [R][tpr]
-  __shared__ double red[kNT / 32];
-  __shared__ double wts[kNT];
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (int64_t j = tid; j < 64 * W; j += kNT) vsh[j] = j < d ? v[j] : 0.0;
-  __syncthreads();
-  const int R = kNT / tpr;
-  const int r_loc = tid / tpr, w = tid - r_loc * tpr;
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  double sc = 0.0;
-  const int64_t ntiles = (N + R - 1) / R;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r = tile * R + r_loc;
-    const uint64_t m0 = (r < N && w < W) ? __ldg(bits + r * W + w) : 0ULL;
-    __syncthreads();  // previous tile's tb / wts fully consumed
-    tb[tid] = m0;
-    double s = 0.0;
-    uint64_t m = m0;
-    const double* vw = vsh + 64 * w;
-    while (m) {
-      const int b = __ffsll((long long)m) - 1;
-      s += vw[b];
-      m &= m - 1;
-    }
-    // reduce the tpr word partials of each row, in word order
-    if (tpr <= 32) {
-      for (int o = 1; o < tpr; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    } else {
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) red[tid >> 5] = s;
-      __syncthreads();
-      if (w == 0) {
-        s = 0.0;
-        for (int q = 0; q < tpr / 32; ++q) s += red[(tid >> 5) + q];
-      }
-    }
-    if (w == 0) {
-      double wt = 0.0;
-      if (r < N) {
-        const double t = s;
-        if (MODE == SIMOPT_FUSED_LR_GRAD) {
-          const double z = rowaux[r];
-          const double c = dev_sigmoid(t);
-          wt = c - z;
-          if (dw_out) dw_out[r] = c * (1.0 - c);
-          sc += glibc_logistic_loss_term(t, z, simopt_exptab_dev);
-        } else {
-          wt = rowaux[r] * t;
-        }
-        if (t_out) t_out[r] = t;
-      }
-      wts[r_loc] = wt;
-    }
-    __syncthreads();
-    if (accumulate) {
-      for (int i = 0; i < R; ++i) {
-        const double wt = wts[i];
-        const uint64_t* rb = tb + i * tpr;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int j = tid + k * kNT;
-          if (j < d && ((rb[j >> 6] >> (j & 63)) & 1ULL)) acc[k] += wt;
-        }
-      }
-    }
-  }
-  if (accumulate) {
-    double* out = col_part + blockIdx.x * d;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int j = tid + k * kNT;
-      if (j < d) out[j] = acc[k];
-    }
-  }
-  // scalar side sum (held by the w == 0 threads), reduced in thread order
-  for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-  __syncthreads();
-  if (lane == 0) red[tid >> 5] = sc;
-  __syncthreads();
-  if (tid == 0) {
-    double p = 0.0;
-    for (int q = 0; q < kNT / 32; ++q) p += red[q];
-    scal_part[blockIdx.x] = p;
-  }
-}
-
+// The same pass on bit-packed binary features (csrc/bits.cu layout, W = ceil(d/64)
+// words per row): one read of N*W*8 bytes, 1/64 of the fp64 layout, so the pass is
+// issue-bound and the work per element is what matters.
 // Nibble-table variant for d <= 1024 (G = ceil(d/4) <= 256 four-column groups), one
 // tile row per thread:
 //   row dot     t_r = sum over the row's nibbles of T[c][p], T[c][p] = sum of v over the
@@ -511,7 +410,7 @@ __global__ void __launch_bounds__(kNT) k_fused_nib(const uint64_t* __restrict__ 
 //   k_nibb_colsum  grid (x, band): the band's pattern accumulators A[p][c] += wt_r,
 //                  expanded to column sums per CTA (col_part[x][band columns])
 // and the usual finish kernel folds col_part over x.  ~3 instructions per element
-// against ~32 for the per-bit k_fused_bits it replaces at this width.
+// against ~32 for a per-bit walk (the earlier kernel at this width, 13x slower).
 constexpr int kBandW = 16;                    // words per band (1024 columns)
 constexpr int kBandWS = kBandW + 1;           // padded tile row stride (u64 words)
 
@@ -663,19 +562,6 @@ __global__ void __launch_bounds__(kNT) k_nibb_colsum(const uint64_t* __restrict_
 
 using BitsFn = void (*)(const uint64_t*, int64_t, int64_t, int64_t, int, const double*,
                         const double*, double*, double*, double*, double*, int);
-
-template <int MODE>
-BitsFn pick_bits_k(int K) {
-  switch (K) {
-    case 1: return k_fused_bits<MODE, 1>;
-    case 2: return k_fused_bits<MODE, 2>;
-    case 4: return k_fused_bits<MODE, 4>;
-    case 8: return k_fused_bits<MODE, 8>;
-    case 16: return k_fused_bits<MODE, 16>;
-    case 32: return k_fused_bits<MODE, 32>;
-    default: return k_fused_bits<MODE, 64>;
-  }
-}
 
 // Cross-rank finish over peer memory (SimoptPeerReduce).  kFB blocks, all resident, so
 // the spin waits cannot starve a block another rank waits for.
@@ -977,18 +863,10 @@ extern "C" int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bi
     return finish(st, cpart, spart, gxb, cols, raw ? 1.0 : col_scale, nullptr, acc ? col_out : nullptr,
                   scalar_out, peer);
   }
-  int tpr = 1;
-  while (tpr < W) tpr <<= 1;
-  int K = 1;
-  while ((int64_t)K * kNT < cols) K <<= 1;
-  const bool nib = ceil_div(cols, 4) <= kMaxNibG;
-  BitsFn fn = nib ? (mode == SIMOPT_FUSED_LR_GRAD ? k_fused_nib<SIMOPT_FUSED_LR_GRAD>
-                                                  : k_fused_nib<SIMOPT_FUSED_LR_HVP>)
-                  : (mode == SIMOPT_FUSED_LR_GRAD ? pick_bits_k<SIMOPT_FUSED_LR_GRAD>(K)
-                                                  : pick_bits_k<SIMOPT_FUSED_LR_HVP>(K));
+  BitsFn fn = mode == SIMOPT_FUSED_LR_GRAD ? k_fused_nib<SIMOPT_FUSED_LR_GRAD>
+                                           : k_fused_nib<SIMOPT_FUSED_LR_HVP>;
   const int64_t G = ceil_div(cols, 4), Gp = (G + 31) & ~31LL;
-  const size_t smem = nib ? (size_t)(16 * 16 * W + 16 * Gp + kNT + kNT * (W + 1)) * sizeof(double)
-                          : (size_t)64 * W * sizeof(double);
+  const size_t smem = (size_t)(16 * 16 * W + 16 * Gp + kNT + kNT * (W + 1)) * sizeof(double);
   static std::mutex mu;
   static std::vector<std::pair<std::pair<BitsFn, int64_t>, int>> grids;  // (fn, W) -> grid
   int grid = 0;
@@ -1009,10 +887,10 @@ extern "C" int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bi
   double* part = static_cast<double*>(simopt_scratch(st, ((int64_t)grid * cols + grid) * sizeof(double)));
   SIMOPT_REQUIRE(part != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
   const int acc = (accumulate && col_out) ? 1 : 0;
-  fn<<<grid, kNT, smem, st>>>(bits, rows, cols, W, tpr, v, rowaux, t_out,
+  fn<<<grid, kNT, smem, st>>>(bits, rows, cols, W, 0, v, rowaux, t_out,
                               mode == SIMOPT_FUSED_LR_GRAD ? dw_out : nullptr, part,
                               part + (int64_t)grid * cols, acc);
-  SIMOPT_CHECK_LAUNCH("k_fused_bits");
+  SIMOPT_CHECK_LAUNCH("k_fused_nib");
   return finish(st, part, part + (int64_t)grid * cols, grid, cols, raw ? 1.0 : col_scale, nullptr,
                 acc ? col_out : nullptr, scalar_out, peer);
 }

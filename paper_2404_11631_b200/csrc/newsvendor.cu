@@ -157,7 +157,11 @@ __device__ __noinline__ int nv_resolve(NvStreamPos sp, int64_t i, double mu, dou
   return (dv <= x) ? 1 : 0;
 }
 
-constexpr int kQueue = 256;  // ambiguous draws buffered per warp (>= one batch: 32 lanes x 8)
+#ifndef NV_KEY_BATCH
+#define NV_KEY_BATCH 8
+#endif
+constexpr int kBatch = NV_KEY_BATCH;  // window keys per lane per round (loads in flight)
+constexpr int kQueue = 32 * kBatch;   // ambiguous draws buffered per warp (>= one round)
 
 // Lanes scan segments and count certain-below draws; ambiguous draws are queued in
 // shared memory and then resolved with the exact glibc Box-Muller, one per lane.
@@ -190,19 +194,19 @@ __device__ __forceinline__ int64_t nv_count_warp(const uint32_t* __restrict__ ke
       base = j * S + e0;
       c = start;
     }
-    // walk the window buckets in lock-step batches of 8 keys per lane (all loads of a
+    // walk the window buckets in lock-step batches of kBatch keys per lane (all loads of a
     // batch in flight together); ambiguous draws are queued warp-wide
     const int span = end - start;
     int maxspan = span;
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) maxspan = max(maxspan, __shfl_xor_sync(0xffffffffu, maxspan, o2));
-    for (int p0 = 0; p0 < maxspan; p0 += 8) {
-      uint32_t kv[8];
+    for (int p0 = 0; p0 < maxspan; p0 += kBatch) {
+      uint32_t kv[kBatch];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) kv[k] = (p0 + k < span) ? seg[start + p0 + k] : 0u;
+      for (int k = 0; k < kBatch; ++k) kv[k] = (p0 + k < span) ? seg[start + p0 + k] : 0u;
       unsigned amb = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < kBatch; ++k) {
         if (p0 + k < span) {
           const int cls = nv_classify(kv[k] >> 12, w);
           c += (cls < 0) ? 1 : 0;
@@ -220,7 +224,7 @@ __device__ __forceinline__ int64_t nv_count_warp(const uint32_t* __restrict__ ke
       if (total) {
         if (nq + total > kQueue) drain();
         int pos = nq + pre - na;
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < kBatch; ++k)
           if (amb & (1u << k)) queue[pos++] = base + (int64_t)(kv[k] & 4095u);
         __syncwarp();
         nq += total;

@@ -271,7 +271,18 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-__device__ __noinline__ void nv_peer_exchange(const NvIterArgs& a, ArgMin r, double sval, NvState* st) {
+// The fields of NvIterArgs the exchange needs, by value: taking the address of the kernel
+// parameter block (a reference into a noinline call) made every thread copy it to the
+// stack at kernel entry.
+struct NvPeerArgs {
+  double* const* peer_mb;
+  int64_t world, rank, j0, d, grad_step;
+  uint64_t seq;
+  uint64_t* seq_ptr;
+  int* flags;
+};
+
+__device__ __noinline__ void nv_peer_exchange(const NvPeerArgs a, ArgMin r, double sval, NvState* st) {
   uint64_t seq = a.seq;
   if (a.seq_ptr) {  // device-resident sequence (graph replay): this exchange's number
     seq = *a.seq_ptr + 1;
@@ -398,7 +409,9 @@ __global__ void __launch_bounds__(kIterWarps * 32, 3)
       st->sval = sval;
       st->best_val = r.v;
     } else {
-      nv_peer_exchange(a, r, sval, st);
+      nv_peer_exchange(NvPeerArgs{a.peer_mb, a.world, a.rank, a.j0, a.d, a.grad_step, a.seq,
+                                  a.seq_ptr, a.flags},
+                       r, sval, st);
     }
   }
 }

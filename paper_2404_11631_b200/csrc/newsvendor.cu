@@ -247,7 +247,10 @@ __device__ __forceinline__ double nv_grad_value(int64_t cnt, int64_t S, double k
 
 namespace {
 
-constexpr int kIterWarps = 8;
+#ifndef NV_ITER_WARPS
+#define NV_ITER_WARPS 8
+#endif
+constexpr int kIterWarps = NV_ITER_WARPS;  // products (warps) per step block
 
 // Fused product-shard LMO exchange over NVLink peer memory (one thread of the step's
 // last block): publish (value, global index, vertex value) into slot `rank` of every
@@ -331,7 +334,7 @@ __device__ __noinline__ void nv_peer_exchange(const NvPeerArgs a, ArgMin r, doub
 //       previous LMO (frank_wolfe.py:69-82), record x_j < -FEAS_TOL, objective term;
 //   (2) if do_grad: g_j at the (new) x_j, LMO values g_j * (C / c_j), argmin over all
 //       products (last-block reduction), NaN flag.
-__global__ void __launch_bounds__(kIterWarps * 32, 3)
+__global__ void __launch_bounds__(kIterWarps * 32, 24 / kIterWarps)
     k_nv_iter(NvIterArgs a) {
   __shared__ ArgMin warp_best[kIterWarps];
   __shared__ int64_t queues[kIterWarps][kQueue];

@@ -67,18 +67,61 @@ def dist_setup(n, backend="nccl"):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling of SM clock + throttle reasons during the timed region."""
+    """SM clock + throttle reasons sampled every 10 ms during the timed region.
+
+    NVML (pynvml) is initialised before the region so the first sample lands at its
+    start; a sample is also taken on entry and on exit, so even a short region has
+    readings.  Falls back to `nvidia-smi -lms` when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits: hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown,
+    # sw_power_cap (the order of Q's reason columns)
+    BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, index=0):
         self.index = index
         self.rows = []
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            try:
+                import torch
+                nidx = torch.cuda._get_nvml_device_index(index)
+            except Exception:  # noqa: BLE001 -- older torch: the visible index
+                nidx = index
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(nidx)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.nvml = pynvml
+        except Exception:  # noqa: BLE001 -- no NVML: nvidia-smi below
+            self.nvml = None
+
+    def _sample_nvml(self):
+        nv = self.nvml
+        sm = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        bits = int(fn(self.handle))
+        self.rows.append([str(sm), str(self.max_sm)] +
+                         ["Active" if bits & b else "Not Active" for b in self.BITS])
+
+    def _poll(self):
+        while not self.stop.wait(0.01):
+            try:
+                self._sample_nvml()
+            except Exception:  # noqa: BLE001
+                return
 
     def __enter__(self):
+        if self.nvml is not None:
+            self._sample_nvml()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -97,6 +140,13 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join(timeout=1)
+            try:
+                self._sample_nvml()
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
@@ -109,7 +159,8 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def peaks():

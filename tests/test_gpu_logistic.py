@@ -105,3 +105,40 @@ def test_full_gradient_hvp_vs_oracle(pkg, packed):
     assert np.array_equal(T.logistic_gradient(w, data, None, b), orc.logistic_gradient(w, x, z))
     assert np.array_equal(T.logistic_hvp(w, v, data, None, b), orc.logistic_hvp(w, v, x, z))
     assert T.logistic_loss(w, data, None, b) == orc.logistic_loss(w, x, z)
+
+
+@pytest.mark.parametrize("packed", [False, True])
+def test_sqn_graph_equals_eager_with_warnings(pkg, packed):
+    """Graph and eager iterations give the same trace, iterate and warnings on a
+    configuration with pair iterations every 3 steps and 2-sample HVP batches."""
+    from paper_2404_11631_b200.sampling import synth_classification
+    from paper_2404_11631_b200.sqn import SqnConfig, sqn_run
+    from paper_2404_11631_b200.tasks import LogisticTask
+    b = pkg.make_backend("cuda")
+    data = synth_classification(24, pkg.RngStream(11, 0), packed=packed)
+    recs = [sqn_run(LogisticTask(data), SqnConfig(3, 3, 0.5, 5, 2, 40, pkg.RngStream(11, 2)), b, graph=g)
+            for g in (True, False)]
+    assert np.array_equal(recs[0].objectives, recs[1].objectives)
+    assert np.array_equal(recs[0].final_iterate, recs[1].final_iterate)
+    assert recs[0].warnings == recs[1].warnings
+
+
+def test_sqn_abort_path_graph_equals_eager(pkg):
+    """A 1-sample HVP batch eventually yields a pair whose y.y underflows to zero: the
+    reference's hessian_update raises DegeneratePair (sqn.py:94-95) and sqn_run turns it
+    into RunAborted with the partial trace (sqn.py:186-193).  Both iteration modes must
+    stop at the same iteration with the same partial record."""
+    from paper_2404_11631_b200.sampling import synth_classification
+    from paper_2404_11631_b200.sqn import SqnConfig, sqn_run
+    from paper_2404_11631_b200.tasks import LogisticTask
+    b = pkg.make_backend("cuda")
+    data = synth_classification(24, pkg.RngStream(11, 0))
+    parts = []
+    for g in (True, False):
+        with pytest.raises(pkg.RunAborted) as ei:
+            sqn_run(LogisticTask(data), SqnConfig(2, 3, 0.5, 5, 1, 40, pkg.RngStream(11, 2)), b, graph=g)
+        assert isinstance(ei.value.__cause__, pkg.DegeneratePair)
+        parts.append(ei.value.partial_record)
+    assert len(parts[0].objectives) == len(parts[1].objectives) > 0
+    assert np.array_equal(parts[0].objectives, parts[1].objectives)
+    assert np.array_equal(parts[0].final_iterate, parts[1].final_iterate)

@@ -317,10 +317,12 @@ int simopt_fisher_yates_host(int64_t n, int64_t b, const double* u, int64_t* out
  * *status |= INVALID_GRADIENT), w_out = (gamma * ((-1 * w_in) + s)) + w_in with *gamma
  * read on the device, *wmin_out = min(w_out), and the fixed-tree *wsum_out = sum(w_out),
  * *lin_out = dot(w_out, mean) (frank_wolfe.py:106-117, lmo.py:56-65, backend.py:80-111);
- * bitwise equal to the separate lmo / axpy / axpy_ptr / min / dot / vec_sum calls. */
+ * bitwise equal to the separate lmo / axpy / axpy_ptr / min / dot / vec_sum calls.
+ * exact == 0 (fused mode): the two sums are block-parallel in a fixed order instead
+ * (deterministic, not the reference tree; the update and min stay bitwise). */
 int simopt_mv_fw_tail(void* stream, const double* g, const double* w_in, const double* gamma,
                       const double* mean, int64_t d, int64_t chunk, double* w_out, int* status,
-                      double* wmin_out, double* wsum_out, double* lin_out);
+                      double* wmin_out, double* wsum_out, double* lin_out, int exact);
 
 /* ------------------------------------------------------------ projections (projected SGD) */
 /* Euclidean projection of y onto {x >= 0, c . x <= budget} (c == NULL: all ones, i.e.

@@ -135,9 +135,11 @@ __global__ void __launch_bounds__(kTailThreads)
                  const double* __restrict__ gamma, const double* __restrict__ mean, int64_t d,
                  int64_t chunk, double* __restrict__ w_out, int* __restrict__ status,
                  double* __restrict__ wmin_out, double* __restrict__ wsum_out,
-                 double* __restrict__ lin_out, double* __restrict__ part, bool use_smem) {
+                 double* __restrict__ lin_out, double* __restrict__ part, bool use_smem,
+                 bool exact) {
   __shared__ ArgMin wb[kTailThreads / 32];
   __shared__ double wm[kTailThreads / 32];
+  __shared__ double rs[kTailThreads / 32], rd[kTailThreads / 32];  // fast-mode warp sums
   __shared__ int nan_seen;
   __shared__ int64_t jstar_sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -164,17 +166,30 @@ __global__ void __launch_bounds__(kTailThreads)
   extern __shared__ double tail_sm[];  // [d] w_out, [d] mean when they fit (chains read smem)
   const bool in_smem = use_smem;
   double m = INFINITY;
+  double ps = 0.0, pd = 0.0;  // fast mode: this thread's strided share of sum(w'), dot(w', mean)
   for (int64_t i = tid; i < d; i += kTailThreads) {
     const double wi = w_in[i];
     const double si = (i == js) ? 1.0 : 0.0;
     const double dir = -1.0 * wi + si;
     const double wo = gm * dir + wi;
     w_out[i] = wo;
-    if (in_smem) {
+    if (!exact) {
+      ps += wo;
+      pd += wo * mean[i];
+    } else if (in_smem) {
       tail_sm[i] = wo;
       tail_sm[d + i] = mean[i];
     }
     m = (wo < m || wo != wo) ? wo : m;
+  }
+  if (!exact) {
+    // fused (tolerance) mode: block-parallel sums in a fixed order -- deterministic run to
+    // run, not the reference tree; the 1000-long sequential chains are 8 us at C1's d
+    for (int o = 16; o > 0; o >>= 1) {
+      ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      pd += __shfl_xor_sync(0xffffffffu, pd, o);
+    }
+    if (lane == 0) { rs[warp] = ps; rd[warp] = pd; }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const double t = __shfl_xor_sync(0xffffffffu, m, o);
@@ -185,6 +200,18 @@ __global__ void __launch_bounds__(kTailThreads)
   if (tid == 0) {
     for (int w = 1; w < kTailThreads / 32; ++w) m = (wm[w] < m || wm[w] != wm[w]) ? wm[w] : m;
     *wmin_out = (wm[0] != wm[0]) ? wm[0] : m;
+  }
+  if (!exact) {
+    if (tid == 0) {
+      double a = 0.0, b2 = 0.0;
+      for (int w = 0; w < kTailThreads / 32; ++w) {
+        a += rs[w];
+        b2 += rd[w];
+      }
+      *wsum_out = a;
+      *lin_out = b2;
+    }
+    return;
   }
   if (!in_smem) return;  // large d: the host wrapper runs the exact sums as a tree kernel
   // exact chains: threads [0, nch) sum(w'), threads [nch, 2 nch) dot(w', mean)
@@ -215,7 +242,7 @@ __global__ void __launch_bounds__(kTailThreads)
 extern "C" int simopt_mv_fw_tail(void* stream, const double* g, const double* w_in,
                                  const double* gamma, const double* mean, int64_t d, int64_t chunk,
                                  double* w_out, int* status, double* wmin_out, double* wsum_out,
-                                 double* lin_out) {
+                                 double* lin_out, int exact) {
   SIMOPT_REQUIRE(d >= 1, SIMOPT_E_DIMENSION, "empty gradient");
   SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1");
   const int64_t nch = ceil_div(d, chunk);
@@ -223,8 +250,8 @@ extern "C" int simopt_mv_fw_tail(void* stream, const double* g, const double* w_
   cudaStream_t st = as_stream(stream);
   double* part = static_cast<double*>(simopt_scratch(st, 2 * nch * sizeof(double)));
   SIMOPT_REQUIRE(part != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
-  const size_t smem = (size_t)2 * d * sizeof(double);
-  const bool use_smem = smem <= 96 * 1024;
+  const size_t smem = exact ? (size_t)2 * d * sizeof(double) : 0;
+  const bool use_smem = exact && smem <= 96 * 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_mv_fw_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
@@ -232,8 +259,9 @@ extern "C" int simopt_mv_fw_tail(void* stream, const double* g, const double* w_
   }
   k_mv_fw_tail<<<1, kTailThreads, use_smem ? smem : 0, st>>>(g, w_in, gamma, mean, d, chunk, w_out,
                                                              status, wmin_out, wsum_out, lin_out,
-                                                             part, use_smem);
+                                                             part, use_smem, exact != 0);
   SIMOPT_CHECK_LAUNCH("k_mv_fw_tail");
+  if (!exact) return SIMOPT_OK;
   // vectors too large for one block's shared memory: the exact sums as a warp-per-chunk
   // tree kernel (one chain per 4096-chunk in a single block would wait on L2 per batch)
   if (!use_smem)

@@ -1049,7 +1049,7 @@ class MvFwEngine:
         _lib.check(self.lib.simopt_mv_fw_tail(sp, P(self.g), P(w_in), P(self.gamma[m:]), P(mean),
                                               self.prob.dimension, self.chunk, P(w_out),
                                               P(self.status[m:]), P(self.wmin[m:]), P(self.wsum[m:]),
-                                              P(self.lin[m:])))
+                                              P(self.lin[m:]), 0 if self.prob.fused else 1))
 
     def _sharded_steps(self, ws, x, mean, n_k, inv):
         """Row-sharded step: exact mode gathers chunk partials (bit-identical to one

@@ -21,7 +21,6 @@
 // by ldmatrix (48-byte padded rows: conflict-free), the limb applied to the B fragment
 // with two integer ops per 4 samples: (b * 255) & L.
 #include <stdlib.h>
-#include <string.h>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -678,181 +677,6 @@ __global__ void __launch_bounds__(kQT, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr));
 }
 
-// ---------------------------------------------------------------------------------------
-// TMA-fed tcgen05 version with the limbs on the A side (k_xtdx_ts): the 128 x 80 tile's
-// five accumulators take 400 TMEM columns; the five limb-scaled copies of A for a K step
-// (5 x 8 columns) are written straight into TMEM by the four A warps (tcgen05.st, one
-// row per thread: (x * 255) & L_k on 32-bit words) in two alternating 40-column slots,
-// and every MMA reads A from TMEM and the raw 0/1 B rows from shared memory as TMA left
-// them (64-byte swizzled boxes).  Shared memory then carries only the TMA writes, one
-// read of A and the MMAs' B reads -- about 45% of the expanded-B design's traffic, which
-// made k_xtdx_tma shared-memory-bandwidth bound.
-constexpr int kSN = 80;                       // tile columns (N of every MMA)
-constexpr int kSR = 10;                       // TMA ring depth
-constexpr int kSAcol = kLimbs * kSN;          // first A column: 400; A slot s at 400 + 40 s
-constexpr int kST = 192;                      // 4 A warps + TMA warp + MMA warp
-constexpr uint32_t kSTx = (kTM + kSN) * 64 + kLimbs * kTK;
-
-struct TsSmem {
-  uint8_t a[kSR][kTM * 64];                   // [row][64 B], 64-byte swizzle
-  uint8_t b[kSR][kSN * 64];
-  uint8_t limb[kSR][384];
-  uint64_t tma_full[kSR], done[kSR], a_full[2], a_done[2];
-  uint32_t taddr;
-};
-
-__global__ void __launch_bounds__(kST, 1)
-    k_xtdx_ts(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-              const __grid_constant__ CUtensorMap map_l, int lg_ch, int64_t d,
-              const int2* __restrict__ tiles, int64_t s0, int64_t s1, double inv_n, int beta,
-              double* __restrict__ h) {
-  extern __shared__ __align__(1024) uint8_t smraw[];
-  TsSmem& sm = *reinterpret_cast<TsSmem*>(smraw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int2 tile = tiles[blockIdx.x];
-  const int64_t i0 = (int64_t)tile.x * kTM, j0 = (int64_t)tile.y * kSN;
-  const int64_t ch = 1LL << lg_ch;
-  if (tid == 0) {
-    for (int q = 0; q < kSR; ++q) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.tma_full[q])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.done[q])));
-    }
-    for (int q = 0; q < 2; ++q) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.a_full[q])), "r"(128));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.a_done[q])));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.taddr)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t taddr = sm.taddr;
-  const uint32_t idesc = (2u << 4) | ((uint32_t)(kSN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
-  const int64_t T = (s1 - s0) / kTK;
-  if (warp < 4) {
-    // ===== A warps: row r = tid; per K step j (slot j & 1) five limb-scaled copies into TMEM =====
-    const int r = tid;
-    const uint32_t trow = taddr + ((uint32_t)(warp * 32) << 16) + (uint32_t)kSAcol;
-    for (int64_t t = 0; t < T; ++t) {
-      const int q = (int)(t % kSR);
-      mbar_wait(&sm.tma_full[q], (uint32_t)((t / kSR) & 1));
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int64_t j = 2 * t + ks;
-        const int sl = (int)(j & 1);
-        // the row's 32 samples of this K step: logical 16-byte chunks 2ks, 2ks+1
-        const int sw = (r >> 1) & 3;
-        const uint4 x0 = *reinterpret_cast<const uint4*>(&sm.a[q][r * 64 + (((2 * ks) ^ sw) * 16)]);
-        const uint4 x1 = *reinterpret_cast<const uint4*>(&sm.a[q][r * 64 + (((2 * ks + 1) ^ sw) * 16)]);
-        const uint32_t m[8] = {x0.x * 255u, x0.y * 255u, x0.z * 255u, x0.w * 255u,
-                               x1.x * 255u, x1.y * 255u, x1.z * 255u, x1.w * 255u};
-        if (j >= 2) mbar_wait(&sm.a_done[sl], (uint32_t)(((j - 2) >> 1) & 1));
-        asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-        for (int k = 0; k < kLimbs; ++k) {
-          const uint4 L0 = *reinterpret_cast<const uint4*>(&sm.limb[q][k * kTK + ks * 32]);
-          const uint4 L1 = *reinterpret_cast<const uint4*>(&sm.limb[q][k * kTK + ks * 32 + 16]);
-          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                           trow + (uint32_t)(sl * (kLimbs * 8) + k * 8)),
-                       "r"(m[0] & L0.x), "r"(m[1] & L0.y), "r"(m[2] & L0.z), "r"(m[3] & L0.w),
-                       "r"(m[4] & L1.x), "r"(m[5] & L1.y), "r"(m[6] & L1.z), "r"(m[7] & L1.w));
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.a_full[sl])) : "memory");
-      }
-    }
-  } else if (warp == 4) {
-    if (lane == 0) {  // ===== TMA issue =====
-      for (int64_t t = 0; t < T; ++t) {
-        const int q = (int)(t % kSR);
-        if (t >= kSR) mbar_wait(&sm.done[(t - kSR) % kSR], (uint32_t)(((t - kSR) / kSR) & 1));
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.tma_full[q])),
-                     "r"(kSTx) : "memory");
-        const int64_t smp = s0 + t * kTK;
-        const int blk = (int)(smp >> lg_ch), so = (int)(smp & (ch - 1));
-        tma_3d(sm.a[q], &map_a, so, (int)i0, blk, &sm.tma_full[q]);
-        tma_3d(sm.b[q], &map_b, so, (int)j0, blk, &sm.tma_full[q]);
-        tma_2d(sm.limb[q], &map_l, (int)smp, 0, &sm.tma_full[q]);
-      }
-    }
-  } else if (lane == 0) {
-    // ===== MMA issuer: per K step five MMAs (A_k from TMEM, raw B from smem) =====
-    for (int64_t t = 0; t < T; ++t) {
-      const int q = (int)(t % kSR);
-      mbar_wait(&sm.tma_full[q], (uint32_t)((t / kSR) & 1));
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int64_t j = 2 * t + ks;
-        const int sl = (int)(j & 1);
-        mbar_wait(&sm.a_full[sl], (uint32_t)((j >> 1) & 1));
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint64_t db = umma_desc_sw64(&sm.b[q][ks * 32]);
-#pragma unroll
-        for (int k = 0; k < kLimbs; ++k) {
-          const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
-                  taddr + (uint32_t)(k * kSN)),
-              "r"(taddr + (uint32_t)(kSAcol + sl * (kLimbs * 8) + k * 8)), "l"(db), "r"(idesc), "r"(acc),
-              "r"(0), "r"(0), "r"(0), "r"(0));
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(&sm.a_done[sl])));
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(&sm.done[q])));
-    }
-  }
-  if (T > 0) mbar_wait(&sm.done[(T - 1) % kSR], (uint32_t)(((T - 1) / kSR) & 1));
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp < 4) {  // epilogue: row i = i0 + 32*warp + lane, columns j0 .. j0+79
-    const int64_t i = i0 + warp * 32 + lane;
-    for (int c0 = 0; c0 < kSN; c0 += 16) {
-      double hv[16];
-#pragma unroll
-      for (int qq = 0; qq < 16; ++qq) hv[qq] = 0.0;
-#pragma unroll
-      for (int k = 0; k < kLimbs; ++k) {
-        uint32_t v[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-              "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr + ((uint32_t)(warp * 32) << 16) + (uint32_t)(k * kSN + c0)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-        const double sc = ldexp(1.0, kLimbBits * k - kFixBits) * inv_n;
-#pragma unroll
-        for (int qq = 0; qq < 16; ++qq) hv[qq] += (double)(int)v[qq] * sc;
-      }
-      if (i < d) {
-#pragma unroll
-        for (int qq = 0; qq < 16; ++qq) {
-          const int64_t jj = j0 + c0 + qq;
-          if (jj < d && i <= jj) {
-            if (beta) {
-              h[i * d + jj] += hv[qq];
-              if (i != jj) h[jj * d + i] += hv[qq];
-            } else {
-              h[i * d + jj] = hv[qq];
-              if (i != jj) h[jj * d + i] = hv[qq];
-            }
-          }
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr));
-}
-
 // out[block r/ch][j][r%ch] = bit (r, j) of the packed rows, 0 for r >= rows (16 samples
 // per thread)
 __global__ void k_bits_to_u8t(const uint64_t* __restrict__ bits, int64_t rows, int64_t d, int64_t W,
@@ -1063,38 +887,7 @@ extern "C" int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t
   SIMOPT_REQUIRE(r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS && r3 == CUDA_SUCCESS, SIMOPT_E_CUDA,
                  "tensor map encoding failed (%d, %d, %d)", (int)r1, (int)r2, (int)r3);
   const size_t smem = sizeof(TmaSmem) + 1024;
-  static const bool ts = [] {
-    const char* e = getenv("SIMOPT_XTDX_TMA_KERNEL");
-    return e && strcmp(e, "ts") == 0;
-  }();
-  if (ts) {  // limbs on the A side in TMEM (k_xtdx_ts): 128 x 80 tiles, 64-byte swizzled boxes
-    int2* tl = nullptr;
-    int ntl = 0;
-    SIMOPT_REQUIRE(upper_tiles(d, &tl, &ntl, kSN) == SIMOPT_OK, SIMOPT_E_CUDA, "%s", simopt_last_error());
-    CUtensorMap ta, tb;
-    const cuuint32_t ba[3] = {64, (cuuint32_t)kTM, 1}, bbx[3] = {64, (cuuint32_t)kSN, 1};
-    CUresult q1 = encode(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xt), gdim, gstr, ba, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    CUresult q2 = encode(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xt), gdim, gstr, bbx, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    SIMOPT_REQUIRE(q1 == CUDA_SUCCESS && q2 == CUDA_SUCCESS, SIMOPT_E_CUDA, "tensor map encoding failed");
-    const size_t smem_ts = sizeof(TsSmem) + 1024;
-    static bool attr_ts = false;
-    if (!attr_ts) {
-      SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ts));
-      attr_ts = true;
-    }
-    int beta = 0;
-    for (int64_t c0 = 0; c0 < np; c0 += kChunk) {
-      const int64_t c1 = c0 + kChunk < np ? c0 + kChunk : np;
-      k_xtdx_ts<<<ntl, kST, smem_ts, st>>>(ta, tb, ml, lg, d, tl, c0, c1, 1.0 / (double)n, beta, h);
-      SIMOPT_CHECK_LAUNCH("k_xtdx_ts");
-      beta = 1;
-    }
-    return SIMOPT_OK;
-  }
+  // SIMOPT_XTDX_TMA_WIDE=0: five N = 96 MMAs per K step instead of two N = 240 (comparison)
   static const bool wide = [] {
     const char* e = getenv("SIMOPT_XTDX_TMA_WIDE");
     return !(e && atoi(e) == 0);

@@ -414,6 +414,9 @@ int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t np, int64_t
  * sample-blocked X^T and the limb rows); same operands and result as xtdx_tc. */
 int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
                              const double* dw, uint8_t* limbs, double* h);
+/* The same on CTA pairs (cta_group::2, 256 x 96 tiles; slower on this B200, see DESIGN). */
+int simopt_logistic_xtdx_pair(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
+                              const double* dw, uint8_t* limbs, double* h);
 /* Same result on the 5th-generation tensor cores: tcgen05.mma.kind::i8 with the five limb
  * accumulators resident in TMEM (128 x 96 tiles, one CTA per SM). */
 int simopt_logistic_xtdx_tc(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,

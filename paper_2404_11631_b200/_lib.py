@@ -93,6 +93,7 @@ SIGNATURES = {
     "simopt_logistic_xtdx_i8": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_logistic_xtdx_tc": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_logistic_xtdx_tma": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
+    "simopt_logistic_xtdx_pair": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_mv_fw_tail": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32],
     "simopt_project_budget": [_vp, _vp, _vp, _d, _i64, _vp, _vp],
     "simopt_project_box": [_vp, _vp, _d, _d, _i64, _vp],

@@ -677,6 +677,223 @@ __global__ void __launch_bounds__(kQT, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr));
 }
 
+// ---------------------------------------------------------------------------------------
+// CTA-pair version (cta_group::2): a cluster of two CTAs on one TPC owns a 256 x 96 tile.
+// Each CTA TMA-loads its own 128 A rows, the 96 raw B rows and the limb rows; the
+// limb-scaled B' of each 48-column half (240 rows: 5 limbs x 48) is SPLIT between the two
+// CTAs -- rows 0..119 in CTA 0, 120..239 in CTA 1, at the same shared-memory offset -- so
+// each CTA expands and each SM's tensor core reads half of what the single-CTA kernel
+// does, which was its shared-memory bound.  The leader's single thread issues the M = 256
+// MMAs (A and B' from both CTAs' shared memory); their commits are multicast to both
+// CTAs' `done` barriers; both CTAs' expansion warps arrive on the leader's `full`
+// barrier.  Each CTA's TMEM holds its 128 accumulator rows (2 x 240 columns).
+// Measured on the C5 slice: 19.6 ms against 17.7 ms for k_xtdx_tma<64, wide> -- the pair
+// MMAs themselves run at the full 4.5 POPS (tools/micro/tc_i8_pair_rate.cu), but each
+// stage's expansion waits on the multicast completion of the MMAs kPBB stages back, and the
+// shared memory left after the TMA ring allows only 7 buffers.  Opt-in: SIMOPT_XTDX_PAIR=1.
+constexpr int kPR = 8;                   // TMA ring depth (slot/phase kept as counters)
+constexpr int kPBB = 7;                   // expanded-B' buffers
+constexpr int kPH = 120;                  // B' rows per CTA per half
+// `done` barriers are indexed by TMA slot: an expansion buffer may not outlive its slot
+static_assert(kPBB <= kPR, "expanded-B' reuse waits on the done barrier of a live TMA slot");
+struct PairSmem {
+  uint8_t a[kPR][kTM * 64];
+  uint8_t braw[kPR][kTN * 64];
+  uint8_t limb[kPR][384];
+  uint8_t b[kPBB][2][kPH * 64];
+  uint64_t tma_full[kPR], full[kPR], done[kPR], fwd[kPR];
+  uint32_t taddr;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kQT, 1)
+    k_xtdx_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                const __grid_constant__ CUtensorMap map_l, int lg_ch, int64_t d,
+                const int2* __restrict__ tiles, int64_t s0, int64_t s1, double inv_n, int beta,
+                double* __restrict__ h) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  PairSmem& sm = *reinterpret_cast<PairSmem*>(smraw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const int2 tile = tiles[blockIdx.x >> 1];
+  const int64_t i0 = (int64_t)tile.x * (2 * kTM), j0 = (int64_t)tile.y * kTN;
+  const int64_t ia = i0 + (int64_t)rank * kTM;  // this CTA's A rows
+  const int64_t ch = 1LL << lg_ch;
+  constexpr int kHN = kTN / 2, kWN = kLimbs * kHN;  // 48, 240
+  if (tid == 0) {
+    for (int q = 0; q < kPR; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.tma_full[q])));
+      // leader: its own 12 expansion warps + one forwarded arrival from the follower
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.full[q])),
+                   "r"(kQThreads / 32 + 1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.done[q])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.fwd[q])),
+                   "r"(kQThreads / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.taddr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t taddr = sm.taddr;
+  const uint32_t idesc = (2u << 4) | ((uint32_t)(kWN >> 3) << 17) | ((uint32_t)((2 * kTM) >> 4) << 24);
+  const int64_t T = (s1 - s0) / kTK;
+  if (warp < kQThreads / 32) {
+    // ===== expansion: raw row f (0..95), logical chunk lc -> this CTA's limb rows =====
+    // leader's full barrier, in the cluster window
+    uint32_t full0;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(full0) : "r"(smem_u32(&sm.full[0])));
+    const int wv = tid >> 5, f = (wv >> 2) * 32 + lane, lc = wv & 3;
+    const int hh = f >= kHN ? 1 : 0, c = f - hh * kHN;
+    const int off = f * 64 + ((lc ^ ((f >> 1) & 3)) * 16);
+    const int pc = off & 63;  // physical chunk offset (same swizzle phase in B')
+    int bb = 0, q = 0, dq = 0;
+    uint32_t ph = 0, dph = 0;  // (slot, phase) of stage t and of stage t - kPBB
+    for (int64_t t = 0; t < T; ++t, bb = (bb + 1 == kPBB ? 0 : bb + 1)) {
+      if (t >= kPBB) {
+        mbar_wait(&sm.done[dq], dph);
+        if (++dq == kPR) { dq = 0; dph ^= 1u; }
+      }
+      mbar_wait(&sm.tma_full[q], ph);
+      const uint4 x = *reinterpret_cast<const uint4*>(&sm.braw[q][off]);      const uint4 m = make_uint4(x.x * 255u, x.y * 255u, x.z * 255u, x.w * 255u);
+#pragma unroll
+      for (int k = 0; k < kLimbs; ++k) {
+        const int R = k * kHN + c - (int)rank * kPH;  // B'_h row in this CTA
+        if (R >= 0 && R < kPH) {
+          const uint4 L = *reinterpret_cast<const uint4*>(&sm.limb[q][k * kTK + lc * 16]);
+          *reinterpret_cast<uint4*>(&sm.b[bb][hh][R * 64 + pc]) =
+              make_uint4(m.x & L.x, m.y & L.y, m.z & L.z, m.w & L.w);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      __syncwarp();
+      // CTA-scope arrivals (cheap): the leader's warps on its full barrier, the
+      // follower's on a local barrier that one thread forwards across the pair
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                         smem_u32(rank == 0 ? &sm.full[q] : &sm.fwd[q])) : "memory");
+      if (++q == kPR) { q = 0; ph ^= 1u; }
+    }
+    (void)full0;
+  } else if (warp == kQThreads / 32) {
+    if (lane == 0) {  // ===== TMA issue (own rows, own smem, own barrier) =====
+      int q = 0;
+      uint32_t ph = 0;
+      for (int64_t t = 0; t < T; ++t) {
+        if (t >= kPR) mbar_wait(&sm.done[q], ph ^ 1u);  // stage t - kPR used this slot
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.tma_full[q])),
+                     "r"(kStageTx) : "memory");
+        const int64_t smp = s0 + t * kTK;
+        const int blk = (int)(smp >> lg_ch), so = (int)(smp & (ch - 1));
+        tma_3d(sm.a[q], &map_a, so, (int)ia, blk, &sm.tma_full[q]);
+        tma_3d(sm.braw[q], &map_b, so, (int)j0, blk, &sm.tma_full[q]);
+        tma_2d(sm.limb[q], &map_l, (int)smp, 0, &sm.tma_full[q]);
+        if (++q == kPR) { q = 0; ph ^= 1u; }
+      }
+    }
+  } else if (rank == 1) {
+    // ===== follower: forward each stage's local arrivals to the leader's full barrier,
+    // one lane per ring slot so the cluster-scope releases overlap =====
+    if (lane < kPR) {
+      uint32_t full0;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(full0) : "r"(smem_u32(&sm.full[0])));
+      uint32_t ph = 0;
+      for (int64_t t = lane; t < T; t += kPR, ph ^= 1u) {
+        mbar_wait(&sm.fwd[lane], ph);
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                         full0 + (uint32_t)(lane * 8)) : "memory");
+      }
+    }
+  } else if (lane == 0) {
+    // ===== MMA issuer (leader): per K step 2 MMAs of M = 256, N = 240 =====
+    int bb = 0, q = 0;
+    uint32_t ph = 0;
+    for (int64_t t = 0; t < T; ++t, bb = (bb + 1 == kPBB ? 0 : bb + 1)) {
+      mbar_wait_cluster(&sm.full[q], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint64_t da = umma_desc_sw64(&sm.a[q][ks * 32]);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint64_t db = umma_desc_sw64(&sm.b[bb][hh][ks * 32]);
+          const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(
+                  taddr + (uint32_t)(hh * kWN)),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              smem_u32(&sm.done[q])), "h"((uint16_t)3));
+      if (++q == kPR) { q = 0; ph ^= 1u; }
+    }
+  }
+  if (T > 0) mbar_wait(&sm.done[(T - 1) % kPR], (uint32_t)(((T - 1) / kPR) & 1));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp < 4) {  // epilogue: this CTA's row i = ia + 32*warp + lane
+    const int64_t i = ia + warp * 32 + lane;
+    for (int hc = 0; hc < 6; ++hc) {
+      const int hh = hc / 3, c0 = (hc % 3) * 16;
+      double hv[16];
+#pragma unroll
+      for (int qq = 0; qq < 16; ++qq) hv[qq] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kLimbs; ++k) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr + ((uint32_t)(warp * 32) << 16) + (uint32_t)(hh * kWN + k * kHN + c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        const double sc = ldexp(1.0, kLimbBits * k - kFixBits) * inv_n;
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) hv[qq] += (double)(int)v[qq] * sc;
+      }
+      if (i < d) {
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) {
+          const int64_t j = j0 + hh * kHN + c0 + qq;
+          if (j < d && i <= j) {
+            if (beta) {
+              h[i * d + j] += hv[qq];
+              if (i != j) h[j * d + i] += hv[qq];
+            } else {
+              h[i * d + j] = hv[qq];
+              if (i != j) h[j * d + i] = hv[qq];
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(taddr));
+}
+
 // out[block r/ch][j][r%ch] = bit (r, j) of the packed rows, 0 for r >= rows (16 samples
 // per thread)
 __global__ void k_bits_to_u8t(const uint64_t* __restrict__ bits, int64_t rows, int64_t d, int64_t W,
@@ -771,11 +988,11 @@ extern "C" int simopt_logistic_xtdx_i8(void* stream, const uint8_t* xt, int64_t 
 }
 
 // upper-triangle list of 128 x 96 tiles (tile (bi, bj) holds some j >= i), cached per d
-static int upper_tiles(int64_t d, int2** out, int* count, int tn = kTN) {
+static int upper_tiles(int64_t d, int2** out, int* count, int tn = kTN, int tm = kTM) {
   static std::mutex mu;
   static std::vector<std::pair<int64_t, std::pair<int2*, int>>> cache;
   std::lock_guard<std::mutex> lock(mu);
-  const int64_t key = d * 1024 + tn;
+  const int64_t key = (d * 1024 + tn) * 1024 + tm;
   for (auto& e : cache)
     if (e.first == key) {
       *out = e.second.first;
@@ -783,9 +1000,9 @@ static int upper_tiles(int64_t d, int2** out, int* count, int tn = kTN) {
       return SIMOPT_OK;
     }
   std::vector<int2> v;
-  for (int64_t bi = 0; bi * kTM < d; ++bi)
+  for (int64_t bi = 0; bi * tm < d; ++bi)
     for (int64_t bj = 0; bj * tn < d; ++bj)
-      if (bj * tn + tn - 1 >= bi * kTM) v.push_back(make_int2((int)bi, (int)bj));
+      if (bj * tn + tn - 1 >= bi * tm) v.push_back(make_int2((int)bi, (int)bj));
   int2* tiles = nullptr;
   SIMOPT_CUDA(cudaMalloc(&tiles, v.size() * sizeof(int2)));
   SIMOPT_CUDA(cudaMemcpy(tiles, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice));
@@ -840,8 +1057,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-extern "C" int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t np, int64_t n,
-                                        int64_t d, const double* dw, uint8_t* limbs, double* h) {
+static int xtdx_tma(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
+                    const double* dw, uint8_t* limbs, double* h, bool force_pair) {
   SIMOPT_REQUIRE(n >= 1 && d >= 1, SIMOPT_E_DIMENSION, "empty design matrix");
   SIMOPT_REQUIRE(d < (1LL << 31), SIMOPT_E_CONFIG, "d too large for a tensor map");
   int64_t ch = 0, np_want = 0;
@@ -886,6 +1103,30 @@ extern "C" int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   SIMOPT_REQUIRE(r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS && r3 == CUDA_SUCCESS, SIMOPT_E_CUDA,
                  "tensor map encoding failed (%d, %d, %d)", (int)r1, (int)r2, (int)r3);
+  static const bool pair_env = [] {
+    const char* e = getenv("SIMOPT_XTDX_PAIR");
+    return e && atoi(e) == 1;
+  }();
+  if ((pair_env || force_pair) && sw == 64) {  // CTA pairs (k_xtdx_pair): 256 x 96 tiles
+    int2* tp = nullptr;
+    int ntp = 0;
+    SIMOPT_REQUIRE(upper_tiles(d, &tp, &ntp, kTN, 2 * kTM) == SIMOPT_OK, SIMOPT_E_CUDA, "%s",
+                   simopt_last_error());
+    const size_t smem_p = sizeof(PairSmem) + 1024;
+    static bool attr_p = false;
+    if (!attr_p) {
+      SIMOPT_CUDA(cudaFuncSetAttribute(k_xtdx_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+      attr_p = true;
+    }
+    int beta = 0;
+    for (int64_t c0 = 0; c0 < np; c0 += kChunk) {
+      const int64_t c1 = c0 + kChunk < np ? c0 + kChunk : np;
+      k_xtdx_pair<<<2 * ntp, kQT, smem_p, st>>>(ma, mb, ml, lg, d, tp, c0, c1, 1.0 / (double)n, beta, h);
+      SIMOPT_CHECK_LAUNCH("k_xtdx_pair");
+      beta = 1;
+    }
+    return SIMOPT_OK;
+  }
   const size_t smem = sizeof(TmaSmem) + 1024;
   // SIMOPT_XTDX_TMA_WIDE=0: five N = 96 MMAs per K step instead of two N = 240 (comparison)
   static const bool wide = [] {
@@ -908,4 +1149,14 @@ extern "C" int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t
     beta = 1;
   }
   return SIMOPT_OK;
+}
+
+extern "C" int simopt_logistic_xtdx_tma(void* stream, const uint8_t* xt, int64_t np, int64_t n,
+                                        int64_t d, const double* dw, uint8_t* limbs, double* h) {
+  return xtdx_tma(stream, xt, np, n, d, dw, limbs, h, false);
+}
+
+extern "C" int simopt_logistic_xtdx_pair(void* stream, const uint8_t* xt, int64_t np, int64_t n,
+                                         int64_t d, const double* dw, uint8_t* limbs, double* h) {
+  return xtdx_tma(stream, xt, np, n, d, dw, limbs, h, true);
 }

@@ -228,13 +228,13 @@ def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.T
     shard = getattr(data, "shard", None)
     if method == "auto":
         method = "tma" if data.packed else "dmma"
-    if nl and method in ("i8", "tc", "tma"):
+    if nl and method in ("i8", "tc", "tma", "pair"):
         xt, np_ = data.feature_major_u8()
         limbs = getattr(data, "_limbs", None)
         if limbs is None or limbs.numel() != 5 * np_:
             limbs = data._limbs = torch.empty(5 * np_, dtype=torch.uint8, device="cuda")
         fn = {"tc": "simopt_logistic_xtdx_tc", "tma": "simopt_logistic_xtdx_tma",
-              "i8": "simopt_logistic_xtdx_i8"}[method]
+              "pair": "simopt_logistic_xtdx_pair", "i8": "simopt_logistic_xtdx_i8"}[method]
         _lib.call(fn,
                   _lib.stream_ptr(), _lib.ptr(xt), np_, nl, d, _lib.ptr(dw), _lib.ptr(limbs),
                   _lib.ptr(out))

@@ -118,7 +118,7 @@ def test_xtdx_bits_equals_dense(pkg, d, n):
     assert torch.equal(logistic_hessian_device(dense, dw), logistic_hessian_device(packed, dw, method="dmma"))
 
 
-@pytest.mark.parametrize("method", ["i8", "tc", "tma"])
+@pytest.mark.parametrize("method", ["i8", "tc", "tma", "pair"])
 @pytest.mark.parametrize("d,n", [(128, 4096), (200, 3001), (13, 777), (1000, 2000), (300, 40),
                                  (97, 9000)])
 def test_xtdx_i8_vs_oracle(pkg, d, n, method):
@@ -150,8 +150,9 @@ def test_xtdx_tma_equals_tc(pkg, d, n):
     from paper_2404_11631_b200.sampling import synth_classification
     data = synth_classification(d, pkg.RngStream(8, 0), n_rows=n, packed=True)
     dw = torch.rand(n, dtype=torch.float64, device="cuda") * 0.25
-    assert torch.equal(logistic_hessian_device(data, dw, method="tma"),
-                       logistic_hessian_device(data, dw, method="tc"))
+    ref = logistic_hessian_device(data, dw, method="tc")
+    assert torch.equal(logistic_hessian_device(data, dw, method="tma"), ref)
+    assert torch.equal(logistic_hessian_device(data, dw, method="pair"), ref)
 
 
 def test_newton_packed_vs_oracle(pkg):

@@ -108,6 +108,9 @@ SIGNATURES = {
 INT64_RESULT = {"simopt_peer_reduce_bytes"}  # size queries; every other entry point returns status
 
 
+ABI_VERSION = 2  # csrc/capi.cu simopt_abi_version; bumped when an entry point's signature changes
+
+
 def load(require_device: bool = True):
     """Load the library (idempotent).  Raises DeviceError when unusable."""
     global _lib, _device_ok
@@ -122,6 +125,10 @@ def load(require_device: bool = True):
             lib = ctypes.CDLL(LIB_PATH)
             lib.simopt_last_error.restype = ctypes.c_char_p
             lib.simopt_abi_version.restype = ctypes.c_int
+            if lib.simopt_abi_version() != ABI_VERSION:
+                raise DeviceError(
+                    f"{LIB_PATH} has ABI {lib.simopt_abi_version()}, this package expects "
+                    f"{ABI_VERSION}: rebuild with `python -m paper_2404_11631_b200.build`")
             for name, argt in SIGNATURES.items():
                 fn = getattr(lib, name)
                 fn.argtypes = argt

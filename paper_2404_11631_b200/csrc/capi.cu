@@ -18,7 +18,7 @@ void simopt_set_error(const char* fmt, ...) {
 }
 
 extern "C" const char* simopt_last_error(void) { return g_err; }
-extern "C" int simopt_abi_version(void) { return 1; }
+extern "C" int simopt_abi_version(void) { return 2; }
 
 namespace {
 __global__ void k_stamp(int64_t* out) {

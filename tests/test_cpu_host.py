@@ -28,7 +28,7 @@ def test_abi_exports_every_declared_symbol():
     assert not missing, missing
     assert set(_lib.exported_symbols()) <= declared
     lib.simopt_abi_version.restype = ctypes.c_int
-    assert lib.simopt_abi_version() == 1
+    assert lib.simopt_abi_version() == _lib.ABI_VERSION
 
 
 def test_no_device_means_loud_failure(monkeypatch):

@@ -173,7 +173,7 @@ typedef struct NvState {
   int64_t jstar;          /* LMO vertex index of the last gradient            */
   double sval;            /* vertex value C/c_j* if g_j* < 0 else 0            */
   unsigned blocks_done;   /* last-block-done counter (kept 0 between launches) */
-  unsigned pad;
+  unsigned pad;           /* product counter of gradient steps (kept 0 between launches) */
   double best_val;        /* LMO value g_j* (C/c_j*) of the vertex (shard exchange) */
   int64_t exchange_failed; /* sticky: a peer exchange timed out; later ones do not wait */
 } NvState;

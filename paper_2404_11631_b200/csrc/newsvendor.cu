@@ -352,8 +352,21 @@ __global__ void __launch_bounds__(kIterWarps * 32, 24 / kIterWarps)
                             : NvStreamPos{a.seed, a.sid, a.ctr_lo, a.ctr_hi};
   // frank_wolfe.py:62-66: gamma = 2 / (epoch * inner_iters + inner + 2), IEEE double division
   const double gamma = a.epoch_ctr ? 2.0 / (double)(*a.epoch_ctr * a.inner_iters + a.m + 2) : a.gamma;
-  for (int64_t j = (int64_t)blockIdx.x * kIterWarps + warp; j < a.d;
-       j += (int64_t)gridDim.x * kIterWarps) {
+  // gradient steps hand products out dynamically (NvState.pad is the counter, reset by
+  // the last block): a product's cost varies with its window and ambiguous draws, and a
+  // static split left warps idle at the block barrier behind the slowest of their block.
+  // The next index is fetched before the current product is processed.
+  const bool dyn = a.do_grad != 0;
+  unsigned* next = &st->pad;
+  int64_t j;
+  {
+    unsigned jn = 0;
+    if (dyn && lane == 0) jn = atomicAdd(next, 1u);
+    j = dyn ? (int64_t)__shfl_sync(0xffffffffu, jn, 0) : (int64_t)blockIdx.x * kIterWarps + warp;
+  }
+  while (j < a.d) {
+    unsigned jn = 0;
+    if (dyn && lane == 0) jn = atomicAdd(next, 1u);
     double x = a.x_in[j];
     if (a.do_update) {
       const double sj = (j == jstar) ? sval : 0.0;
@@ -376,6 +389,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, 24 / kIterWarps)
         best = amin(best, ArgMin{val, j});
       }
     }
+    j = dyn ? (int64_t)__shfl_sync(0xffffffffu, jn, 0) : j + (int64_t)gridDim.x * kIterWarps;
   }
   if (!a.do_grad) return;
   if (lane == 0) warp_best[warp] = best;
@@ -407,6 +421,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, 24 / kIterWarps)
     const double gj = a.g[r.i];
     const double sval = (gj < 0.0) ? a.budget / a.c[r.i] : 0.0;
     st->blocks_done = 0;
+    st->pad = 0;  // the product counter of the next gradient step
     if (a.peer_mb == nullptr) {
       st->jstar = r.i;
       st->sval = sval;
@@ -519,8 +534,10 @@ extern "C" int simopt_nv_decode(void* stream, const uint32_t* keys, const double
 
 extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   NvIterArgs a = *args;
-  const int grid = (int)(ceil_div(a.d, kIterWarps) < 16 * SIMOPT_NUM_SMS ? ceil_div(a.d, kIterWarps)
-                                                                          : 16 * SIMOPT_NUM_SMS);
+  // gradient steps: one resident wave of blocks pulling products from a counter; update-only
+  // steps: a static split
+  const int64_t cap = a.do_grad ? (int64_t)(24 / kIterWarps) * SIMOPT_NUM_SMS : 16 * SIMOPT_NUM_SMS;
+  const int grid = (int)(ceil_div(a.d, kIterWarps) < cap ? ceil_div(a.d, kIterWarps) : cap);
   SIMOPT_REQUIRE(grid <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
   k_nv_iter<<<grid, kIterWarps * 32, 0, as_stream(stream)>>>(a);
   SIMOPT_CHECK_LAUNCH("k_nv_iter");

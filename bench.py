@@ -373,8 +373,8 @@ def run_ours(args, rank, world):
 def run_e2e(args, task, backend, shard=None):
     """Same metric through the public API with host inputs, the way the reference's
     run_cell (bench.py:152-184) runs a cell: build the problem from the host instance
-    arrays (H2D of mu, sigma, k, h, v, c) and call fw_run for `steps` epochs (one step =
-    one resampling epoch, capped at the reference's 1500/25 = 60).  Every epoch's draw
+    arrays (H2D of mu, sigma, k, h, v, c) and call fw_run for the reference's 60 epochs
+    (1500 FW iterations, bench.py:88; one step = one resampling epoch).  Every epoch's draw
     state goes to the device with its launches and every epoch's trace rows (flags,
     feasibility sums, objectives, stamps) come back to the host for the reference's
     checks before the run continues; the RunRecord (trace + final iterate) is returned.
@@ -383,7 +383,7 @@ def run_e2e(args, task, backend, shard=None):
     import paper_2404_11631_b200 as pkg
     from paper_2404_11631_b200.frank_wolfe import FwConfig, fw_run
     from paper_2404_11631_b200.tasks import NewsvendorProblem
-    steps = max(3, min(args.steps, 60))
+    steps = 60  # the reference bench's run length: 1500 FW iterations = 60 epochs (bench.py:88)
     rec = fw_run(NewsvendorProblem(task, backend, shard=shard), FwConfig(2, M, S, pkg.RngStream(SEED, 2)),
                  backend)  # warm: allocations, layouts, streams
     torch.cuda.synchronize()

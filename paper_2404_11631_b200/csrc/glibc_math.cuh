@@ -467,6 +467,93 @@ SIMOPT_HD double glibc_exp(double x, const uint64_t* etab) {
   return gm_fma(scale, tmp, scale);
 }
 
+// ---------------------------------------------------------------------------
+// erf (glibc 2.39 s_erf.c as compiled into libm.so.6: `erf` @0x2df70, SSE2 code, no
+// FMA; the two exp calls go through the exp IFUNC, i.e. __exp_fma = glibc_exp).  Every
+// operation below follows the disassembly's order and operands; constants are the
+// .rodata words the code loads (tools/extract_glibc_tables.py prints them).  Used by
+// newsvendor_cost_block (_kernels.py:219-220) through numba's math.erf.
+// ---------------------------------------------------------------------------
+SIMOPT_HD double glibc_erf(double x, const uint64_t* etab) {
+  const int32_t hx = gm_hi(x);
+  const int32_t ix = hx & 0x7fffffff;
+  if (ix > 0x7fefffff) {  // inf or NaN: (1 - 2 sign) + 1/x
+    const double one = 1.0 / x;
+    return (double)(1 - ((hx >> 31) & 1) * 2) + one;
+  }
+  if (ix <= 0x3feaffff) {  // |x| < 0.84375
+    if (ix <= 0x3e2fffff) {  // |x| < 2^-28
+      if ((hx & 0x7f800000) == 0)  // avoid underflow: 0.0625 * (16 x + efx8 x)
+        return ((x * 16.0) + (x * 0x1.06eba8214db69p+1)) * 0.0625;
+      return (x * 0x1.06eba8214db69p-3) + x;
+    }
+    const double z = x * x;
+    const double z2 = z * z;
+    double r = (z * -0x1.7a291236668e4p-8) - 0x1.d2a51dbd7194fp-6;
+    r = (r * z2) + ((z * -0x1.4cd7d691cb913p-2) + 0x1.06eba8214db68p-3);
+    const double z4 = z2 * z2;
+    r = r + (z4 * -0x1.8ead6120016acp-16);
+    double q3 = ((z * 0x1.4d022c4d36b0fp-8) + 0x1.0a54c5536cebap-4) * z2;
+    const double q1 = (z * 0x1.97779cddadc09p-2) + 1.0;
+    double q5 = ((z * -0x1.09c4342a26120p-18) + 0x1.15dc9221c1a10p-13) * z4;
+    const double s = q5 + (q3 + q1);
+    return ((r / s) * x) + x;
+  }
+  if (ix <= 0x3ff3ffff) {  // 0.84375 <= |x| < 1.25
+    const double s = gm_abs(x) - 1.0;
+    const double s2 = s * s;
+    double p = ((s * 0x1.45fca805120e4p-2) - 0x1.7d240fbb8c3f1p-2) * s2;
+    const double s4 = s2 * s2;
+    p = p + ((s * 0x1.a8d00ad92b34dp-2) - 0x1.359b8bef77538p-9);
+    const double s6 = s2 * s4;
+    p = p + (((s * 0x1.22a36599795ebp-5) - 0x1.c63983d3e28ecp-4) * s4);
+    p = p + (s6 * -0x1.1bf380a96073fp-9);
+    double q = ((s * 0x1.2635cd99fe9a7p-4) + 0x1.14af092eb6f33p-1) * s2;
+    q = q + ((s * 0x1.b3e6618eee323p-4) + 1.0);
+    q = q + (((s * 0x1.bedc26b51dd1cp-7) + 0x1.02660e763351fp-3) * s4);
+    q = q + (s6 * 0x1.88b545735151dp-7);
+    const double pq = p / q;
+    return hx >= 0 ? pq + 0x1.b0ac160000000p-1 : -0x1.b0ac160000000p-1 - pq;
+  }
+  if (ix > 0x4017ffff) {  // |x| >= 6
+    return hx >= 0 ? 1.0 - 0x1.56e1fc2f8f359p-997 : 0x1.56e1fc2f8f359p-997 - 1.0;
+  }
+  const double ax = gm_abs(x);
+  const double s = 1.0 / (x * x);
+  const double s2 = s * s;
+  const double s4 = s2 * s2;
+  const double s6 = s2 * s4;
+  double R, S;
+  if (ix > 0x4006db6d) {  // |x| >= 1/0.35: rb / sb
+    R = ((s * -0x1.4145d43c5ed98p+7) - 0x1.1c209555f995ap+4) * s2;
+    R = R + ((s * -0x1.993ba70c285dep-1) - 0x1.4341239e86f4ap-7);
+    R = R + (((s * -0x1.004616a2e5992p+10) - 0x1.3ec881375f228p+9) * s4);
+    R = R + (s6 * -0x1.e384e9bdc383fp+8);
+    double A = ((s * 0x1.802eb189d5118p+10) + 0x1.45cae221b9f0ap+8) * s2;
+    A = A + ((s * 0x1.e568b261d5190p+4) + 1.0);
+    const double B = ((s * 0x1.3f219cedf3be6p+11) + 0x1.8ffb7688c246ap+11) * s4;
+    const double C = ((s * -0x1.670e242712d62p+4) + 0x1.da874e79fe763p+8) * s6;
+    S = (B + A) + C;
+  } else {  // 1.25 <= |x| < 1/0.35: ra / sa
+    R = ((s * -0x1.f300ae4cba38dp+5) - 0x1.51e0441b0e726p+3) * s2;
+    R = R + ((s * -0x1.63416e4ba7360p-1) - 0x1.43412600d6435p-7);
+    R = R + (((s * -0x1.7135cebccabb2p+7) - 0x1.44cb184282266p+7) * s4);
+    R = R + (((s * -0x1.3a0efc69ac25cp+3) - 0x1.4526557e4d2f2p+6) * s6);
+    double A = ((s * 0x1.b290dd58a1a71p+8) + 0x1.1350c526ae721p+7) * s2;
+    A = A + ((s * 0x1.3a6b9bd707687p+4) + 1.0);
+    const double B = ((s * 0x1.ad02157700314p+8) + 0x1.42b1921ec2868p+9) * s4;
+    const double C = ((s * 0x1.a47ef8e484a93p+2) + 0x1.b28a3ee48ae2cp+6) * s6;
+    const double s8 = s4 * s4;
+    S = (C + (A + B)) + (s8 * -0x1.eeff2ee749a62p-5);
+  }
+  const double z = gm_from_bits(gm_bits(ax) & 0xffffffff00000000ULL);
+  const double e1 = glibc_exp(((-z) * z) - 0.5625, etab);
+  const double rs = R / S;
+  const double e2 = glibc_exp(((z - ax) * (z + ax)) + rs, etab);
+  const double r = e2 * e1;
+  return hx >= 0 ? 1.0 - (r / ax) : (r / ax) - 1.0;
+}
+
 // Stable logistic as sigmoid_block (sobench/_kernels.py:159-169).
 SIMOPT_HD double glibc_sigmoid(double t, const uint64_t* etab) {
   if (t >= 0.0) {

@@ -124,7 +124,7 @@ __device__ __forceinline__ double nv_cost_term(double x, double mu, double sigma
   const double INV_SQRT_TAU = 0.3989422804014327, SQRT1_2 = 0.7071067811865476;
   const double zj = (x - mu) / sigma;
   const double pdf = INV_SQRT_TAU * glibc_exp(-0.5 * zj * zj, simopt_exptab_dev);
-  const double cdf = 0.5 * (1.0 + erf(zj * SQRT1_2));
+  const double cdf = 0.5 * (1.0 + glibc_erf(zj * SQRT1_2, simopt_exptab_dev));
   const double over = sigma * (zj * cdf + pdf);
   const double under = sigma * (pdf - zj * (1.0 - cdf));
   return unit * x + hold * over + sell * under;

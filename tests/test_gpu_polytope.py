@@ -67,4 +67,4 @@ def test_newsvendor_polytope_fw_trace_golden(pkg, golden):
     b = pkg.make_backend("cuda")
     rec = fw_run(NewsvendorProblem(task, b), FwConfig(2, 5, 400, pkg.RngStream(42, 2)), b)
     assert np.array_equal(rec.final_iterate, g["fw_x"])                 # iterates bit-exact
-    np.testing.assert_allclose(rec.objectives, g["fw_obj"], rtol=1e-13, atol=0)  # CUDA erf
+    assert np.array_equal(rec.objectives, g["fw_obj"])

@@ -54,10 +54,7 @@ def test_cells_match_reference(sob, task, size):
     assert ours.backend == "cuda" and ref.backend == "sequential"
     assert np.array_equal(ours.iterations, ref.iterations)
     assert np.array_equal(np.asarray(ours.final_iterate), np.asarray(ref.final_iterate))
-    if task == "newsvendor":   # recorded objective uses CUDA's erf (<= 1e-13 relative)
-        np.testing.assert_allclose(ours.objectives, ref.objectives, rtol=1e-13)
-    else:
-        assert np.array_equal(ours.objectives, ref.objectives)
+    assert np.array_equal(ours.objectives, ref.objectives)  # newsvendor too: glibc-exact erf
 
 
 @pytest.mark.gpu

@@ -767,11 +767,11 @@ extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_
                  SIMOPT_E_CONFIG, "unknown fused mode %d", mode);
   SIMOPT_REQUIRE(rows >= 0 && cols >= 0, SIMOPT_E_DIMENSION, "negative extent");
   SIMOPT_REQUIRE(mode != SIMOPT_FUSED_MV || center != nullptr, SIMOPT_E_CONFIG, "MV needs the mean");
-  SIMOPT_REQUIRE(mode == SIMOPT_FUSED_MV || rowaux != nullptr, SIMOPT_E_CONFIG, "row weights missing");
   if (cols == 0 || rows == 0)  // empty local sums: col_out = 0 * scale [- center], scalar 0
     return finish(st, nullptr, nullptr, 0, cols, col_scale,
                   (mode == SIMOPT_FUSED_MV && !raw) ? center : nullptr,
                   (accumulate && cols) ? col_out : nullptr, scalar_out, peer);
+  SIMOPT_REQUIRE(mode == SIMOPT_FUSED_MV || rowaux != nullptr, SIMOPT_E_CONFIG, "row weights missing");
   int C = 1, K = 1;
   SIMOPT_REQUIRE(geometry(cols, &C, &K), SIMOPT_E_CONFIG,
                  "fused pass supports up to %d columns (got %lld)", 8 * 8 * 2 * kNT, (long long)cols);
@@ -819,12 +819,12 @@ extern "C" int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bi
   cudaStream_t st = as_stream(stream);
   SIMOPT_REQUIRE(mode == SIMOPT_FUSED_LR_GRAD || mode == SIMOPT_FUSED_LR_HVP, SIMOPT_E_CONFIG,
                  "bit-packed fused pass: logistic modes only (got %d)", mode);
-  SIMOPT_REQUIRE(rowaux != nullptr, SIMOPT_E_CONFIG, "row weights missing");
   SIMOPT_REQUIRE(rows >= 0 && cols >= 0, SIMOPT_E_DIMENSION, "negative extent");
   SIMOPT_REQUIRE(cols <= 64 * kNT, SIMOPT_E_CONFIG, "bit-packed fused pass supports d <= %d", 64 * kNT);
-  if (cols == 0 || rows == 0)
+  if (cols == 0 || rows == 0)  // an empty row shard still joins the cross-rank sums
     return finish(st, nullptr, nullptr, 0, cols, col_scale, nullptr,
                   (accumulate && cols) ? col_out : nullptr, scalar_out, peer);
+  SIMOPT_REQUIRE(rowaux != nullptr, SIMOPT_E_CONFIG, "row weights missing");
   const int64_t W = ceil_div(cols, 64);
   if (ceil_div(cols, 4) > kMaxNibG) {  // banded nibble-table sweeps (d > 1024)
     const int nb = (int)ceil_div(W, kBandW);

@@ -58,6 +58,9 @@ def main(rank, world, port, out):
     res["ncgp_obj"], res["ncgp_w"] = rec.objectives, rec.final_iterate
     rec = newton_explicit(LogisticTask(packed), 3, 20, b)
     res["nexp_obj"], res["nexp_w"] = rec.objectives, rec.final_iterate
+    wide = synth_classification(1100, p.RngStream(42, 0), n_rows=3000, shard=sh, packed=True)
+    rec = newton_cg(LogisticTask(wide), 2, 4, b)   # banded nibble passes (d > 1024), peer sums
+    res["ncgw_obj"], res["ncgw_w"] = rec.objectives, rec.final_iterate
     nv = gen_newsvendor_instance(1003, p.RngStream(42, 0))
     for ex in ("nccl", "peer"):
         rec = fw_run(NewsvendorProblem(nv, b, shard=sh, exchange=ex),

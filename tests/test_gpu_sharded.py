@@ -77,6 +77,11 @@ def test_logistic_sharded(ranks):
     assert _rel(r["nex_w"], w) < 1e-8
     np.testing.assert_allclose(r["nexp_obj"], objs, rtol=1e-8)
     assert _rel(r["nexp_w"], w) < 1e-8
+    # d = 1100 > 1024: the banded two-sweep bit-packed passes, cross-rank sums in peer memory
+    x, z, _ = orc.synth_classification(1100, orc.Stream(42, 0), n_rows=3000)
+    objs, w = orc.newton_cg(x, z, iterations=2, cg_iters=4)
+    np.testing.assert_allclose(r["ncgw_obj"], objs, rtol=1e-8)
+    assert _rel(r["ncgw_w"], w) < 1e-8
 
 
 def test_newsvendor_sharded(ranks):

@@ -211,6 +211,11 @@ class NewsvendorProblem:
             raise ConfigurationError("product sharding needs the single-budget set (the "
                                      "multi-resource LMO couples all products)")
         j0, j1 = (0, task.dimension) if shard is None else shard.range(task.dimension, 4)
+        if shard is not None and any(b <= a for a, b in shard.ranges(task.dimension, 4)):
+            # every rank takes part in each step's LMO exchange with its own products
+            raise ConfigurationError(
+                f"product sharding of {task.dimension} products over {shard.world} ranks leaves "
+                "a rank without products (shards are multiples of 4)")
         self.dev = _NvDevice(task, j0, j1)
         self._stream = None
 

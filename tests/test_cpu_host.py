@@ -192,3 +192,27 @@ def test_shifted_counter_matches_block_offset():
     part = orc.standard_normal(st, 8 * S)
     assert np.array_equal(part, full[j0 * S:(j0 + 8) * S])
     assert shifted_counter((1 << 128) - 1, 2) == 1
+
+
+def test_product_sharding_rejects_empty_ranks():
+    """Every rank must own products (each step's LMO exchange waits for all ranks): a
+    product count that leaves a rank empty is rejected up front, not a 10 s exchange timeout."""
+    import numpy as np
+    import paper_2404_11631_b200 as p
+    from paper_2404_11631_b200.sharding import shard_range
+    from paper_2404_11631_b200.tasks import NewsvendorProblem, NewsvendorTask
+
+    class Shard:  # the ShardGroup interface NewsvendorProblem uses before touching the GPU
+        world, rank = 8, 0
+
+        def range(self, n, align=1):
+            return shard_range(n, self.world, self.rank, align)
+
+        def ranges(self, n, align=1):
+            return [shard_range(n, self.world, r, align) for r in range(self.world)]
+
+    task = NewsvendorTask(unit_cost=np.full(10, 1.5), holding_cost=np.full(10, 0.7),
+                          selling_value=np.full(10, 4.0), demand_mean=np.full(10, 30.0),
+                          demand_std=np.full(10, 15.0), budget_costs=np.ones(10), budget=150.0)
+    with pytest.raises(p.ConfigurationError):
+        NewsvendorProblem(task, None, shard=Shard())

@@ -690,20 +690,14 @@ def _nv_fw_run_device(prob: "NewsvendorProblem", config, backend, label, size, r
         raise RunAborted(f"frank-wolfe run failed at step {len(trace) + 1}: {exc}", partial) from exc
 
     eng.start()
-    events = []
     for k in range(config.epochs):
         nxt = config.epoch_sample_size(k + 1) if k + 1 < config.epochs else None
         eng.enqueue_epoch(k, config.stream, config.epoch_sample_size(k), next_samples=nxt)
-        ev = torch.cuda.Event()
-        ev.record()
-        events.append(ev)
-        if k >= 1:  # validate the previous epoch while this one runs
-            events[k - 1].synchronize()
+        if k >= 1:  # validate the previous epoch (waits for its records) while this one runs
             bad = eng.check_epoch(k - 1, trace)
             if bad:
                 abort(*bad)
     eng.finish()
-    events[-1].synchronize()
     bad = eng.check_epoch(config.epochs - 1, trace)
     if bad:
         abort(*bad)

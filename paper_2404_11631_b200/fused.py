@@ -14,6 +14,7 @@ import ctypes
 import torch
 
 from . import _lib
+from .errors import ConfigurationError
 
 MV, LR_GRAD, LR_HVP = 0, 1, 2
 
@@ -71,6 +72,8 @@ def fused_rows(mode: int, x: torch.Tensor, v: torch.Tensor, *, center=None, rowa
     """One read of x (N x d, fp64, row-major, on the device); see include/simopt_b200.h.
     peer: sum the column sums and the scalar over the shard's ranks inside the pass."""
     n, d = x.shape
+    if mode != MV and rowaux is None:  # (an empty row shard passes an empty weight tensor)
+        raise ConfigurationError("row weights missing")
     P = _lib.ptr
     pa = None if peer is None else ctypes.byref(peer.args())
     _lib.call("simopt_fused_rows", _lib.stream_ptr(), int(mode), P(x), n, d, P(v), P(center),
@@ -83,6 +86,8 @@ def fused_rows_bits(mode: int, bits: torch.Tensor, d: int, v: torch.Tensor, *, r
                     col_scale: float = 1.0, col_out=None, scalar_out=None, t_out=None, dw_out=None,
                     accumulate: bool = True, raw: bool = False, peer: PeerReducer | None = None):
     """The logistic passes on bit-packed features (N x ceil(d/64) words)."""
+    if rowaux is None:
+        raise ConfigurationError("row weights missing")
     P = _lib.ptr
     pa = None if peer is None else ctypes.byref(peer.args())
     _lib.call("simopt_fused_rows_bits", _lib.stream_ptr(), int(mode), P(bits), bits.shape[0], d,

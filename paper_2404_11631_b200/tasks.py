@@ -913,6 +913,30 @@ class MeanVarProblem:
                                   chunk=self.backend.chunk_size)
         self.sample_set = build_sample_set(x, self.backend, mean_out=self._mean)
 
+    def resample_slot(self, stream: RngStream, n_samples: int, slot: int) -> MeanVarSampleSet:
+        """Epoch draw into buffer `slot` (0/1) on the current stream: the device FW loop
+        double-buffers X so the next epoch's draw overlaps this epoch's steps.  Diagonal
+        model, unsharded; the same draws and exact-tree mean as resample()."""
+        spec, d = self.task.spec, self.dimension
+        if n_samples < 2:
+            raise InsufficientSamples(f"need at least 2 samples for a sample covariance, got {n_samples}")
+        if not hasattr(self, "_slots"):
+            self._slots = {}
+            self._mu_dev, self._sd_dev = vec_dev(spec.mean), vec_dev(spec.diag_std)
+        cur = self._slots.get(slot)
+        if cur is None or cur[0].shape[0] != n_samples:
+            self._slots[slot] = None
+            self._slots[slot] = (empty(n_samples, d), empty(d),
+                                 torch.ones(n_samples, dtype=F64, device="cuda"))
+        x, mean, ones = self._slots[slot]
+        _lib.call("simopt_sample_returns_diag", _lib.stream_ptr(), *stream.words(), n_samples, d,
+                  _lib.ptr(self._mu_dev), _lib.ptr(self._sd_dev), _lib.ptr(x))
+        stream.advance(2 * ((n_samples * d + 1) // 2))
+        col = self.backend.matvec_t_device(x, ones)          # build_sample_set (tasks.py:56-64)
+        _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(col), 1.0 / n_samples, None, d,
+                  _lib.ptr(mean))
+        return MeanVarSampleSet(x, mean)
+
     def _resample_shard(self, stream: RngStream, n_samples: int) -> None:
         """Rows [lo, hi) of sample_returns (no RNG communication) + the exact global mean."""
         spec, d, chunk = self.task.spec, self.dimension, self.backend.chunk_size
@@ -1193,13 +1217,48 @@ def _mv_fw_run_device(prob: MeanVarProblem, config, backend, label, size, rep):
         partial = trace.build(label, size, backend.kind, rep, config.stream.seed, to_host(it))
         raise RunAborted(f"frank-wolfe run failed at step {len(trace) + 1}: {exc}", partial) from exc
 
+    # Double-buffered epochs (unsharded diagonal model, when two copies of X fit): epoch
+    # k+1's draw runs on a low-priority stream into the other buffer while epoch k's
+    # HBM-bound steps run -- the exact glibc normals are FP64/INT-issue-bound, so the two
+    # overlap instead of adding up.  The draws keep the sequential stream order.
+    sizes = [config.epoch_sample_size(k) for k in range(K)]
+    nbytes = 8 * max(sizes) * prob.dimension
+    pipelined = (prob.shard is None and prob.task.spec.diag_std is not None and K > 1
+                 and 2 * nbytes < 0.4 * torch.cuda.get_device_properties(0).total_memory)
+    main = torch.cuda.current_stream()
+    if pipelined:
+        lo_pri = torch.cuda.Stream.priority_range()[0] if hasattr(torch.cuda.Stream, "priority_range") else 0
+        gen = eng.gen_stream = getattr(eng, "gen_stream", None) or torch.cuda.Stream(priority=lo_pri)
+        sets, ready, steps_done = {}, {}, {}
+        start = torch.cuda.Event()
+        start.record(main)  # the run's setup; slot 1 is free before epoch 0's steps end
+
+        def draw(k):
+            slot = k % 2
+            gen.wait_event(start if k < 2 else steps_done[k - 2])  # last reader of the slot
+            with torch.cuda.stream(gen):
+                sets[k] = prob.resample_slot(config.stream, sizes[k], slot)
+                ev = torch.cuda.Event()
+                ev.record()
+            ready[k] = ev
+        draw(0)
     for k in range(K):
-        n_k = config.epoch_sample_size(k)
+        n_k = sizes[k]
         n_of.append(n_k)
         if k >= 1:
             eng.rings[k % 2][0].copy_(eng.rings[(k - 1) % 2][M])  # roll the iterate
-        prob.resample(config.stream, n_k)
-        eng.run_epoch(k, n_k)
+        if pipelined:
+            main.wait_event(ready.pop(k))
+            prob.sample_set = sets.pop(k)
+            eng.run_epoch(k, n_k)
+            done = torch.cuda.Event()
+            done.record(main)
+            steps_done[k] = done
+            if k + 1 < K:
+                draw(k + 1)
+        else:
+            prob.resample(config.stream, n_k)
+            eng.run_epoch(k, n_k)
         sl = slice(k * M, (k + 1) * M)
         for dst, src in ((status, eng.status), (wmin, eng.wmin), (wsum, eng.wsum),
                          (quad, eng.quad), (lin, eng.lin), (stamps, eng.stamps)):

@@ -324,8 +324,11 @@ def run_ours(args, rank, world):
     stored_bytes = d_loc * S * 4 + d_loc * nseg * nbuck * 2
     peak, peak_kind = peaks()
     achieved = alg_bytes / (res_ms / 1e3) / 1e9
+    traffic = profiled_traffic()  # captured at N=1 (all d products): this rank's share
+    if traffic is not None:
+        traffic = int(round(traffic * d_loc / D))
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": profiled_traffic(),
+                "frac": achieved / peak, "traffic": traffic,
                 "kernel": "k_nv_resample", "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "algorithmic_bytes_per_launch": alg_bytes, "stored_bytes_per_launch": stored_bytes,
                 "kernel_ms": res_ms, "share_of_step": res_ms / (ms / args.steps),

@@ -66,9 +66,8 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
         uint32_t kk[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint32_t code = nv_code(z[k]);
-          kk[k] = (code << 12) | (uint32_t)(l0 + k);
-          atomicAdd(&hist[code >> (NV_QBITS - 10)], 1);
+          kk[k] = nv_key(z[k], (uint32_t)(l0 + k));
+          atomicAdd(&hist[kk[k] >> (12 + NV_QBITS - 10)], 1);
         }
         reinterpret_cast<uint4*>(raw)[l0 >> 2] = make_uint4(kk[0], kk[1], kk[2], kk[3]);
       } else {
@@ -76,9 +75,9 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
         for (int k = 0; k < 4; ++k) {
           const int l = l0 + k;
           if (l >= 0 && l < len) {
-            const uint32_t code = nv_code(z[k]);
-            raw[l] = (code << 12) | (uint32_t)l;
-            atomicAdd(&hist[code >> (NV_QBITS - 10)], 1);
+            const uint32_t key = nv_key(z[k], (uint32_t)l);
+            raw[l] = key;
+            atomicAdd(&hist[key >> (12 + NV_QBITS - 10)], 1);
           }
         }
       }

@@ -73,9 +73,16 @@ __device__ __forceinline__ void nv_approx_pair(uint64_t w0, uint64_t w1, float* 
   *z1 = -r * s;
 }
 
-__device__ __forceinline__ uint32_t nv_code(float z) {
-  const float t = (z + (float)NV_Z0) * (float)NV_QSCALE;
-  return (uint32_t)fminf(fmaxf(t, 0.0f), (float)NV_QMAX);  // branch-free clamp, then trunc
+// The key q << 12 | local in three instructions: one FFMA evaluates the code scaled by
+// 2^12 (one rounding, < 0.07 code, inside the 0.15 nv_classify assumes), and the
+// saturating float -> u32 conversion is the clamp (below 0 -> 0, at or above 2^32 ->
+// all ones, i.e. q = 2^20 - 1); the low 12 bits are masked off and replaced by local.
+__device__ __forceinline__ uint32_t nv_key(float z, uint32_t local) {
+  constexpr float kScale = (float)(NV_QSCALE * 4096.0);
+  constexpr float kBias = (float)(NV_Z0 * NV_QSCALE * 4096.0);
+  uint32_t k;
+  asm("cvt.rzi.sat.u32.f32 %0, %1;" : "=r"(k) : "f"(fmaf(z, kScale, kBias)));
+  return (k & 0xFFFFF000u) | local;
 }
 
 // Exact standard normal #i of the epoch's draw (glibc-exact Box-Muller, _kernels.py:184-190).

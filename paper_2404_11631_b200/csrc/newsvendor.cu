@@ -53,15 +53,19 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     const int64_t i0 = j * S + e0;
     const int64_t q0 = i0 >> 2, q1 = (i0 + len - 1) >> 2;
     const bool aligned = ((i0 & 3) == 0) && ((len & 3) == 0);
-    for (int64_t q = q0 + threadIdx.x; q <= q1; q += blockDim.x) {
+    const int nq = (int)(q1 - q0);             // <= NV_SEG / 4: 32-bit loop arithmetic
+    const uint64_t c0 = clo + (uint64_t)q0 + 1;
+    const int lbase = (int)((q0 << 2) - i0);   // local index of block q0's first normal
+    for (int t = threadIdx.x; t <= nq; t += kResampleThreads) {
+      const int64_t q = q0 + t;
       // kNoCarry: no carry into the counter's word 1 within this launch (checked on the
       // host), so block q's counter is (clo + q + 1, chi, 0, 0) -- see stream_block_counter
-      const phx4 w = kNoCarry ? philox4x64_10_rk_c0(clo + (uint64_t)q + 1, rk, pre)
+      const phx4 w = kNoCarry ? philox4x64_10_rk_c0(c0 + (uint64_t)t, rk, pre)
                               : philox4x64_10_rk(stream_block_counter(clo, chi, (uint64_t)q), rk);
       float z[4];
       nv_approx_pair(w.v[0], w.v[1], &z[0], &z[1]);
       nv_approx_pair(w.v[2], w.v[3], &z[2], &z[3]);
-      const int l0 = (int)((q << 2) - i0);
+      const int l0 = lbase + (t << 2);
       if (aligned) {
         uint32_t kk[4];
 #pragma unroll

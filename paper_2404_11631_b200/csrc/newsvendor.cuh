@@ -6,7 +6,7 @@
 // approximation z~ of its standard normal z:
 //     q = clamp(floor((z~ + 9.5) * 2^20 / 19), 0, 2^20 - 1).
 // |z~ - z| <= NV_EPSZ is guaranteed by construction (error budget at
-// nv_approx_pair; NV_EPSZ is > 3x the worst case and tests/test_gpu_newsvendor.py
+// nv_approx_pair; NV_EPSZ is > 7x the measured worst case and tests/test_gpu_newsvendor.py
 // measures the maximum over 2^26 draws), and q is
 // monotone in z~ up to one code of fp32 rounding.  Keys are counting-sorted by
 // bucket (the top 10 bits of q) inside each segment.  An ECDF query x_j then
@@ -32,8 +32,8 @@
 #define NV_Z0 9.5
 #define NV_QSCALE (1048576.0 / 19.0)  // codes per unit of z
 #define NV_W (19.0 / 1048576.0)       // z width of one code
-#define NV_EPSZ 1.5e-5                // guaranteed |z~ - z| bound (analytic worst case < 1e-5,
-                                      // measured max 3.7e-6 over 2^28 draws)
+#define NV_EPSZ 1.5e-5                // guaranteed |z~ - z| bound (analytic worst case < 1.1e-5,
+                                      // measured max 2.1e-6 over 2^26 draws)
 
 // fp32 approximation of one Box-Muller pair (both components) from the raw
 // Philox words, on the SFU (MUFU) path.  Error budget, |z~ - z|:
@@ -42,30 +42,33 @@
 //       1 - u1 an exact integer times 2^-53 (the __logf bound: abs error <= 3.6e-7 on
 //       [0.5, 2], 3 ulp relative below; the ftz forms never see subnormals here):
 //       |dr| = |dl| / r <= 2.7e-6 (worst at u1 = 2^-6, r = 0.177).
-//   r = y * rsqrt.approx(y), y = -2l: relative 2 ulp -> |dr| <= 2.1e-6 at r = 8.57.
-//   theta' = 2pi(u2 - 1/2) in [-pi, pi): sin/cos.approx abs error <= 2^-21.41, plus
-//       2pi * 2^-24 from rounding u2: |dcos|, |dsin| <= 7.3e-7.
-//   => |z~ - z| <= 2.7e-6 + 8.57 * 7.3e-7 + 1e-6 < 1e-5;  NV_EPSZ = 1.5e-5.
+//   r = sqrt.approx(y), y = -2l (one MUFU.SQRT; sqrt.approx(0) = 0, so no zero guard):
+//       relative error 1.0e-7 (2^-23.25), measured exhaustively over every fp32 y in
+//       [2^-60, 80] on B200 (tools/micro/sqrt_approx_err.cu) -> |dr| <= 8.6e-7 at r = 8.57.
+//   theta' = 2pi(u2 - 1/2) in [-pi, pi), from the word's top 32 bits read as a signed
+//       integer (hi ^ 2^31 = hi - 2^31) converted once (rounding < 2^-25): sin/cos.approx
+//       abs error <= 2^-21.41, plus 2pi * 2^-24 from u2 and the constant: |dcos|, |dsin| <= 7.3e-7.
+//   => |z~ - z| <= 2.7e-6 + 8.6e-7 + 8.57 * 7.3e-7 + 1e-6 < 1.1e-5;  NV_EPSZ = 1.5e-5.
 __device__ __forceinline__ void nv_approx_pair(uint64_t w0, uint64_t w1, float* z0, float* z1) {
   const uint64_t k1 = w0 >> 11;                        // u1 = k1 * 2^-53
   const float u1f = (float)k1 * 0x1p-53f;
   const float vf = (float)((1ULL << 53) - k1) * 0x1p-53f;  // 1 - u1 (exact integer)
-  // series for small u1 (Horner), SFU log otherwise; both evaluated, one selected
-  float ser = fmaf(u1f, 0.2f, 0.25f);
-  ser = fmaf(u1f, ser, 0.33333334f);
-  ser = fmaf(u1f, ser, 0.5f);
-  ser = fmaf(u1f, ser, 1.0f);
-  const float ls = -u1f * ser;
+  // y = -2 l: series for small u1 (Horner), SFU log otherwise; both evaluated, one
+  // selected.  The factor -2 is folded into the coefficients (power-of-two scaling
+  // commutes with rounding), so y is bitwise -2 * fl(l) of the unscaled forms.
+  float ser = fmaf(u1f, 2.0f * 0.2f, 2.0f * 0.25f);
+  ser = fmaf(u1f, ser, 2.0f * 0.33333334f);
+  ser = fmaf(u1f, ser, 2.0f * 0.5f);
+  ser = fmaf(u1f, ser, 2.0f * 1.0f);
+  const float ys = u1f * ser;
   float lg;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(vf));  // vf >= 2^-53: never subnormal
-  const float ll = lg * 0.69314718055994531f;
-  const float l = (k1 < (1ULL << 47)) ? ls : ll;      // u1 < 2^-6
-  const float y = -2.0f * l;
-  float rs;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(y));   // y >= 2^-52 or exactly 0
-  const float r = (y > 0.0f) ? y * rs : 0.0f;
-  const float u2f = (float)(uint32_t)(w1 >> 40) * 0x1p-24f;  // |u2f - u2| < 2^-24
-  const float th = 6.2831853071795865f * (u2f - 0.5f);      // theta - pi, in [-pi, pi)
+  const float yl = lg * (-2.0f * 0.69314718055994531f);
+  const float y = ((uint32_t)(w0 >> 32) < (1u << 26)) ? ys : yl;  // u1 < 2^-6 (k1 < 2^47)
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(y));     // y >= 2^-52 or exactly 0
+  const int32_t h2 = (int32_t)((uint32_t)(w1 >> 32) ^ 0x80000000u);  // 2^32 (u2 - 1/2), truncated
+  const float th = (float)h2 * (float)(6.2831853071795865 * 0x1p-32);  // theta - pi, in [-pi, pi)
   float s, c;
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));

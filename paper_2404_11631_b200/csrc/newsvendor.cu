@@ -125,10 +125,20 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
     }
     __syncthreads();
     // 3) scatter into bucket order (order inside a bucket is irrelevant to every count)
-    for (int l = threadIdx.x; l < len; l += blockDim.x) {
-      const uint32_t key = raw[l];
-      const int pos = atomicAdd(&hist[key >> (12 + NV_QBITS - 10)], 1);
-      sorted_[pos] = key;
+    constexpr int kBucketShift = 12 + NV_QBITS - 10;
+    if (aligned) {  // four keys per 16-byte shared load
+      for (int l4 = threadIdx.x; l4 < (len >> 2); l4 += kResampleThreads) {
+        const uint4 k4 = reinterpret_cast<const uint4*>(raw)[l4];
+        sorted_[atomicAdd(&hist[k4.x >> kBucketShift], 1)] = k4.x;
+        sorted_[atomicAdd(&hist[k4.y >> kBucketShift], 1)] = k4.y;
+        sorted_[atomicAdd(&hist[k4.z >> kBucketShift], 1)] = k4.z;
+        sorted_[atomicAdd(&hist[k4.w >> kBucketShift], 1)] = k4.w;
+      }
+    } else {
+      for (int l = threadIdx.x; l < len; l += kResampleThreads) {
+        const uint32_t key = raw[l];
+        sorted_[atomicAdd(&hist[key >> kBucketShift], 1)] = key;
+      }
     }
     __syncthreads();
     uint32_t* dst = keys + j * S + e0;

@@ -27,7 +27,7 @@
 namespace {
 
 constexpr int kResampleThreads = 256;
-constexpr int kResampleMinBlocks = 4;
+constexpr int kResampleMinBlocks = 6;  // = the shared-memory limit (6 x 36.9 KB); 32 registers
 
 // Persistent CTAs walk (product j, segment s) pairs: generate the segment's keys
 // (Philox4x64-10 + fp32 Box-Muller approximation), histogram them by bucket in
@@ -499,13 +499,14 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   const int64_t nseg = ceil_div(S, NV_SEG);
   const int64_t nblk = d * nseg;
   SIMOPT_REQUIRE(nblk < (1LL << 31), SIMOPT_E_CONFIG, "too many segments");
-  // Persistent grid of 5 CTAs per SM (6 fit): one wave, and room on every SM for the
-  // high-priority FW step kernels of the previous epoch that run concurrently in the
-  // pipelined device loop (measured best of 3..10 per SM at C2).
+  // Persistent grid of kResampleMinBlocks CTAs per SM: one full wave (the step kernels
+  // of the previous epoch, at high stream priority, still find room as CTAs retire).
+  // Measured at C2: 6 per SM at 32 registers 5.45k FW it/s vs 5 per SM at 46 registers
+  // 5.33k.
   // SIMOPT_NV_RESAMPLE_GRID overrides it for tuning sweeps.
   static const int64_t cap = [] {
     const char* e = getenv("SIMOPT_NV_RESAMPLE_GRID");
-    return e ? atoll(e) : (int64_t)SIMOPT_NUM_SMS * 5;
+    return e ? atoll(e) : (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks;
   }();
   const int64_t grid = nblk < cap ? nblk : cap;
   const phx_keys rk = phx_round_keys(seed, sid);

@@ -311,15 +311,18 @@ def fw_run_meanvar(mu, sigma, epochs, inner_iters, n_samples, stream, chunk=CHUN
     return np.array(objs), w
 
 
-def fw_run_newsvendor(task, epochs, inner_iters, n_samples, stream, chunk=CHUNK):
-    """frank_wolfe.py:91-121 driving NewsvendorProblem (tasks.py:293-334)."""
+def fw_run_newsvendor(task, epochs, inner_iters, n_samples, stream, chunk=CHUNK,
+                      schedule="constant"):
+    """frank_wolfe.py:91-121 driving NewsvendorProblem (tasks.py:293-334); `schedule`
+    is FwConfig.sample_schedule (frank_wolfe.py:41-46: "linear" draws n*(k+1) in epoch k)."""
     mu, sigma, k_, h, v, c, budget = (task[n] for n in ("mu", "sigma", "k", "h", "v", "c",
                                                         "budget"))
     d = mu.size
     x = np.zeros(d)
     objs = []
     for k in range(epochs):
-        dem = sample_demands(mu, sigma, n_samples, stream)
+        n_k = n_samples * (k + 1) if schedule == "linear" else n_samples
+        dem = sample_demands(mu, sigma, n_k, stream)
         for m in range(inner_iters):
             g = nv_gradient_hat(x, dem, k_, h, v)
             s = lmo_single_budget(g, c, budget)

@@ -108,7 +108,7 @@ SIGNATURES = {
 INT64_RESULT = {"simopt_peer_reduce_bytes"}  # size queries; every other entry point returns status
 
 
-ABI_VERSION = 2  # csrc/capi.cu simopt_abi_version; bumped when an entry point's signature changes
+ABI_VERSION = 3  # csrc/capi.cu simopt_abi_version; bumped when an entry point's signature changes
 
 
 def load(require_device: bool = True):

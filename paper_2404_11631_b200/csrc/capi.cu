@@ -3,6 +3,7 @@
 #include <stdio.h>
 
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -18,7 +19,21 @@ void simopt_set_error(const char* fmt, ...) {
 }
 
 extern "C" const char* simopt_last_error(void) { return g_err; }
-extern "C" int simopt_abi_version(void) { return 2; }
+extern "C" int simopt_abi_version(void) { return 3; }
+
+int simopt_num_sms() {
+  static std::mutex mu;
+  static std::unordered_map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  cache[dev] = n;
+  return n;
+}
 
 namespace {
 __global__ void k_stamp(int64_t* out) {
@@ -39,14 +54,28 @@ struct Scratch {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
+struct ScratchKey {
+  cudaStream_t stream;
+  std::thread::id thread;
+  bool operator==(const ScratchKey& o) const { return stream == o.stream && thread == o.thread; }
+};
+struct ScratchKeyHash {
+  size_t operator()(const ScratchKey& k) const {
+    return std::hash<void*>()(reinterpret_cast<void*>(k.stream)) ^
+           (std::hash<std::thread::id>()(k.thread) * 0x9e3779b97f4a7c15ULL);
+  }
+};
 std::mutex g_scratch_mu;
-std::unordered_map<cudaStream_t, Scratch> g_scratch;
+// keyed by (stream, host thread): a multi-kernel op (partials, then fold) enqueued by
+// one thread must not share its buffer with another thread's op on the same stream
+// (the reference's kernels are reentrant on disjoint data, backend.py:12-14)
+std::unordered_map<ScratchKey, Scratch, ScratchKeyHash> g_scratch;
 std::vector<void*> g_retired;  // superseded buffers, kept alive for captured graphs
 }  // namespace
 
 void* simopt_scratch(cudaStream_t st, size_t bytes) {
   std::lock_guard<std::mutex> lock(g_scratch_mu);
-  Scratch& s = g_scratch[st];
+  Scratch& s = g_scratch[ScratchKey{st, std::this_thread::get_id()}];
   if (s.bytes >= bytes) return s.ptr;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {

@@ -6,7 +6,11 @@
 
 #include "../../include/simopt_b200.h"
 
-#define SIMOPT_NUM_SMS 148
+// Streaming multiprocessors of the current device (queried once per device and
+// cached; 148 on B200).  Grids of persistent and grid-stride kernels are sized
+// from it.
+int simopt_num_sms();
+#define SIMOPT_NUM_SMS (simopt_num_sms())
 
 // Thread-local last-error text (simopt_last_error()).
 void simopt_set_error(const char* fmt, ...);
@@ -39,9 +43,9 @@ void simopt_set_error(const char* fmt, ...);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Per-stream scratch.  Every ABI call that needs scratch (chunk partials, argmin
-// partials) takes it from its stream's buffer: uses are stream-ordered, so one
-// buffer per stream is race-free, and no allocation happens on the hot path or
+// Per-(stream, host thread) scratch.  Every ABI call that needs scratch (chunk
+// partials, argmin partials) takes it from its buffer: one thread's uses are
+// stream-ordered, and two threads enqueueing on one stream get separate buffers, and no allocation happens on the hot path or
 // inside a captured CUDA graph.  Buffers only grow; a superseded buffer is kept
 // alive (graphs captured earlier may still reference it).  Returns nullptr and
 // sets the error text on failure.

@@ -563,9 +563,10 @@ __global__ void __launch_bounds__(kNT) k_nibb_colsum(const uint64_t* __restrict_
 using BitsFn = void (*)(const uint64_t*, int64_t, int64_t, int64_t, int, const double*,
                         const double*, double*, double*, double*, double*, int);
 
-// Cross-rank finish over peer memory (SimoptPeerReduce).  kFB blocks, all resident, so
-// the spin waits cannot starve a block another rank waits for.
-constexpr int kFB = SIMOPT_NUM_SMS;
+// Cross-rank finish over peer memory (SimoptPeerReduce).  kFB blocks (a layout
+// constant of the flag area, the same on every rank), all resident at 256 threads
+// on any sm_100 part, so the spin waits cannot starve a block another rank waits for.
+constexpr int kFB = 148;
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

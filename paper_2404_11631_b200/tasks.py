@@ -143,12 +143,19 @@ class _NvDevice:
         # epoch's resample can run while this epoch's steps read the current one
         self.slots = {}   # slot -> [S, nseg, keys, off, draw]
 
-    def ensure_layout(self, S: int, slot: int = 0):
+    def ensure_layout(self, S: int, slot: int = 0, streams=()):
+        """Layout slot for S draws per product.  `streams`: the side streams that read
+        the slot's current buffers; a superseded buffer is kept from reuse until their
+        queued work has run (the caching allocator only orders its own stream)."""
         cur = self.slots.get(slot)
         if cur is None or cur[0] != S:
             ns, ke, oe = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
             _lib.call("simopt_nv_layout", self.d, S, ctypes.byref(ns), ctypes.byref(ke),
                       ctypes.byref(oe))
+            if cur is not None:
+                for st in streams:
+                    cur[2].record_stream(st)
+                    cur[3].record_stream(st)
             self.slots[slot] = None
             self.slots[slot] = [S, ns.value, torch.empty(ke.value, dtype=torch.int32, device="cuda"),
                                 torch.empty(oe.value, dtype=torch.int16, device="cuda"), None]
@@ -363,7 +370,7 @@ class NvFwEngine:
             self.gen.wait_event(old)
         # allocate on the caller's stream: the caching allocator keeps blocks per stream,
         # and a fresh engine's generator stream would otherwise cudaMalloc the layout anew
-        self.dev.ensure_layout(n_samples, slot)
+        self.dev.ensure_layout(n_samples, slot, streams=(self.hi, self.gen))
         with torch.cuda.stream(self.gen):
             if time_it:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -508,14 +515,15 @@ class NvFwEngine:
             if fl[i] & NV_FLAG_EXCHANGE_TIMEOUT:
                 raise DeviceError(f"peer-memory LMO exchange timed out at step {t + 1}")
             if fl[i] & NV_FLAG_NAN_GRADIENT:
-                return t, InvalidGradient("gradient contains NaN"), self.iterate(t)
+                return t, InvalidGradient("gradient contains NaN"), self.iterate(t, k)
             if (fl[i] & NV_FLAG_NEGATIVE) or not sp_[i] <= self.dev.budget * (1.0 + FEAS_TOL):
-                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), self.iterate(t + 1)
+                return t, InvalidConstraint(f"iterate infeasible at step {t + 1}"), self.iterate(t + 1, k)
             trace.append(t + 1, float(ob[i]), int(ts[i]) - self.t0)
         return None
 
-    def iterate(self, t: int) -> torch.Tensor:
-        """Full iterate after step t (the product slices gathered when sharded)."""
+    def iterate(self, t: int, epoch: int | None = None) -> torch.Tensor:
+        """Full iterate after step t (the product slices gathered when sharded); the
+        ring of 2M+1 slots keeps it until two epochs later."""
         x = self.xs[t % self.H]
         if self.shard is None:
             return x
@@ -553,6 +561,12 @@ class NvFwGraphEngine(NvFwEngine):
         self.host_params = [torch.zeros(5, dtype=torch.int64).pin_memory() for _ in range(2)]
         self.dev_params = [torch.zeros(5, dtype=torch.int64, device="cuda") for _ in range(2)]
         self.param_ev = [None, None]  # H2D of the parity's parameters (host buffer reuse)
+        # the starting iterate of the last epoch of each parity (rings[1-p][M] is rewritten
+        # by the next epoch of parity 1-p, which may already be queued when an epoch's
+        # check needs it for RunAborted's final_iterate)
+        self.starts = [torch.zeros(d, dtype=F64, device="cuda") for _ in range(2)]
+        # graphs are keyed on everything a capture bakes in: parity and the layout slot's
+        # (S, nseg, buffers) -- a sample schedule that changes S reallocates the slot
         self.graphs = {}
         self.warm = set()
         # captured kernel nodes keep the capture stream's priority: capture at high priority
@@ -585,6 +599,7 @@ class NvFwGraphEngine(NvFwEngine):
         lib, dev, M = self.lib, self.dev, self.M
         sp, ssp = _lib.stream_ptr(main), _lib.stream_ptr(side)
         P = _lib.ptr
+        self.starts[p].copy_(self.rings[1 - p][M])
         _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(self._step_args(p, -1, False))))
         fork = torch.cuda.Event()
         for m in range(M):
@@ -623,19 +638,21 @@ class NvFwGraphEngine(NvFwEngine):
             pe = torch.cuda.Event()
             pe.record(main)
             self.param_ev[p] = pe
-            g = self.graphs.get(p)
+            sl = self.dev.slots[p]
+            key = (p, sl[0], sl[1], sl[2].data_ptr(), sl[3].data_ptr())
+            g = self.graphs.get(key)
             if g is not None:
                 g.replay()
-            elif p not in self.warm:  # first epoch of this parity: eager (allocations, setup)
+            elif key not in self.warm:  # first epoch of this layout: eager (allocations, setup)
                 self._steps(p, main, self.side)
-                self.warm.add(p)
+                self.warm.add(key)
             else:
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
                 self.cstream.wait_stream(main)
                 with torch.cuda.graph(g, stream=self.cstream):
                     self._steps(p, self.cstream, self.side)
-                self.graphs[p] = g
+                self.graphs[key] = g
                 g.replay()
             steps = torch.cuda.Event()
             steps.record(main)
@@ -657,10 +674,14 @@ class NvFwGraphEngine(NvFwEngine):
         if next_samples is not None:
             self._resample(k + 1, stream, next_samples, time_resample)
 
-    def iterate(self, t: int) -> torch.Tensor:
-        """Full iterate after t steps (product slices gathered when sharded)."""
-        k, m = divmod(t, self.M)
-        x = self.rings[(k - 1) & 1][self.M] if m == 0 else self.rings[k & 1][m]
+    def iterate(self, t: int, epoch: int | None = None) -> torch.Tensor:
+        """Full iterate after t steps (product slices gathered when sharded), read as
+        of `epoch` (default: the epoch whose steps produced it).  t = epoch*M is that
+        epoch's start: its snapshot, which later epochs of the other parity cannot
+        overwrite."""
+        ke = max(t - 1, 0) // self.M if epoch is None else epoch
+        m = t - ke * self.M
+        x = self.starts[ke & 1] if m == 0 else self.rings[ke & 1][m]
         if self.shard is None:
             return x
         counts = [b - a for a, b in self.shard.ranges(self.dev.d_total, 4)]

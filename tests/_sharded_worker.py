@@ -66,6 +66,11 @@ def main(rank, world, port, out):
         rec = fw_run(NewsvendorProblem(nv, b, shard=sh, exchange=ex),
                      FwConfig(5, 6, 5000, p.RngStream(42, 2)), b)
         res[f"nv_{ex}_obj"], res[f"nv_{ex}_w"] = rec.objectives, rec.final_iterate
+    # a linear sample schedule: S (and the layout slots) change every epoch, so the
+    # graph engine must re-capture per layout (stale captured S/keys)
+    rec = fw_run(NewsvendorProblem(nv, b, shard=sh, exchange="peer"),
+                 FwConfig(5, 4, 2000, p.RngStream(42, 2), "linear"), b)
+    res["nv_lin_obj"], res["nv_lin_w"] = rec.objectives, rec.final_iterate
     from paper_2404_11631_b200.sharding import PeerMailbox
     res["nv_peer_used"] = np.array([PeerMailbox.get(sh) is not None])
     np.savez(os.path.join(out, f"rank{rank}.npz"), **res)

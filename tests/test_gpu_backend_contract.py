@@ -186,3 +186,24 @@ def test_concurrent_calls_on_disjoint_data(cuda):
     with ThreadPoolExecutor(max_workers=4) as pool:
         got = list(pool.map(lambda xy: cuda.dot(*xy), data))
     assert got == expected
+
+
+def test_reentrant_multi_kernel_ops(cuda):
+    """Ops that run as partials + fold (> 64 chunks: dot/vec_sum; matvec with several
+    column chunks) from worker threads on one stream: per-thread scratch keeps each
+    thread's partials its own (the reference's run_cell runs reps on a ThreadPool)."""
+    from concurrent.futures import ThreadPoolExecutor
+    rng = np.random.default_rng(13)
+    vecs = [(rng.standard_normal(700_000), rng.standard_normal(700_000)) for _ in range(8)]
+    mats = [(rng.standard_normal((64, 20_000)), rng.standard_normal(20_000)) for _ in range(8)]
+    want_d = [orc.dot(x, y) for x, y in vecs]
+    want_s = [orc.vec_sum(x) for x, _ in vecs]
+    want_m = [orc.matvec(a, x) for a, x in mats]
+    for _ in range(3):
+        with ThreadPoolExecutor(max_workers=8) as pool:
+            got_d = list(pool.map(lambda xy: cuda.dot(*xy), vecs))
+            got_s = list(pool.map(lambda xy: cuda.vec_sum(xy[0]), vecs))
+            got_m = list(pool.map(lambda ax: cuda.matvec(*ax), mats))
+        assert got_d == want_d and got_s == want_s
+        for g, w in zip(got_m, want_m):
+            assert np.array_equal(g, w)

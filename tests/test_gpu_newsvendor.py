@@ -202,3 +202,51 @@ def test_graph_engine_matches_eager(pkg):
             assert eng.check_epoch(k, tr) is None
         out.append((tr.build("nv", 700, "cuda", 0, 42, None).objectives, eng.iterate(K * M).cpu().numpy()))
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_graph_engine_linear_schedule(pkg):
+    """A linear sample schedule changes S (and reallocates the layout slots) every epoch:
+    the graph engine re-captures per layout and still gives the oracle's trace bit for bit."""
+    from paper_2404_11631_b200.instances import gen_newsvendor_instance
+    from paper_2404_11631_b200.records import TraceBuilder
+    from paper_2404_11631_b200.tasks import NewsvendorProblem, make_nv_engine
+    d, K, M, S = 333, 5, 4, 1500
+    task = gen_newsvendor_instance(d, pkg.RngStream(42, 0))
+    for graph in (False, True):
+        prob = NewsvendorProblem(task, pkg.make_backend("cuda"))
+        eng = make_nv_engine(prob, M, K, 4096, graph=graph)
+        stream = pkg.RngStream(42, 2)
+        eng.start()
+        for k in range(K):
+            eng.enqueue_epoch(k, stream, S * (k + 1), next_samples=S * (k + 2) if k + 1 < K else None)
+        eng.finish()
+        tr = TraceBuilder()
+        for k in range(K):
+            assert eng.check_epoch(k, tr) is None
+        objs, x = orc.fw_run_newsvendor(orc.gen_newsvendor_instance(d, orc.Stream(42, 0)), K, M, S,
+                                        orc.Stream(42, 2), schedule="linear")
+        assert np.array_equal(eng.iterate(K * M).cpu().numpy(), x), graph
+        np.testing.assert_allclose(tr.build("nv", d, "cuda", 0, 42, None).objectives, objs, rtol=1e-13)
+
+
+def test_graph_engine_epoch_start_iterate(pkg):
+    """RunAborted's final_iterate for a failure at an epoch's first step is the epoch's
+    starting iterate, even while the next epoch (whose ring parity holds it) runs: the
+    check of epoch k-1 happens after epoch k is enqueued, as in _nv_fw_run_device."""
+    from paper_2404_11631_b200.instances import gen_newsvendor_instance
+    from paper_2404_11631_b200.tasks import NewsvendorProblem, make_nv_engine
+    d, K, M, S = 300, 4, 3, 2000
+    task = gen_newsvendor_instance(d, pkg.RngStream(42, 0))
+    otask = orc.gen_newsvendor_instance(d, orc.Stream(42, 0))
+    want = [np.zeros(d)] + [orc.fw_run_newsvendor(otask, k, M, S, orc.Stream(42, 2))[1]
+                            for k in range(1, K + 1)]
+    eng = make_nv_engine(NewsvendorProblem(task, pkg.make_backend("cuda")), M, K, 4096, graph=True)
+    stream = pkg.RngStream(42, 2)
+    eng.start()
+    for k in range(K):
+        eng.enqueue_epoch(k, stream, S, next_samples=S if k + 1 < K else None)
+        if k >= 1:
+            torch.cuda.synchronize()
+            assert np.array_equal(eng.iterate((k - 1) * M, k - 1).cpu().numpy(), want[k - 1]), k
+            assert np.array_equal(eng.iterate(k * M, k - 1).cpu().numpy(), want[k]), k
+    eng.finish()

@@ -92,3 +92,6 @@ def test_newsvendor_sharded(ranks):
     for ex in ("nccl", "peer"):
         assert np.array_equal(r[f"nv_{ex}_w"], x)          # counts are exact integers
         np.testing.assert_allclose(r[f"nv_{ex}_obj"], objs, rtol=1e-13)
+    objs, x = orc.fw_run_newsvendor(task, 5, 4, 2000, orc.Stream(42, 2), schedule="linear")
+    assert np.array_equal(r["nv_lin_w"], x)
+    np.testing.assert_allclose(r["nv_lin_obj"], objs, rtol=1e-13)

@@ -150,22 +150,24 @@ def _cg(apply, g, n, cg_iters, dot, p):
     _vop(_SCALE, -1.0, g, g, r)                  # r = -1.0 * g
     dd = r.clone()
     hd = empty(n)
-    sc = torch.empty(3, dtype=F64, device="cuda")  # rr, dHd, rr_new
+    sc = torch.empty(3, dtype=F64, device="cuda")  # rr (ping), dHd, rr (pong)
     dot(r, r, sc[0:])
-    for _ in range(cg_iters):
+    for i in range(cg_iters):
+        # rr and rr_new swap slots each step (rr <- rr_new without a copy).  Once rr == 0
+        # the steps are no-ops, r stays put and every later r.r is 0 again: the oracle's
+        # `break`
+        rr, rr_new = (sc[0:], sc[2:]) if i % 2 == 0 else (sc[2:], sc[0:])
         apply(dd, hd)
         dot(dd, hd, sc[1:])
         _lib.call("simopt_cg_step1", _lib.stream_ptr(), _lib.ptr(p), _lib.ptr(r), _lib.ptr(dd),
-                  _lib.ptr(hd), _lib.ptr(sc[0:]), _lib.ptr(sc[1:]), n)
-        dot(r, r, sc[2:])
-        _lib.call("simopt_cg_step2", _lib.stream_ptr(), _lib.ptr(dd), _lib.ptr(r), _lib.ptr(sc[2:]),
-                  _lib.ptr(sc[0:]), n)
-        # rr <- rr_new unless CG already stopped (rr == 0 keeps every later step a no-op)
-        sc[0:1].copy_(torch.where(sc[0:1] == 0.0, sc[0:1], sc[2:3]))
+                  _lib.ptr(hd), _lib.ptr(rr), _lib.ptr(sc[1:]), n)
+        dot(r, r, rr_new)
+        _lib.call("simopt_cg_step2", _lib.stream_ptr(), _lib.ptr(dd), _lib.ptr(r), _lib.ptr(rr_new),
+                  _lib.ptr(rr), n)
     return p
 
 
-def _run(task, iterations, backend, step, label, fused=False, exchange="peer"):
+def _run(task, iterations, backend, step, label, fused=False, exchange="peer", on_iteration=None):
     data = task.data
     L = _Logistic(data, backend, exchange if fused else "nccl")
     n = L.d
@@ -195,6 +197,8 @@ def _run(task, iterations, backend, step, label, fused=False, exchange="peer"):
             L.xw(w)                               # shared by the loss and the next gradient
             L.loss_sum_from_t(sums[it:])
         _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[it:])))
+        if on_iteration is not None:  # e.g. bench.py records a CUDA event per iteration
+            on_iteration(it)
     if L.pr is not None:
         L.pr.check()
     trace = TraceBuilder()
@@ -205,11 +209,13 @@ def _run(task, iterations, backend, step, label, fused=False, exchange="peer"):
 
 
 def newton_cg(task, iterations: int, cg_iters: int, backend, fused: bool = True,
-              exchange: str = "peer") -> RunRecord:
-    """Newton-CG on the full-data logistic loss (BASELINE.json configs[2])."""
+              exchange: str = "peer", on_iteration=None) -> RunRecord:
+    """Newton-CG on the full-data logistic loss (BASELINE.json configs[2]).
+    on_iteration(it): called after iteration it is enqueued (host side)."""
     def step(L, g, p, dot):
         _cg(L.fused_hvp if fused else L.hvp, g, L.d, cg_iters, dot, p)
-    return _run(task, iterations, backend, step, "classification-newton-cg", fused, exchange)
+    return _run(task, iterations, backend, step, "classification-newton-cg", fused, exchange,
+                on_iteration)
 
 
 def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.Tensor:
@@ -254,7 +260,7 @@ def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.T
 
 
 def newton_explicit(task, iterations: int, cg_iters: int, backend, fused: bool = True,
-                    hessian: str = "auto", exchange: str = "peer") -> RunRecord:
+                    hessian: str = "auto", exchange: str = "peer", on_iteration=None) -> RunRecord:
     """Newton with the explicit X^T D X Hessian and a CG solve (BASELINE.json configs[4])."""
     d = task.data.n_features
     H = torch.empty(d, d, dtype=F64, device="cuda")
@@ -262,4 +268,5 @@ def newton_explicit(task, iterations: int, cg_iters: int, backend, fused: bool =
     def step(L, g, p, dot):
         logistic_hessian_device(L.data, L.dw, out=H, method=hessian)
         _cg(lambda v, out: backend.matvec_device(H, v, out=out), g, d, cg_iters, dot, p)
-    return _run(task, iterations, backend, step, "classification-newton-explicit", fused, exchange)
+    return _run(task, iterations, backend, step, "classification-newton-explicit", fused, exchange,
+                on_iteration)

@@ -403,8 +403,9 @@ int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bits, int64_t
                            double* scalar_out, const SimoptPeerReduce* peer);
 /* Binary X on the integer tensor cores (csrc/hessian_i8.cu): bits_to_u8t builds X^T as u8 in
  * sample blocks [np/ch][d][ch + 32] (ch, np from u8t_geometry; padded rows are zero); xtdx_i8 computes
- * H = (1/n) X^T diag(dw) X exactly for dw rounded to 2^-41 (5 x 8-bit limbs, u8 IMMA with
- * int32 accumulation); limbs = u8 scratch [5][np]. */
+ * H = (1/n) X^T diag(dw) X exactly for dw rounded to 2^-e (5 x 8-bit limbs, u8 IMMA with
+ * int32 accumulation; e from max(dw), read back once per call: not capturable), plus two
+ * exact-residual refinement passes when 2^-40 max(dw)/mean(dw) > 1e-11; limbs = u8 scratch [5][np]. */
 int simopt_u8t_geometry(int64_t n, int64_t* ch, int64_t* np);
 int simopt_bits_to_u8t(void* stream, const uint64_t* bits, int64_t rows, int64_t d, int64_t np,
                        uint8_t* out);
@@ -421,6 +422,9 @@ int simopt_logistic_xtdx_pair(void* stream, const uint8_t* xt, int64_t np, int64
  * accumulators resident in TMEM (128 x 96 tiles, one CTA per SM). */
 int simopt_logistic_xtdx_tc(void* stream, const uint8_t* xt, int64_t np, int64_t n, int64_t d,
                             const double* dw, uint8_t* limbs, double* h);
+/* Limb passes the calling thread's last xtdx_{i8,tc,tma,pair} call ran: 1, or 3 when the
+ * precision guard added the two residual refinement passes (2^-40 max(dw)/mean(dw) > 1e-11). */
+int simopt_xtdx_last_passes(void);
 /* simopt_logistic_xtdx on bit-packed features (DMMA fragments expanded in registers). */
 int simopt_logistic_xtdx_bits(void* stream, const uint64_t* xbits, const double* dw, int64_t n,
                               int64_t d, double* h);

@@ -94,6 +94,7 @@ SIGNATURES = {
     "simopt_logistic_xtdx_tc": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_logistic_xtdx_tma": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_logistic_xtdx_pair": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
+    "simopt_xtdx_last_passes": [],
     "simopt_mv_fw_tail": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32],
     "simopt_project_budget": [_vp, _vp, _vp, _d, _i64, _vp, _vp],
     "simopt_project_box": [_vp, _vp, _d, _d, _i64, _vp],
@@ -105,7 +106,8 @@ SIGNATURES = {
 }
 
 
-INT64_RESULT = {"simopt_peer_reduce_bytes"}  # size queries; every other entry point returns status
+# value-returning queries; every other entry point returns a status
+INT64_RESULT = {"simopt_peer_reduce_bytes", "simopt_xtdx_last_passes"}
 
 
 ABI_VERSION = 3  # csrc/capi.cu simopt_abi_version; bumped when an entry point's signature changes

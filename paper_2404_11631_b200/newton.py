@@ -225,7 +225,9 @@ def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.T
     "i8" / "tc" / "tma" -- bit-packed binary X only: exact 5-limb split of dw on the
     integer tensor cores, warp-level IMMA ("i8") or tcgen05 with TMEM accumulators, its
     operands by cp.async ("tc") or TMA ("tma") (csrc/hessian_i8.cu); "auto" = "tma" for
-    bit-packed data, else "dmma".
+    bit-packed data, else "dmma".  The limb methods quantise dw with an exponent taken
+    from max(dw) and add exact-residual refinement passes when the worst-case bound
+    2^-40 max(dw)/mean(dw) exceeds 1e-11 (`logistic_hessian_device.last_passes`).
     Row-sharded data: each rank's (1/N_loc) X_loc^T D X_loc is weighted by N_loc/N and
     summed over ranks with one allreduce of the d x d matrix."""
     d = data.n_features
@@ -244,6 +246,8 @@ def logistic_hessian_device(data, dw, out=None, method: str = "auto") -> torch.T
         _lib.call(fn,
                   _lib.stream_ptr(), _lib.ptr(xt), np_, nl, d, _lib.ptr(dw), _lib.ptr(limbs),
                   _lib.ptr(out))
+        # 1, or 3 when the precision guard refined a wide spread of dw (csrc/hessian_i8.cu)
+        logistic_hessian_device.last_passes = int(_lib.load().simopt_xtdx_last_passes())
     elif nl and data.packed:
         _lib.call("simopt_logistic_xtdx_bits", _lib.stream_ptr(), _lib.ptr(data.bits), _lib.ptr(dw),
                   nl, d, _lib.ptr(out))
@@ -270,3 +274,6 @@ def newton_explicit(task, iterations: int, cg_iters: int, backend, fused: bool =
         _cg(lambda v, out: backend.matvec_device(H, v, out=out), g, d, cg_iters, dot, p)
     return _run(task, iterations, backend, step, "classification-newton-explicit", fused, exchange,
                 on_iteration)
+
+
+logistic_hessian_device.last_passes = 0  # set by the limb methods

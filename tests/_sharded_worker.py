@@ -71,6 +71,21 @@ def main(rank, world, port, out):
     rec = fw_run(NewsvendorProblem(nv, b, shard=sh, exchange="peer"),
                  FwConfig(5, 4, 2000, p.RngStream(42, 2), "linear"), b)
     res["nv_lin_obj"], res["nv_lin_w"] = rec.objectives, rec.final_iterate
+    # BASELINE sizes (tests/golden/full_*.npz): C2 products sharded, graph engine + peer LMO
+    nvf = gen_newsvendor_instance(10_000, p.RngStream(42, 0))
+    rec = fw_run(NewsvendorProblem(nvf, b, shard=sh), FwConfig(3, 25, 100_000, p.RngStream(42, 2)), b)
+    res["full_c2_obj"], res["full_c2_w"] = rec.objectives, rec.final_iterate
+    del nvf
+    for fused in (False, True):  # C4's d at N = 2*10^4, rows sharded
+        mvf = gen_meanvar_instance(20_000, p.RngStream(42, 0))
+        rec = fw_run(MeanVarProblem(mvf, b, fused=fused, shard=sh),
+                     FwConfig(1, 25, 20_000, p.RngStream(42, 2)), b)
+        res[f"full_c4_{int(fused)}_obj"], res[f"full_c4_{int(fused)}_w"] = rec.objectives, rec.final_iterate
+    big = synth_classification(1_000, p.RngStream(42, 0), n_rows=1_000_000, shard=sh, packed=True)
+    for fused in (False, True):  # C3 rows sharded, bit-packed features
+        rec = newton_cg(LogisticTask(big), 2, 10, b, fused=fused)
+        res[f"full_c3_{int(fused)}_obj"], res[f"full_c3_{int(fused)}_w"] = rec.objectives, rec.final_iterate
+    del big
     from paper_2404_11631_b200.sharding import PeerMailbox
     res["nv_peer_used"] = np.array([PeerMailbox.get(sh) is not None])
     np.savez(os.path.join(out, f"rank{rank}.npz"), **res)

@@ -95,3 +95,24 @@ def test_newsvendor_sharded(ranks):
     objs, x = orc.fw_run_newsvendor(task, 5, 4, 2000, orc.Stream(42, 2), schedule="linear")
     assert np.array_equal(r["nv_lin_w"], x)
     np.testing.assert_allclose(r["nv_lin_obj"], objs, rtol=1e-13)
+
+
+def test_full_size_sharded(ranks, golden):
+    """BASELINE sizes with two ranks: C2 (products, peer-memory LMO, graph epochs) and the
+    exact C3/C4 modes bit for bit vs the reference's trajectories; fused within 1e-8."""
+    r = ranks[0]
+    g = golden("full_c2")
+    assert np.array_equal(r["full_c2_w"], g["final_iterate"])
+    # the recorded objective sums the two shards' exact-tree sums (not the reference's
+    # one 4096-chunk tree over all d products): last-bit differences only
+    np.testing.assert_allclose(r["full_c2_obj"], g["objectives"], rtol=1e-13)
+    g = golden("full_c4")
+    assert np.array_equal(r["full_c4_0_obj"], g["objectives"])
+    assert np.array_equal(r["full_c4_0_w"], g["final_iterate"])
+    np.testing.assert_allclose(r["full_c4_1_obj"], g["objectives"], rtol=1e-8)
+    assert _rel(r["full_c4_1_w"], g["final_iterate"]) < 1e-8
+    g = golden("full_c3")
+    assert np.array_equal(r["full_c3_0_obj"], g["objectives"])
+    assert np.array_equal(r["full_c3_0_w"], g["final_iterate"])
+    np.testing.assert_allclose(r["full_c3_1_obj"], g["objectives"], rtol=1e-8)
+    assert _rel(r["full_c3_1_w"], g["final_iterate"]) < 1e-8

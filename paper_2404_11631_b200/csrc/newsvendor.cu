@@ -15,6 +15,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 #include "fw.cuh"
 #include "glibc_math.cuh"
@@ -149,6 +152,184 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
       for (int l = threadIdx.x; l < len; l += blockDim.x) dst[l] = sorted_[l];
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised resample.  Generation is bound by the heavy FMA pipe (the Philox
+// 64x64->128 products); the scan, scatter and store use the ALU and LSU.  Eight producer
+// warps only generate: segment k's keys into raw[k&1] and its bucket counts into
+// hist[k&1]; four consumer warps scan, scatter into bucket order and store.  The two
+// roles meet at named barriers (full[slot]: producers arrive, consumers wait; empty[slot]:
+// consumers arrive once they have read raw[slot] and re-zeroed hist[slot], producers
+// wait), so producer warps never stop at a CTA-wide barrier and the heavy pipe keeps a
+// steady supply of multiplies while the consumers' memory work runs beside it.
+// Measured at C2 (tools/nv_resample_ab.py): 8 producer + 4 consumer warps, 3 CTAs per SM
+// (48 registers) 3.76 ms; 12 + 4 warps 3.88; 16 + 4 at 2 CTAs per SM 3.97; consumers also
+// counting the buckets 3.88; the single-role k_nv_resample 4.12; a software-pipelined
+// variant (generate i || scatter i-1 in one phase) 4.38-4.62.
+constexpr int kWsProd = 256, kWsCons = 128, kWsPerSm = 3;
+
+struct WsSmem {
+  uint32_t raw[2][NV_SEG];
+  uint32_t sorted[NV_SEG];
+  int hist[2][NV_B];
+  int wsum[kWsCons / 32];
+};  // 56 KB: up to three CTAs per SM
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <bool kNoCarry>
+__global__ void __launch_bounds__(kWsProd + kWsCons, kWsPerSm)
+    k_nv_resample_ws(const phx_keys rk, const phx_pre pre, uint64_t clo, uint64_t chi, int64_t d,
+                     int64_t S, int nseg, uint32_t* __restrict__ keys, uint16_t* __restrict__ off) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WsSmem& sm = *reinterpret_cast<WsSmem*>(smem_raw);
+  constexpr int kBucketShift = 12 + NV_QBITS - 10;
+  constexpr int kWsThreads = kWsProd + kWsCons;
+  const int tid = threadIdx.x;
+  const int64_t nblk = d * nseg;
+  for (int i = tid; i < 2 * NV_B; i += kWsThreads) (&sm.hist[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t gq = gridDim.x / nseg;
+  const int gr = (int)(gridDim.x - gq * nseg);
+  int64_t j = blockIdx.x / nseg;
+  int s = (int)(blockIdx.x - j * nseg);
+  if (tid < kWsProd) {
+    // ---- producers: Philox4x64-10 + fp32 key + bucket count, segment after segment
+    for (int64_t blk = blockIdx.x, k = 0; blk < nblk; blk += gridDim.x, ++k) {
+      const int p = (int)(k & 1);
+      if (k >= 2) named_sync(3 + p, kWsThreads);  // consumers are done with slot p
+      const int64_t e0 = (int64_t)s * NV_SEG;
+      const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
+      const int64_t i0 = j * S + e0;
+      const bool aligned = ((i0 & 3) == 0) && ((len & 3) == 0);
+      const int64_t q0 = i0 >> 2, q1 = (i0 + len - 1) >> 2;
+      const int nq = (int)(q1 - q0);
+      const uint64_t c0 = clo + (uint64_t)q0 + 1;
+      const int lbase = (int)((q0 << 2) - i0);
+      uint32_t* raw = sm.raw[p];
+      int* hist = sm.hist[p];
+      for (int t = tid; t <= nq; t += kWsProd) {
+        const phx4 w = kNoCarry ? philox4x64_10_rk_c0(c0 + (uint64_t)t, rk, pre)
+                                : philox4x64_10_rk(stream_block_counter(clo, chi, (uint64_t)(q0 + t)), rk);
+        float z[4];
+        nv_approx_pair(w.v[0], w.v[1], &z[0], &z[1]);
+        nv_approx_pair(w.v[2], w.v[3], &z[2], &z[3]);
+        const int l0 = lbase + (t << 2);
+        if (aligned) {
+          uint32_t kk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            kk[u] = nv_key(z[u], (uint32_t)(l0 + u));
+            atomicAdd(&hist[kk[u] >> kBucketShift], 1);
+          }
+          reinterpret_cast<uint4*>(raw)[l0 >> 2] = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int l = l0 + u;
+            if (l >= 0 && l < len) {
+              const uint32_t key = nv_key(z[u], (uint32_t)l);
+              raw[l] = key;
+              atomicAdd(&hist[key >> kBucketShift], 1);
+            }
+          }
+        }
+      }
+      named_arrive(1 + p, kWsThreads);  // slot p holds segment blk
+      j += gq;
+      s += gr;
+      if (s >= nseg) {
+        s -= nseg;
+        ++j;
+      }
+    }
+    return;
+  }
+  // ---- consumers: scan, scatter into bucket order, store
+  const int ct = tid - kWsProd, lane = ct & 31, cw = ct >> 5;
+  constexpr int kPer = NV_B / kWsCons;  // 8 buckets per thread
+  for (int64_t blk = blockIdx.x, k = 0; blk < nblk; blk += gridDim.x, ++k) {
+    const int p = (int)(k & 1);
+    const int64_t e0 = (int64_t)s * NV_SEG;
+    const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
+    const bool aligned = (((j * S + e0) & 3) == 0) && ((len & 3) == 0);
+    named_sync(1 + p, kWsThreads);  // segment blk is in slot p
+    int* hist = sm.hist[p];
+    const uint32_t* raw = sm.raw[p];
+    int v[kPer];
+    {
+      const int4 a = reinterpret_cast<const int4*>(hist)[2 * ct];
+      const int4 b = reinterpret_cast<const int4*>(hist)[2 * ct + 1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+    int run = 0;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) run += v[u];
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) sm.wsum[cw] = incl;
+    named_sync(5, kWsCons);
+    int wpre = lane < cw ? sm.wsum[lane] : 0;
+#pragma unroll
+    for (int o = 2; o; o >>= 1) wpre += __shfl_xor_sync(0xffffffffu, wpre, o);  // lanes < 4
+    int base = incl - run + __shfl_sync(0xffffffffu, wpre, 0);
+    int st[kPer];
+    uint32_t pk[kPer / 2];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      st[u] = base;
+      base += v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kPer / 2; ++u) pk[u] = (uint32_t)st[2 * u] | ((uint32_t)st[2 * u + 1] << 16);
+    reinterpret_cast<int4*>(hist)[2 * ct] = make_int4(st[0], st[1], st[2], st[3]);
+    reinterpret_cast<int4*>(hist)[2 * ct + 1] = make_int4(st[4], st[5], st[6], st[7]);
+    reinterpret_cast<uint4*>(off + (j * nseg + s) * (int64_t)NV_B)[ct] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    named_sync(5, kWsCons);  // cursors complete
+    if (aligned) {
+      for (int l4 = ct; l4 < (len >> 2); l4 += kWsCons) {
+        const uint4 k4 = reinterpret_cast<const uint4*>(raw)[l4];
+        sm.sorted[atomicAdd(&hist[k4.x >> kBucketShift], 1)] = k4.x;
+        sm.sorted[atomicAdd(&hist[k4.y >> kBucketShift], 1)] = k4.y;
+        sm.sorted[atomicAdd(&hist[k4.z >> kBucketShift], 1)] = k4.z;
+        sm.sorted[atomicAdd(&hist[k4.w >> kBucketShift], 1)] = k4.w;
+      }
+    } else {
+      for (int l = ct; l < len; l += kWsCons) {
+        const uint32_t key = raw[l];
+        sm.sorted[atomicAdd(&hist[key >> kBucketShift], 1)] = key;
+      }
+    }
+    named_sync(5, kWsCons);  // scatter complete: raw[p] read, cursors final, sorted full
+    reinterpret_cast<int4*>(hist)[2 * ct] = make_int4(0, 0, 0, 0);
+    reinterpret_cast<int4*>(hist)[2 * ct + 1] = make_int4(0, 0, 0, 0);
+    named_arrive(3 + p, kWsThreads);  // slot p free for the producers
+    uint32_t* dst = keys + j * S + e0;
+    if (aligned) {
+      for (int l4 = ct; l4 < (len >> 2); l4 += kWsCons)
+        reinterpret_cast<uint4*>(dst)[l4] = reinterpret_cast<const uint4*>(sm.sorted)[l4];
+    } else {
+      for (int l = ct; l < len; l += kWsCons) dst[l] = sm.sorted[l];
+    }
+    named_sync(5, kWsCons);  // sorted stored: the next scatter may overwrite it
+    j += gq;
+    s += gr;
+    if (s >= nseg) {
+      s -= nseg;
+      ++j;
+    }
   }
 }
 
@@ -499,22 +680,52 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   const int64_t nseg = ceil_div(S, NV_SEG);
   const int64_t nblk = d * nseg;
   SIMOPT_REQUIRE(nblk < (1LL << 31), SIMOPT_E_CONFIG, "too many segments");
-  // Persistent grid of kResampleMinBlocks CTAs per SM: one full wave (the step kernels
-  // of the previous epoch, at high stream priority, still find room as CTAs retire).
-  // Measured at C2: 6 per SM at 32 registers 5.45k FW it/s vs 5 per SM at 46 registers
-  // 5.33k.
-  // SIMOPT_NV_RESAMPLE_GRID overrides it for tuning sweeps.
-  static const int64_t cap = [] {
-    const char* e = getenv("SIMOPT_NV_RESAMPLE_GRID");
-    return e ? atoll(e) : (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks;
-  }();
-  const int64_t grid = nblk < cap ? nblk : cap;
   const phx_keys rk = phx_round_keys(seed, sid);
   // blocks q = 0 .. ceil(d*S/4)-1 use counters clo+1 ..; when they stay within word 0
   // (the span resets of stream_block_counter then add no carry either) the first two
   // Philox rounds are partly constant (philox4x64_10_rk_c0)
   const phx_pre pre = phx_precompute(chi, rk);
-  if (phx_no_carry(clo, (uint64_t)ceil_div(d * S, 4)))
+  const bool no_carry = phx_no_carry(clo, (uint64_t)ceil_div(d * S, 4));
+  // SIMOPT_NV_RESAMPLE=1: the single-role kernel k_nv_resample (comparison); default: the
+  // warp-specialised k_nv_resample_ws (3.76 vs 4.12 ms at C2).  Both are persistent grids
+  // of one full wave; the step kernels of the previous epoch (high stream priority) run in
+  // the registers and shared memory left beside it (ws: 3 x 56 KB shared, 55 K registers
+  // per SM) and on the SMs that finish their share first.
+  const char* ev = getenv("SIMOPT_NV_RESAMPLE");
+  if (!(ev && atoi(ev) == 1)) {
+    const int64_t g = nblk < (int64_t)SIMOPT_NUM_SMS * kWsPerSm ? nblk : (int64_t)SIMOPT_NUM_SMS * kWsPerSm;
+    const size_t smem = sizeof(WsSmem);
+    static std::mutex mu;
+    static std::vector<int> ready;  // devices whose shared-memory limit is raised
+    int dev = 0;
+    SIMOPT_CUDA(cudaGetDevice(&dev));
+    cudaError_t attr_err = cudaSuccess;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      bool have = false;
+      for (int x : ready) have |= x == dev;
+      if (!have) {
+        attr_err = cudaFuncSetAttribute(k_nv_resample_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem);
+        if (attr_err == cudaSuccess)
+          attr_err = cudaFuncSetAttribute(k_nv_resample_ws<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (attr_err == cudaSuccess) ready.push_back(dev);
+      }
+    }
+    SIMOPT_CUDA(attr_err);
+    if (no_carry)
+      k_nv_resample_ws<true><<<(unsigned)g, kWsProd + kWsCons, smem, as_stream(stream)>>>(
+          rk, pre, clo, chi, d, S, (int)nseg, keys, off);
+    else
+      k_nv_resample_ws<false><<<(unsigned)g, kWsProd + kWsCons, smem, as_stream(stream)>>>(
+          rk, pre, clo, chi, d, S, (int)nseg, keys, off);
+    SIMOPT_CHECK_LAUNCH("k_nv_resample_ws");
+    return SIMOPT_OK;
+  }
+  const int64_t cap = (int64_t)SIMOPT_NUM_SMS * kResampleMinBlocks;
+  const int64_t grid = nblk < cap ? nblk : cap;
+  if (no_carry)
     k_nv_resample<true><<<(unsigned)grid, kResampleThreads, 0, as_stream(stream)>>>(
         rk, pre, clo, chi, d, S, (int)nseg, keys, off);
   else

@@ -250,3 +250,20 @@ def test_graph_engine_epoch_start_iterate(pkg):
             assert np.array_equal(eng.iterate((k - 1) * M, k - 1).cpu().numpy(), want[k - 1]), k
             assert np.array_equal(eng.iterate(k * M, k - 1).cpu().numpy(), want[k]), k
     eng.finish()
+
+
+@pytest.mark.parametrize("d,S", [(2000, 100_000), (301, 5001), (64, 4096), (7, 3)])
+def test_resample_kernels_agree(pkg, d, S, monkeypatch):
+    """The warp-specialised resample (default) and the single-role kernel write the same
+    layout: identical bucket starts, and the same keys inside every bucket."""
+    from paper_2404_11631_b200.instances import gen_newsvendor_instance
+    from paper_2404_11631_b200.tasks import NewsvendorProblem
+    prob = NewsvendorProblem(gen_newsvendor_instance(d, pkg.RngStream(42, 0)), pkg.make_backend("cuda"))
+    out = []
+    for variant in ("1", "0"):
+        monkeypatch.setenv("SIMOPT_NV_RESAMPLE", variant)
+        prob.dev.resample(pkg.RngStream(9, 4, (1 << 64) - 1000), S)   # 64-bit carry path too
+        keys = (prob.dev.keys.view(torch.int32).to(torch.int64) & 0xFFFFFFFF).view(d, S)
+        canon = torch.cat([torch.sort(keys[:, s0:s0 + 4096], dim=1).values for s0 in range(0, S, 4096)], 1)
+        out.append((prob.dev.off.clone(), canon))
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])

@@ -441,10 +441,6 @@ __device__ __forceinline__ double nv_grad_value(int64_t cnt, int64_t S, double k
 
 namespace {
 
-#ifndef NV_ITER_WARPS
-#define NV_ITER_WARPS 8
-#endif
-constexpr int kIterWarps = NV_ITER_WARPS;  // products (warps) per step block
 
 // Fused product-shard LMO exchange over NVLink peer memory (one thread of the step's
 // last block): publish (value, global index, vertex value) into slot `rank` of every
@@ -528,7 +524,9 @@ __device__ __noinline__ void nv_peer_exchange(const NvPeerArgs a, ArgMin r, doub
 //       previous LMO (frank_wolfe.py:69-82), record x_j < -FEAS_TOL, objective term;
 //   (2) if do_grad: g_j at the (new) x_j, LMO values g_j * (C / c_j), argmin over all
 //       products (last-block reduction), NaN flag.
-__global__ void __launch_bounds__(kIterWarps * 32, 24 / kIterWarps)
+// kIterWarps products (warps) per block.
+template <int kIterWarps, int kMinBlocks>
+__global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
     k_nv_iter(NvIterArgs a) {
   __shared__ ArgMin warp_best[kIterWarps];
   __shared__ int64_t queues[kIterWarps][kQueue];
@@ -761,10 +759,15 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   NvIterArgs a = *args;
   // gradient steps: one resident wave of blocks pulling products from a counter; update-only
   // steps: a static split
-  const int64_t cap = a.do_grad ? (int64_t)(24 / kIterWarps) * SIMOPT_NUM_SMS : 16 * SIMOPT_NUM_SMS;
-  const int grid = (int)(ceil_div(a.d, kIterWarps) < cap ? ceil_div(a.d, kIterWarps) : cap);
+  // Eight warps per block, three blocks per SM (80 registers).  Measured at C2 with the
+  // next epoch's resample running beside the steps (bench.py, 30 epochs): 5.80k FW it/s;
+  // four-warp blocks (which fit beside the resample's three CTAs per SM) 5.63k; eight
+  // warps squeezed to 40 registers 5.87k (within noise, with spills).
+  constexpr int kW = 8;
+  const int64_t cap = a.do_grad ? (int64_t)3 * SIMOPT_NUM_SMS : 16 * SIMOPT_NUM_SMS;
+  const int grid = (int)(ceil_div(a.d, kW) < cap ? ceil_div(a.d, kW) : cap);
   SIMOPT_REQUIRE(grid <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
-  k_nv_iter<<<grid, kIterWarps * 32, 0, as_stream(stream)>>>(a);
+  k_nv_iter<kW, 3><<<grid, kW * 32, 0, as_stream(stream)>>>(a);
   SIMOPT_CHECK_LAUNCH("k_nv_iter");
   return SIMOPT_OK;
 }

@@ -167,6 +167,10 @@ int simopt_ecdf_count_sorted(void* stream, const double* samples, int64_t rows, 
 /* nv_gradient_hat epilogue (tasks.py:158-160): g = (k - v) + ((h + v) * (counts / S)). */
 int simopt_nv_grad_from_counts(void* stream, const int64_t* counts, int64_t S, const double* k,
                                const double* h, const double* v, int64_t d, double* g);
+/* nv_gradient_exact (tasks.py:163-171): (k - v) + ((h + v) * Phi((x - mu) / sigma)), the
+ * CDF as normal_cdf_block (_kernels.py:204-207) with glibc's erf. */
+int simopt_nv_grad_exact(void* stream, const double* x, const double* mu, const double* sigma,
+                         const double* k, const double* h, const double* v, int64_t d, double* g);
 
 /* Device-resident FW state for one newsvendor run. */
 typedef struct NvState {

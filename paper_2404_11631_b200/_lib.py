@@ -51,6 +51,7 @@ SIGNATURES = {
     "simopt_nv_iter": [_vp, _vp],
     "simopt_ecdf_count_sorted": [_vp, _vp, _i64, _i64, _vp, _vp],
     "simopt_nv_grad_from_counts": [_vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp],
+    "simopt_nv_grad_exact": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     "simopt_nv_cost_terms": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     "simopt_logistic_resid": [_vp, _vp, _vp, _vp, _i64, _vp],
     "simopt_logistic_hvp_weights": [_vp, _vp, _vp, _i64, _vp],

@@ -38,16 +38,17 @@ class CudaBackend:
 
     # -- range scheduling (backend.py:68-76) ----------------------------------
     def run_blocks(self, n_units: int, fn, work_per_unit: int = 1):
-        """Host-callback scheduling hook of the reference API.
+        """The reference API's host-callback hook (backend.py:68-76).
 
-        Reference task code passes Python closures over numba kernels here.  The
-        cuda backend's own operations never use it; for foreign callbacks it
-        simply calls ``fn(0, n_units)`` (the partition never affects results,
-        backend.py:68-76).
+        Reference task code passes closures over its numba CPU kernels here.  The cuda
+        backend never runs them: that would be a silent CPU fallback.  The reference's
+        task, sampling and SQN functions are routed to the device implementations
+        instead (``sobench_plugin.install()``); anything else raises.
         """
-        if n_units <= 0:
-            return
-        fn(0, n_units)
+        raise ConfigurationError(
+            "the cuda backend does not run host callbacks (backend.run_blocks): call this "
+            "package's device implementation, or install paper_2404_11631_b200.sobench_plugin "
+            "so sobench's task functions route to it")
 
     # -- reductions (backend.py:80-141) ----------------------------------------
     def dot_device(self, x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None):

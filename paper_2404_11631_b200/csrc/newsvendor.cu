@@ -854,7 +854,32 @@ __global__ void k_nv_grad_counts(const int64_t* __restrict__ cnt, int64_t S,
        j += (int64_t)gridDim.x * blockDim.x)
     g[j] = nv_grad_value(cnt[j], S, k[j], h[j], v[j]);
 }
+
+// nv_gradient_exact (tasks.py:163-171): z = (x - mu)/sigma, cdf = 0.5 (1 + erf(z SQRT1_2))
+// (normal_cdf_block, _kernels.py:204-207, glibc erf), g = (k - v) + ((h + v) cdf)
+__global__ void k_nv_grad_exact(const double* __restrict__ x, const double* __restrict__ mu,
+                                const double* __restrict__ sigma, const double* __restrict__ k,
+                                const double* __restrict__ h, const double* __restrict__ v, int64_t d,
+                                double* __restrict__ g) {
+  const double SQRT1_2 = 0.7071067811865476;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < d;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double z = (x[j] - mu[j]) / sigma[j];
+    const double cdf = 0.5 * (1.0 + glibc_erf(z * SQRT1_2, simopt_exptab_dev));
+    g[j] = (k[j] - v[j]) + ((h[j] + v[j]) * cdf);
+  }
+}
 }  // namespace
+
+extern "C" int simopt_nv_grad_exact(void* stream, const double* x, const double* mu, const double* sigma,
+                                    const double* k, const double* h, const double* v, int64_t d,
+                                    double* g) {
+  if (d == 0) return SIMOPT_OK;
+  k_nv_grad_exact<<<(int)(ceil_div(d, 256) < 4096 ? ceil_div(d, 256) : 4096), 256, 0,
+                    as_stream(stream)>>>(x, mu, sigma, k, h, v, d, g);
+  SIMOPT_CHECK_LAUNCH("k_nv_grad_exact");
+  return SIMOPT_OK;
+}
 
 extern "C" int simopt_ecdf_count_sorted(void* stream, const double* samples, int64_t rows,
                                         int64_t s, const double* x, int64_t* counts) {

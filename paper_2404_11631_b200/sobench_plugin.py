@@ -54,8 +54,187 @@ def install(sobench_pkg=None):
     bench.run_cell = run_cell
     if hasattr(sobench_pkg, "make_backend"):
         sobench_pkg.make_backend = make_backend
+    _unify_errors()
+    _route_functions()
     _INSTALLED[id(sobench_pkg)] = True
     return sobench_pkg
+
+
+_ERROR_NAMES = ("SobenchError", "DimensionMismatch", "ConfigurationError", "EmptyRequest",
+                "InsufficientSamples", "InvalidGradient", "InvalidConstraint", "SolverStall",
+                "UndefinedMetric", "DegeneratePair", "RunAborted")
+
+
+def _unify_errors():
+    """Make what the device path raises catchable as sobench's exceptions (errors.py:4-53).
+
+    For every class, a subclass of both ours and sobench's (same name) replaces ours in
+    this package's modules and in the status-code table, so ``except
+    sobench.errors.RunAborted`` in reference code and ``except
+    paper_2404_11631_b200.errors.RunAborted`` both catch it.  (Python's ``except``
+    matches the real class hierarchy; virtual subclasses do not count.)"""
+    import sobench.errors as se
+
+    from . import errors as oe
+    if issubclass(oe.RunAborted, se.RunAborted):
+        return
+    new = {}
+    for name in _ERROR_NAMES:
+        ours, ref = getattr(oe, name), getattr(se, name)
+        bases = (ours, ref) if name == "SobenchError" else (ours, new[oe.SobenchError], ref)
+        new[ours] = type(name, bases, {"__module__": oe.__name__, "__doc__": ours.__doc__})
+    dev = oe.DeviceError
+    new[dev] = type("DeviceError", (dev, new[oe.SobenchError]),
+                    {"__module__": oe.__name__, "__doc__": dev.__doc__})
+    for mod in list(sys.modules.values()):
+        if not getattr(mod, "__name__", "").startswith(__package__ or "paper_2404_11631_b200"):
+            continue
+        for attr, val in list(vars(mod).items()):
+            if isinstance(val, type) and val in new:
+                setattr(mod, attr, new[val])
+            elif isinstance(val, dict) and any(isinstance(v, type) and v in new for v in val.values()):
+                for k, v in list(val.items()):
+                    if isinstance(v, type) and v in new:
+                        val[k] = new[v]
+
+
+# ---------------------------------------------------------------------------
+# The reference's task, sampling and SQN functions take a backend argument; given the
+# cuda backend they run this package's device implementation (the reference's numba
+# kernels reach the CPU through backend.run_blocks, which the cuda backend refuses).
+# Arguments and results are converted between the reference's dataclasses and ours.
+def _our_stream(st):
+    from .sampling import RngStream
+    return RngStream(st.seed, st.stream_id, st.counter)
+
+
+def _with_stream(fn, st, *args):
+    """Run fn(our_stream, *args) and move the reference stream's counter along with it."""
+    ours = _our_stream(st)
+    out = fn(ours, *args)
+    st.counter = ours.counter
+    return out
+
+
+def _our_spec(spec):
+    from .sampling import GaussianSpec
+    return GaussianSpec(mean=spec.mean, diag_std=spec.diag_std, chol_factor=spec.chol_factor)
+
+
+def _our_data(data):
+    from ._tensors import mat_dev, vec_dev
+    from .sampling import ClassificationData
+    key = (id(data), id(data.features), id(data.labels))
+    hit = _DATA_CACHE.get(id(data))
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    ours = ClassificationData(features=mat_dev(data.features), labels=vec_dev(data.labels),
+                              true_weights=data.true_weights)
+    if len(_DATA_CACHE) >= 4:  # a few recent data sets (an SQN run reuses one many times)
+        _DATA_CACHE.pop(next(iter(_DATA_CACHE)))
+    _DATA_CACHE[id(data)] = (key, ours, data)  # keeps `data` alive while cached
+    return ours
+
+
+_DATA_CACHE = {}
+
+
+def _our_sample_set(ss):
+    from ._tensors import mat_dev, vec_dev
+    from .tasks import MeanVarSampleSet
+    return MeanVarSampleSet(mat_dev(ss.samples), vec_dev(ss.mean), ss.count)
+
+
+def _ref_record(rec):
+    import sobench.records as sr
+    return sr.RunRecord(task=rec.task, size=rec.size, backend=rec.backend, rep=rec.rep, seed=rec.seed,
+                        iterations=rec.iterations, objectives=rec.objectives,
+                        elapsed_ns=rec.elapsed_ns, final_iterate=rec.final_iterate,
+                        warnings=list(rec.warnings))
+
+
+def _is_cuda(backend):
+    return getattr(backend, "kind", None) == "cuda"
+
+
+def _route_functions():
+    import sobench.sampling as ss_
+    import sobench.sqn as sq
+    import sobench.tasks as st
+
+    from . import sampling as os_
+    from . import sqn as oq
+    from . import tasks as ot
+    from ._tensors import to_host
+
+    def route(mod, name, backend_pos, impl):
+        ref = getattr(mod, name)
+        if getattr(ref, "_simopt_routed", False):
+            return
+
+        def fn(*args, **kwargs):
+            backend = kwargs.get("backend", args[backend_pos] if len(args) > backend_pos else None)
+            if _is_cuda(backend):
+                return impl(*args, **kwargs)
+            return ref(*args, **kwargs)
+        fn.__name__, fn.__doc__, fn.__wrapped__ = ref.__name__, ref.__doc__, ref
+        fn._simopt_routed = True
+        # rebind the name in every sobench module that imported it
+        import sys as _sys
+        for m in list(_sys.modules.values()):
+            if getattr(m, "__name__", "").startswith("sobench") and getattr(m, name, None) is ref:
+                setattr(m, name, fn)
+
+    route(ss_, "uniform01", 2, lambda stream, n, backend=None: _with_stream(os_.uniform01, stream, n))
+    route(ss_, "standard_normal", 2,
+          lambda stream, n, backend=None: _with_stream(os_.standard_normal, stream, n))
+    route(ss_, "sample_returns", 3, lambda spec, n, stream, backend=None: _with_stream(
+        lambda s_, sp, n_: os_.sample_returns(sp, n_, s_), stream, _our_spec(spec), n))
+    route(ss_, "sample_demands", 4, lambda mu, sigma, n, stream, backend=None: _with_stream(
+        lambda s_, m, sg, n_: ot.sample_demands(m, sg, n_, s_), stream, mu, sigma, n))
+
+    def synth(n, stream, backend=None):
+        data = _with_stream(lambda s_, n_: os_.synth_classification(n_, s_), stream, n)
+        return ss_.ClassificationData(features=to_host(data.features), labels=to_host(data.labels),
+                                      true_weights=to_host(data.true_weights))
+    route(ss_, "synth_classification", 2, synth)
+
+    def build(samples, backend):
+        ours = ot.build_sample_set(samples, backend)
+        return st.MeanVarSampleSet(samples=to_host(ours.samples), mean=to_host(ours.mean),
+                                   centered=to_host(ours.centered), count=ours.count)
+    route(st, "build_sample_set", 1, build)
+    route(st, "mv_objective", 2, lambda w, ss, backend: ot.mv_objective(w, _our_sample_set(ss), backend))
+    route(st, "mv_gradient", 2, lambda w, ss, backend: ot.mv_gradient(w, _our_sample_set(ss), backend))
+    route(st, "nv_gradient_hat", 3, ot.nv_gradient_hat)
+    route(st, "nv_gradient_exact", 2, ot.nv_gradient_exact)
+    route(st, "nv_objective_exact", 2, ot.nv_objective_exact)
+    route(st, "logistic_loss", 3, lambda w, data, idx, backend: ot.logistic_loss(w, _our_data(data), idx, backend))
+    route(st, "logistic_gradient", 3,
+          lambda w, data, idx, backend: ot.logistic_gradient(w, _our_data(data), idx, backend))
+    route(st, "logistic_hvp", 4,
+          lambda w, v, data, idx, backend: ot.logistic_hvp(w, v, _our_data(data), idx, backend))
+
+    def hupd(pairs, t, memory, backend):
+        ours = [oq.CorrectionPair(p.s, p.y, p.curvature) for p in pairs]
+        return to_host(oq.hessian_update(ours, t, memory, backend))
+    route(sq, "hessian_update", 3, hupd)
+
+    def sqn(task, config, backend, *, task_label="classification", size=None, rep=0):
+        cfg = oq.SqnConfig(config.pair_every, config.memory, config.beta, config.grad_batch,
+                           config.hess_batch, config.iterations, _our_stream(config.stream))
+        try:
+            rec = oq.sqn_run(ot.LogisticTask(_our_data(task.data)), cfg, backend, task_label=task_label,
+                             size=size, rep=rep)
+        except Exception as exc:  # RunAborted: hand the reference's record type back
+            partial = getattr(exc, "partial_record", None)
+            if partial is not None:
+                exc.partial_record = _ref_record(partial)
+            raise
+        finally:
+            config.stream.counter = cfg.stream.counter
+        return _ref_record(rec)
+    route(sq, "sqn_run", 2, sqn)
 
 
 def _run_cell_cuda(config, size, rep, bench):

@@ -777,6 +777,19 @@ def nv_gradient_hat(x, demands, task: NewsvendorTask, backend):
     return like_input(x, g)
 
 
+def nv_gradient_exact(x, task: NewsvendorTask, backend):
+    """k - v + (h+v) * Phi((x - mu)/sigma), the exact Gaussian CDF (tasks.py:163-171)."""
+    xd = vec_dev(x)
+    if xd.numel() != task.dimension:
+        raise DimensionMismatch("stock vector length != product count")
+    dev = [to_dev(a) for a in (task.demand_mean, task.demand_std, task.unit_cost,
+                               task.holding_cost, task.selling_value)]
+    g = empty(xd.numel())
+    _lib.call("simopt_nv_grad_exact", _lib.stream_ptr(), _lib.ptr(xd), *(_lib.ptr(t) for t in dev),
+              xd.numel(), _lib.ptr(g))
+    return like_input(x, g)
+
+
 def nv_objective_exact(x, task: NewsvendorTask, backend) -> float:
     """Expected cost under Gaussian demand, fixed-tree sum (tasks.py:174-188)."""
     xd = vec_dev(x)

@@ -65,3 +65,30 @@ def test_run_bench_writes_reference_csv(sob, tmp_path):
     bench.run_bench(cfg)
     names = os.listdir(tmp_path)
     assert "trace_newsvendor_100_cuda_rep0.csv" in names and "trace_newsvendor_100_cuda_rep1.csv" in names
+
+
+def test_errors_unified(sob):
+    """After install(), what the device path raises is also sobench's exception class."""
+    import sobench.errors as se
+    import paper_2404_11631_b200.errors as oe
+    from paper_2404_11631_b200 import _lib
+    for name in ("DimensionMismatch", "ConfigurationError", "EmptyRequest", "InsufficientSamples",
+                 "InvalidGradient", "InvalidConstraint", "SolverStall", "DegeneratePair", "RunAborted"):
+        assert issubclass(getattr(oe, name), getattr(se, name)), name
+    assert issubclass(oe.DeviceError, se.SobenchError)
+    for code, cls in _lib.STATUS_TO_ERROR.items():
+        assert issubclass(cls, se.SobenchError), code
+    with pytest.raises(se.RunAborted) as ei:
+        raise oe.RunAborted("x", partial_record="p")
+    assert ei.value.partial_record == "p"
+
+
+def test_run_blocks_refuses_host_callbacks(sob):
+    """No silent CPU fallback: the cuda backend never runs the reference's numba callbacks."""
+    import sobench.errors as se
+    from paper_2404_11631_b200.backend import CudaBackend
+    b = CudaBackend.__new__(CudaBackend)  # no device needed to check the refusal
+    ran = []
+    with pytest.raises(se.ConfigurationError):
+        b.run_blocks(10, lambda lo, hi: ran.append((lo, hi)))
+    assert ran == []

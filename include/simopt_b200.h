@@ -454,6 +454,23 @@ int simopt_fused_rows(void* stream, int mode, const double* x, int64_t rows, int
                       double col_scale, int accumulate, int raw, double* t_out, double* dw_out,
                       double* col_out, double* scalar_out, const SimoptPeerReduce* peer);
 
+/* ---- NCCL communicator (csrc/comm.cu; SURVEY 8(b) "NCCL communicator handle init/teardown").
+ * Replaces the reference's in-process data-parallel split (sobench/backend.py:178-204) for
+ * one process per GPU.  libnccl.so.2 is resolved at run time (the copy torch loaded, else the
+ * loader path); without it every call returns SIMOPT_E_CUDA.  Rank 0 creates the 128-byte
+ * unique id, the host broadcasts it (any channel), every rank calls comm_init.  Collectives
+ * are enqueued on `stream` and are asynchronous like every other entry point. */
+int simopt_comm_version(int* version);
+int simopt_comm_unique_id(uint8_t* id128);
+int simopt_comm_init(const uint8_t* id128, int world, int rank, void** comm);
+int simopt_comm_destroy(void* comm);
+int simopt_comm_allreduce_f64(void* comm, void* stream, const double* send, double* recv, int64_t n);
+int simopt_comm_allreduce_min_f64(void* comm, void* stream, const double* send, double* recv,
+                                  int64_t n);
+int simopt_comm_allgather(void* comm, void* stream, const void* send, void* recv, int64_t bytes);
+int simopt_comm_broadcast(void* comm, void* stream, const void* send, void* recv, int64_t bytes,
+                          int root);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,14 @@ SIGNATURES = {
     "simopt_logistic_xtdx_tma": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_logistic_xtdx_pair": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_xtdx_last_passes": [],
+    "simopt_comm_version": [_vp],
+    "simopt_comm_unique_id": [_vp],
+    "simopt_comm_init": [_vp, _i32, _i32, _vp],
+    "simopt_comm_destroy": [_vp],
+    "simopt_comm_allreduce_f64": [_vp, _vp, _vp, _vp, _i64],
+    "simopt_comm_allreduce_min_f64": [_vp, _vp, _vp, _vp, _i64],
+    "simopt_comm_allgather": [_vp, _vp, _vp, _vp, _i64],
+    "simopt_comm_broadcast": [_vp, _vp, _vp, _vp, _i64, _i32],
     "simopt_mv_fw_tail": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32],
     "simopt_project_budget": [_vp, _vp, _vp, _d, _i64, _vp, _vp],
     "simopt_project_box": [_vp, _vp, _d, _d, _i64, _vp],

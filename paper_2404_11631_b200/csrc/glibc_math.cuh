@@ -1,3 +1,11 @@
+// Third-party code notice: the algorithms below are ports of GNU C Library (glibc) 2.39
+// libm routines (sysdeps/ieee754/dbl-64: s_log1p.c, s_sin.c, e_exp.c, s_erf.c), and the
+// tables in glibc_tables.h are data extracted from glibc's libm.so.6.  glibc is licensed
+// under the GNU Lesser General Public License v2.1 or later; these files are
+// distributed under the same terms (LGPL-2.1-or-later, see
+// https://www.gnu.org/licenses/old-licenses/lgpl-2.1.html).  Copyright (C) the Free
+// Software Foundation, Inc. and the glibc contributors.
+//
 // glibc-2.39-faithful double-precision log1p / sin / cos, host+device.
 //
 // Why: the reference draws normals in `boxmuller_block` (sobench/_kernels.py:178-190)

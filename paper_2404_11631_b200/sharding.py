@@ -16,6 +16,56 @@ import torch.distributed as dist
 _U128 = (1 << 128) - 1
 
 
+class SimoptComm:
+    """The library's own NCCL communicator (simopt_comm_*, csrc/comm.cu).
+
+    Rank 0 draws the 128-byte unique id, ``broadcast_id`` carries it to the other ranks
+    (torch.distributed over the existing process group by default), every rank joins.
+    Collectives run on the current CUDA stream, like every other entry point."""
+
+    def __init__(self, rank: int, world: int, broadcast_id=None):
+        import ctypes
+
+        from . import _lib
+        self.lib, self.rank, self.world = _lib.load(), rank, world
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            _lib.check(self.lib.simopt_comm_unique_id(ctypes.c_void_p(uid.data_ptr())))
+        if world > 1:
+            uid = (broadcast_id or _broadcast_id)(uid)
+        self.handle = ctypes.c_void_p()
+        _lib.check(self.lib.simopt_comm_init(ctypes.c_void_p(uid.data_ptr()), world, rank,
+                                             ctypes.byref(self.handle)))
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        from . import _lib
+        if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+            raise TypeError("simopt_comm_allreduce_f64 takes a contiguous float64 CUDA tensor")
+        _lib.check(self.lib.simopt_comm_allreduce_f64(self.handle, _lib.stream_ptr(), _lib.ptr(t),
+                                                      _lib.ptr(t), t.numel()))
+        return t
+
+    def allgather(self, t: torch.Tensor) -> torch.Tensor:
+        from . import _lib
+        t = t.contiguous()
+        out = torch.empty((self.world, *t.shape), dtype=t.dtype, device=t.device)
+        _lib.check(self.lib.simopt_comm_allgather(self.handle, _lib.stream_ptr(), _lib.ptr(t),
+                                                  _lib.ptr(out), t.numel() * t.element_size()))
+        return out
+
+    def close(self):
+        if self.handle:
+            self.lib.simopt_comm_destroy(self.handle)
+            self.handle = None
+
+
+def _broadcast_id(uid: torch.Tensor) -> torch.Tensor:
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
+    t = uid.to(dev)
+    dist.broadcast(t, 0)
+    return t.cpu()
+
+
 class ShardGroup:
     """The ranks that split one solver run's sample (or product) axis.
 
@@ -26,13 +76,21 @@ class ShardGroup:
     the same order everywhere.
     """
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, comm: str | None = None):
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed is not initialised")
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.nccl = dist.get_backend(group) == "nccl"
+        # comm="simopt" (default with NCCL, env SIMOPT_COMM=torch to opt out): fp64 sums
+        # and gathers of CUDA tensors go through the library's own NCCL communicator (the C
+        # ABI a non-Python host uses); "torch": torch.distributed's
+        import os
+        comm = comm or os.environ.get("SIMOPT_COMM", "simopt")
+        self.comm = None
+        if self.nccl and self.world > 1 and group is None and comm == "simopt":
+            self.comm = SimoptComm(self.rank, self.world)
 
     def range(self, n: int, align: int = 1) -> tuple:
         return shard_range(n, self.world, self.rank, align)
@@ -44,6 +102,8 @@ class ShardGroup:
         """In-place sum over ranks."""
         if self.world == 1:
             return t
+        if self.comm is not None and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous():
+            return self.comm.allreduce_(t)
         if self.nccl:
             dist.all_reduce(t, group=self.group)
             return t
@@ -57,6 +117,8 @@ class ShardGroup:
         t = t.contiguous()
         if self.world == 1:
             return t.unsqueeze(0)
+        if self.comm is not None and t.is_cuda:
+            return self.comm.allgather(t)
         if self.nccl:
             out = torch.empty((self.world, *t.shape), dtype=t.dtype, device=t.device)
             dist.all_gather_into_tensor(out, t, group=self.group)

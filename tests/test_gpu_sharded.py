@@ -116,3 +116,15 @@ def test_full_size_sharded(ranks, golden):
     assert np.array_equal(r["full_c3_0_w"], g["final_iterate"])
     np.testing.assert_allclose(r["full_c3_1_obj"], g["objectives"], rtol=1e-8)
     assert _rel(r["full_c3_1_w"], g["final_iterate"]) < 1e-8
+
+
+def test_simopt_comm_world1():
+    """The C-ABI NCCL communicator (simopt_comm_*): a one-rank communicator's all-reduce and
+    all-gather are the identity (a multi-rank NCCL group needs one GPU per rank)."""
+    import torch
+    from paper_2404_11631_b200.sharding import SimoptComm
+    c = SimoptComm(0, 1)
+    x = torch.arange(10, dtype=torch.float64, device="cuda")
+    assert torch.equal(c.allreduce_(x.clone()), x)
+    assert torch.equal(c.allgather(x)[0], x)
+    c.close()

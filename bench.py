@@ -482,11 +482,10 @@ def run_c2(args, rank, world, shard):
         "gpu_launches": launches_per_epoch * args.steps,
         "final_objective": trace.build("newsvendor", dd, "cuda", 0, SEED, None).final_objective,
     }
-    del eng
+    del eng, prob
+    _release()  # the headline run's layouts go back before the end-to-end run allocates its own
     if not args.no_e2e:
         line["e2e"] = run_e2e(task, backend, shard, ss)
-    del prob
-    _release()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_c2(dd, ss)
     return line
@@ -509,6 +508,7 @@ def run_e2e(task, backend, shard, ss):
     dd = task.dimension
     fw_run(NewsvendorProblem(task, backend, shard=shard), FwConfig(2, M, ss, pkg.RngStream(SEED, 2)),
            backend)  # warm: allocations, layouts, streams
+    gc.collect()  # a collection inside the timed call would stall the host's enqueue
     torch.cuda.synchronize()
     if shard is not None:
         shard.barrier()

@@ -55,7 +55,11 @@ def build(verbose=False, force=False):
     if failed:
         raise RuntimeError("nvcc failed")
     if force or procs or not os.path.exists(OUT):
-        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"])
+        # the CUDA runtime is linked statically: a shared libcudart.so.12 would bind to
+        # whichever runtime the host process loaded first (torch ships its own), and a
+        # mismatched runtime fails its first-launch kernel lookup (compute-sanitizer reports
+        # it, profiles/r02_sanitizer.md)
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs])
     return OUT
 
 

@@ -215,9 +215,18 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kWsPerSm)
       const int lbase = (int)((q0 << 2) - i0);
       uint32_t* raw = sm.raw[p];
       int* hist = sm.hist[p];
+      // kNoCarry: round 0's product M0 * (c0 + t) is carried from t to t + kWsProd by a
+      // 128-bit add (phx_r0_advance): 17 products per block instead of 18
+      uint64_t r0h = 0, r0l = 0;
+      if (kNoCarry) phx_mulhilo(PHILOX_M0, c0 + (uint64_t)tid, &r0h, &r0l);
       for (int t = tid; t <= nq; t += kWsProd) {
-        const phx4 w = kNoCarry ? philox4x64_10_rk_c0(c0 + (uint64_t)t, rk, pre)
-                                : philox4x64_10_rk(stream_block_counter(clo, chi, (uint64_t)(q0 + t)), rk);
+        phx4 w;
+        if (kNoCarry) {
+          w = philox4x64_10_rk_r0(r0h, r0l, rk, pre);
+          phx_r0_advance<kWsProd>(r0h, r0l);
+        } else {
+          w = philox4x64_10_rk(stream_block_counter(clo, chi, (uint64_t)(q0 + t)), rk);
+        }
         float z[4];
         nv_approx_pair(w.v[0], w.v[1], &z[0], &z[1]);
         nv_approx_pair(w.v[2], w.v[3], &z[2], &z[3]);

@@ -132,9 +132,12 @@ static inline bool phx_no_carry(uint64_t clo, uint64_t nblocks) {
   return nblocks <= ~clo;
 }
 
-PHX_HD phx4 philox4x64_10_rk_c0(uint64_t c0, const phx_keys& rk, const phx_pre& pre) {
-  uint64_t hi0, lo0, hi1, lo1;
-  phx_mulhilo(PHILOX_M0, c0, &hi0, &lo0);          // round 0 (word 2 == 0: no second product)
+// Rounds 1-9 of the counter (c0, hi, 0, 0) given round 0's product (hi0, lo0) = M0 * c0
+// (word 2 == 0, so round 0 has no second product).  Split out so a caller walking
+// counters c0, c0 + s, c0 + 2s, ... can carry M0 * c0 forward by a 128-bit add
+// (phx_r0_advance) instead of a product.
+PHX_HD phx4 philox4x64_10_rk_r0(uint64_t hi0, uint64_t lo0, const phx_keys& rk, const phx_pre& pre) {
+  uint64_t hi1, lo1;
   phx4 c;                                          // round 1
   phx_mulhilo(PHILOX_M1, hi0 ^ rk.k[1], &hi1, &lo1);
   c.v[0] = hi1 ^ rk.k[2];
@@ -156,3 +159,21 @@ PHX_HD phx4 philox4x64_10_rk_c0(uint64_t c0, const phx_keys& rk, const phx_pre& 
   }
   return c;
 }
+
+PHX_HD phx4 philox4x64_10_rk_c0(uint64_t c0, const phx_keys& rk, const phx_pre& pre) {
+  uint64_t hi0, lo0;
+  phx_mulhilo(PHILOX_M0, c0, &hi0, &lo0);          // round 0
+  return philox4x64_10_rk_r0(hi0, lo0, rk, pre);
+}
+
+#if defined(__CUDACC__)
+// (hi0, lo0) <- M0 * (c0 + S) from M0 * c0, for a compile-time stride S: a 128-bit
+// add of the constant M0 * S (exact mod 2^128, so equal to the product whenever
+// c0 + S < 2^64, which phx_no_carry guarantees for the launch).
+template <uint64_t S>
+__device__ __forceinline__ void phx_r0_advance(uint64_t& hi0, uint64_t& lo0) {
+  constexpr uint64_t kLo = PHILOX_M0 * S;
+  constexpr uint64_t kHi = (uint64_t)(((unsigned __int128)PHILOX_M0 * S) >> 64);
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo0), "+l"(hi0) : "n"(kLo), "n"(kHi));
+}
+#endif

@@ -528,71 +528,252 @@ __device__ __noinline__ void nv_peer_exchange(const NvPeerArgs a, ArgMin r, doub
   st->best_val = best.v;
 }
 
+// Integer form of nv_classify for one query: a key with code q is certainly below iff
+// q < qb, certainly above iff q >= qa, ambiguous otherwise.  The thresholds are the
+// real-number solutions of nv_classify's two inequalities in q, formed once per query
+// in double; their rounding (~1e-15 z) is far inside the 0.1-code margin nv_classify's
+// slack leaves, so every key either test calls certain is certain, and the count --
+// certain-below keys plus the exactly resolved ambiguous ones -- is the same integer.
+struct NvThresh {
+  int qb, qa;
+};
+__device__ __forceinline__ NvThresh nv_thresh(const NvWindow& w) {
+  // below: (q + 1.25) W - Z0 + eps < t  <=>  q < B;  q = QMAX is never below
+  const double B = (w.t - w.eps + NV_Z0) * NV_QSCALE - 1.25;
+  // above: (q - 0.25) W - Z0 - eps > t  <=>  q > A;  q = 0 is never above
+  const double A = (w.t + w.eps + NV_Z0) * NV_QSCALE + 0.25;
+  NvThresh r;
+  r.qb = !(B > 0.0) ? 0 : (B >= (double)NV_QMAX ? NV_QMAX : (int)ceil(B));
+  r.qa = !(A >= 0.0) ? (A < 0.0 ? 1 : NV_QMAX + 1)  // NaN: nothing certain (as nv_classify)
+                     : (A >= (double)NV_QMAX ? NV_QMAX + 1 : max((int)floor(A) + 1, 1));
+  return r;
+}
+
 // Fused FW step for the newsvendor:
 //   (1) if do_update: x_j <- (gamma * ((-1 * x_j) + s_j)) + x_j with the vertex of the
 //       previous LMO (frank_wolfe.py:69-82), record x_j < -FEAS_TOL, objective term;
 //   (2) if do_grad: g_j at the (new) x_j, LMO values g_j * (C / c_j), argmin over all
 //       products (last-block reduction), NaN flag.
-// kIterWarps products (warps) per block.
-template <int kIterWarps, int kMinBlocks>
+// Gradient steps run in CTA rounds:
+//  (A) each warp takes up to kSlotsPerWarp products, one at a time from a device counter
+//      (the next index and the next product's iterate and parameters are fetched while
+//      the current one is processed); lanes = the product's segments: bucket starts of the
+//      query window, then the window's keys in 16-byte loads (several in flight per lane),
+//      integer thresholds count the certainly-below keys and the few ambiguous draws are
+//      appended to one CTA-wide queue;
+//  (B) all threads of the CTA resolve the queue with the exact glibc Box-Muller (full
+//      warps instead of one partly filled pass per product);
+//  (C) one thread per product forms the gradient and its LMO value.
+// Ambiguous draws that do not fit the queue are resolved by the warp that found them.
+constexpr int kSlotsPerWarp = 4;
+constexpr int kCtaQueue = 1024;
+
+struct NvStepCtx {
+  int64_t jstar;
+  double sval, gamma;
+};
+
+// (1) for product j from its current iterate x; `writer` stores the new iterate, flags and
+// objective term
+__device__ __forceinline__ double nv_update(const NvIterArgs& a, const NvStepCtx& cx, int64_t j,
+                                           double x, bool writer) {
+  if (a.do_update) {
+    const double sj = (j == cx.jstar) ? cx.sval : 0.0;
+    const double dir = (-1.0 * x) + sj;
+    x = cx.gamma * dir + x;
+    if (writer) {
+      a.x[j] = x;
+      if (x < -1e-10) atomicOr(&a.flags[a.step], NV_FLAG_NEGATIVE);
+      if (a.terms) a.terms[j] = nv_cost_term(x, a.mu[j], a.sigma[j], a.k[j], a.h[j], a.v[j]);
+    }
+  }
+  return x;
+}
+
+// kVecBatch: 16-byte key loads per lane per pass
+template <int kIterWarps, int kMinBlocks, int kVecBatch>
 __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
     k_nv_iter(NvIterArgs a) {
+  constexpr int kSlots = kIterWarps * kSlotsPerWarp;
   __shared__ ArgMin warp_best[kIterWarps];
-  __shared__ int64_t queues[kIterWarps][kQueue];
+  __shared__ uint64_t queue[kCtaQueue];   // slot << 40 | draw index within the product
+  __shared__ int64_t slot_j[kSlots];       // -1: empty
+  __shared__ double slot_x[kSlots], slot_mu[kSlots], slot_sigma[kSlots];
+  __shared__ int slot_cnt[kSlots];
+  __shared__ int q_len;
   __shared__ int nan_seen;
   __shared__ bool am_last;
-  if (threadIdx.x == 0) nan_seen = 0;
-  __syncthreads();
+  if (threadIdx.x == 0) {
+    nan_seen = 0;
+    q_len = 0;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  ArgMin best{INFINITY, INT64_MAX};
   NvState* st = a.state;
-  const int64_t jstar = st->jstar;
-  const double sval = st->sval;
+  NvStepCtx cx;
+  cx.jstar = st->jstar;
+  cx.sval = st->sval;
+  // frank_wolfe.py:62-66: gamma = 2 / (epoch * inner_iters + inner + 2), IEEE double division
+  cx.gamma = a.epoch_ctr ? 2.0 / (double)(*a.epoch_ctr * a.inner_iters + a.m + 2) : a.gamma;
+  if (!a.do_grad) {  // update-only step: a static split
+    for (int64_t j = (int64_t)blockIdx.x * kIterWarps + warp; j < a.d; j += (int64_t)gridDim.x * kIterWarps)
+      nv_update(a, cx, j, a.x_in[j], lane == 0);
+    return;
+  }
   const NvStreamPos sp = a.epoch_draw
                             ? NvStreamPos{a.epoch_draw[0], a.epoch_draw[1], a.epoch_draw[2], a.epoch_draw[3]}
                             : NvStreamPos{a.seed, a.sid, a.ctr_lo, a.ctr_hi};
-  // frank_wolfe.py:62-66: gamma = 2 / (epoch * inner_iters + inner + 2), IEEE double division
-  const double gamma = a.epoch_ctr ? 2.0 / (double)(*a.epoch_ctr * a.inner_iters + a.m + 2) : a.gamma;
-  // gradient steps hand products out dynamically (NvState.pad is the counter, reset by
-  // the last block): a product's cost varies with its window and ambiguous draws, and a
-  // static split left warps idle at the block barrier behind the slowest of their block.
-  // The next index is fetched before the current product is processed.
-  const bool dyn = a.do_grad != 0;
+  __syncthreads();
+  // products: warp g of the grid takes product g first, then products nwarps + n in the
+  // order of a device counter n (NvState.pad, reset by the last block) -- a product's cost
+  // varies with its window and ambiguous draws.  The counter is read one product ahead
+  // (lane 0's atomic is in flight while the current product is processed) and the next
+  // product's iterate and parameters are loaded one product ahead.
   unsigned* next = &st->pad;
-  int64_t j;
-  {
-    unsigned jn = 0;
-    if (dyn && lane == 0) jn = atomicAdd(next, 1u);
-    j = dyn ? (int64_t)__shfl_sync(0xffffffffu, jn, 0) : (int64_t)blockIdx.x * kIterWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kIterWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kIterWarps + warp;
+  unsigned pend = 0;  // lane 0: the counter value of the product after jn
+  if (lane == 0 && gw < a.d) pend = atomicAdd(next, 1u);
+  int64_t jn = gw;
+  double xn = 0.0, mun = 0.0, sgn = 1.0;  // the next product's iterate and parameters
+  if (jn < a.d) {
+    xn = a.x_in[jn];
+    mun = a.mu[jn];
+    sgn = a.sigma[jn];
   }
-  while (j < a.d) {
-    unsigned jn = 0;
-    if (dyn && lane == 0) jn = atomicAdd(next, 1u);
-    double x = a.x_in[j];
-    if (a.do_update) {
-      const double sj = (j == jstar) ? sval : 0.0;
-      const double dir = (-1.0 * x) + sj;
-      x = gamma * dir + x;
+  ArgMin best{INFINITY, INT64_MAX};
+  const int S32 = (int)a.S;  // S < 2^31 (checked on the host)
+  const int nseg = (int)a.nseg;
+  const bool vec = (a.S & 3) == 0;  // rows start 16-byte aligned: vector key loads
+  for (;;) {
+    // ---- (A) count certain keys, queue ambiguous draws
+    for (int k = 0; k < kSlotsPerWarp; ++k) {
+      const int slot = warp * kSlotsPerWarp + k;
+      const int64_t j = jn;
+      if (j >= a.d) {
+        if (lane == 0) slot_j[slot] = -1;
+        continue;
+      }
+      const double x = nv_update(a, cx, j, xn, lane == 0);
+      const double mu = mun, sigma = sgn;
+      const unsigned got = pend;
+      if (lane == 0) pend = atomicAdd(next, 1u);  // the product after the next one
+      const NvWindow w = nv_window(x, mu, sigma);
+      const NvThresh th = nv_thresh(w);
+      const int blo = (int)(w.qlo >> (NV_QBITS - 10)), bhi = (int)(w.qhi >> (NV_QBITS - 10));
+      int c = 0;  // per lane: certain-below (+ locally resolved) draws
+      for (int s0 = 0; s0 < nseg; s0 += 32) {
+        const int sg = s0 + lane;
+        int start = 0, end = 0;
+        const uint32_t* seg = a.keys;
+        if (sg < nseg) {
+          const int e0 = sg * NV_SEG;
+          const int len = (S32 - e0) < NV_SEG ? (S32 - e0) : NV_SEG;
+          const uint16_t* o = a.off + (j * nseg + sg) * (int64_t)NV_B;
+          start = o[blo];
+          end = (bhi + 1 < NV_B) ? o[bhi + 1] : len;
+          seg = a.keys + j * a.S + e0;
+          c += start;
+        }
+        // keys [a0, end) in 16-byte words (a0 = start rounded down; vec: rows aligned), or
+        // one key per "word" otherwise; elements outside [start, end) are masked
+        const int a0 = vec ? (start & ~3) : start;
+        const int nw = vec ? ((end - a0 + 3) >> 2) : (end - a0);
+        unsigned amb = 0;  // unused outside the pass
+        for (int w0 = 0; w0 < nw; w0 += kVecBatch) {
+          uint32_t kv[kVecBatch][4];
+#pragma unroll
+          for (int v = 0; v < kVecBatch; ++v) {
+            if (w0 + v < nw) {
+              if (vec) {
+                const uint4 t = reinterpret_cast<const uint4*>(seg + a0)[w0 + v];
+                kv[v][0] = t.x;
+                kv[v][1] = t.y;
+                kv[v][2] = t.z;
+                kv[v][3] = t.w;
+              } else {
+                kv[v][0] = seg[a0 + w0 + v];
+                kv[v][1] = kv[v][2] = kv[v][3] = 0xFFFFFFFFu;
+              }
+            } else {
+              kv[v][0] = kv[v][1] = kv[v][2] = kv[v][3] = 0xFFFFFFFFu;
+            }
+          }
+          amb = 0;
+#pragma unroll
+          for (int v = 0; v < kVecBatch; ++v)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int pos = vec ? a0 + 4 * (w0 + v) + u : (u == 0 ? a0 + w0 + v : end);
+              const bool valid = pos >= start && pos < end;
+              const int q = (int)(kv[v][u] >> 12);
+              c += (valid && q < th.qb) ? 1 : 0;
+              amb |= (valid && q >= th.qb && q < th.qa) ? 1u << (4 * v + u) : 0u;
+            }
+          while (amb) {  // ambiguous draws: rare; one call site keeps the register budget
+            const int bit = __ffs(amb) - 1;
+            amb &= amb - 1;
+            uint32_t key = 0;
+#pragma unroll
+            for (int v = 0; v < kVecBatch; ++v)
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (bit == 4 * v + u) key = kv[v][u];
+            const uint64_t idx = (uint64_t)(sg * NV_SEG) + (key & 4095u);
+            const int pos = atomicAdd(&q_len, 1);
+            if (pos < kCtaQueue)
+              queue[pos] = (uint64_t)slot << 40 | idx;
+            else  // queue full: resolve here
+              c += nv_resolve(sp, j * a.S + (int64_t)idx, mu, sigma, x);
+          }
+        }
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o2);
+      jn = nwarps + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+      if (jn < a.d) {
+        xn = a.x_in[jn];
+        mun = a.mu[jn];
+        sgn = a.sigma[jn];
+      }
       if (lane == 0) {
-        a.x[j] = x;
-        if (x < -1e-10) atomicOr(&a.flags[a.step], NV_FLAG_NEGATIVE);
-        if (a.terms) a.terms[j] = nv_cost_term(x, a.mu[j], a.sigma[j], a.k[j], a.h[j], a.v[j]);
+        slot_j[slot] = j;
+        slot_x[slot] = x;
+        slot_mu[slot] = mu;
+        slot_sigma[slot] = sigma;
+        slot_cnt[slot] = c;
       }
     }
-    if (a.do_grad) {
-      const int64_t cnt = nv_count_warp(a.keys, a.off, j, a.S, (int)a.nseg, x, a.mu[j],
-                                        a.sigma[j], sp, queues[warp]);
-      const double g = nv_grad_value(cnt, a.S, a.k[j], a.h[j], a.v[j]);
-      if (lane == 0) {
+    __syncthreads();
+    // ---- (B) resolve the queued draws exactly, all threads
+    const int nq = min(q_len, kCtaQueue);
+    for (int e = threadIdx.x; e < nq; e += kIterWarps * 32) {
+      const uint64_t v = queue[e];
+      const int slot = (int)(v >> 40);
+      const int64_t j = slot_j[slot];
+      if (nv_resolve(sp, j * a.S + (int64_t)(v & ((1ULL << 40) - 1)), slot_mu[slot], slot_sigma[slot],
+                     slot_x[slot]))
+        atomicAdd(&slot_cnt[slot], 1);
+    }
+    __syncthreads();
+    // ---- (C) gradient and LMO value per product
+    if (threadIdx.x < kSlots) {
+      const int64_t j = slot_j[threadIdx.x];
+      if (j >= 0) {
+        const double g = nv_grad_value((int64_t)slot_cnt[threadIdx.x], a.S, a.k[j], a.h[j], a.v[j]);
         a.g[j] = g;
         if (g != g) nan_seen = 1;
         const double val = g * (a.budget / a.c[j]);  // lmo.py:84
         best = amin(best, ArgMin{val, j});
       }
     }
-    j = dyn ? (int64_t)__shfl_sync(0xffffffffu, jn, 0) : j + (int64_t)gridDim.x * kIterWarps;
+    if (threadIdx.x == 0) q_len = 0;
+    // another round while any warp holds a product
+    if (!__syncthreads_or(jn < a.d)) break;
   }
-  if (!a.do_grad) return;
+  // the last counter read must have returned before this block reports done (the last
+  // block resets the counter)
+  if (lane == 0) asm volatile("" ::"r"(pend));
+  best = warp_amin(best);
   if (lane == 0) warp_best[warp] = best;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -766,17 +947,25 @@ extern "C" int simopt_nv_decode(void* stream, const uint32_t* keys, const double
 
 extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   NvIterArgs a = *args;
+  SIMOPT_REQUIRE(a.S < (1LL << 31), SIMOPT_E_CONFIG, "S >= 2^31 samples per product");
   // gradient steps: one resident wave of blocks pulling products from a counter; update-only
-  // steps: a static split
-  // Eight warps per block, three blocks per SM (80 registers).  Measured at C2 with the
-  // next epoch's resample running beside the steps (bench.py, 30 epochs): 5.80k FW it/s;
-  // four-warp blocks (which fit beside the resample's three CTAs per SM) 5.63k; eight
-  // warps squeezed to 40 registers 5.87k (within noise, with spills).
-  constexpr int kW = 8;
-  const int64_t cap = a.do_grad ? (int64_t)3 * SIMOPT_NUM_SMS : 16 * SIMOPT_NUM_SMS;
-  const int grid = (int)(ceil_div(a.d, kW) < cap ? ceil_div(a.d, kW) : cap);
+  // steps: a static split.  SIMOPT_NV_ITER=W,B,V (A/B): W warps per block, B blocks per SM,
+  // V 16-byte key loads per lane per pass.  Measured on the pipelined C2 epoch (the steps
+  // run beside the next epoch's resample; tools/nv_iter_ab.py, interleaved medians):
+  // 4,3,4 3.88 ms; 4,3,8 3.94; 4,6,4 3.94; 8,3,4 3.95; 8,3,8 4.03; 8,2,4 4.15.  Fewer,
+  // smaller blocks take fewer issue slots from the resample.
+  int kw = 4, bps = 3, vb = 4;
+  if (const char* ev = getenv("SIMOPT_NV_ITER")) sscanf(ev, "%d,%d,%d", &kw, &bps, &vb);
+  const int64_t cap = a.do_grad ? (int64_t)bps * SIMOPT_NUM_SMS : 16 * SIMOPT_NUM_SMS;
+  const int grid = (int)(ceil_div(a.d, kw) < cap ? ceil_div(a.d, kw) : cap);
   SIMOPT_REQUIRE(grid <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
-  k_nv_iter<kW, 3><<<grid, kW * 32, 0, as_stream(stream)>>>(a);
+  cudaStream_t s = as_stream(stream);
+  if (kw == 4)
+    (vb == 4 ? k_nv_iter<4, 6, 4> : k_nv_iter<4, 6, 8>)<<<grid, 4 * 32, 0, s>>>(a);
+  else if (bps <= 2)
+    (vb == 4 ? k_nv_iter<8, 2, 4> : k_nv_iter<8, 2, 8>)<<<grid, 8 * 32, 0, s>>>(a);
+  else
+    (vb == 4 ? k_nv_iter<8, 3, 4> : k_nv_iter<8, 3, 8>)<<<grid, 8 * 32, 0, s>>>(a);
   SIMOPT_CHECK_LAUNCH("k_nv_iter");
   return SIMOPT_OK;
 }

@@ -462,7 +462,7 @@ def run_c2(args, rank, world, shard):
                      "frac": value / it_roof,
                      "basis": "SURVEY 8(d) C2: 8*d*S*(1+1/M) bytes per FW iteration at hbm peak "
                               "(x n_gpus)"}
-    launches_per_epoch = 4 * M + 2  # resample, M+1 fused steps, M x (terms, sums, stamp)
+    launches_per_epoch = M + 3  # resample, M+1 fused steps (stamping themselves), the epoch's records
     if world > 1 and eng.mailbox is None:
         launches_per_epoch += 2 * M  # LMO pack + apply around each NCCL exchange
     cfg = _c2_config(args, dd, ss, world)

@@ -227,8 +227,22 @@ typedef struct NvIterArgs {
   const int64_t* epoch_ctr;
   int64_t inner_iters, m;
   uint64_t* seq_ptr;
+  /* When non-NULL, the step's last block writes %globaltimer here once the step is
+   * complete (the per-step elapsed time of the FW record, frank_wolfe.py:116). */
+  int64_t* stamp;
 } NvIterArgs;
 int simopt_nv_iter(void* stream, const NvIterArgs* args);
+
+/* The recorded quantities of M consecutive newsvendor FW steps in one launch
+ * (frank_wolfe.py:110-117 for NewsvendorProblem): iterate m is row (r0 + m) % H of xs
+ * (H rows of d doubles); spent[m] = fixed-tree dot(c, x_m) (check_feasible, tasks.py:326)
+ * and objs[m] = fixed-tree sum of newsvendor_cost_block(x_m) (tasks.py:171-173,
+ * _kernels.py:210-223) -- bit for bit what simopt_nv_cost_terms followed by
+ * simopt_tree_sums2 give, with chunk_size `chunk`. */
+int simopt_nv_epoch_records(void* stream, const double* xs, int64_t H, int64_t r0, int64_t M,
+                            const double* c, const double* mu, const double* sigma,
+                            const double* unit, const double* hold, const double* sell, int64_t d,
+                            int64_t chunk, double* spent, double* objs);
 
 /* Peer mailboxes (CUDA IPC over NVLink/NVSwitch): alloc returns a zeroed device buffer and
  * its 64-byte IPC handle; open maps a peer's handle (cudaIpcMemLazyEnablePeerAccess);

@@ -53,6 +53,8 @@ SIGNATURES = {
     "simopt_nv_grad_from_counts": [_vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp],
     "simopt_nv_grad_exact": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     "simopt_nv_cost_terms": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
+    "simopt_nv_epoch_records": [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
+                                _vp, _vp],
     "simopt_logistic_resid": [_vp, _vp, _vp, _vp, _i64, _vp],
     "simopt_logistic_hvp_weights": [_vp, _vp, _vp, _i64, _vp],
     "simopt_logistic_loss_terms": [_vp, _vp, _vp, _vp, _i64, _vp],
@@ -119,7 +121,7 @@ SIGNATURES = {
 INT64_RESULT = {"simopt_peer_reduce_bytes", "simopt_xtdx_last_passes"}
 
 
-ABI_VERSION = 3  # csrc/capi.cu simopt_abi_version; bumped when an entry point's signature changes
+ABI_VERSION = 4  # csrc/capi.cu simopt_abi_version; bumped when an entry point's signature changes
 
 
 def load(require_device: bool = True):

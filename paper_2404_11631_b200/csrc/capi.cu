@@ -19,7 +19,7 @@ void simopt_set_error(const char* fmt, ...) {
 }
 
 extern "C" const char* simopt_last_error(void) { return g_err; }
-extern "C" int simopt_abi_version(void) { return 3; }
+extern "C" int simopt_abi_version(void) { return 4; }
 
 int simopt_num_sms() {
   static std::mutex mu;

@@ -184,8 +184,10 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <bool kNoCarry>
-__global__ void __launch_bounds__(kWsProd + kWsCons, kWsPerSm)
+// kRegCap: launch-bound blocks per SM used only to cap registers (3: 48 registers;
+// 4: 40 registers, leaving room on the SM for the step kernel that runs beside it)
+template <bool kNoCarry, int kRegCap>
+__global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
     k_nv_resample_ws(const phx_keys rk, const phx_pre pre, uint64_t clo, uint64_t chi, int64_t d,
                      int64_t S, int nseg, uint32_t* __restrict__ keys, uint16_t* __restrict__ off) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -617,6 +619,17 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
   if (!a.do_grad) {  // update-only step: a static split
     for (int64_t j = (int64_t)blockIdx.x * kIterWarps + warp; j < a.d; j += (int64_t)gridDim.x * kIterWarps)
       nv_update(a, cx, j, a.x_in[j], lane == 0);
+    if (a.stamp) {  // the last block to finish stamps the step
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1) {
+          __threadfence();
+          *a.stamp = (int64_t)globaltimer();
+          st->blocks_done = 0;
+        }
+      }
+    }
     return;
   }
   const NvStreamPos sp = a.epoch_draw
@@ -813,6 +826,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
                                   a.seq_ptr, a.flags},
                        r, sval, st);
     }
+    if (a.stamp) *a.stamp = (int64_t)globaltimer();
   }
 }
 
@@ -883,6 +897,8 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   if (!(ev && atoi(ev) == 1)) {
     const int64_t g = nblk < (int64_t)SIMOPT_NUM_SMS * kWsPerSm ? nblk : (int64_t)SIMOPT_NUM_SMS * kWsPerSm;
     const size_t smem = sizeof(WsSmem);
+    int regcap = 3;
+    if (const char* rc = getenv("SIMOPT_NV_WS_REGCAP")) regcap = atoi(rc) == 4 ? 4 : 3;
     static std::mutex mu;
     static std::vector<int> ready;  // devices whose shared-memory limit is raised
     int dev = 0;
@@ -893,21 +909,19 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
       bool have = false;
       for (int x : ready) have |= x == dev;
       if (!have) {
-        attr_err = cudaFuncSetAttribute(k_nv_resample_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem);
-        if (attr_err == cudaSuccess)
-          attr_err = cudaFuncSetAttribute(k_nv_resample_ws<false>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const void* fns[4] = {(const void*)k_nv_resample_ws<true, 3>, (const void*)k_nv_resample_ws<false, 3>,
+                              (const void*)k_nv_resample_ws<true, 4>, (const void*)k_nv_resample_ws<false, 4>};
+        for (const void* f : fns)
+          if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (attr_err == cudaSuccess) ready.push_back(dev);
       }
     }
     SIMOPT_CUDA(attr_err);
-    if (no_carry)
-      k_nv_resample_ws<true><<<(unsigned)g, kWsProd + kWsCons, smem, as_stream(stream)>>>(
-          rk, pre, clo, chi, d, S, (int)nseg, keys, off);
-    else
-      k_nv_resample_ws<false><<<(unsigned)g, kWsProd + kWsCons, smem, as_stream(stream)>>>(
-          rk, pre, clo, chi, d, S, (int)nseg, keys, off);
+    auto k = no_carry ? (regcap == 4 ? k_nv_resample_ws<true, 4> : k_nv_resample_ws<true, 3>)
+                      : (regcap == 4 ? k_nv_resample_ws<false, 4> : k_nv_resample_ws<false, 3>);
+    k<<<(unsigned)g, kWsProd + kWsCons, smem, as_stream(stream)>>>(rk, pre, clo, chi, d, S, (int)nseg,
+                                                                   keys, off);
     SIMOPT_CHECK_LAUNCH("k_nv_resample_ws");
     return SIMOPT_OK;
   }
@@ -1016,7 +1030,96 @@ __global__ void k_nv_cost(const double* __restrict__ x, const double* __restrict
        j += (int64_t)gridDim.x * blockDim.x)
     out[j] = nv_cost_term(x[j], mu[j], sigma[j], unit[j], hold[j], sell[j]);
 }
+
+// One epoch's records (simopt_nv_epoch_records): warp g takes unit (m, job, chunk),
+// job 0 = dot(c, x_m), job 1 = sum of newsvendor_cost_block(x_m); the chunk's terms are
+// staged a 256-element tile at a time by all lanes and added by lane 0 in index order
+// from 0.0 (_kernels.py:45-68, the dot_partials / sum_partials chains).  The warp that
+// completes a unit's last chunk folds its partials pairwise (the fixed tree).
+constexpr int kRecWarps = 4, kRecTile = 256;
+__global__ void __launch_bounds__(kRecWarps * 32)
+    k_nv_records(const double* __restrict__ xs, int64_t H, int64_t r0, int64_t M,
+                 const double* __restrict__ c, const double* __restrict__ mu,
+                 const double* __restrict__ sigma, const double* __restrict__ unit,
+                 const double* __restrict__ hold, const double* __restrict__ sell, int64_t d,
+                 int64_t chunk, int64_t nch, double* __restrict__ part, unsigned* __restrict__ cnt,
+                 double* __restrict__ spent, double* __restrict__ objs) {
+  __shared__ double buf[kRecWarps][kRecTile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = M * 2 * nch;
+  for (int64_t g = (int64_t)blockIdx.x * kRecWarps + warp; g < total;
+       g += (int64_t)gridDim.x * kRecWarps) {
+    const int64_t ch = g % nch, u = g / nch;  // u = m * 2 + job
+    const int job = (int)(u & 1);
+    const int64_t m = u >> 1;
+    const double* x = xs + ((r0 + m) % H) * d;
+    const int64_t lo = ch * chunk, hi = lo + chunk < d ? lo + chunk : d;
+    double s = 0.0;
+    double* b = buf[warp];
+    for (int64_t base = lo; base < hi; base += kRecTile) {
+#pragma unroll 2
+      for (int t = lane; t < kRecTile; t += 32) {
+        const int64_t i = base + t;
+        double v = 0.0;
+        if (i < hi)
+          v = job == 0 ? c[i] * x[i] : nv_cost_term(x[i], mu[i], sigma[i], unit[i], hold[i], sell[i]);
+        b[t] = v;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int n = (int)(hi - base < kRecTile ? hi - base : kRecTile);
+        for (int t = 0; t < n; ++t) s = s + b[t];
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      part[u * nch + ch] = s;
+      __threadfence();
+      if (atomicAdd(&cnt[u], 1u) == (unsigned)(nch - 1)) {
+        __threadfence();
+        volatile double* q = part + u * nch;
+        int64_t n = nch;
+        while (n > 1) {  // pairwise levels, odd tail carried (k_fold_strided's tree)
+          const int64_t h = n >> 1;
+          for (int64_t i = 0; i < h; ++i) q[i] = q[2 * i] + q[2 * i + 1];
+          if (n & 1) { q[h] = q[n - 1]; n = h + 1; } else { n = h; }
+        }
+        (job == 0 ? spent : objs)[m] = q[0];
+      }
+    }
+  }
+}
 }  // namespace
+
+extern "C" int simopt_nv_epoch_records(void* stream, const double* xs, int64_t H, int64_t r0,
+                                       int64_t M, const double* c, const double* mu,
+                                       const double* sigma, const double* unit, const double* hold,
+                                       const double* sell, int64_t d, int64_t chunk, double* spent,
+                                       double* objs) {
+  SIMOPT_REQUIRE(chunk >= 1, SIMOPT_E_CONFIG, "chunk_size must be >= 1, got %lld", (long long)chunk);
+  SIMOPT_REQUIRE(H >= 1 && M >= 0 && r0 >= 0, SIMOPT_E_CONFIG, "bad iterate ring");
+  if (M == 0) return SIMOPT_OK;
+  cudaStream_t st = as_stream(stream);
+  if (d == 0) {  // empty sums are 0.0
+    SIMOPT_CUDA(cudaMemsetAsync(spent, 0, M * sizeof(double), st));
+    SIMOPT_CUDA(cudaMemsetAsync(objs, 0, M * sizeof(double), st));
+    return SIMOPT_OK;
+  }
+  const int64_t nch = ceil_div(d, chunk);
+  const int64_t units = M * 2;
+  unsigned char* ws = static_cast<unsigned char*>(
+      simopt_scratch(st, units * nch * sizeof(double) + units * sizeof(unsigned) + 64));
+  SIMOPT_REQUIRE(ws != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
+  double* part = reinterpret_cast<double*>(ws);
+  unsigned* cnt = reinterpret_cast<unsigned*>(ws + units * nch * sizeof(double));
+  SIMOPT_CUDA(cudaMemsetAsync(cnt, 0, units * sizeof(unsigned), st));
+  const int64_t g = ceil_div(units * nch, kRecWarps);
+  const int grid = (int)(g < 8 * SIMOPT_NUM_SMS ? g : 8 * SIMOPT_NUM_SMS);
+  k_nv_records<<<grid, kRecWarps * 32, 0, st>>>(xs, H, r0, M, c, mu, sigma, unit, hold, sell, d, chunk,
+                                                nch, part, cnt, spent, objs);
+  SIMOPT_CHECK_LAUNCH("k_nv_records");
+  return SIMOPT_OK;
+}
 
 extern "C" int simopt_nv_cost_terms(void* stream, const double* x, const double* mu,
                                     const double* sigma, const double* unit, const double* hold,

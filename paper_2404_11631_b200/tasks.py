@@ -49,6 +49,7 @@ class NvIterArgs(ctypes.Structure):
         ("j0", ctypes.c_int64), ("seq", ctypes.c_uint64),
         ("epoch_draw", ctypes.c_void_p), ("epoch_ctr", ctypes.c_void_p),
         ("inner_iters", ctypes.c_int64), ("m", ctypes.c_int64), ("seq_ptr", ctypes.c_void_p),
+        ("stamp", ctypes.c_void_p),
     ]
 
 
@@ -292,13 +293,13 @@ class NvFwEngine:
     """Device-resident Frank-Wolfe loop for one newsvendor run (frank_wolfe.py:91-121).
 
     Per step t (epoch k, inner m) the main stream runs ONE fused kernel: update x
-    with the previous LMO vertex, write the objective terms of the new iterate,
-    compute the next ECDF gradient and its LMO argmin.  The recorded quantities
-    (exact-tree dot(c, x) for check_feasible, exact-tree objective sum, a
-    %globaltimer stamp) run on a side stream, off the critical path.  Iterates and
-    objective terms live in rings of 2M+1 slots (the side stream is throttled so a
-    slot is never overwritten before it is read), which also keeps the
-    reference's final_iterate at hand when an epoch check finds a failure.
+    with the previous LMO vertex, compute the next ECDF gradient and its LMO argmin,
+    and stamp %globaltimer when the step is done.  The recorded quantities of the
+    epoch's M steps (exact-tree dot(c, x) for check_feasible, exact-tree objective
+    sum) are formed by one launch on a side stream behind the epoch, off the critical
+    path.  Iterates live in a ring of 2M+1 slots (an epoch's steps wait for the
+    records of the epoch two back, the last reader of their slots), which also keeps
+    the reference's final_iterate at hand when an epoch check finds a failure.
     """
 
     def __init__(self, prob: "NewsvendorProblem", inner_iters: int, epochs: int, chunk: int):
@@ -309,7 +310,6 @@ class NvFwEngine:
         T = epochs * M
         self.T, self.H = T, 2 * M + 1
         self.xs = torch.zeros(self.H, d, dtype=F64, device="cuda")
-        self.terms = torch.empty(self.H, d, dtype=F64, device="cuda")
         self.g = empty(d)
         self.flags = torch.zeros(T + 1, dtype=torch.int32, device="cuda")
         self.spent = empty(T)
@@ -351,7 +351,6 @@ class NvFwEngine:
         self.hi = torch.cuda.Stream(priority=hi_pri)
         self.gen = torch.cuda.Stream(priority=lo_pri)
         self.side = torch.cuda.Stream()
-        self.side_done = {}   # step -> event recorded on the side stream
         self.epoch_done = {}  # epoch -> event after its last recorded step
         self.ready = {}       # epoch -> (layout slot, event: its resample is done)
         self.steps_done = {}  # epoch -> event after its last step kernel
@@ -409,8 +408,14 @@ class NvFwEngine:
         a.keys, a.off = dev.keys.data_ptr(), dev.off.data_ptr()
         a.seed, a.sid, a.ctr_lo, a.ctr_hi = dev.draw
         t0 = k * M
+        # ring slots (t0 + m + 1) % H were last written by epoch k-2's steps: its records
+        # must have read them (H = 2M + 1)
+        old = self.epoch_done.get(k - 2)
+        if old is not None:
+            main.wait_event(old)
         a.x_in = a.x = self.xs[t0 % H].data_ptr()  # gradient + LMO at the epoch's first iterate
-        a.terms = None  # objective terms are formed on the side stream
+        a.terms = None  # objective terms are formed with the epoch's records
+        a.stamp = None
         a.do_update, a.do_grad, a.step, a.grad_step, a.gamma = 0, 1, t0, t0, 0.0
         self._seq()
         _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
@@ -418,39 +423,33 @@ class NvFwEngine:
         for m in range(M):
             t = t0 + m
             slot = (t + 1) % H
-            old = self.side_done.pop(t + 1 - H, None)  # slot last read by step t+1-H
-            if old is not None:
-                main.wait_event(old)
             xin, xout = self.xs[t % H], self.xs[slot]
             a.x_in, a.x = xin.data_ptr(), xout.data_ptr()
             a.gamma = fw_step_size(k, M, m)
             a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), t, t + 1
+            a.stamp = self.stamps[t:].data_ptr()  # elapsed time of step t+1, on the device
             if m + 1 < M:
                 self._seq()
             _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
             if m + 1 < M:
                 self._exchange(sp)
-            ev = torch.cuda.Event()
-            ev.record(main)
-            if m + 1 == M:
-                self.steps_done[k] = ev
-            self.side.wait_event(ev)
-            # objective terms of x_{t+1} (newsvendor_cost_block), then dot(c, x_{t+1}) for
-            # check_feasible and the objective's vec_sum in one launch -- all off the
-            # critical path
-            _lib.check(lib.simopt_nv_cost_terms(ssp, _lib.ptr(xout), _lib.ptr(dev.mu),
-                                                _lib.ptr(dev.sigma), _lib.ptr(dev.k), _lib.ptr(dev.h),
-                                                _lib.ptr(dev.v), dev.d, _lib.ptr(self.terms[slot])))
-            _lib.check(lib.simopt_tree_sums2(ssp, _lib.ptr(dev.c), _lib.ptr(xout), dev.d,
-                                             _lib.ptr(self.spent[t:]), _lib.ptr(self.terms[slot]),
-                                             None, dev.d, _lib.ptr(self.objs[t:]), self.chunk))
-            _lib.check(lib.simopt_timestamp(ssp, _lib.ptr(self.stamps[t:])))
+        a.stamp = None
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self.steps_done[k] = ev
+        # the epoch's records in one launch, off the critical path: dot(c, x) for
+        # check_feasible and the objective's vec_sum of newsvendor_cost_block, per step
+        self.side.wait_event(ev)
+        _lib.check(lib.simopt_nv_epoch_records(
+            ssp, _lib.ptr(self.xs), H, (t0 + 1) % H, M, _lib.ptr(dev.c), _lib.ptr(dev.mu),
+            _lib.ptr(dev.sigma), _lib.ptr(dev.k), _lib.ptr(dev.h), _lib.ptr(dev.v), dev.d, self.chunk,
+            _lib.ptr(self.spent[t0:]), _lib.ptr(self.objs[t0:])))
+        if self.shard is not None:
+            self.epoch_done[k] = self._reduce_epoch(k)
+        else:
             done = torch.cuda.Event()
             done.record(self.side)
-            self.side_done[t] = done
-        if self.shard is not None:
-            self.side_done[t0 + M - 1] = self._reduce_epoch(k)
-        self.epoch_done[k] = self.side_done[t0 + M - 1]
+            self.epoch_done[k] = done
 
     def _reduce_epoch(self, k: int):
         """Epoch totals over the product shards: one allreduce on the side stream, into a
@@ -553,7 +552,6 @@ class NvFwGraphEngine(NvFwEngine):
         super().__init__(prob, inner_iters, epochs, chunk)
         d, M = self.dev.d, self.M
         self.rings = [torch.zeros(M + 1, d, dtype=F64, device="cuda") for _ in range(2)]
-        self.terms_e = torch.empty(M, d, dtype=F64, device="cuda")
         self.flags_e = [torch.zeros(M + 1, dtype=torch.int32, device="cuda") for _ in range(2)]
         self.spent_e = [empty(M) for _ in range(2)]
         self.objs_e = [empty(M) for _ in range(2)]
@@ -595,25 +593,24 @@ class NvFwGraphEngine(NvFwEngine):
         return a
 
     def _steps(self, p: int, main, side):
-        """The epoch's step sequence on `main` (+ recording on `side`), capture-safe."""
+        """The epoch's step sequence on `main` (+ its records on `side`), capture-safe."""
         lib, dev, M = self.lib, self.dev, self.M
         sp, ssp = _lib.stream_ptr(main), _lib.stream_ptr(side)
         P = _lib.ptr
         self.starts[p].copy_(self.rings[1 - p][M])
         _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(self._step_args(p, -1, False))))
-        fork = torch.cuda.Event()
         for m in range(M):
-            _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(self._step_args(p, m, True))))
-            ev = torch.cuda.Event()
-            ev.record(main)
-            side.wait_event(ev)
-            xout = self.rings[p][m + 1]
-            _lib.check(lib.simopt_nv_cost_terms(ssp, P(xout), P(dev.mu), P(dev.sigma), P(dev.k), P(dev.h),
-                                                P(dev.v), dev.d, P(self.terms_e[m])))
-            _lib.check(lib.simopt_tree_sums2(ssp, P(dev.c), P(xout), dev.d, P(self.spent_e[p][m:]),
-                                             P(self.terms_e[m]), None, dev.d, P(self.objs_e[p][m:]),
-                                             self.chunk))
-            _lib.check(lib.simopt_timestamp(ssp, P(self.stamps_e[p][m:])))
+            a = self._step_args(p, m, True)
+            a.stamp = self.stamps_e[p][m:].data_ptr()
+            _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)
+        # rings[p][1..M] are the epoch's iterates
+        _lib.check(lib.simopt_nv_epoch_records(
+            ssp, P(self.rings[p]), M + 1, 1, M, P(dev.c), P(dev.mu), P(dev.sigma), P(dev.k),
+            P(dev.h), P(dev.v), dev.d, self.chunk, P(self.spent_e[p]), P(self.objs_e[p])))
+        fork = torch.cuda.Event()
         fork.record(side)
         main.wait_event(fork)  # join: the epoch ends when its recording ends
 

@@ -267,3 +267,28 @@ def test_resample_kernels_agree(pkg, d, S, monkeypatch):
         canon = torch.cat([torch.sort(keys[:, s0:s0 + 4096], dim=1).values for s0 in range(0, S, 4096)], 1)
         out.append((prob.dev.off.clone(), canon))
     assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("d,chunk,H,r0,M", [(10_000, 4096, 51, 40, 25), (3_001, 16, 7, 5, 6),
+                                            (1, 4096, 3, 2, 3), (5_000, 7, 4, 0, 4)])
+def test_epoch_records_match_per_step_sums(pkg, d, chunk, H, r0, M):
+    """simopt_nv_epoch_records = per step nv_cost_terms + tree_sums2, bit for bit (ring
+    wrap, chunk counts 1..715 incl. > 64, a ragged last chunk, one product)."""
+    from paper_2404_11631_b200 import _lib
+    g = torch.Generator().manual_seed(d + chunk)
+    xs = (torch.rand(H, d, generator=g, dtype=torch.float64) * 50).cuda()
+    mu = (torch.rand(d, generator=g, dtype=torch.float64) * 40 + 5).cuda()
+    sd = (torch.rand(d, generator=g, dtype=torch.float64) * 10 + 0.5).cuda()
+    c, k, h, v = ((torch.rand(d, generator=g, dtype=torch.float64) * 3).cuda() for _ in range(4))
+    spent, objs = torch.empty(M, dtype=torch.float64, device="cuda"), torch.empty(M, dtype=torch.float64, device="cuda")
+    P = _lib.ptr
+    _lib.call("simopt_nv_epoch_records", _lib.stream_ptr(), P(xs), H, r0, M, P(c), P(mu), P(sd),
+              P(k), P(h), P(v), d, chunk, P(spent), P(objs))
+    terms = torch.empty(d, dtype=torch.float64, device="cuda")
+    ref = torch.empty(2, M, dtype=torch.float64, device="cuda")
+    for m in range(M):
+        x = xs[(r0 + m) % H]
+        _lib.call("simopt_nv_cost_terms", _lib.stream_ptr(), P(x), P(mu), P(sd), P(k), P(h), P(v), d, P(terms))
+        _lib.call("simopt_tree_sums2", _lib.stream_ptr(), P(c), P(x), d, P(ref[0, m:]), P(terms), None, d,
+                  P(ref[1, m:]), chunk)
+    assert torch.equal(spent, ref[0]) and torch.equal(objs, ref[1])

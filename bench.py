@@ -382,6 +382,8 @@ def _c2_config(args, dd, ss, world):
                          "TINY test configuration (not the C2 bench)"),
             "d": dd, "S": ss, "M": M, "seed": SEED,
             "step": f"1 resampling epoch = 1 resample + {M} FW iterations",
+            "timing": ("steady-state pipeline: the timed region holds K resample launches and K "
+                       "epochs of FW steps, each epoch's steps overlapping the next epoch's resample"),
             "l2": "inputs larger than L2 (8 GB of fp64 demands per epoch in the reference's data "
                   "model; 4.5 GB of keyed layout here)",
             "parallelism": (f"products sharded x{world}" if world > 1 else "single GPU")}
@@ -403,9 +405,12 @@ def run_c2(args, rank, world, shard):
     eng = make_nv_engine(prob, M, epochs, backend.chunk_size)  # CUDA-graph epochs when sharded
     stream = pkg.RngStream(SEED, 2)
     eng.start()
-    for k in range(args.warmup):  # the next epoch's resample overlaps this epoch's steps,
-        nxt = ss if k + 1 < args.warmup else None  # never across the timed-region boundary
-        eng.enqueue_epoch(k, stream, ss, next_samples=nxt)
+    # steady-state pipeline: every epoch's steps overlap the next epoch's resample.  The
+    # timed region holds exactly K resample launches and K epochs of steps: the first timed
+    # epoch's resample is the warm-up's last overlap, the resample behind the last timed
+    # epoch runs inside the region.
+    for k in range(args.warmup):
+        eng.enqueue_epoch(k, stream, ss, next_samples=ss)
     eng.finish()
     torch.cuda.synchronize()
     if shard is not None:
@@ -415,8 +420,7 @@ def run_c2(args, rank, world, shard):
     with ClockSampler(torch.cuda.current_device()) as clk:
         e0.record()
         for k in range(args.warmup, epochs):
-            nxt = ss if k + 1 < epochs else None
-            eng.enqueue_epoch(k, stream, ss, time_resample=True, next_samples=nxt)
+            eng.enqueue_epoch(k, stream, ss, time_resample=True, next_samples=ss)
         eng.finish()
         e1.record()
         torch.cuda.synchronize()
@@ -462,7 +466,7 @@ def run_c2(args, rank, world, shard):
                      "frac": value / it_roof,
                      "basis": "SURVEY 8(d) C2: 8*d*S*(1+1/M) bytes per FW iteration at hbm peak "
                               "(x n_gpus)"}
-    launches_per_epoch = M + 3  # resample, M+1 fused steps (stamping themselves), the epoch's records
+    launches_per_epoch = M + 4  # resample, M+1 fused steps (stamping themselves), records (terms + sums)
     if world > 1 and eng.mailbox is None:
         launches_per_epoch += 2 * M  # LMO pack + apply around each NCCL exchange
     cfg = _c2_config(args, dd, ss, world)

@@ -328,9 +328,12 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
     reinterpret_cast<int4*>(hist)[2 * ct + 1] = make_int4(0, 0, 0, 0);
     named_arrive(3 + p, kWsThreads);  // slot p free for the producers
     uint32_t* dst = keys + j * S + e0;
-    if (aligned) {
-      for (int l4 = ct; l4 < (len >> 2); l4 += kWsCons)
-        reinterpret_cast<uint4*>(dst)[l4] = reinterpret_cast<const uint4*>(sm.sorted)[l4];
+    if (aligned) {  // pointer walk: one 64-bit add per 16-byte store, no per-store IMAD.WIDE
+      uint4* dp = reinterpret_cast<uint4*>(dst) + ct;
+      const uint4* sp = reinterpret_cast<const uint4*>(sm.sorted) + ct;
+      const uint4* se = reinterpret_cast<const uint4*>(sm.sorted) + (len >> 2);
+#pragma unroll 4
+      for (; sp < se; sp += kWsCons, dp += kWsCons) *dp = *sp;
     } else {
       for (int l = ct; l < len; l += kWsCons) dst[l] = sm.sorted[l];
     }
@@ -569,6 +572,8 @@ __device__ __forceinline__ NvThresh nv_thresh(const NvWindow& w) {
 // Ambiguous draws that do not fit the queue are resolved by the warp that found them.
 constexpr int kSlotsPerWarp = 4;
 constexpr int kCtaQueue = 1024;
+// usable queue entries (tests shrink it through SIMOPT_NV_QCAP to drive the overflow path)
+__device__ int g_nv_qcap = kCtaQueue;
 
 struct NvStepCtx {
   int64_t jstar;
@@ -656,6 +661,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
   ArgMin best{INFINITY, INT64_MAX};
   const int S32 = (int)a.S;  // S < 2^31 (checked on the host)
   const int nseg = (int)a.nseg;
+  const int qcap = min(g_nv_qcap, kCtaQueue);
   const bool vec = (a.S & 3) == 0;  // rows start 16-byte aligned: vector key loads
   for (;;) {
     // ---- (A) count certain keys, queue ambiguous draws
@@ -733,7 +739,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
                 if (bit == 4 * v + u) key = kv[v][u];
             const uint64_t idx = (uint64_t)(sg * NV_SEG) + (key & 4095u);
             const int pos = atomicAdd(&q_len, 1);
-            if (pos < kCtaQueue)
+            if (pos < qcap)
               queue[pos] = (uint64_t)slot << 40 | idx;
             else  // queue full: resolve here
               c += nv_resolve(sp, j * a.S + (int64_t)idx, mu, sigma, x);
@@ -758,7 +764,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
     }
     __syncthreads();
     // ---- (B) resolve the queued draws exactly, all threads
-    const int nq = min(q_len, kCtaQueue);
+    const int nq = min(q_len, qcap);
     for (int e = threadIdx.x; e < nq; e += kIterWarps * 32) {
       const uint64_t v = queue[e];
       const int slot = (int)(v >> 40);
@@ -962,6 +968,17 @@ extern "C" int simopt_nv_decode(void* stream, const uint32_t* keys, const double
 extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   NvIterArgs a = *args;
   SIMOPT_REQUIRE(a.S < (1LL << 31), SIMOPT_E_CONFIG, "S >= 2^31 samples per product");
+  {  // test hook: SIMOPT_NV_QCAP shrinks the ambiguous-draw queue (set once per process)
+    static std::once_flag once;
+    static cudaError_t qerr = cudaSuccess;
+    std::call_once(once, [] {
+      if (const char* qc = getenv("SIMOPT_NV_QCAP")) {
+        const int v = atoi(qc);
+        qerr = cudaMemcpyToSymbol(g_nv_qcap, &v, sizeof(int));
+      }
+    });
+    SIMOPT_CUDA(qerr);
+  }
   // gradient steps: one resident wave of blocks pulling products from a counter; update-only
   // steps: a static split.  SIMOPT_NV_ITER=W,B,V (A/B): W warps per block, B blocks per SM,
   // V 16-byte key loads per lane per pass.  Measured on the pipelined C2 epoch (the steps
@@ -1031,20 +1048,34 @@ __global__ void k_nv_cost(const double* __restrict__ x, const double* __restrict
     out[j] = nv_cost_term(x[j], mu[j], sigma[j], unit[j], hold[j], sell[j]);
 }
 
-// One epoch's records (simopt_nv_epoch_records): warp g takes unit (m, job, chunk),
-// job 0 = dot(c, x_m), job 1 = sum of newsvendor_cost_block(x_m); the chunk's terms are
-// staged a 256-element tile at a time by all lanes and added by lane 0 in index order
-// from 0.0 (_kernels.py:45-68, the dot_partials / sum_partials chains).  The warp that
-// completes a unit's last chunk folds its partials pairwise (the fixed tree).
+// One epoch's records (simopt_nv_epoch_records), two launches:
+//  k_nv_records_terms  newsvendor_cost_block of every (step, product), all threads;
+//  k_nv_records        warp g takes unit (m, job, chunk), job 0 = dot(c, x_m), job 1 = sum
+//                      of step m's terms; lane 0 adds the chunk in index order from 0.0
+//                      (_kernels.py:45-68, the dot_partials / sum_partials chains) from
+//                      256-element tiles the warp stages in shared memory; the warp that
+//                      completes a unit's last chunk folds its partials pairwise (the tree
+//                      of k_fold_strided).
+__global__ void k_nv_records_terms(const double* __restrict__ xs, int64_t H, int64_t r0, int64_t M,
+                                   const double* __restrict__ mu, const double* __restrict__ sigma,
+                                   const double* __restrict__ unit, const double* __restrict__ hold,
+                                   const double* __restrict__ sell, int64_t d,
+                                   double* __restrict__ terms) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * d;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / d, i = e - m * d;
+    const double x = xs[((r0 + m) % H) * d + i];
+    terms[e] = nv_cost_term(x, mu[i], sigma[i], unit[i], hold[i], sell[i]);
+  }
+}
+
 constexpr int kRecWarps = 4, kRecTile = 256;
 __global__ void __launch_bounds__(kRecWarps * 32)
     k_nv_records(const double* __restrict__ xs, int64_t H, int64_t r0, int64_t M,
-                 const double* __restrict__ c, const double* __restrict__ mu,
-                 const double* __restrict__ sigma, const double* __restrict__ unit,
-                 const double* __restrict__ hold, const double* __restrict__ sell, int64_t d,
+                 const double* __restrict__ c, const double* __restrict__ terms, int64_t d,
                  int64_t chunk, int64_t nch, double* __restrict__ part, unsigned* __restrict__ cnt,
                  double* __restrict__ spent, double* __restrict__ objs) {
-  __shared__ double buf[kRecWarps][kRecTile];
+  __shared__ double buf[kRecWarps][2][kRecTile];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t total = M * 2 * nch;
   for (int64_t g = (int64_t)blockIdx.x * kRecWarps + warp; g < total;
@@ -1053,25 +1084,50 @@ __global__ void __launch_bounds__(kRecWarps * 32)
     const int job = (int)(u & 1);
     const int64_t m = u >> 1;
     const double* x = xs + ((r0 + m) % H) * d;
+    const double* y = terms + m * d;
     const int64_t lo = ch * chunk, hi = lo + chunk < d ? lo + chunk : d;
-    double s = 0.0;
-    double* b = buf[warp];
-    for (int64_t base = lo; base < hi; base += kRecTile) {
-#pragma unroll 2
-      for (int t = lane; t < kRecTile; t += 32) {
-        const int64_t i = base + t;
-        double v = 0.0;
-        if (i < hi)
-          v = job == 0 ? c[i] * x[i] : nv_cost_term(x[i], mu[i], sigma[i], unit[i], hold[i], sell[i]);
-        b[t] = v;
+    constexpr int kPer = kRecTile / 32;
+    double v[kPer];
+    auto load = [&](int64_t base) {  // raw loads, consumed one tile later (in flight meanwhile)
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) {
+        const int64_t i = base + lane + 32 * t;
+        v[t] = i < hi ? (job == 0 ? c[i] * x[i] : y[i]) : 0.0;
       }
+    };
+    double s = 0.0;
+    load(lo);
+    int par = 0;
+    for (int64_t base = lo; base < hi; base += kRecTile) {
+      double* b = buf[warp][par];
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) b[lane + 32 * t] = v[t];
       __syncwarp();
+      if (base + kRecTile < hi) load(base + kRecTile);
       if (lane == 0) {
         const int n = (int)(hi - base < kRecTile ? hi - base : kRecTile);
-        for (int t = 0; t < n; ++t) s = s + b[t];
+        if (n == kRecTile) {  // 16-element register batches: the chain runs at DADD latency
+          double w[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) w[k] = b[k];
+          for (int t = 0; t < kRecTile; t += 16) {
+            double z[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) z[k] = w[k];
+            if (t + 16 < kRecTile) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) w[k] = b[t + 16 + k];
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) s = s + z[k];
+          }
+        } else {
+          for (int t = 0; t < n; ++t) s = s + b[t];
+        }
       }
-      __syncwarp();
+      par ^= 1;
     }
+    __syncwarp();
     if (lane == 0) {
       part[u * nch + ch] = s;
       __threadfence();
@@ -1107,16 +1163,22 @@ extern "C" int simopt_nv_epoch_records(void* stream, const double* xs, int64_t H
   }
   const int64_t nch = ceil_div(d, chunk);
   const int64_t units = M * 2;
+  const size_t tbytes = (size_t)(M * d) * sizeof(double);
   unsigned char* ws = static_cast<unsigned char*>(
-      simopt_scratch(st, units * nch * sizeof(double) + units * sizeof(unsigned) + 64));
+      simopt_scratch(st, tbytes + units * nch * sizeof(double) + units * sizeof(unsigned) + 64));
   SIMOPT_REQUIRE(ws != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
-  double* part = reinterpret_cast<double*>(ws);
-  unsigned* cnt = reinterpret_cast<unsigned*>(ws + units * nch * sizeof(double));
+  double* terms = reinterpret_cast<double*>(ws);
+  double* part = reinterpret_cast<double*>(ws + tbytes);
+  unsigned* cnt = reinterpret_cast<unsigned*>(ws + tbytes + units * nch * sizeof(double));
   SIMOPT_CUDA(cudaMemsetAsync(cnt, 0, units * sizeof(unsigned), st));
+  const int64_t tg = ceil_div(M * d, 256);
+  k_nv_records_terms<<<(int)(tg < 16 * SIMOPT_NUM_SMS ? tg : 16 * SIMOPT_NUM_SMS), 256, 0, st>>>(
+      xs, H, r0, M, mu, sigma, unit, hold, sell, d, terms);
+  SIMOPT_CHECK_LAUNCH("k_nv_records_terms");
   const int64_t g = ceil_div(units * nch, kRecWarps);
   const int grid = (int)(g < 8 * SIMOPT_NUM_SMS ? g : 8 * SIMOPT_NUM_SMS);
-  k_nv_records<<<grid, kRecWarps * 32, 0, st>>>(xs, H, r0, M, c, mu, sigma, unit, hold, sell, d, chunk,
-                                                nch, part, cnt, spent, objs);
+  k_nv_records<<<grid, kRecWarps * 32, 0, st>>>(xs, H, r0, M, c, terms, d, chunk, nch, part, cnt,
+                                                spent, objs);
   SIMOPT_CHECK_LAUNCH("k_nv_records");
   return SIMOPT_OK;
 }

@@ -292,3 +292,18 @@ def test_epoch_records_match_per_step_sums(pkg, d, chunk, H, r0, M):
         _lib.call("simopt_tree_sums2", _lib.stream_ptr(), P(c), P(x), d, P(ref[0, m:]), P(terms), None, d,
                   P(ref[1, m:]), chunk)
     assert torch.equal(spent, ref[0]) and torch.equal(objs, ref[1])
+
+
+@pytest.mark.parametrize("qcap", ["0", "1"])
+def test_step_queue_overflow_path(qcap):
+    """Ambiguous draws that do not fit the step kernel's CTA queue are resolved by the warp
+    that found them: with the queue shrunk to 0/1 entries (SIMOPT_NV_QCAP) FW traces still
+    match the oracle bit for bit (scalar and 16-byte key-load paths)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SIMOPT_NV_QCAP=qcap)
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_paths.py"), "nv"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "nv ok" in r.stdout, r.stdout + r.stderr

@@ -28,14 +28,15 @@ def nv():
     from paper_2404_11631_b200.instances import gen_newsvendor_instance
     from paper_2404_11631_b200.tasks import NewsvendorProblem
     b = p.make_backend("cuda")
-    # d = 37 products, S = 9001: three 4096-segments, the last ragged, rows not 4-aligned
-    d, S, K, M = 37, 9001, 2, 3
-    rec = fw_run(NewsvendorProblem(gen_newsvendor_instance(d, p.RngStream(42, 0)), b),
-                 FwConfig(K, M, S, p.RngStream(42, 2)), b)
-    task = orc.gen_newsvendor_instance(d, orc.Stream(42, 0))
-    objs, x = orc.fw_run_newsvendor(task, K, M, S, orc.Stream(42, 2))
-    assert np.array_equal(rec.final_iterate, x), "iterate differs from the oracle"
-    assert np.allclose(rec.objectives, objs, rtol=1e-13, atol=0)
+    # d = 37 products; S = 9001: three 4096-segments, the last ragged, rows not 4-aligned
+    # (scalar key loads); S = 8192: aligned rows (16-byte key loads)
+    for d, S, K, M in ((37, 9001, 2, 3), (37, 8192, 2, 3)):
+        rec = fw_run(NewsvendorProblem(gen_newsvendor_instance(d, p.RngStream(42, 0)), b),
+                     FwConfig(K, M, S, p.RngStream(42, 2)), b)
+        task = orc.gen_newsvendor_instance(d, orc.Stream(42, 0))
+        objs, x = orc.fw_run_newsvendor(task, K, M, S, orc.Stream(42, 2))
+        assert np.array_equal(rec.final_iterate, x), f"iterate differs from the oracle (S={S})"
+        assert np.allclose(rec.objectives, objs, rtol=1e-13, atol=0)
     print("nv ok")
 
 

@@ -390,6 +390,31 @@ def _c2_config(args, dd, ss, world):
 
 
 # ---------------------------------------------------------------- ours: C2 headline
+def philox_floor(nblocks, kernel_ms):
+    """The resample's arithmetic floor, timed in this run: the same Philox4x64-10 core over
+    the launch's blocks with nothing stored (simopt_philox_floor), CUDA events."""
+    import torch
+    from paper_2404_11631_b200 import _lib
+    out = torch.empty(8 * torch.cuda.get_device_properties(0).multi_processor_count * 256,
+                      dtype=torch.int64, device="cuda")
+    call = lambda: _lib.call("simopt_philox_floor", _lib.stream_ptr(), SEED, 2, 0, nblocks,
+                             _lib.ptr(out), out.numel())
+    call()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for _ in range(3):
+        e0.record()
+        call()
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    floor = min(times)
+    return {"bound": "issue: heavy-FMA pipe (IMAD.WIDE of the Philox 64x64->128 products)",
+            "floor_ms": floor, "kernel_ms": kernel_ms, "frac": floor / kernel_ms,
+            "basis": f"Philox4x64-10 of the launch's {nblocks} blocks through the resample's own "
+                     "17-product core with nothing stored, timed in this run"}
+
+
 def run_c2(args, rank, world, shard):
     import torch
     import paper_2404_11631_b200 as pkg
@@ -449,6 +474,7 @@ def run_c2(args, rank, world, shard):
     traffic = profiled_traffic()  # captured at N=1 (all d products): this rank's share
     if traffic is not None:
         traffic = int(round(traffic * d_loc / D))
+    compute_roof = philox_floor(d_loc * ss // 4, res_ms)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": "k_nv_resample", "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
@@ -457,7 +483,8 @@ def run_c2(args, rank, world, shard):
                 "note": ("instruction-bound by design: Philox4x64-10 + an fp32 SFU Box-Muller key "
                          "per draw, exact glibc Box-Muller only for the few ambiguous draws at "
                          "query time; kernel_ms is measured (CUDA events on the generator stream) "
-                         "while the previous epoch's FW steps run; see profiles/")}
+                         "while the previous epoch's FW steps run; see profiles/"),
+                "compute_roof": compute_roof}
     # the step against SURVEY 8(d)'s per-iteration roof (8 d S (1 + 1/M) bytes: one scan of
     # the epoch's demands per gradient + the amortised write) -- the keyed ECDF reads a
     # window of buckets per product instead of all S demands, so it runs above that roof

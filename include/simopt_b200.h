@@ -50,6 +50,13 @@ int simopt_abi_version(void);
 /* Write the device %globaltimer (ns) to *out when the stream reaches this point. */
 int simopt_timestamp(void* stream, int64_t* out);
 
+/* Measurement (bench.py roofline.compute_roof): Philox4x64-10 blocks clo+1 .. clo+nblocks
+ * of key (seed, sid), counter word 1 = 0, through the newsvendor resample's Philox core
+ * with the words XOR-folded per thread into out[0 .. 8*SMs*256) -- the arithmetic floor of
+ * a resample of nblocks blocks (nothing stored per block). */
+int simopt_philox_floor(void* stream, uint64_t seed, uint64_t sid, uint64_t clo, int64_t nblocks,
+                        uint64_t* out, int64_t out_len);
+
 /* ------------------------------------------------------------ sampling.py */
 /* uniform01 (sampling.py:87-102): n doubles of stream (seed, stream_id) at the
  * 128-bit block counter (ctr_hi:ctr_lo).  The caller advances the counter by

@@ -38,6 +38,7 @@ SIGNATURES = {
     "simopt_axpy_ptr": [_vp, _vp, _vp, _vp, _i64, _vp],
     "simopt_map_kernel": [_vp, _i32, _vp, _i64, _vp],
     "simopt_timestamp": [_vp, _vp],
+    "simopt_philox_floor": [_vp, _u64, _u64, _u64, _i64, _vp, _i64],
     "simopt_scale_sub": [_vp, _vp, _d, _vp, _i64, _vp],
     "simopt_min_value": [_vp, _vp, _i64, _vp],
     "simopt_lmo_simplex_slack": [_vp, _vp, _i64, _vp, _vp],

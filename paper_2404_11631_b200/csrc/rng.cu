@@ -174,3 +174,41 @@ extern "C" int simopt_threshold(void* stream, const double* x, double thr, int64
   SIMOPT_CHECK_LAUNCH("k_threshold");
   return SIMOPT_OK;
 }
+
+// --- measurement: the Philox-only floor of the newsvendor resample ---------------------
+// Blocks clo+1 .. clo+n of key (seed, sid) through the resample's own Philox core (round 0
+// carried by a 128-bit add, 17 products per block), words XOR-folded into out[thread] so
+// nothing is stored per block: the heavy-FMA-pipe time a resample of n blocks cannot beat.
+namespace {
+constexpr int kFloorThreads = 256;
+__global__ void __launch_bounds__(kFloorThreads) k_philox_floor(const phx_keys rk, const phx_pre pre,
+                                                                 uint64_t clo, int64_t n,
+                                                                 uint64_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * kFloorThreads;
+  const int64_t t0 = (int64_t)blockIdx.x * kFloorThreads + threadIdx.x;
+  uint64_t acc = 0, h0 = 0, l0 = 0;
+  if (t0 < n) phx_mulhilo(PHILOX_M0, clo + 1 + (uint64_t)t0, &h0, &l0);
+  const uint64_t sl = (uint64_t)stride * PHILOX_M0;  // M0 * stride mod 2^128, formed once
+  const uint64_t sh = __umul64hi((uint64_t)stride, PHILOX_M0);
+  for (int64_t t = t0; t < n; t += stride) {
+    const phx4 w = philox4x64_10_rk_r0(h0, l0, rk, pre);
+    acc ^= w.v[0] ^ w.v[1] ^ w.v[2] ^ w.v[3];
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(l0), "+l"(h0) : "l"(sl), "l"(sh));
+  }
+  out[t0] = acc;
+}
+}  // namespace
+
+extern "C" int simopt_philox_floor(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
+                                   int64_t nblocks, uint64_t* out, int64_t out_len) {
+  SIMOPT_REQUIRE(nblocks > 0, SIMOPT_E_EMPTY, "requested %lld blocks", (long long)nblocks);
+  SIMOPT_REQUIRE(phx_no_carry(clo, (uint64_t)nblocks), SIMOPT_E_CONFIG, "counter would carry");
+  const int grid = 8 * SIMOPT_NUM_SMS;
+  SIMOPT_REQUIRE(out_len >= (int64_t)grid * kFloorThreads, SIMOPT_E_CONFIG,
+                 "out needs %lld words", (long long)grid * kFloorThreads);
+  const phx_keys rk = phx_round_keys(seed, sid);
+  k_philox_floor<<<grid, kFloorThreads, 0, as_stream(stream)>>>(rk, phx_precompute(0, rk), clo,
+                                                               nblocks, out);
+  SIMOPT_CHECK_LAUNCH("k_philox_floor");
+  return SIMOPT_OK;
+}

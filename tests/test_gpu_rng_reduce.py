@@ -131,3 +131,20 @@ def test_errors(pkg):
         pkg.make_backend("gpu")
     with pytest.raises(pkg.EmptyRequest):
         pkg.uniform01(pkg.RngStream(1, 0), 0)
+
+
+def test_philox_floor_words():
+    """simopt_philox_floor runs the resample's Philox core: the XOR of every word of blocks
+    clo+1 .. clo+n equals numpy's Philox4x64 stream (bench.py's compute_roof measures it)."""
+    import numpy as np
+    import torch
+    from paper_2404_11631_b200 import _lib
+    seed, sid, clo, n = 42, 2, 12345, 100_003
+    nw = 8 * torch.cuda.get_device_properties(0).multi_processor_count * 256
+    out = torch.empty(nw, dtype=torch.int64, device="cuda")
+    _lib.call("simopt_philox_floor", _lib.stream_ptr(), seed, sid, clo, n, _lib.ptr(out), nw)
+    got = np.bitwise_xor.reduce(out.cpu().numpy().view(np.uint64))
+    bg = np.random.Philox(key=np.array([seed, sid], dtype=np.uint64),
+                          counter=np.array([clo, 0, 0, 0], dtype=np.uint64))
+    want = np.bitwise_xor.reduce(bg.random_raw(4 * n).astype(np.uint64))
+    assert got == want

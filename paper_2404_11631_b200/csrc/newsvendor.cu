@@ -575,6 +575,21 @@ constexpr int kCtaQueue = 1024;
 // usable queue entries (tests shrink it through SIMOPT_NV_QCAP to drive the overflow path)
 __device__ int g_nv_qcap = kCtaQueue;
 
+// One ambiguous draw of a step (rare): appended to the CTA queue, or resolved here when the
+// queue is full (returns the draw's count then, 0 when queued).  Out of line so the scan
+// loops keep their register budget.
+__device__ __noinline__ int nv_amb_push(uint32_t key, int sg, int slot, int64_t j, int64_t S,
+                                        double mu, double sigma, double x, NvStreamPos sp,
+                                        uint64_t* queue, int* q_len, int qcap) {
+  const uint64_t idx = (uint64_t)(sg * NV_SEG) + (key & 4095u);
+  const int pos = atomicAdd(q_len, 1);
+  if (pos < qcap) {
+    queue[pos] = (uint64_t)slot << 40 | idx;
+    return 0;
+  }
+  return nv_resolve(sp, j * S + (int64_t)idx, mu, sigma, x);
+}
+
 struct NvStepCtx {
   int64_t jstar;
   double sval, gamma;
@@ -678,6 +693,10 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
       if (lane == 0) pend = atomicAdd(next, 1u);  // the product after the next one
       const NvWindow w = nv_window(x, mu, sigma);
       const NvThresh th = nv_thresh(w);
+      // as raw keys (q << 12 | local): key < kb <=> q < qb (certainly below);
+      // key - kb <= kspan (unsigned) <=> qb <= q < qa (ambiguous); qa > qb always
+      const uint32_t kb = (uint32_t)th.qb << 12;
+      const uint32_t kspan = (uint32_t)((((uint64_t)th.qa) << 12) - 1 - kb);
       const int blo = (int)(w.qlo >> (NV_QBITS - 10)), bhi = (int)(w.qhi >> (NV_QBITS - 10));
       int c = 0;  // per lane: certain-below (+ locally resolved) draws
       for (int s0 = 0; s0 < nseg; s0 += 32) {
@@ -693,56 +712,82 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
           seg = a.keys + j * a.S + e0;
           c += start;
         }
-        // keys [a0, end) in 16-byte words (a0 = start rounded down; vec: rows aligned), or
-        // one key per "word" otherwise; elements outside [start, end) are masked
-        const int a0 = vec ? (start & ~3) : start;
-        const int nw = vec ? ((end - a0 + 3) >> 2) : (end - a0);
-        unsigned amb = 0;  // unused outside the pass
-        for (int w0 = 0; w0 < nw; w0 += kVecBatch) {
-          uint32_t kv[kVecBatch][4];
-#pragma unroll
-          for (int v = 0; v < kVecBatch; ++v) {
-            if (w0 + v < nw) {
-              if (vec) {
-                const uint4 t = reinterpret_cast<const uint4*>(seg + a0)[w0 + v];
-                kv[v][0] = t.x;
-                kv[v][1] = t.y;
-                kv[v][2] = t.z;
-                kv[v][3] = t.w;
-              } else {
-                kv[v][0] = seg[a0 + w0 + v];
-                kv[v][1] = kv[v][2] = kv[v][3] = 0xFFFFFFFFu;
-              }
-            } else {
-              kv[v][0] = kv[v][1] = kv[v][2] = kv[v][3] = 0xFFFFFFFFu;
-            }
-          }
-          amb = 0;
-#pragma unroll
-          for (int v = 0; v < kVecBatch; ++v)
+        // (1) the window's ends: vec -> the 16-byte words holding start and end - 1, masked
+        //     to [start, end) (one batch); otherwise the whole window, 8 single keys per batch
+        const int hb = start & ~3, tb = (end - 1) & ~3;
+        const bool two = vec && end > start && tb > hb;  // the tail word is not the head word
+        const int hend = vec ? hb + 4 : end;             // body: [hb + 4, tb) when two
+        const int bend = two ? tb : hend;
+        for (int p0 = start, first = 1; vec ? (first != 0 && end > start) : p0 < end; p0 += 8, first = 0) {
+          uint32_t kv[8];
+          unsigned ok = 0, amb = 0;
+          if (vec) {
+            const uint4 h = *reinterpret_cast<const uint4*>(seg + hb);
+            uint4 t = h;
+            if (two) t = *reinterpret_cast<const uint4*>(seg + tb);
+            kv[0] = h.x; kv[1] = h.y; kv[2] = h.z; kv[3] = h.w;
+            kv[4] = t.x; kv[5] = t.y; kv[6] = t.z; kv[7] = t.w;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const int pos = vec ? a0 + 4 * (w0 + v) + u : (u == 0 ? a0 + w0 + v : end);
-              const bool valid = pos >= start && pos < end;
-              const int q = (int)(kv[v][u] >> 12);
-              c += (valid && q < th.qb) ? 1 : 0;
-              amb |= (valid && q >= th.qb && q < th.qa) ? 1u << (4 * v + u) : 0u;
+              ok |= (hb + u >= start && hb + u < end) ? 1u << u : 0u;
+              ok |= (two && tb + u < end) ? 1u << (4 + u) : 0u;
             }
-          while (amb) {  // ambiguous draws: rare; one call site keeps the register budget
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const bool v = p0 + i < end;
+              kv[i] = v ? seg[p0 + i] : 0u;
+              ok |= v ? 1u << i : 0u;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const bool v = (ok >> i) & 1u;
+            c += (v && kv[i] < kb) ? 1 : 0;
+            amb |= (v && kv[i] - kb <= kspan) ? 1u << i : 0u;
+          }
+          while (amb) {  // ambiguous draws: rare
             const int bit = __ffs(amb) - 1;
             amb &= amb - 1;
             uint32_t key = 0;
 #pragma unroll
-            for (int v = 0; v < kVecBatch; ++v)
+            for (int i = 0; i < 8; ++i) key = (bit == i) ? kv[i] : key;
+            c += nv_amb_push(key, sg, slot, j, a.S, mu, sigma, x, sp, queue, &q_len, qcap);
+          }
+        }
+        // (2) the 16-byte body [hend, bend): per key one unsigned compare for "certainly
+        //     below" and one for "ambiguous" (key - kb <= kspan)
+        const int nvec = bend > hend ? (bend - hend) >> 2 : 0;
+        const uint4* vrow = reinterpret_cast<const uint4*>(seg + hend);
+        for (int v0 = 0; v0 < nvec; v0 += kVecBatch) {
+          uint4 t[kVecBatch];
 #pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (bit == 4 * v + u) key = kv[v][u];
-            const uint64_t idx = (uint64_t)(sg * NV_SEG) + (key & 4095u);
-            const int pos = atomicAdd(&q_len, 1);
-            if (pos < qcap)
-              queue[pos] = (uint64_t)slot << 40 | idx;
-            else  // queue full: resolve here
-              c += nv_resolve(sp, j * a.S + (int64_t)idx, mu, sigma, x);
+          for (int v = 0; v < kVecBatch; ++v)
+            if (v0 + v < nvec) t[v] = vrow[v0 + v];
+          unsigned amb = 0;
+#pragma unroll
+          for (int v = 0; v < kVecBatch; ++v) {
+            if (v0 + v < nvec) {
+              const uint32_t k4[4] = {t[v].x, t[v].y, t[v].z, t[v].w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                c += k4[u] < kb ? 1 : 0;
+                amb |= (k4[u] - kb <= kspan) ? 1u << (4 * v + u) : 0u;
+              }
+            }
+          }
+          while (amb) {  // ambiguous draws: rare
+            const int bit = __ffs(amb) - 1;
+            amb &= amb - 1;
+            uint32_t key = 0;
+#pragma unroll
+            for (int v = 0; v < kVecBatch; ++v) {
+              key = (bit == 4 * v) ? t[v].x : key;
+              key = (bit == 4 * v + 1) ? t[v].y : key;
+              key = (bit == 4 * v + 2) ? t[v].z : key;
+              key = (bit == 4 * v + 3) ? t[v].w : key;
+            }
+            c += nv_amb_push(key, sg, slot, j, a.S, mu, sigma, x, sp, queue, &q_len, qcap);
           }
         }
       }

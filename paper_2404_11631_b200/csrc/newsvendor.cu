@@ -176,12 +176,25 @@ struct WsSmem {
   int hist[2][NV_B];
   int wsum[kWsCons / 32];
 };  // 56 KB: up to three CTAs per SM
+static_assert(sizeof(int) * NV_B == 4096, "ws_counter: hist[1] follows hist[0] at +4 KB");
+
+// The bucket counter of key k in hist[p]: hist[0] and hist[1] are adjacent 4 KB arrays, so
+// the byte offset is ((k >> 20) & 0xffc) | (p << 12) -- one LOP3 after the shift, and the
+// struct offset becomes the shared-memory instruction's immediate (no IMAD.IADD per key on
+// the heavy pipe, which the Philox products saturate).
+__device__ __forceinline__ int* ws_counter(unsigned char* smem, uint32_t k, uint32_t pbase);
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ int* ws_counter(unsigned char* smem, uint32_t k, uint32_t pbase) {
+  constexpr int kBucketByteShift = 12 + NV_QBITS - 10 - 2;  // bucket index * 4 bytes
+  return reinterpret_cast<int*>(smem + offsetof(WsSmem, hist) +
+                                (((k >> kBucketByteShift) & 0xffcu) | pbase));
 }
 
 // kRegCap: launch-bound blocks per SM used only to cap registers (3: 48 registers;
@@ -217,6 +230,7 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
       const int lbase = (int)((q0 << 2) - i0);
       uint32_t* raw = sm.raw[p];
       int* hist = sm.hist[p];
+      const uint32_t pbase = (uint32_t)p << 12;
       // kNoCarry: round 0's product M0 * (c0 + t) is carried from t to t + kWsProd by a
       // 128-bit add (phx_r0_advance): 17 products per block instead of 18
       uint64_t r0h = 0, r0l = 0;
@@ -238,7 +252,7 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             kk[u] = nv_key(z[u], (uint32_t)(l0 + u));
-            atomicAdd(&hist[kk[u] >> kBucketShift], 1);
+            atomicAdd(ws_counter(smem_raw, kk[u], pbase), 1);
           }
           reinterpret_cast<uint4*>(raw)[l0 >> 2] = make_uint4(kk[0], kk[1], kk[2], kk[3]);
         } else {
@@ -310,12 +324,13 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
     reinterpret_cast<uint4*>(off + (j * nseg + s) * (int64_t)NV_B)[ct] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     named_sync(5, kWsCons);  // cursors complete
     if (aligned) {
+      const uint32_t pbase = (uint32_t)p << 12;
       for (int l4 = ct; l4 < (len >> 2); l4 += kWsCons) {
         const uint4 k4 = reinterpret_cast<const uint4*>(raw)[l4];
-        sm.sorted[atomicAdd(&hist[k4.x >> kBucketShift], 1)] = k4.x;
-        sm.sorted[atomicAdd(&hist[k4.y >> kBucketShift], 1)] = k4.y;
-        sm.sorted[atomicAdd(&hist[k4.z >> kBucketShift], 1)] = k4.z;
-        sm.sorted[atomicAdd(&hist[k4.w >> kBucketShift], 1)] = k4.w;
+        sm.sorted[atomicAdd(ws_counter(smem_raw, k4.x, pbase), 1)] = k4.x;
+        sm.sorted[atomicAdd(ws_counter(smem_raw, k4.y, pbase), 1)] = k4.y;
+        sm.sorted[atomicAdd(ws_counter(smem_raw, k4.z, pbase), 1)] = k4.z;
+        sm.sorted[atomicAdd(ws_counter(smem_raw, k4.w, pbase), 1)] = k4.w;
       }
     } else {
       for (int l = ct; l < len; l += kWsCons) {

@@ -349,6 +349,17 @@ int simopt_mv_fw_tail(void* stream, const double* g, const double* w_in, const d
                       const double* mean, int64_t d, int64_t chunk, double* w_out, int* status,
                       double* wmin_out, double* wsum_out, double* lin_out, int exact);
 
+/* One mean-variance FW epoch in fused mode as ONE cooperative launch (frank_wolfe.py:106-117
+ * for MeanVarProblem, tasks.py:67-85): ring row 0 holds the epoch's first iterate; for
+ * m < M: g = inv * Xc^T Xc w_m - mean, lmo_simplex_slack, ring[m+1] = w_{m+1}, status[m]
+ * (NaN -> INVALID_GRADIENT), wmin/wsum/lin of w_{m+1}, quad[m] = |Xc w_{m+1}|^2, stamps[m]
+ * (%globaltimer).  Sums in fixed block-parallel orders, like simopt_fused_rows + the fused
+ * simopt_mv_fw_tail.  X row-major rows x cols, cols <= 2048; SIMOPT_E_CONFIG otherwise. */
+int simopt_mv_fw_epoch(void* stream, const double* X, int64_t rows, int64_t cols,
+                       const double* mean, double inv, double* ring, int64_t M,
+                       const double* gamma, int* status, double* wmin, double* wsum, double* lin,
+                       double* quad, int64_t* stamps);
+
 /* ------------------------------------------------------------ projections (projected SGD) */
 /* Euclidean projection of y onto {x >= 0, c . x <= budget} (c == NULL: all ones, i.e.
  * the simplex-with-slack of lmo.py:20-24 for budget 1).  One CTA: bisection on the

@@ -108,6 +108,7 @@ SIGNATURES = {
     "simopt_comm_allgather": [_vp, _vp, _vp, _vp, _i64],
     "simopt_comm_broadcast": [_vp, _vp, _vp, _vp, _i64, _i32],
     "simopt_mv_fw_tail": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32],
+    "simopt_mv_fw_epoch": [_vp, _vp, _i64, _i64, _vp, _d, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "simopt_project_budget": [_vp, _vp, _vp, _d, _i64, _vp, _vp],
     "simopt_project_box": [_vp, _vp, _d, _d, _i64, _vp],
     "simopt_philox4x32": [_vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _i64, _vp],

@@ -28,12 +28,16 @@
 // (16-byte loads) p = tid + k*256, k < K.  A tile is R rows; one thread holds
 // R*K double2 of it.
 #include <cooperative_groups.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include <mutex>
 #include <utility>
 #include <vector>
 
 #include "common.cuh"
+#include "fw.cuh"
 #include "reduce_device.cuh"
 
 namespace cg = cooperative_groups;
@@ -256,6 +260,258 @@ __global__ void __launch_bounds__(256) k_fused_finish(const double* __restrict__
       double t = 0.0;
       for (int k = 0; k < 8; ++k) t += ws[k];
       *scalar_out = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent mean-variance FW epoch (fused mode, one GPU, d <= 2*K*256 in one CTA band).
+// At C1's size (N = 10^4 rows x d = 10^3, 80 MB, L2-resident) a step is ~15 us of work
+// split over a pass, a fold and a tail: as separate launches it is launch- and
+// latency-bound (~44 us per step).  One cooperative launch runs the epoch's M+1 passes
+// with two grid barriers per step:
+//   pass (all CTAs, rows striped by tile as in k_fused_rows): q = Xc w, per-CTA column
+//        partials of Xc^T q and the partial |q|^2  -> barrier
+//   fold (columns split over CTAs, a warp per column, lane-strided over the CTA partials
+//        then a fixed xor tree; CTA 0 folds |q|^2): g = inv * sum - mean, quad  -> barrier
+//   tail (every CTA, redundantly: g is 8-16 KB in L2): NaN check, argmin (lmo.py:56-65),
+//        w' = (gamma * ((-1 * w) + s)) + w straight into the CTA's shared v for the next
+//        pass; CTA 0 also writes the ring row, min, the block-parallel sum / dot and the
+//        step's %globaltimer stamp.
+// Summation orders are fixed (deterministic run to run); like every fused pass they are
+// not the reference tree (trajectories within the north-star 1e-8).
+struct MvEpochArgs {
+  const double* X;
+  int64_t N, d;
+  const double* mean;
+  double inv;          // 1 / (N - 1)
+  double* ring;        // (M+1) x d: row 0 = the epoch's first iterate, rows 1..M written
+  int64_t M;
+  const double* gamma;  // M step sizes
+  int* status;          // M
+  double *wmin, *wsum, *lin, *quad;  // M each
+  int64_t* stamps;      // M
+  double* col_part;     // [G][d]
+  double* scal_part;    // [G]
+  double* g;            // d
+  unsigned* bar;        // grid barrier counter, zero at launch
+};
+
+__device__ __forceinline__ void mv_grid_sync(unsigned* bar, unsigned& target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += gridDim.x;
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+template <int K, bool VEC>
+__global__ void __launch_bounds__(kNT, 2) k_mv_fw_epoch(MvEpochArgs a) {
+  constexpr int R = (16 / K) < 1 ? 1 : 16 / K;
+  extern __shared__ __align__(16) double vs[];  // [2*K*256] w (the pass's v), then the mean
+  __shared__ double red[2][R][kNW];
+  __shared__ double part[2][R];
+  __shared__ double wts[2][R];
+  __shared__ double sred[kNW];
+  __shared__ ArgMin wb[kNW];
+  __shared__ double wm[kNW], rs[kNW], rd[kNW];
+  __shared__ int nan_seen;
+  __shared__ int64_t js_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t d = a.d, N = a.N, G = gridDim.x, cta = blockIdx.x;
+  double* ms = vs + 2 * K * kNT;
+  for (int i = tid; i < 2 * K * kNT; i += kNT) {
+    vs[i] = i < d ? a.ring[i] : 0.0;
+    ms[i] = i < d ? a.mean[i] : 0.0;
+  }
+  __syncthreads();
+  const double2* v2 = reinterpret_cast<const double2*>(vs);
+  const double2* m2 = reinterpret_cast<const double2*>(ms);
+  unsigned target = 0;
+  const int64_t ntiles = (N + R - 1) / R;
+  for (int64_t it = 0; it <= a.M; ++it) {
+    // ---- pass at w_it: columns for step it's gradient (it < M), |q|^2 for step it-1
+    const bool cols = it < a.M;
+    double2 acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
+    double sc = 0.0;
+    int par = 0;
+    for (int64_t tile = cta; tile < ntiles; tile += G, par ^= 1) {
+      const int64_t r0 = tile * R;
+      double2 x[R][K];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const bool rv = r0 + i < N;
+        const double* row = a.X + (rv ? r0 + i : 0) * d;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int64_t c = 2 * (int64_t)(tid + k * kNT);
+          if (VEC) {
+            x[i][k] = (rv && c < d) ? ld2(row + c) : make_double2(0.0, 0.0);
+          } else {
+            x[i][k].x = (rv && c < d) ? __ldg(row + c) : 0.0;
+            x[i][k].y = (rv && c + 1 < d) ? __ldg(row + c + 1) : 0.0;
+          }
+        }
+      }
+      double s[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        double acc_s = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double2 vk = v2[tid + k * kNT];
+          const double2 mk = m2[tid + k * kNT];
+          x[i][k].x = x[i][k].x - mk.x;  // Xc = X - mean (tasks.py:63)
+          x[i][k].y = x[i][k].y - mk.y;
+          acc_s = fma(x[i][k].x, vk.x, acc_s);
+          acc_s = fma(x[i][k].y, vk.y, acc_s);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc_s += __shfl_xor_sync(0xffffffffu, acc_s, o);
+        s[i] = acc_s;
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) red[par][i][warp] = s[i];
+      }
+      __syncthreads();
+      if (tid < R) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kNW; ++w) t += red[par][tid][w];
+        const int64_t r = r0 + tid;
+        double wt = 0.0;
+        if (r < N) {
+          wt = t;
+          sc = fma(t, t, sc);
+        }
+        wts[par][tid] = wt;
+      }
+      __syncthreads();
+      if (cols) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const double wt = wts[par][i];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            acc[k].x = fma(x[i][k].x, wt, acc[k].x);
+            acc[k].y = fma(x[i][k].y, wt, acc[k].y);
+          }
+        }
+      }
+    }
+    if (cols) {
+      double* out = a.col_part + cta * d;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int64_t c = 2 * (int64_t)(tid + k * kNT);
+        if (c < d) out[c] = acc[k].x;
+        if (c + 1 < d) out[c + 1] = acc[k].y;
+      }
+    }
+    {
+      double v = sc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) sred[warp] = v;
+      __syncthreads();
+      if (tid == 0) {
+        double p = 0.0;
+        for (int w = 0; w < kNW; ++w) p += sred[w];
+        a.scal_part[cta] = p;
+      }
+    }
+    mv_grid_sync(a.bar, target);
+    // ---- fold: column j by warp (j - c0) of CTA j / cpc; CTA 0 also folds |q|^2
+    const int64_t cpc = (d + G - 1) / G;
+    const int64_t c0 = cta * cpc;
+    for (int64_t j = c0 + warp; cols && j < c0 + cpc && j < d; j += kNW) {
+      double t = 0.0;
+      for (int64_t c = lane; c < G; c += 32) t += __ldcg(a.col_part + c * d + j);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) a.g[j] = t * a.inv - ms[j];
+    }
+    if (cta == 0 && it > 0 && warp == kNW - 1) {
+      double t = 0.0;
+      for (int64_t c = lane; c < G; c += 32) t += __ldcg(a.scal_part + c);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) a.quad[it - 1] = t;
+    }
+    if (it == a.M) break;
+    mv_grid_sync(a.bar, target);
+    // ---- tail of step it (every CTA): LMO, update into vs; CTA 0 records
+    if (tid == 0) nan_seen = 0;
+    __syncthreads();
+    ArgMin b{INFINITY, INT64_MAX};
+    for (int64_t i = tid; i < d; i += kNT) {
+      const double gi = __ldcg(a.g + i);
+      if (gi != gi) nan_seen = 1;
+      b = amin(b, ArgMin{gi, i});
+    }
+    b = warp_amin(b);
+    if (lane == 0) wb[warp] = b;
+    __syncthreads();
+    if (tid == 0) {
+      ArgMin r = wb[0];
+      for (int w = 1; w < kNW; ++w) r = amin(r, wb[w]);
+      if (cta == 0 && nan_seen) atomicOr(a.status + it, SIMOPT_E_INVALID_GRADIENT);
+      js_sh = (r.i < d && __ldcg(a.g + r.i) < 0.0) ? r.i : -1;  // vertex e_j* iff g_j* < 0
+    }
+    __syncthreads();
+    const int64_t js = js_sh;
+    const double gm = a.gamma[it];
+    double mn = INFINITY, ps = 0.0, pd = 0.0;
+    for (int64_t i = tid; i < d; i += kNT) {
+      const double wi = vs[i];
+      const double si = (i == js) ? 1.0 : 0.0;
+      const double dir = -1.0 * wi + si;
+      const double wo = gm * dir + wi;
+      vs[i] = wo;
+      if (cta == 0) {
+        a.ring[(it + 1) * d + i] = wo;
+        ps += wo;
+        pd += wo * ms[i];
+        mn = (wo < mn || wo != wo) ? wo : mn;
+      }
+    }
+    if (cta == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ps += __shfl_xor_sync(0xffffffffu, ps, o);
+        pd += __shfl_xor_sync(0xffffffffu, pd, o);
+        const double t = __shfl_xor_sync(0xffffffffu, mn, o);
+        mn = (t < mn || t != t) ? t : mn;
+      }
+      if (lane == 0) {
+        rs[warp] = ps;
+        rd[warp] = pd;
+        wm[warp] = mn;
+      }
+    }
+    __syncthreads();  // vs holds w_{it+1} for the next pass
+    if (cta == 0 && tid == 0) {
+      double sa = 0.0, sb = 0.0, m = wm[0];
+      for (int w = 0; w < kNW; ++w) {
+        sa += rs[w];
+        sb += rd[w];
+        if (w > 0) m = (wm[w] < m || wm[w] != wm[w]) ? wm[w] : m;
+      }
+      a.wsum[it] = sa;
+      a.lin[it] = sb;
+      a.wmin[it] = m;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.stamps[it] = (int64_t)t;
     }
   }
 }
@@ -898,4 +1154,53 @@ extern "C" int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bi
 
 extern "C" int64_t simopt_peer_reduce_bytes(int64_t world, int64_t cols) {
   return (2 * world * (cols + 1)) * (int64_t)sizeof(double) + 2 * world * kFB * (int64_t)sizeof(uint64_t);
+}
+
+extern "C" int simopt_mv_fw_epoch(void* stream, const double* X, int64_t rows, int64_t cols,
+                                  const double* mean, double inv, double* ring, int64_t M,
+                                  const double* gamma, int* status, double* wmin, double* wsum,
+                                  double* lin, double* quad, int64_t* stamps) {
+  cudaStream_t st = as_stream(stream);
+  SIMOPT_REQUIRE(rows >= 1 && cols >= 1 && M >= 1, SIMOPT_E_DIMENSION, "empty epoch");
+  int K = (int)((cols + 2 * kNT - 1) / (2 * kNT));
+  SIMOPT_REQUIRE(K <= 4, SIMOPT_E_CONFIG, "persistent epoch supports up to %d columns", 8 * kNT);
+  if (K == 3) K = 4;
+  const bool vec = (cols % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  using Fn = void (*)(MvEpochArgs);
+  Fn fn = K == 1 ? (vec ? k_mv_fw_epoch<1, true> : k_mv_fw_epoch<1, false>)
+        : K == 2 ? (vec ? k_mv_fw_epoch<2, true> : k_mv_fw_epoch<2, false>)
+                 : (vec ? k_mv_fw_epoch<4, true> : k_mv_fw_epoch<4, false>);
+  const size_t smem = (size_t)2 * 2 * K * kNT * sizeof(double);
+  int per_sm = 0;
+  SIMOPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SIMOPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT, smem));
+  SIMOPT_REQUIRE(per_sm >= 1, SIMOPT_E_CONFIG, "persistent epoch kernel does not fit an SM");
+  if (const char* ev = getenv("SIMOPT_MV_EPOCH_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(ev)));
+  const int64_t G = (int64_t)per_sm * SIMOPT_NUM_SMS;
+  unsigned char* ws = static_cast<unsigned char*>(
+      simopt_scratch(st, (G * cols + G + cols) * sizeof(double) + 64));
+  SIMOPT_REQUIRE(ws != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
+  MvEpochArgs a;
+  a.X = X;
+  a.N = rows;
+  a.d = cols;
+  a.mean = mean;
+  a.inv = inv;
+  a.ring = ring;
+  a.M = M;
+  a.gamma = gamma;
+  a.status = status;
+  a.wmin = wmin;
+  a.wsum = wsum;
+  a.lin = lin;
+  a.quad = quad;
+  a.stamps = stamps;
+  a.col_part = reinterpret_cast<double*>(ws);
+  a.scal_part = a.col_part + G * cols;
+  a.g = a.scal_part + G;
+  a.bar = reinterpret_cast<unsigned*>(a.g + cols);
+  SIMOPT_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), st));
+  void* params[] = {&a};
+  SIMOPT_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)G), dim3(kNT), params, smem, st));
+  return SIMOPT_OK;
 }

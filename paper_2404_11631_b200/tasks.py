@@ -9,6 +9,7 @@ stream and its trace is read back once per epoch.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -1184,6 +1185,15 @@ class MvFwEngine:
         ws = self.rings[k % 2]
         self.status.zero_()
         self.gamma.copy_(torch.tensor([fw_step_size(k, M, m) for m in range(M)], dtype=F64))
+        if (self.prob.fused and self.prob.shard is None and self.prob.dimension <= 2048
+                and os.environ.get("SIMOPT_MV_PERSISTENT", "1") != "0"):
+            # the whole epoch as one cooperative launch (simopt_mv_fw_epoch)
+            P = _lib.ptr
+            _lib.check(self.lib.simopt_mv_fw_epoch(
+                _lib.stream_ptr(), P(x), n_k, self.prob.dimension, P(mean), 1.0 / (n_k - 1), P(ws), M,
+                P(self.gamma), P(self.status), P(self.wmin), P(self.wsum), P(self.lin), P(self.quad),
+                P(self.stamps)))
+            return
         key = (k % 2, x.data_ptr(), mean.data_ptr(), n_k, self.prob.fused)
         g = self.graphs.get(key)
         if not self.use_graph or self.prob.shard is not None:  # collectives: eager

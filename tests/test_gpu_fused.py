@@ -119,3 +119,27 @@ def test_meanvar_fw_fused_vs_oracle(pkg, d, n):
     objs, w = orc.fw_run_meanvar(mu, sigma, K, M, n, orc.Stream(42, 2))
     np.testing.assert_allclose(rec.objectives, objs, rtol=1e-8)
     assert _rel(rec.final_iterate, w) < 1e-8
+
+
+@pytest.mark.parametrize("d,n", [(1000, 10_000), (513, 2001), (2048, 1500), (2, 50)])
+def test_meanvar_persistent_epoch_vs_launch_sequence(pkg, d, n, monkeypatch):
+    """The one-launch fused epoch (simopt_mv_fw_epoch, cooperative grid) against the launch
+    sequence it replaces (fused pass + finish + tail per step, CUDA graphs) and the oracle:
+    same trajectory to 1e-10, oracle to 1e-8 (odd d: scalar loads; d = 2048: K = 4)."""
+    from paper_2404_11631_b200.frank_wolfe import FwConfig, fw_run
+    from paper_2404_11631_b200.instances import gen_meanvar_instance
+    from paper_2404_11631_b200.tasks import MeanVarProblem
+    K, M = 3, 25
+    b = pkg.make_backend("cuda")
+    task = gen_meanvar_instance(d, pkg.RngStream(42, 0))
+    recs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SIMOPT_MV_PERSISTENT", flag)
+        recs.append(fw_run(MeanVarProblem(task, b, fused=True), FwConfig(K, M, n, pkg.RngStream(42, 2)), b))
+    np.testing.assert_allclose(recs[0].objectives, recs[1].objectives, rtol=1e-10)
+    assert _rel(recs[0].final_iterate, recs[1].final_iterate) < 1e-10
+    assert np.all(np.diff(recs[0].elapsed_ns) >= 0)
+    mu, sigma = orc.gen_meanvar_instance(d, orc.Stream(42, 0))
+    objs, w = orc.fw_run_meanvar(mu, sigma, K, M, n, orc.Stream(42, 2))
+    np.testing.assert_allclose(recs[0].objectives, objs, rtol=1e-8)
+    assert _rel(recs[0].final_iterate, w) < 1e-8

@@ -311,6 +311,193 @@ __device__ __forceinline__ void mv_grid_sync(unsigned* bar, unsigned& target) {
   __syncthreads();
 }
 
+// Between two passes (both epoch kernels): barrier, fold the CTA partials into g (columns
+// split over CTAs, a warp per column lane-strided over the partials then an xor tree; CTA 0
+// folds |q|^2 into quad[it-1]), barrier, then every CTA runs step it's tail: NaN check,
+// argmin (lmo.py:56-65), w' = (gamma * ((-1 * w) + s)) + w into vs[0..d); CTA 0 writes the
+// ring row, min, the block-parallel sum / dot and the step's %globaltimer stamp.  Returns
+// false after the last pass (it == M).
+__device__ __noinline__ bool mv_epoch_fold_tail(const MvEpochArgs& a, int64_t it, bool cols,
+                                                double* vs, const double* ms, unsigned& target) {
+  __shared__ ArgMin wb[32];
+  __shared__ double wm[32], rs[32], rd[32];
+  __shared__ int nan_seen;
+  __shared__ int64_t js_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int64_t d = a.d, G = gridDim.x, cta = blockIdx.x;
+  mv_grid_sync(a.bar, target);
+  const int64_t cpc = (d + G - 1) / G;
+  const int64_t c0 = cta * cpc;
+  for (int64_t j = c0 + warp; cols && j < c0 + cpc && j < d; j += nw) {
+    double t = 0.0;
+    for (int64_t c = lane; c < G; c += 32) t += __ldcg(a.col_part + c * d + j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) a.g[j] = t * a.inv - ms[j];
+  }
+  if (cta == 0 && it > 0 && warp == nw - 1) {
+    double t = 0.0;
+    for (int64_t c = lane; c < G; c += 32) t += __ldcg(a.scal_part + c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) a.quad[it - 1] = t;
+  }
+  if (it == a.M) return false;
+  mv_grid_sync(a.bar, target);
+  if (tid == 0) nan_seen = 0;
+  __syncthreads();
+  ArgMin b{INFINITY, INT64_MAX};
+  for (int64_t i = tid; i < d; i += blockDim.x) {
+    const double gi = __ldcg(a.g + i);
+    if (gi != gi) nan_seen = 1;
+    b = amin(b, ArgMin{gi, i});
+  }
+  b = warp_amin(b);
+  if (lane == 0) wb[warp] = b;
+  __syncthreads();
+  if (tid == 0) {
+    ArgMin r = wb[0];
+    for (int w = 1; w < nw; ++w) r = amin(r, wb[w]);
+    if (cta == 0 && nan_seen) atomicOr(a.status + it, SIMOPT_E_INVALID_GRADIENT);
+    js_sh = (r.i < d && __ldcg(a.g + r.i) < 0.0) ? r.i : -1;  // vertex e_j* iff g_j* < 0
+  }
+  __syncthreads();
+  const int64_t js = js_sh;
+  const double gm = a.gamma[it];
+  double mn = INFINITY, ps = 0.0, pd = 0.0;
+  for (int64_t i = tid; i < d; i += blockDim.x) {
+    const double wi = vs[i];
+    const double si = (i == js) ? 1.0 : 0.0;
+    const double dir = -1.0 * wi + si;
+    const double wo = gm * dir + wi;
+    vs[i] = wo;
+    if (cta == 0) {
+      a.ring[(it + 1) * d + i] = wo;
+      ps += wo;
+      pd += wo * ms[i];
+      mn = (wo < mn || wo != wo) ? wo : mn;
+    }
+  }
+  if (cta == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      pd += __shfl_xor_sync(0xffffffffu, pd, o);
+      const double t = __shfl_xor_sync(0xffffffffu, mn, o);
+      mn = (t < mn || t != t) ? t : mn;
+    }
+    if (lane == 0) {
+      rs[warp] = ps;
+      rd[warp] = pd;
+      wm[warp] = mn;
+    }
+  }
+  __syncthreads();  // vs holds w_{it+1} for the next pass
+  if (cta == 0 && tid == 0) {
+    double sa = 0.0, sb = 0.0, m = wm[0];
+    for (int w = 0; w < nw; ++w) {
+      sa += rs[w];
+      sb += rd[w];
+      if (w > 0) m = (wm[w] < m || wm[w] != wm[w]) ? wm[w] : m;
+    }
+    a.wsum[it] = sa;
+    a.lin[it] = sb;
+    a.wmin[it] = m;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.stamps[it] = (int64_t)t;
+  }
+  return true;
+}
+
+// Warp-per-row variant (d <= 1024): lane l holds columns 2(l + 32k), k < KW, of one row at
+// a time, so a row dot is one warp's xor tree (no block barrier per tile) and the column
+// accumulators stay per warp; a pass ends with the warps' partials combined in warp order
+// through shared memory.  ~4.5 instructions per element instead of ~12 for the CTA-per-row
+// tiles at C1's d = 1000.
+template <int KW, bool VEC>
+__global__ void __launch_bounds__(kNT, 1) k_mv_fw_epoch_wr(MvEpochArgs a) {
+  constexpr int CW = 64 * KW;  // columns covered
+  extern __shared__ __align__(16) double smw[];
+  double* vs = smw;            // [CW] w (the pass's v)
+  double* ms = smw + CW;       // [CW] mean
+  double* wp = smw + 2 * CW;   // [kNW][CW] per-warp column partials
+  __shared__ double wsc[kNW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t d = a.d, N = a.N, G = gridDim.x, cta = blockIdx.x;
+  for (int i = tid; i < CW; i += kNT) {
+    vs[i] = i < d ? a.ring[i] : 0.0;
+    ms[i] = i < d ? a.mean[i] : 0.0;
+  }
+  __syncthreads();
+  const double2* v2 = reinterpret_cast<const double2*>(vs);
+  const double2* m2 = reinterpret_cast<const double2*>(ms);
+  const int64_t gw = cta * kNW + warp, nwg = G * kNW;
+  unsigned target = 0;
+  for (int64_t it = 0; it <= a.M; ++it) {
+    const bool cols = it < a.M;
+    double2 acc[KW];
+#pragma unroll
+    for (int k = 0; k < KW; ++k) acc[k] = make_double2(0.0, 0.0);
+    double sc = 0.0;
+    for (int64_t r = gw; r < N; r += nwg) {
+      const double* row = a.X + r * d;
+      double2 x[KW];
+#pragma unroll
+      for (int k = 0; k < KW; ++k) {
+        const int64_t c = 2 * (int64_t)(lane + 32 * k);
+        if (VEC) {
+          x[k] = c < d ? ld2(row + c) : make_double2(0.0, 0.0);
+        } else {
+          x[k].x = c < d ? __ldg(row + c) : 0.0;
+          x[k].y = c + 1 < d ? __ldg(row + c + 1) : 0.0;
+        }
+      }
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < KW; ++k) {
+        const double2 mk = m2[lane + 32 * k];
+        const double2 vk = v2[lane + 32 * k];
+        x[k].x = x[k].x - mk.x;  // Xc = X - mean (tasks.py:63); padded columns stay 0
+        x[k].y = x[k].y - mk.y;
+        t = fma(x[k].x, vk.x, t);
+        t = fma(x[k].y, vk.y, t);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      sc = fma(t, t, sc);  // identical on every lane; lane 0's is used
+      if (cols) {
+#pragma unroll
+        for (int k = 0; k < KW; ++k) {
+          acc[k].x = fma(x[k].x, t, acc[k].x);
+          acc[k].y = fma(x[k].y, t, acc[k].y);
+        }
+      }
+    }
+    if (cols) {
+      double2* w2 = reinterpret_cast<double2*>(wp + warp * CW);
+#pragma unroll
+      for (int k = 0; k < KW; ++k) w2[lane + 32 * k] = acc[k];
+    }
+    if (lane == 0) wsc[warp] = sc;
+    __syncthreads();
+    if (cols) {
+      for (int64_t c = tid; c < d; c += kNT) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kNW; ++w) t += wp[w * CW + c];
+        a.col_part[cta * d + c] = t;
+      }
+    }
+    if (tid == 0) {
+      double p = 0.0;
+      for (int w = 0; w < kNW; ++w) p += wsc[w];
+      a.scal_part[cta] = p;
+    }
+    if (!mv_epoch_fold_tail(a, it, cols, vs, ms, target)) break;
+  }
+}
+
 template <int K, bool VEC>
 __global__ void __launch_bounds__(kNT, 2) k_mv_fw_epoch(MvEpochArgs a) {
   constexpr int R = (16 / K) < 1 ? 1 : 16 / K;
@@ -319,10 +506,6 @@ __global__ void __launch_bounds__(kNT, 2) k_mv_fw_epoch(MvEpochArgs a) {
   __shared__ double part[2][R];
   __shared__ double wts[2][R];
   __shared__ double sred[kNW];
-  __shared__ ArgMin wb[kNW];
-  __shared__ double wm[kNW], rs[kNW], rd[kNW];
-  __shared__ int nan_seen;
-  __shared__ int64_t js_sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t d = a.d, N = a.N, G = gridDim.x, cta = blockIdx.x;
   double* ms = vs + 2 * K * kNT;
@@ -429,90 +612,7 @@ __global__ void __launch_bounds__(kNT, 2) k_mv_fw_epoch(MvEpochArgs a) {
         a.scal_part[cta] = p;
       }
     }
-    mv_grid_sync(a.bar, target);
-    // ---- fold: column j by warp (j - c0) of CTA j / cpc; CTA 0 also folds |q|^2
-    const int64_t cpc = (d + G - 1) / G;
-    const int64_t c0 = cta * cpc;
-    for (int64_t j = c0 + warp; cols && j < c0 + cpc && j < d; j += kNW) {
-      double t = 0.0;
-      for (int64_t c = lane; c < G; c += 32) t += __ldcg(a.col_part + c * d + j);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0) a.g[j] = t * a.inv - ms[j];
-    }
-    if (cta == 0 && it > 0 && warp == kNW - 1) {
-      double t = 0.0;
-      for (int64_t c = lane; c < G; c += 32) t += __ldcg(a.scal_part + c);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0) a.quad[it - 1] = t;
-    }
-    if (it == a.M) break;
-    mv_grid_sync(a.bar, target);
-    // ---- tail of step it (every CTA): LMO, update into vs; CTA 0 records
-    if (tid == 0) nan_seen = 0;
-    __syncthreads();
-    ArgMin b{INFINITY, INT64_MAX};
-    for (int64_t i = tid; i < d; i += kNT) {
-      const double gi = __ldcg(a.g + i);
-      if (gi != gi) nan_seen = 1;
-      b = amin(b, ArgMin{gi, i});
-    }
-    b = warp_amin(b);
-    if (lane == 0) wb[warp] = b;
-    __syncthreads();
-    if (tid == 0) {
-      ArgMin r = wb[0];
-      for (int w = 1; w < kNW; ++w) r = amin(r, wb[w]);
-      if (cta == 0 && nan_seen) atomicOr(a.status + it, SIMOPT_E_INVALID_GRADIENT);
-      js_sh = (r.i < d && __ldcg(a.g + r.i) < 0.0) ? r.i : -1;  // vertex e_j* iff g_j* < 0
-    }
-    __syncthreads();
-    const int64_t js = js_sh;
-    const double gm = a.gamma[it];
-    double mn = INFINITY, ps = 0.0, pd = 0.0;
-    for (int64_t i = tid; i < d; i += kNT) {
-      const double wi = vs[i];
-      const double si = (i == js) ? 1.0 : 0.0;
-      const double dir = -1.0 * wi + si;
-      const double wo = gm * dir + wi;
-      vs[i] = wo;
-      if (cta == 0) {
-        a.ring[(it + 1) * d + i] = wo;
-        ps += wo;
-        pd += wo * ms[i];
-        mn = (wo < mn || wo != wo) ? wo : mn;
-      }
-    }
-    if (cta == 0) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        ps += __shfl_xor_sync(0xffffffffu, ps, o);
-        pd += __shfl_xor_sync(0xffffffffu, pd, o);
-        const double t = __shfl_xor_sync(0xffffffffu, mn, o);
-        mn = (t < mn || t != t) ? t : mn;
-      }
-      if (lane == 0) {
-        rs[warp] = ps;
-        rd[warp] = pd;
-        wm[warp] = mn;
-      }
-    }
-    __syncthreads();  // vs holds w_{it+1} for the next pass
-    if (cta == 0 && tid == 0) {
-      double sa = 0.0, sb = 0.0, m = wm[0];
-      for (int w = 0; w < kNW; ++w) {
-        sa += rs[w];
-        sb += rd[w];
-        if (w > 0) m = (wm[w] < m || wm[w] != wm[w]) ? wm[w] : m;
-      }
-      a.wsum[it] = sa;
-      a.lin[it] = sb;
-      a.wmin[it] = m;
-      uint64_t t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.stamps[it] = (int64_t)t;
-    }
+    if (!mv_epoch_fold_tail(a, it, cols, vs, ms, target)) break;
   }
 }
 
@@ -1170,7 +1270,18 @@ extern "C" int simopt_mv_fw_epoch(void* stream, const double* X, int64_t rows, i
   Fn fn = K == 1 ? (vec ? k_mv_fw_epoch<1, true> : k_mv_fw_epoch<1, false>)
         : K == 2 ? (vec ? k_mv_fw_epoch<2, true> : k_mv_fw_epoch<2, false>)
                  : (vec ? k_mv_fw_epoch<4, true> : k_mv_fw_epoch<4, false>);
-  const size_t smem = (size_t)2 * 2 * K * kNT * sizeof(double);
+  size_t smem = (size_t)2 * 2 * K * kNT * sizeof(double);
+  const char* wr_env = getenv("SIMOPT_MV_EPOCH_WR");
+  if (cols <= 1024 && !(wr_env && atoi(wr_env) == 0)) {  // warp-per-row pass
+    int kw = 1;
+    while (64 * kw < cols) kw *= 2;
+    fn = kw == 1 ? (vec ? k_mv_fw_epoch_wr<1, true> : k_mv_fw_epoch_wr<1, false>)
+       : kw == 2 ? (vec ? k_mv_fw_epoch_wr<2, true> : k_mv_fw_epoch_wr<2, false>)
+       : kw == 4 ? (vec ? k_mv_fw_epoch_wr<4, true> : k_mv_fw_epoch_wr<4, false>)
+       : kw == 8 ? (vec ? k_mv_fw_epoch_wr<8, true> : k_mv_fw_epoch_wr<8, false>)
+                 : (vec ? k_mv_fw_epoch_wr<16, true> : k_mv_fw_epoch_wr<16, false>);
+    smem = (size_t)(2 + kNW) * 64 * kw * sizeof(double);
+  }
   int per_sm = 0;
   SIMOPT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SIMOPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT, smem));

@@ -616,7 +616,10 @@ def task_c1(args, world, shard):
             "roofline": {"bound": "hbm", "achieved": alg * it_s / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg * it_s / 1e9 / peak, "traffic": None,
                          "basis": "SURVEY 8(d) C1: 8 N d (1 + 1/M) algorithmic bytes per FW iteration",
-                         "peak_kind": pk, "note": "launch-latency bound (4 launches per step)"},
+                         "peak_kind": pk,
+                         "note": ("one cooperative launch per epoch (simopt_mv_fw_epoch): latency-bound "
+                                  "-- per step a pass over 80 MB of L2-resident X, two grid barriers, "
+                                  "the column fold and the LMO tail")},
             "clocks": clk, "final_objective": float(rec.objectives[-1])}
 
 

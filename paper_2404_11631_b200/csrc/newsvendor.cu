@@ -955,10 +955,12 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   const phx_pre pre = phx_precompute(chi, rk);
   const bool no_carry = phx_no_carry(clo, (uint64_t)ceil_div(d * S, 4));
   // SIMOPT_NV_RESAMPLE=1: the single-role kernel k_nv_resample (comparison); default: the
-  // warp-specialised k_nv_resample_ws (3.76 vs 4.12 ms at C2).  Both are persistent grids
-  // of one full wave; the step kernels of the previous epoch (high stream priority) run in
-  // the registers and shared memory left beside it (ws: 3 x 56 KB shared, 55 K registers
-  // per SM) and on the SMs that finish their share first.
+  // warp-specialised k_nv_resample_ws (3.72 vs 4.12 ms at C2).  Both are persistent grids
+  // of one full wave.  The previous epoch's step kernels (high stream priority) share the
+  // SMs with it: a 4-warp step block (10 K registers, 9 KB shared) fits beside the three
+  // resample CTAs (55 K registers, 3 x 57 KB); further step blocks take an SM slot whenever
+  // the scheduler has one, which costs the resample ~0.3 ms per epoch (4,3,4 is the best
+  // measured trade-off, tools/nv_iter_ab.py).
   const char* ev = getenv("SIMOPT_NV_RESAMPLE");
   if (!(ev && atoi(ev) == 1)) {
     const int64_t g = nblk < (int64_t)SIMOPT_NUM_SMS * kWsPerSm ? nblk : (int64_t)SIMOPT_NUM_SMS * kWsPerSm;

@@ -64,7 +64,21 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-template <int MODE, int C, int K, bool VEC>
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t peer_addr(uint32_t local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+
+// Wide rows (C > 1): ASYNC exchanges each tile's per-CTA row-dot partials by pushing them
+// into every peer's receive slots with st.async (DSMEM) completing on the peer's mbarrier,
+// instead of a cluster-wide barrier per tile; a CTA waits only for its peers' partials of
+// the tile it is on.  Slots and barriers are double-buffered by tile parity: a CTA can be
+// at most one tile ahead of its slowest peer (each tile needs every peer's previous one).
+template <int MODE, int C, int K, bool VEC, bool ASYNC = false>
 __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
   constexpr int R = (16 / K) < 1 ? 1 : 16 / K;
   extern __shared__ __align__(16) double vs[];  // [band] v, then [band] mean (MV)
@@ -72,9 +86,20 @@ __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
   __shared__ double part[2][R];
   __shared__ double wts[2][R];
   __shared__ double sred[kNW];
+  __shared__ __align__(8) double rcv[2][C][R];  // ASYNC: partials pushed by every peer
+  __shared__ __align__(8) uint64_t rbar[2];     // ASYNC: full barriers of rcv[par]
   const int tid = threadIdx.x;
   int rank = 0;
   if constexpr (C > 1) rank = (int)cg::this_cluster().block_rank();
+  if constexpr (ASYNC) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&rbar[0])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&rbar[1])));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cg::this_cluster().sync();  // peers' barriers initialised before the first push
+  }
+  uint32_t phase = 0;  // ASYNC: bit par = the parity of rbar[par]'s current phase
   const int64_t cl = blockIdx.x / C, ncl = gridDim.x / C;
   const int64_t d = a.d, N = a.N;
   int64_t band = (d + C - 1) / C;
@@ -147,14 +172,40 @@ __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
       for (int w = 0; w < kNW; ++w) p += red[par][tid][w];
       part[par][tid] = p;
     }
-    if constexpr (C > 1) {
+    if constexpr (ASYNC) {
+      if (tid == 0)  // this phase completes once all C*R partials have landed
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&rbar[par])),
+                     "r"((uint32_t)(C * R * sizeof(double))) : "memory");
+      if (tid < R) {
+        const double pv = part[par][tid];
+        const uint32_t la = smem_addr(&rcv[par][rank][tid]), lb = smem_addr(&rbar[par]);
+#pragma unroll
+        for (int q = 0; q < C; ++q)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                           peer_addr(la, q)),
+                       "l"(__double_as_longlong(pv)), "r"(peer_addr(lb, q))
+                       : "memory");
+        const uint32_t want = (phase >> par) & 1u;
+        asm volatile(
+            "{\n\t.reg .pred P1;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_addr(&rbar[par])),
+            "r"(want)
+            : "memory");
+      }
+      phase ^= 1u << par;
+    } else if constexpr (C > 1) {
       cg::this_cluster().sync();
     } else {
       __syncthreads();
     }
     if (tid < R) {
       double t = 0.0;
-      if constexpr (C > 1) {
+      if constexpr (ASYNC) {
+#pragma unroll
+        for (int q = 0; q < C; ++q) t += rcv[par][q][tid];
+      } else if constexpr (C > 1) {
         cg::cluster_group cluster = cg::this_cluster();
 #pragma unroll
         for (int q = 0; q < C; ++q) t += *cluster.map_shared_rank(&part[par][tid], q);
@@ -1020,6 +1071,11 @@ using KernelFn = void (*)(FusedArgs);
 
 template <int MODE, int C, int K>
 KernelFn pick_vec(bool vec) {
+  if constexpr (C > 1) {
+    const char* ev = getenv("SIMOPT_FUSED_ASYNC");
+    if (!(ev && atoi(ev) == 0))
+      return vec ? k_fused_rows<MODE, C, K, true, true> : k_fused_rows<MODE, C, K, false, true>;
+  }
   return vec ? k_fused_rows<MODE, C, K, true> : k_fused_rows<MODE, C, K, false>;
 }
 

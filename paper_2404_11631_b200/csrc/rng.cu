@@ -32,9 +32,15 @@ __global__ void __launch_bounds__(256) k_uniform01(uint64_t seed, uint64_t sid, 
 // Normals e0 .. e0+n-1 of the stream (optionally affine per column: mu[j] + sigma[j]*z,
 // j = e % d), written to out[e - e0].  e0 > 0 addresses a row shard of a larger draw
 // (sample sharding): the values are those of the full draw.
-template <bool kAffine>
-__global__ void __launch_bounds__(256) k_normal(uint64_t seed, uint64_t sid, uint64_t clo,
-                                                uint64_t chi, int64_t e0, int64_t n, int64_t d,
+// kNoCarry (checked on the host: the launch's counters clo + b + 1 stay in word 0): the
+// Philox round keys come from the constant bank, rounds 0-1 use the launch-constant word 1
+// (phx_pre), and round 0's product is carried from one grid-stride block to the next by a
+// 128-bit add -- the resample's 17-product core.  The affine column index j = e % d is
+// formed once per thread and advanced by the stride's residue.
+template <bool kAffine, bool kNoCarry>
+__global__ void __launch_bounds__(256) k_normal(const phx_keys rk, const phx_pre pre, uint64_t seed,
+                                                uint64_t sid, uint64_t clo, uint64_t chi,
+                                                int64_t e0, int64_t n, int64_t d,
                                                 const double* __restrict__ mu,
                                                 const double* __restrict__ sigma,
                                                 double* __restrict__ out) {
@@ -44,18 +50,38 @@ __global__ void __launch_bounds__(256) k_normal(uint64_t seed, uint64_t sid, uin
   const int64_t e1 = e0 + n;
   const int64_t nblk = ((e1 + 3) >> 2) - b0;
   const bool aligned = (e0 & 3) == 0;
-  for (int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; bi < nblk;
-       bi += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t bi0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  uint64_t r0h = 0, r0l = 0, sh = 0, sl = 0;
+  if (kNoCarry) {
+    phx_mulhilo(PHILOX_M0, clo + (uint64_t)(b0 + bi0) + 1, &r0h, &r0l);
+    phx_mulhilo(PHILOX_M0, (uint64_t)stride, &sh, &sl);
+  }
+  int64_t j = 0, jstep = 0;  // affine column of the block's first element, and its advance
+  if (kAffine) {
+    j = ((b0 + bi0) << 2) % d;
+    jstep = (stride << 2) % d;
+  }
+  for (int64_t bi = bi0; bi < nblk; bi += stride) {
     const int64_t b = b0 + bi;
     double z[4];
-    normals4(seed, sid, clo, chi, b, tab, z);
+    if (kNoCarry) {
+      const phx4 w = philox4x64_10_rk_r0(r0h, r0l, rk, pre);
+      asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r0l), "+l"(r0h) : "l"(sl), "l"(sh));
+      glibc_boxmuller_fast(phx_u01(w.v[0]), phx_u01(w.v[1]), tab, &z[0], &z[1]);
+      glibc_boxmuller_fast(phx_u01(w.v[2]), phx_u01(w.v[3]), tab, &z[2], &z[3]);
+    } else {
+      normals4(seed, sid, clo, chi, b, tab, z);
+    }
     const int64_t e = b << 2;
     if (kAffine) {
-      int64_t j = e % d;
+      int64_t jj = j;
       for (int k = 0; k < 4; ++k) {
-        z[k] = mu[j] + sigma[j] * z[k];
-        if (++j == d) j = 0;
+        z[k] = mu[jj] + sigma[jj] * z[k];
+        if (++jj == d) jj = 0;
       }
+      j += jstep;
+      if (j >= d) j -= d;
     }
     if (aligned && e + 4 <= e1) {
       double2* o = reinterpret_cast<double2*>(out + (e - e0));
@@ -66,6 +92,19 @@ __global__ void __launch_bounds__(256) k_normal(uint64_t seed, uint64_t sid, uin
         if (e + k >= e0 && e + k < e1) out[e + k - e0] = z[k];
     }
   }
+}
+
+// Launch k_normal for blocks b0 .. b0+nb-1 (the no-carry path when it applies).
+template <bool kAffine>
+void launch_normal(cudaStream_t st, int grid, uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi,
+                   int64_t e0, int64_t n, int64_t d, const double* mu, const double* sigma, double* out) {
+  const phx_keys rk = phx_round_keys(seed, sid);
+  const phx_pre pre = phx_precompute(chi, rk);
+  const uint64_t last = (uint64_t)((e0 + n + 3) >> 2);  // counters clo + 1 .. clo + last
+  if (phx_no_carry(clo, last))
+    k_normal<kAffine, true><<<grid, 256, 0, st>>>(rk, pre, seed, sid, clo, chi, e0, n, d, mu, sigma, out);
+  else
+    k_normal<kAffine, false><<<grid, 256, 0, st>>>(rk, pre, seed, sid, clo, chi, e0, n, d, mu, sigma, out);
 }
 
 int grid_for(int64_t nblk) {
@@ -87,8 +126,8 @@ extern "C" int simopt_uniform01(void* stream, uint64_t seed, uint64_t sid, uint6
 extern "C" int simopt_standard_normal(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
                                       uint64_t chi, int64_t n, double* out) {
   SIMOPT_REQUIRE(n > 0, SIMOPT_E_EMPTY, "requested %lld normals", (long long)n);
-  k_normal<false><<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, 0, n,
-                                                                      1, nullptr, nullptr, out);
+  launch_normal<false>(as_stream(stream), grid_for((n + 3) / 4), seed, sid, clo, chi, 0, n, 1, nullptr,
+                       nullptr, out);
   SIMOPT_CHECK_LAUNCH("k_normal");
   return SIMOPT_OK;
 }
@@ -100,8 +139,8 @@ extern "C" int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t 
                  "need at least 2 samples for a sample covariance, got %lld", (long long)n_samples);
   SIMOPT_REQUIRE(d >= 1, SIMOPT_E_DIMENSION, "empty return dimension");
   const int64_t n = n_samples * d;
-  k_normal<true><<<grid_for((n + 3) / 4), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi, 0, n,
-                                                                     d, mu, sigma, out);
+  launch_normal<true>(as_stream(stream), grid_for((n + 3) / 4), seed, sid, clo, chi, 0, n, d, mu, sigma,
+                      out);
   SIMOPT_CHECK_LAUNCH("k_normal<affine>");
   return SIMOPT_OK;
 }
@@ -114,9 +153,8 @@ extern "C" int simopt_sample_returns_diag_rows(void* stream, uint64_t seed, uint
   SIMOPT_REQUIRE(0 <= row_lo && row_lo <= row_hi, SIMOPT_E_CONFIG, "bad row range");
   const int64_t n = (row_hi - row_lo) * d;
   if (n == 0) return SIMOPT_OK;
-  k_normal<true><<<grid_for((n + 3) / 4 + 1), 256, 0, as_stream(stream)>>>(seed, sid, clo, chi,
-                                                                         row_lo * d, n, d, mu, sigma,
-                                                                         out);
+  launch_normal<true>(as_stream(stream), grid_for((n + 3) / 4 + 1), seed, sid, clo, chi, row_lo * d, n, d,
+                      mu, sigma, out);
   SIMOPT_CHECK_LAUNCH("k_normal<affine,rows>");
   return SIMOPT_OK;
 }

@@ -3,8 +3,9 @@
   compute-sanitizer --tool {memcheck|racecheck|synccheck} python tools/sanitize_paths.py PATH
   PATH: nv         newsvendor resample (warp-specialised, named barriers) + fused FW steps
                    (last-block reduction, dynamic product counter) + recording sums
-        fused      mean-variance / logistic fused row passes, every cluster width (DSMEM
-                   cluster reductions), dense and bit-packed X
+        fused      mean-variance / logistic fused row passes, every cluster width (st.async
+                   DSMEM exchange on mbarriers), dense and bit-packed X; the persistent
+                   mean-variance epoch (cooperative grid barriers)
         hessian    limb Hessians: tcgen05 cp.async (tc), TMA + mbarrier ring (tma), CTA pair
         peer RANK WORLD PORT  one rank of a product-sharded newsvendor run and a sharded fused
                    mean-variance run whose sums cross ranks over CUDA-IPC peer mailboxes
@@ -69,6 +70,19 @@ def fused():
         r0 = newton_cg(LogisticTask(dense), 2, 4, b, fused=True)
         r1 = newton_cg(LogisticTask(packed), 2, 4, b, fused=True)
         np.testing.assert_allclose(r1.objectives, r0.objectives, rtol=1e-8)  # fused: north-star 1e-8
+    # the persistent mean-variance epoch (cooperative launch, grid barriers, redundant tails):
+    # warp-per-row (d = 300) and CTA-per-row (d = 1500) passes against the launch sequence
+    from paper_2404_11631_b200.frank_wolfe import FwConfig, fw_run
+    from paper_2404_11631_b200.instances import gen_meanvar_instance
+    from paper_2404_11631_b200.tasks import MeanVarProblem
+    for d, n in [(300, 2000), (1500, 1200)]:
+        task = gen_meanvar_instance(d, p.RngStream(42, 0))
+        recs = []
+        for flag in ("1", "0"):
+            os.environ["SIMOPT_MV_PERSISTENT"] = flag
+            recs.append(fw_run(MeanVarProblem(task, b, fused=True), FwConfig(2, 5, n, p.RngStream(42, 2)), b))
+        os.environ.pop("SIMOPT_MV_PERSISTENT")
+        np.testing.assert_allclose(recs[0].objectives, recs[1].objectives, rtol=1e-10)
     print("fused ok")
 
 

@@ -169,14 +169,20 @@ __global__ void __launch_bounds__(kResampleThreads, kResampleMinBlocks)
 // counting the buckets 3.88; the single-role k_nv_resample 4.12; a software-pipelined
 // variant (generate i || scatter i-1 in one phase) 4.38-4.62.
 constexpr int kWsProd = 256, kWsCons = 128, kWsPerSm = 3;
+// ring depth of raw segments between producers and consumers; named barriers 1..S (full),
+// S+1..2S (empty), 2S+1 (consumers only)
+#ifndef NV_WS_SLOTS
+#define NV_WS_SLOTS 2
+#endif
+constexpr int kWsSlots = NV_WS_SLOTS, kWsConsBar = 2 * kWsSlots + 1;
 
 struct WsSmem {
-  uint32_t raw[2][NV_SEG];
+  uint32_t raw[kWsSlots][NV_SEG];
   uint32_t sorted[NV_SEG];
-  int hist[2][NV_B];
+  int hist[kWsSlots][NV_B];
   int wsum[kWsCons / 32];
 };  // 56 KB: up to three CTAs per SM
-static_assert(sizeof(int) * NV_B == 4096, "ws_counter: hist[1] follows hist[0] at +4 KB");
+static_assert(sizeof(int) * NV_B == 4096, "ws_counter: hist[p] at +4 KB * p");
 
 // The bucket counter of key k in hist[p]: hist[0] and hist[1] are adjacent 4 KB arrays, so
 // the byte offset is ((k >> 20) & 0xffc) | (p << 12) -- one LOP3 after the shift, and the
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
   constexpr int kWsThreads = kWsProd + kWsCons;
   const int tid = threadIdx.x;
   const int64_t nblk = d * nseg;
-  for (int i = tid; i < 2 * NV_B; i += kWsThreads) (&sm.hist[0][0])[i] = 0;
+  for (int i = tid; i < kWsSlots * NV_B; i += kWsThreads) (&sm.hist[0][0])[i] = 0;
   __syncthreads();
   const int64_t gq = gridDim.x / nseg;
   const int gr = (int)(gridDim.x - gq * nseg);
@@ -218,8 +224,8 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
   if (tid < kWsProd) {
     // ---- producers: Philox4x64-10 + fp32 key + bucket count, segment after segment
     for (int64_t blk = blockIdx.x, k = 0; blk < nblk; blk += gridDim.x, ++k) {
-      const int p = (int)(k & 1);
-      if (k >= 2) named_sync(3 + p, kWsThreads);  // consumers are done with slot p
+      const int p = (int)(k % kWsSlots);
+      if (k >= kWsSlots) named_sync(1 + kWsSlots + p, kWsThreads);  // consumers are done with slot p
       const int64_t e0 = (int64_t)s * NV_SEG;
       const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
       const int64_t i0 = j * S + e0;
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
   const int ct = tid - kWsProd, lane = ct & 31, cw = ct >> 5;
   constexpr int kPer = NV_B / kWsCons;  // 8 buckets per thread
   for (int64_t blk = blockIdx.x, k = 0; blk < nblk; blk += gridDim.x, ++k) {
-    const int p = (int)(k & 1);
+    const int p = (int)(k % kWsSlots);
     const int64_t e0 = (int64_t)s * NV_SEG;
     const int len = (int)((S - e0) < NV_SEG ? (S - e0) : NV_SEG);
     const bool aligned = (((j * S + e0) & 3) == 0) && ((len & 3) == 0);
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
       if (lane >= o) incl += t;
     }
     if (lane == 31) sm.wsum[cw] = incl;
-    named_sync(5, kWsCons);
+    named_sync(kWsConsBar, kWsCons);
     int wpre = lane < cw ? sm.wsum[lane] : 0;
 #pragma unroll
     for (int o = 2; o; o >>= 1) wpre += __shfl_xor_sync(0xffffffffu, wpre, o);  // lanes < 4
@@ -322,7 +328,7 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
     reinterpret_cast<int4*>(hist)[2 * ct] = make_int4(st[0], st[1], st[2], st[3]);
     reinterpret_cast<int4*>(hist)[2 * ct + 1] = make_int4(st[4], st[5], st[6], st[7]);
     reinterpret_cast<uint4*>(off + (j * nseg + s) * (int64_t)NV_B)[ct] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    named_sync(5, kWsCons);  // cursors complete
+    named_sync(kWsConsBar, kWsCons);  // cursors complete
     if (aligned) {
       const uint32_t pbase = (uint32_t)p << 12;
       for (int l4 = ct; l4 < (len >> 2); l4 += kWsCons) {
@@ -338,10 +344,10 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
         sm.sorted[atomicAdd(&hist[key >> kBucketShift], 1)] = key;
       }
     }
-    named_sync(5, kWsCons);  // scatter complete: raw[p] read, cursors final, sorted full
+    named_sync(kWsConsBar, kWsCons);  // scatter complete: raw[p] read, cursors final, sorted full
     reinterpret_cast<int4*>(hist)[2 * ct] = make_int4(0, 0, 0, 0);
     reinterpret_cast<int4*>(hist)[2 * ct + 1] = make_int4(0, 0, 0, 0);
-    named_arrive(3 + p, kWsThreads);  // slot p free for the producers
+    named_arrive(1 + kWsSlots + p, kWsThreads);  // slot p free for the producers
     uint32_t* dst = keys + j * S + e0;
     if (aligned) {  // pointer walk: one 64-bit add per 16-byte store, no per-store IMAD.WIDE
       uint4* dp = reinterpret_cast<uint4*>(dst) + ct;
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
     } else {
       for (int l = ct; l < len; l += kWsCons) dst[l] = sm.sorted[l];
     }
-    named_sync(5, kWsCons);  // sorted stored: the next scatter may overwrite it
+    named_sync(kWsConsBar, kWsCons);  // sorted stored: the next scatter may overwrite it
     j += gq;
     s += gr;
     if (s >= nseg) {

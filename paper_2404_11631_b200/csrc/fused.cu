@@ -185,6 +185,13 @@ __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
                            peer_addr(la, q)),
                        "l"(__double_as_longlong(pv)), "r"(peer_addr(lb, q))
                        : "memory");
+      }
+      // MV in 8-CTA clusters: every thread waits for the tile's partials and forms the R row
+      // weights itself (wt = t), so no block barrier is needed before the accumulation
+      // (C4, d = 2e4: 6.00 -> 6.25 TB/s); otherwise the R owner threads wait and publish the
+      // weights through shared memory
+      constexpr bool kAllWait = MODE == SIMOPT_FUSED_MV && C >= 8;
+      if (kAllWait || tid < R) {
         const uint32_t want = (phase >> par) & 1u;
         asm volatile(
             "{\n\t.reg .pred P1;\n"
@@ -195,6 +202,32 @@ __global__ void __launch_bounds__(kNT, 2) k_fused_rows(FusedArgs a) {
             : "memory");
       }
       phase ^= 1u << par;
+      if constexpr (kAllWait) {
+        double wv[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          double t = 0.0;
+#pragma unroll
+          for (int q = 0; q < C; ++q) t += rcv[par][q][i];
+          const bool rv = r0 + i < N;
+          wv[i] = rv ? t : 0.0;
+          if (tid == i && rv) {
+            sc = fma(t, t, sc);
+            if (rank == 0 && a.t_out) a.t_out[r0 + i] = t;
+          }
+        }
+        if (a.accumulate) {
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              acc[k].x = fma(x[i][k].x, wv[i], acc[k].x);
+              acc[k].y = fma(x[i][k].y, wv[i], acc[k].y);
+            }
+          }
+        }
+        continue;  // next tile
+      }
     } else if constexpr (C > 1) {
       cg::this_cluster().sync();
     } else {
@@ -1071,7 +1104,8 @@ using KernelFn = void (*)(FusedArgs);
 
 template <int MODE, int C, int K>
 KernelFn pick_vec(bool vec) {
-  if constexpr (C > 1) {
+  if constexpr (C >= 8) {  // measured: 8-CTA clusters gain (5.45 -> 6.26 TB/s at d = 2e4),
+                           // 4-CTA clusters lose (4.58 -> 4.3 TB/s at d = 1e4)
     const char* ev = getenv("SIMOPT_FUSED_ASYNC");
     if (!(ev && atoi(ev) == 0))
       return vec ? k_fused_rows<MODE, C, K, true, true> : k_fused_rows<MODE, C, K, false, true>;

@@ -1402,6 +1402,10 @@ extern "C" int simopt_mv_fw_epoch(void* stream, const double* X, int64_t rows, i
   a.bar = reinterpret_cast<unsigned*>(a.g + cols);
   SIMOPT_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), st));
   void* params[] = {&a};
-  SIMOPT_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)G), dim3(kNT), params, smem, st));
+  const char* coop = getenv("SIMOPT_MV_EPOCH_COOP");
+  if (coop && atoi(coop) == 0)  // A/B: ordinary launch (co-residency by grid size only)
+    SIMOPT_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)G), dim3(kNT), params, smem, st));
+  else
+    SIMOPT_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)G), dim3(kNT), params, smem, st));
   return SIMOPT_OK;
 }

@@ -95,16 +95,24 @@ __global__ void __launch_bounds__(256) k_normal(const phx_keys rk, const phx_pre
 }
 
 // Launch k_normal for blocks b0 .. b0+nb-1 (the no-carry path when it applies).
+// (128-thread blocks, which fit beside the persistent mean-variance epoch kernel, measured
+// 1% slower alone and no better in the pipeline: the co-running draw is starved of warps)
+constexpr int kNormalThreads = 256;
+
 template <bool kAffine>
-void launch_normal(cudaStream_t st, int grid, uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi,
+void launch_normal(cudaStream_t st, int64_t nblk, uint64_t seed, uint64_t sid, uint64_t clo, uint64_t chi,
                    int64_t e0, int64_t n, int64_t d, const double* mu, const double* sigma, double* out) {
   const phx_keys rk = phx_round_keys(seed, sid);
   const phx_pre pre = phx_precompute(chi, rk);
   const uint64_t last = (uint64_t)((e0 + n + 3) >> 2);  // counters clo + 1 .. clo + last
+  const int64_t want = ceil_div(nblk, kNormalThreads), cap = (int64_t)SIMOPT_NUM_SMS * 8;
+  const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
   if (phx_no_carry(clo, last))
-    k_normal<kAffine, true><<<grid, 256, 0, st>>>(rk, pre, seed, sid, clo, chi, e0, n, d, mu, sigma, out);
+    k_normal<kAffine, true><<<grid, kNormalThreads, 0, st>>>(rk, pre, seed, sid, clo, chi, e0, n, d, mu,
+                                                            sigma, out);
   else
-    k_normal<kAffine, false><<<grid, 256, 0, st>>>(rk, pre, seed, sid, clo, chi, e0, n, d, mu, sigma, out);
+    k_normal<kAffine, false><<<grid, kNormalThreads, 0, st>>>(rk, pre, seed, sid, clo, chi, e0, n, d, mu,
+                                                             sigma, out);
 }
 
 int grid_for(int64_t nblk) {
@@ -126,8 +134,7 @@ extern "C" int simopt_uniform01(void* stream, uint64_t seed, uint64_t sid, uint6
 extern "C" int simopt_standard_normal(void* stream, uint64_t seed, uint64_t sid, uint64_t clo,
                                       uint64_t chi, int64_t n, double* out) {
   SIMOPT_REQUIRE(n > 0, SIMOPT_E_EMPTY, "requested %lld normals", (long long)n);
-  launch_normal<false>(as_stream(stream), grid_for((n + 3) / 4), seed, sid, clo, chi, 0, n, 1, nullptr,
-                       nullptr, out);
+  launch_normal<false>(as_stream(stream), (n + 3) / 4, seed, sid, clo, chi, 0, n, 1, nullptr, nullptr, out);
   SIMOPT_CHECK_LAUNCH("k_normal");
   return SIMOPT_OK;
 }
@@ -139,8 +146,7 @@ extern "C" int simopt_sample_returns_diag(void* stream, uint64_t seed, uint64_t 
                  "need at least 2 samples for a sample covariance, got %lld", (long long)n_samples);
   SIMOPT_REQUIRE(d >= 1, SIMOPT_E_DIMENSION, "empty return dimension");
   const int64_t n = n_samples * d;
-  launch_normal<true>(as_stream(stream), grid_for((n + 3) / 4), seed, sid, clo, chi, 0, n, d, mu, sigma,
-                      out);
+  launch_normal<true>(as_stream(stream), (n + 3) / 4, seed, sid, clo, chi, 0, n, d, mu, sigma, out);
   SIMOPT_CHECK_LAUNCH("k_normal<affine>");
   return SIMOPT_OK;
 }
@@ -153,8 +159,8 @@ extern "C" int simopt_sample_returns_diag_rows(void* stream, uint64_t seed, uint
   SIMOPT_REQUIRE(0 <= row_lo && row_lo <= row_hi, SIMOPT_E_CONFIG, "bad row range");
   const int64_t n = (row_hi - row_lo) * d;
   if (n == 0) return SIMOPT_OK;
-  launch_normal<true>(as_stream(stream), grid_for((n + 3) / 4 + 1), seed, sid, clo, chi, row_lo * d, n, d,
-                      mu, sigma, out);
+  launch_normal<true>(as_stream(stream), (n + 3) / 4 + 1, seed, sid, clo, chi, row_lo * d, n, d, mu, sigma,
+                      out);
   SIMOPT_CHECK_LAUNCH("k_normal<affine,rows>");
   return SIMOPT_OK;
 }

@@ -542,8 +542,10 @@ class NvFwGraphEngine(NvFwEngine):
       H2D copy per epoch); the step kernel reads them and forms
       gamma = 2 / (k M + m + 2) itself (frank_wolfe.py:62-66);
     * the peer LMO exchange's sequence number is a device counter;
-    * flags, recorded sums and stamps go to per-parity buffers, copied into the
-      per-epoch records right behind the replay.
+    * flags and stamps go to per-parity buffers, copied into the per-epoch records
+      right behind the replay; the epoch's recorded sums are one eager launch on the
+      side stream behind the replay (simopt_nv_epoch_records), overlapping the next
+      epoch.
     The host then enqueues one H2D copy and one graph launch per epoch instead of
     ~100 launches: the per-step host cost disappears, which is what bounds the
     product-sharded run at 8 GPUs (device time per step ~10 us).
@@ -554,8 +556,6 @@ class NvFwGraphEngine(NvFwEngine):
         d, M = self.dev.d, self.M
         self.rings = [torch.zeros(M + 1, d, dtype=F64, device="cuda") for _ in range(2)]
         self.flags_e = [torch.zeros(M + 1, dtype=torch.int32, device="cuda") for _ in range(2)]
-        self.spent_e = [empty(M) for _ in range(2)]
-        self.objs_e = [empty(M) for _ in range(2)]
         self.stamps_e = [torch.zeros(M, dtype=torch.int64, device="cuda") for _ in range(2)]
         self.host_params = [torch.zeros(5, dtype=torch.int64).pin_memory() for _ in range(2)]
         self.dev_params = [torch.zeros(5, dtype=torch.int64, device="cuda") for _ in range(2)]
@@ -593,27 +593,17 @@ class NvFwGraphEngine(NvFwEngine):
             a.do_update, a.do_grad, a.step, a.grad_step = 1, int(m + 1 < M), m, m + 1
         return a
 
-    def _steps(self, p: int, main, side):
-        """The epoch's step sequence on `main` (+ its records on `side`), capture-safe."""
-        lib, dev, M = self.lib, self.dev, self.M
-        sp, ssp = _lib.stream_ptr(main), _lib.stream_ptr(side)
-        P = _lib.ptr
+    def _steps(self, p: int, main):
+        """The epoch's step sequence on `main`, capture-safe (the epoch's records are
+        launched eagerly behind the replay, so they overlap the next epoch)."""
+        lib, M = self.lib, self.M
+        sp = _lib.stream_ptr(main)
         self.starts[p].copy_(self.rings[1 - p][M])
         _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(self._step_args(p, -1, False))))
         for m in range(M):
             a = self._step_args(p, m, True)
             a.stamp = self.stamps_e[p][m:].data_ptr()
             _lib.check(lib.simopt_nv_iter(sp, ctypes.byref(a)))
-        ev = torch.cuda.Event()
-        ev.record(main)
-        side.wait_event(ev)
-        # rings[p][1..M] are the epoch's iterates
-        _lib.check(lib.simopt_nv_epoch_records(
-            ssp, P(self.rings[p]), M + 1, 1, M, P(dev.c), P(dev.mu), P(dev.sigma), P(dev.k),
-            P(dev.h), P(dev.v), dev.d, self.chunk, P(self.spent_e[p]), P(self.objs_e[p])))
-        fork = torch.cuda.Event()
-        fork.record(side)
-        main.wait_event(fork)  # join: the epoch ends when its recording ends
 
     def enqueue_epoch(self, k: int, stream: RngStream, n_samples: int, time_resample: bool = False,
                       next_samples: int | None = None):
@@ -625,6 +615,9 @@ class NvFwGraphEngine(NvFwEngine):
         main = self.hi
         main.wait_event(ready)
         self.dev.use_slot(p)
+        old = self.epoch_done.get(k - 2)  # its records read rings[p]
+        if old is not None:
+            main.wait_event(old)
         hp = self.host_params[p]
         if self.param_ev[p] is not None:  # the previous copy from this pinned buffer has run
             self.param_ev[p].synchronize()
@@ -641,33 +634,41 @@ class NvFwGraphEngine(NvFwEngine):
             g = self.graphs.get(key)
             if g is not None:
                 g.replay()
-            elif key not in self.warm:  # first epoch of this layout: eager (allocations, setup)
-                self._steps(p, main, self.side)
-                self.warm.add(key)
             else:
+                # first epoch of this layout: eager (allocations, library setup), then the
+                # graph is captured right away, so a run's captures (a device sync each)
+                # happen in its first two epochs -- inside any warm-up, never later
+                self._steps(p, main)
+                self.warm.add(key)
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
                 self.cstream.wait_stream(main)
                 with torch.cuda.graph(g, stream=self.cstream):
-                    self._steps(p, self.cstream, self.side)
+                    self._steps(p, self.cstream)
                 self.graphs[key] = g
-                g.replay()
             steps = torch.cuda.Event()
             steps.record(main)
-            # the parity buffers serve every epoch of that parity: copy this epoch's
-            # records out (on main, so epoch k+2's replay cannot overwrite them first)
+            # the parity buffers serve every epoch of that parity: copy this epoch's flags
+            # and stamps out (on main, so epoch k+2's replay cannot overwrite them first)
             lo, hi, M = k * self.M, (k + 1) * self.M, self.M
             self.flags[lo:hi].copy_(self.flags_e[p][:M])
             self.flags_e[p].zero_()
-            self.spent[lo:hi].copy_(self.spent_e[p])
-            self.objs[lo:hi].copy_(self.objs_e[p])
             self.stamps[lo:hi].copy_(self.stamps_e[p])
-            done = torch.cuda.Event()
-            done.record(main)
+            copied = torch.cuda.Event()
+            copied.record(main)
+        # the epoch's records (dot(c, x), objective) on the side stream, off the critical
+        # path; rings[p] stays intact until epoch k+2, which waits for them
+        dev, P = self.dev, _lib.ptr
+        self.side.wait_event(steps)
+        _lib.check(self.lib.simopt_nv_epoch_records(
+            _lib.stream_ptr(self.side), P(self.rings[p]), M + 1, 1, M, P(dev.c), P(dev.mu), P(dev.sigma),
+            P(dev.k), P(dev.h), P(dev.v), dev.d, self.chunk, P(self.spent[lo:]), P(self.objs[lo:])))
+        self.side.wait_event(copied)
+        done = torch.cuda.Event()
+        done.record(self.side)
         self.steps_done[k] = steps
         self.epoch_done[k] = done
         if self.shard is not None:
-            self.side.wait_event(done)
             self.epoch_done[k] = self._reduce_epoch(k)
         if next_samples is not None:
             self._resample(k + 1, stream, next_samples, time_resample)

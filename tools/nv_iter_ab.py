@@ -20,7 +20,7 @@ from paper_2404_11631_b200.tasks import NewsvendorProblem, make_nv_engine  # noq
 cfgs = sys.argv[1].split() if len(sys.argv) > 1 else ["8,3,8", "4,3,4"]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 K = int(sys.argv[3]) if len(sys.argv) > 3 else 12
-d, S, M = 10_000, 100_000, 25
+d, S, M = int(os.environ.get("AB_D", 10_000)), 100_000, 25
 b = p.make_backend("cuda")
 task = gen_newsvendor_instance(d, p.RngStream(42, 0))
 

@@ -11,7 +11,10 @@ B200 path unchanged:
   this package's device-resident problems, instance generators and drivers with the same
   streams (instance ``RngStream(seed, 0)``, repetition ``RngStream(seed, 2 + rep)``), and
   returns a RunRecord with the reference's fields, which ``write_trace_csv`` /
-  ``summarize`` consume as they are.
+  ``summarize`` consume as they are;
+* ``sobench.bench.run_bench`` additionally writes ``kernels.csv`` for the cuda cells: the
+  dominant kernels' CUDA-event times with their algorithmic bytes and fraction of the
+  measured HBM peak (the per-kernel roofline columns).
 
     python -m paper_2404_11631_b200.sobench_plugin run --task newsvendor --sizes 1000 \\
         --backend cuda,parallel --reps 3
@@ -20,6 +23,7 @@ runs the reference CLI (sobench/cli.py) with the cuda backend registered.
 """
 from __future__ import annotations
 
+import os
 import sys
 
 _INSTALLED = {}
@@ -49,9 +53,22 @@ def install(sobench_pkg=None):
             return ref_run_cell(config, size, backend_kind, rep)
         return _run_cell_cuda(config, size, rep, bench)
 
+    ref_run_bench = bench.run_bench
+
+    def run_bench(config):
+        written = ref_run_bench(config)
+        if "cuda" in config.backends:  # the per-kernel roofline columns of the cuda cells
+            path = os.path.join(config.out, "kernels.csv")
+            write_kernel_csv(config, path)
+            written.append(path)
+        return written
+
     sb.make_backend = make_backend
     bench.make_backend = make_backend
     bench.run_cell = run_cell
+    bench.run_bench = run_bench
+    import sobench.cli as cli  # noqa: PLC0415 -- it imported run_bench by name
+    cli.run_bench = run_bench
     if hasattr(sobench_pkg, "make_backend"):
         sobench_pkg.make_backend = make_backend
     _unify_errors()
@@ -267,8 +284,106 @@ def _run_cell_cuda(config, size, rep, bench):
     return fw_run(problem, fw_cfg, backend, task_label=config.task, size=size, rep=rep)
 
 
+KERNEL_HEADER = ["task", "size", "kernel", "launches", "mean_us", "algorithmic_bytes",
+                 "achieved_GBps", "peak_GBps", "frac_of_hbm", "bound", "basis"]
+
+
+def _hbm_peak():
+    """MEASURED_PEAKS.json hbm_gbs of this pool's B200s (repo root), else the copy-bandwidth
+    fallback of the profiling recipe."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    try:
+        with open(os.path.join(root, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0
+
+
+def _event_us(fn, reps=3):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e3)
+    return best
+
+
+def kernel_rows(config, size):
+    """Roofline columns of the dominant kernels of one cuda cell (task, size): each kernel
+    timed alone with CUDA events at the cell's shapes, algorithmic bytes in the reference's
+    data model (fp64 scenarios, demands and features)."""
+    from .backend import CudaBackend
+    from .fused import MV, fused_rows
+    from .instances import gen_meanvar_instance, gen_newsvendor_instance
+    from .sampling import RngStream, synth_classification
+    from .tasks import MeanVarProblem, NewsvendorProblem
+    import torch
+    peak = _hbm_peak()
+    b = CudaBackend(config.chunk_size)
+    rows = []
+
+    def row(kernel, us, nbytes, bound, basis):
+        gbs = nbytes / (us * 1e-6) / 1e9
+        rows.append([config.task, size, kernel, 1, f"{us:.3f}", nbytes, f"{gbs:.1f}", f"{peak:.1f}",
+                     f"{gbs / peak:.4f}", bound, basis])
+
+    if config.task == "newsvendor":
+        S = config.sample_size_for(size)
+        prob = NewsvendorProblem(gen_newsvendor_instance(size, RngStream(config.seed, 0)), b)
+        st = RngStream(config.seed, 2)
+        row("k_nv_resample_ws", _event_us(lambda: prob.resample(st, S)), 8 * size * S,
+            "issue (heavy-FMA pipe: Philox4x64-10)", "8 B per demand draw (the sorted fp64 matrix)")
+    elif config.task == "meanvar":
+        n = config.sample_size_for(size)
+        prob = MeanVarProblem(gen_meanvar_instance(size, RngStream(config.seed, 0)), b, fused=True)
+        st = RngStream(config.seed, 2)
+        row("k_normal<affine> + exact mean", _event_us(lambda: prob.resample(st, n)), 8 * n * size,
+            "fp64 issue (glibc-exact Box-Muller)", "8 B per return draw written")
+        ss = prob.sample_set
+        w = torch.full((size,), 1.0 / size, dtype=torch.float64, device="cuda")
+        g = torch.empty(size, dtype=torch.float64, device="cuda")
+        q = torch.empty(1, dtype=torch.float64, device="cuda")
+        row("k_fused_rows<MV>", _event_us(lambda: fused_rows(MV, ss.samples, w, center=ss.mean,
+                                                              col_scale=1.0 / (n - 1), col_out=g,
+                                                              scalar_out=q)),
+            8 * n * size, "hbm", "8 B per element of X (one read per FW iteration)")
+    else:  # classification: the SQN's full-data loss pass (exact row dots)
+        data = synth_classification(size, RngStream(config.seed, 0))
+        x = torch.full((size,), 1.0 / size, dtype=torch.float64, device="cuda")
+        feats = data.features
+        n = feats.shape[0]
+        row("k_matvec_rows (exact loss pass)", _event_us(lambda: b.matvec_device(feats, x)), 8 * n * size,
+            "hbm / latency", "8 B per feature element")
+    return rows
+
+
+def write_kernel_csv(config, path):
+    """kernels.csv beside the reference's summary.csv: one row per (task, size, kernel)."""
+    import csv
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(KERNEL_HEADER)
+        for size in config.sizes:
+            for r in kernel_rows(config, size):
+                w.writerow(r)
+
+
 def main(argv=None) -> int:
-    """The reference CLI (sobench.cli.main) with the cuda backend registered."""
+    """The reference CLI (sobench.cli.main) with the cuda backend registered (the reference
+    is taken from sys.path, else from the repo's baseline/_ref install)."""
+    try:
+        import sobench  # noqa: F401,PLC0415
+    except ImportError:
+        ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+        sys.path.insert(0, ref)
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_simopt")
     install()
     from sobench import cli
     return cli.main(argv)

@@ -65,6 +65,26 @@ def test_run_bench_writes_reference_csv(sob, tmp_path):
     bench.run_bench(cfg)
     names = os.listdir(tmp_path)
     assert "trace_newsvendor_100_cuda_rep0.csv" in names and "trace_newsvendor_100_cuda_rep1.csv" in names
+    assert "kernels.csv" in names  # the per-kernel roofline columns of the cuda cells
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("task,size", [("meanvar", 120), ("newsvendor", 100), ("classification", 20)])
+def test_kernel_roofline_csv(sob, tmp_path, task, size):
+    """kernels.csv: one row per dominant kernel of each cuda cell, with
+    its CUDA-event time, algorithmic bytes and fraction of the measured HBM peak."""
+    import csv
+    import sobench.bench as bench
+    from paper_2404_11631_b200.sobench_plugin import KERNEL_HEADER
+    cfg = bench.BenchConfig(task=task, sizes=[size], backends=["cuda"], reps=1, iterations=25,
+                            sample_size=200, out=str(tmp_path))
+    bench.run_bench(cfg)
+    with open(os.path.join(tmp_path, "kernels.csv")) as fh:
+        rows = list(csv.reader(fh))
+    assert rows[0] == KERNEL_HEADER and len(rows) >= 2
+    for r in rows[1:]:
+        assert r[0] == task and int(r[1]) == size and float(r[4]) > 0 and int(r[5]) > 0
+        assert 0 < float(r[8]) < 2
 
 
 def test_errors_unified(sob):

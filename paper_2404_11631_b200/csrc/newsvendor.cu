@@ -197,6 +197,14 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+#ifndef NV_WS_STREAM_STORES
+#define NV_WS_STREAM_STORES 1
+#endif
+__device__ __forceinline__ void ws_store(uint4* p, uint4 v) {
+  if (NV_WS_STREAM_STORES) __stcs(p, v);
+  else *p = v;
+}
+
 __device__ __forceinline__ int* ws_counter(unsigned char* smem, uint32_t k, uint32_t pbase) {
   constexpr int kBucketByteShift = 12 + NV_QBITS - 10 - 2;  // bucket index * 4 bytes
   return reinterpret_cast<int*>(smem + offsetof(WsSmem, hist) +
@@ -327,7 +335,10 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
     for (int u = 0; u < kPer / 2; ++u) pk[u] = (uint32_t)st[2 * u] | ((uint32_t)st[2 * u + 1] << 16);
     reinterpret_cast<int4*>(hist)[2 * ct] = make_int4(st[0], st[1], st[2], st[3]);
     reinterpret_cast<int4*>(hist)[2 * ct + 1] = make_int4(st[4], st[5], st[6], st[7]);
-    reinterpret_cast<uint4*>(off + (j * nseg + s) * (int64_t)NV_B)[ct] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    // streaming stores (evict-first): the layout is read an epoch later, and the previous
+    // epoch's FW steps, running beside this resample, keep their windows in L2
+    ws_store(reinterpret_cast<uint4*>(off + (j * nseg + s) * (int64_t)NV_B) + ct,
+             make_uint4(pk[0], pk[1], pk[2], pk[3]));
     named_sync(kWsConsBar, kWsCons);  // cursors complete
     if (aligned) {
       const uint32_t pbase = (uint32_t)p << 12;
@@ -354,7 +365,7 @@ __global__ void __launch_bounds__(kWsProd + kWsCons, kRegCap)
       const uint4* sp = reinterpret_cast<const uint4*>(sm.sorted) + ct;
       const uint4* se = reinterpret_cast<const uint4*>(sm.sorted) + (len >> 2);
 #pragma unroll 4
-      for (; sp < se; sp += kWsCons, dp += kWsCons) *dp = *sp;
+      for (; sp < se; sp += kWsCons, dp += kWsCons) ws_store(dp, *sp);
     } else {
       for (int l = ct; l < len; l += kWsCons) dst[l] = sm.sorted[l];
     }

@@ -83,10 +83,11 @@ __global__ void __launch_bounds__(256) k_normal(const phx_keys rk, const phx_pre
       j += jstep;
       if (j >= d) j -= d;
     }
-    if (aligned && e + 4 <= e1) {
+    if (aligned && e + 4 <= e1) {  // evict-first: a double-buffered draw must not push the
+      // X the running epoch re-reads out of L2 (C1: 80 MB, read by every FW iteration)
       double2* o = reinterpret_cast<double2*>(out + (e - e0));
-      o[0] = make_double2(z[0], z[1]);
-      o[1] = make_double2(z[2], z[3]);
+      __stcs(o, make_double2(z[0], z[1]));
+      __stcs(o + 1, make_double2(z[2], z[3]));
     } else {
       for (int k = 0; k < 4; ++k)
         if (e + k >= e0 && e + k < e1) out[e + k - e0] = z[k];

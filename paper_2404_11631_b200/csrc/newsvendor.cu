@@ -913,6 +913,195 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
   }
 }
 
+// Gradient steps on small product shards (d <= the grid's warps, e.g. one rank of an 8-way
+// C2 run): one product per warp, statically assigned, so a step is one pass of dependent
+// loads per warp with no product counter, no CTA rounds and no block barrier before the
+// argmin; the few ambiguous draws of the product are queued per warp and resolved by its
+// lanes (overflow resolved in place).  Same counts and LMO as k_nv_iter.
+constexpr int kWarpQueue = 64;
+
+template <int kIterWarps, int kVecBatch = 4>
+__global__ void __launch_bounds__(kIterWarps * 32, 6) k_nv_iter_small(NvIterArgs a) {
+  __shared__ ArgMin warp_best[kIterWarps];
+  __shared__ uint64_t wq[kIterWarps][kWarpQueue];
+  __shared__ int wql[kIterWarps];
+  __shared__ int nan_seen;
+  __shared__ bool am_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) nan_seen = 0;
+  if (lane == 0) wql[warp] = 0;
+  NvState* st = a.state;
+  NvStepCtx cx;
+  cx.jstar = st->jstar;
+  cx.sval = st->sval;
+  cx.gamma = a.epoch_ctr ? 2.0 / (double)(*a.epoch_ctr * a.inner_iters + a.m + 2) : a.gamma;
+  const NvStreamPos sp = a.epoch_draw
+                            ? NvStreamPos{a.epoch_draw[0], a.epoch_draw[1], a.epoch_draw[2], a.epoch_draw[3]}
+                            : NvStreamPos{a.seed, a.sid, a.ctr_lo, a.ctr_hi};
+  __syncthreads();
+  ArgMin best{INFINITY, INT64_MAX};
+  const int S32 = (int)a.S;  // S < 2^31 (checked on the host)
+  const int nseg = (int)a.nseg;
+  const bool vec = (a.S & 3) == 0;
+  const int64_t j = (int64_t)blockIdx.x * kIterWarps + warp;
+  if (j < a.d) {
+    const double x = nv_update(a, cx, j, a.x_in[j], lane == 0);
+    const double mu = a.mu[j], sigma = a.sigma[j];
+    const NvWindow w = nv_window(x, mu, sigma);
+    const NvThresh th = nv_thresh(w);
+    const uint32_t kb = (uint32_t)th.qb << 12;
+    const uint32_t kspan = (uint32_t)((((uint64_t)th.qa) << 12) - 1 - kb);
+    const int blo = (int)(w.qlo >> (NV_QBITS - 10)), bhi = (int)(w.qhi >> (NV_QBITS - 10));
+    int c = 0;
+      for (int s0 = 0; s0 < nseg; s0 += 32) {
+      const int sg = s0 + lane;
+      int start = 0, end = 0;
+      const uint32_t* seg = a.keys;
+      if (sg < nseg) {
+        const int e0 = sg * NV_SEG;
+        const int len = (S32 - e0) < NV_SEG ? (S32 - e0) : NV_SEG;
+        const uint16_t* o = a.off + (j * nseg + sg) * (int64_t)NV_B;
+        start = o[blo];
+        end = (bhi + 1 < NV_B) ? o[bhi + 1] : len;
+        seg = a.keys + j * a.S + e0;
+        c += start;
+      }
+      // (1) the window's ends: vec -> the 16-byte words holding start and end - 1, masked
+      //     to [start, end) (one batch); otherwise the whole window, 8 single keys per batch
+      const int hb = start & ~3, tb = (end - 1) & ~3;
+      const bool two = vec && end > start && tb > hb;  // the tail word is not the head word
+      const int hend = vec ? hb + 4 : end;             // body: [hb + 4, tb) when two
+      const int bend = two ? tb : hend;
+      for (int p0 = start, first = 1; vec ? (first != 0 && end > start) : p0 < end; p0 += 8, first = 0) {
+        uint32_t kv[8];
+        unsigned ok = 0, amb = 0;
+        if (vec) {
+          const uint4 h = *reinterpret_cast<const uint4*>(seg + hb);
+          uint4 t = h;
+          if (two) t = *reinterpret_cast<const uint4*>(seg + tb);
+          kv[0] = h.x; kv[1] = h.y; kv[2] = h.z; kv[3] = h.w;
+          kv[4] = t.x; kv[5] = t.y; kv[6] = t.z; kv[7] = t.w;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ok |= (hb + u >= start && hb + u < end) ? 1u << u : 0u;
+            ok |= (two && tb + u < end) ? 1u << (4 + u) : 0u;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const bool v = p0 + i < end;
+            kv[i] = v ? seg[p0 + i] : 0u;
+            ok |= v ? 1u << i : 0u;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const bool v = (ok >> i) & 1u;
+          c += (v && kv[i] < kb) ? 1 : 0;
+          amb |= (v && kv[i] - kb <= kspan) ? 1u << i : 0u;
+        }
+        while (amb) {  // ambiguous draws: rare
+          const int bit = __ffs(amb) - 1;
+          amb &= amb - 1;
+          uint32_t key = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) key = (bit == i) ? kv[i] : key;
+          c += nv_amb_push(key, sg, 0, j, a.S, mu, sigma, x, sp, wq[warp], &wql[warp], kWarpQueue);
+        }
+      }
+      // (2) the 16-byte body [hend, bend): per key one unsigned compare for "certainly
+      //     below" and one for "ambiguous" (key - kb <= kspan)
+      const int nvec = bend > hend ? (bend - hend) >> 2 : 0;
+      const uint4* vrow = reinterpret_cast<const uint4*>(seg + hend);
+      for (int v0 = 0; v0 < nvec; v0 += kVecBatch) {
+        uint4 t[kVecBatch];
+#pragma unroll
+        for (int v = 0; v < kVecBatch; ++v)
+          if (v0 + v < nvec) t[v] = vrow[v0 + v];
+        unsigned amb = 0;
+#pragma unroll
+        for (int v = 0; v < kVecBatch; ++v) {
+          if (v0 + v < nvec) {
+            const uint32_t k4[4] = {t[v].x, t[v].y, t[v].z, t[v].w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              c += k4[u] < kb ? 1 : 0;
+              amb |= (k4[u] - kb <= kspan) ? 1u << (4 * v + u) : 0u;
+            }
+          }
+        }
+        while (amb) {  // ambiguous draws: rare
+          const int bit = __ffs(amb) - 1;
+          amb &= amb - 1;
+          uint32_t key = 0;
+#pragma unroll
+          for (int v = 0; v < kVecBatch; ++v) {
+            key = (bit == 4 * v) ? t[v].x : key;
+            key = (bit == 4 * v + 1) ? t[v].y : key;
+            key = (bit == 4 * v + 2) ? t[v].z : key;
+            key = (bit == 4 * v + 3) ? t[v].w : key;
+          }
+          c += nv_amb_push(key, sg, 0, j, a.S, mu, sigma, x, sp, wq[warp], &wql[warp], kWarpQueue);
+        }
+      }
+    }
+    __syncwarp();
+    const int nq = min(wql[warp], kWarpQueue);
+    for (int e = lane; e < nq; e += 32)
+      c += nv_resolve(sp, j * a.S + (int64_t)(wq[warp][e] & ((1ULL << 40) - 1)), mu, sigma, x);
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o2);
+    if (lane == 0) {
+      const double g = nv_grad_value((int64_t)c, a.S, a.k[j], a.h[j], a.v[j]);
+      a.g[j] = g;
+      if (g != g) nan_seen = 1;
+      best = ArgMin{g * (a.budget / a.c[j]), j};  // lmo.py:84
+    }
+  }
+  best = warp_amin(best);
+  if (lane == 0) warp_best[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ArgMin b = warp_best[0];
+    for (int w = 1; w < kIterWarps; ++w) b = amin(b, warp_best[w]);
+    a.part_v[blockIdx.x] = b.v;
+    a.part_i[blockIdx.x] = b.i;
+    if (nan_seen) atomicOr(&a.flags[a.grad_step], NV_FLAG_NAN_GRADIENT);
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->blocks_done, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  // last block: reduce the per-block partials (deterministic: lexicographic min).
+  ArgMin b{INFINITY, INT64_MAX};
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+    b = amin(b, ArgMin{((volatile double*)a.part_v)[i], ((volatile int64_t*)a.part_i)[i]});
+  b = warp_amin(b);
+  if (lane == 0) warp_best[warp] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ArgMin r = warp_best[0];
+    for (int w = 1; w < kIterWarps; ++w) r = amin(r, warp_best[w]);
+    // lmo_single_budget (lmo.py:84-89): s_j* = C / c_j* iff g_j* < 0
+    const double gj = a.g[r.i];
+    const double sval = (gj < 0.0) ? a.budget / a.c[r.i] : 0.0;
+    st->blocks_done = 0;
+    st->pad = 0;  // the product counter of the next gradient step
+    if (a.peer_mb == nullptr) {
+      st->jstar = r.i;
+      st->sval = sval;
+      st->best_val = r.v;
+    } else {
+      nv_peer_exchange(NvPeerArgs{a.peer_mb, a.world, a.rank, a.j0, a.d, a.grad_step, a.seq,
+                                  a.seq_ptr, a.flags},
+                       r, sval, st);
+    }
+    if (a.stamp) *a.stamp = (int64_t)globaltimer();
+  }
+}
+
 __global__ void k_nv_counts(const uint32_t* __restrict__ keys, const uint16_t* __restrict__ off,
                             const double* __restrict__ mu, const double* __restrict__ sigma,
                             int64_t d, int64_t S, int nseg, NvStreamPos sp,
@@ -1070,6 +1259,16 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   const int grid = (int)(ceil_div(a.d, kw) < cap ? ceil_div(a.d, kw) : cap);
   SIMOPT_REQUIRE(grid <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
   cudaStream_t s = as_stream(stream);
+  // small shards (one product per warp fits in one wave): k_nv_iter_small
+  const char* sm_env = getenv("SIMOPT_NV_ITER_SMALL");
+  const int64_t small_max = (int64_t)4 * 3 * SIMOPT_NUM_SMS;
+  if (a.do_grad && a.d <= small_max && !(sm_env && atoi(sm_env) == 0)) {
+    const int g4 = (int)ceil_div(a.d, 4);
+    SIMOPT_REQUIRE(g4 <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
+    k_nv_iter_small<4><<<g4, 4 * 32, 0, s>>>(a);
+    SIMOPT_CHECK_LAUNCH("k_nv_iter_small");
+    return SIMOPT_OK;
+  }
   if (kw == 4)
     (vb == 4 ? k_nv_iter<4, 6, 4> : k_nv_iter<4, 6, 8>)<<<grid, 4 * 32, 0, s>>>(a);
   else if (bps <= 2)

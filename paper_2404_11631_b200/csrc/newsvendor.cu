@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
 constexpr int kWarpQueue = 64;
 
 template <int kIterWarps, int kVecBatch = 4>
-__global__ void __launch_bounds__(kIterWarps * 32, 6) k_nv_iter_small(NvIterArgs a) {
+__global__ void __launch_bounds__(kIterWarps * 32, 24 / kIterWarps) k_nv_iter_small(NvIterArgs a) {
   __shared__ ArgMin warp_best[kIterWarps];
   __shared__ uint64_t wq[kIterWarps][kWarpQueue];
   __shared__ int wql[kIterWarps];
@@ -945,8 +945,10 @@ __global__ void __launch_bounds__(kIterWarps * 32, 6) k_nv_iter_small(NvIterArgs
   const bool vec = (a.S & 3) == 0;
   const int64_t j = (int64_t)blockIdx.x * kIterWarps + warp;
   if (j < a.d) {
-    const double x = nv_update(a, cx, j, a.x_in[j], lane == 0);
-    const double mu = a.mu[j], sigma = a.sigma[j];
+    // every per-product load issued up front (the gradient's k, h, v, c too): one round trip
+    const double x0 = a.x_in[j], mu = a.mu[j], sigma = a.sigma[j];
+    const double pk = a.k[j], ph = a.h[j], pv = a.v[j], pc = a.c[j];
+    const double x = nv_update(a, cx, j, x0, lane == 0);
     const NvWindow w = nv_window(x, mu, sigma);
     const NvThresh th = nv_thresh(w);
     const uint32_t kb = (uint32_t)th.qb << 12;
@@ -1052,10 +1054,10 @@ __global__ void __launch_bounds__(kIterWarps * 32, 6) k_nv_iter_small(NvIterArgs
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o2);
     if (lane == 0) {
-      const double g = nv_grad_value((int64_t)c, a.S, a.k[j], a.h[j], a.v[j]);
+      const double g = nv_grad_value((int64_t)c, a.S, pk, ph, pv);
       a.g[j] = g;
       if (g != g) nan_seen = 1;
-      best = ArgMin{g * (a.budget / a.c[j]), j};  // lmo.py:84
+      best = ArgMin{g * (a.budget / pc), j};  // lmo.py:84
     }
   }
   best = warp_amin(best);
@@ -1262,10 +1264,14 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   // small shards (one product per warp fits in one wave): k_nv_iter_small
   const char* sm_env = getenv("SIMOPT_NV_ITER_SMALL");
   const int64_t small_max = (int64_t)4 * 3 * SIMOPT_NUM_SMS;
-  if (a.do_grad && a.d <= small_max && !(sm_env && atoi(sm_env) == 0)) {
-    const int g4 = (int)ceil_div(a.d, 4);
-    SIMOPT_REQUIRE(g4 <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
-    k_nv_iter_small<4><<<g4, 4 * 32, 0, s>>>(a);
+  const int sw = sm_env ? atoi(sm_env) : 4;  // warps per block (0: off)
+  if (a.do_grad && a.d <= small_max && sw > 0) {
+    const int ws = sw >= 16 ? 16 : (sw >= 8 ? 8 : 4);
+    const int gs = (int)ceil_div(a.d, ws);
+    SIMOPT_REQUIRE(gs <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
+    if (ws == 16) k_nv_iter_small<16><<<gs, 16 * 32, 0, s>>>(a);
+    else if (ws == 8) k_nv_iter_small<8><<<gs, 8 * 32, 0, s>>>(a);
+    else k_nv_iter_small<4><<<gs, 4 * 32, 0, s>>>(a);
     SIMOPT_CHECK_LAUNCH("k_nv_iter_small");
     return SIMOPT_OK;
   }

@@ -644,7 +644,112 @@ __device__ __forceinline__ double nv_update(const NvIterArgs& a, const NvStepCtx
   return x;
 }
 
-// kVecBatch: 16-byte key loads per lane per pass
+// One product's window in one segment (a lane's share of a gradient step): the keys in
+// [start, end) -- vec: the 16-byte words holding start and end - 1 masked to the window,
+// then the 16-byte body between them -- certainly-below keys counted, ambiguous draws
+// queued (nv_amb_push).  Returns the count excluding `start` (the keys of lower buckets).
+template <int kVecBatch>
+__device__ __forceinline__ int nv_scan_window(const uint32_t* seg, int start, int end, bool vec,
+                                              uint32_t kb, uint32_t kspan, int sg, int slot,
+                                              int64_t j, int64_t S, double mu, double sigma,
+                                              double x, const NvStreamPos& sp, uint64_t* queue,
+                                              int* q_len, int qcap) {
+  int c = 0;
+  // (1) the window's ends: vec -> the 16-byte words holding start and end - 1, masked
+  //     to [start, end) (one batch); otherwise the whole window, 8 single keys per batch
+  const int hb = start & ~3, tb = (end - 1) & ~3;
+  const bool two = vec && end > start && tb > hb;  // the tail word is not the head word
+  const int hend = vec ? hb + 4 : end;             // body: [hb + 4, tb) when two
+  const int bend = two ? tb : hend;
+  for (int p0 = start, first = 1; vec ? (first != 0 && end > start) : p0 < end; p0 += 8, first = 0) {
+    uint32_t kv[8];
+    unsigned ok = 0, amb = 0;
+    if (vec) {
+      const uint4 h = *reinterpret_cast<const uint4*>(seg + hb);
+      uint4 t = h;
+      if (two) t = *reinterpret_cast<const uint4*>(seg + tb);
+      kv[0] = h.x; kv[1] = h.y; kv[2] = h.z; kv[3] = h.w;
+      kv[4] = t.x; kv[5] = t.y; kv[6] = t.z; kv[7] = t.w;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ok |= (hb + u >= start && hb + u < end) ? 1u << u : 0u;
+        ok |= (two && tb + u < end) ? 1u << (4 + u) : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool v = p0 + i < end;
+        kv[i] = v ? seg[p0 + i] : 0u;
+        ok |= v ? 1u << i : 0u;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool v = (ok >> i) & 1u;
+      c += (v && kv[i] < kb) ? 1 : 0;
+      amb |= (v && kv[i] - kb <= kspan) ? 1u << i : 0u;
+    }
+    while (amb) {  // ambiguous draws: rare
+      const int bit = __ffs(amb) - 1;
+      amb &= amb - 1;
+      uint32_t key = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) key = (bit == i) ? kv[i] : key;
+      c += nv_amb_push(key, sg, slot, j, S, mu, sigma, x, sp, queue, q_len, qcap);
+    }
+  }
+  // (2) the 16-byte body [hend, bend): per key one unsigned compare for "certainly
+  //     below" and one for "ambiguous" (key - kb <= kspan)
+  const int nvec = bend > hend ? (bend - hend) >> 2 : 0;
+  const uint4* vrow = reinterpret_cast<const uint4*>(seg + hend);
+  for (int v0 = 0; v0 < nvec; v0 += kVecBatch) {
+    uint4 t[kVecBatch];
+#pragma unroll
+    for (int v = 0; v < kVecBatch; ++v)
+      if (v0 + v < nvec) t[v] = vrow[v0 + v];
+    unsigned amb = 0;
+#pragma unroll
+    for (int v = 0; v < kVecBatch; ++v) {
+      if (v0 + v < nvec) {
+        const uint32_t k4[4] = {t[v].x, t[v].y, t[v].z, t[v].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          c += k4[u] < kb ? 1 : 0;
+          amb |= (k4[u] - kb <= kspan) ? 1u << (4 * v + u) : 0u;
+        }
+      }
+    }
+    while (amb) {  // ambiguous draws: rare
+      const int bit = __ffs(amb) - 1;
+      amb &= amb - 1;
+      uint32_t key = 0;
+#pragma unroll
+      for (int v = 0; v < kVecBatch; ++v) {
+        key = (bit == 4 * v) ? t[v].x : key;
+        key = (bit == 4 * v + 1) ? t[v].y : key;
+        key = (bit == 4 * v + 2) ? t[v].z : key;
+        key = (bit == 4 * v + 3) ? t[v].w : key;
+      }
+      c += nv_amb_push(key, sg, slot, j, S, mu, sigma, x, sp, queue, q_len, qcap);
+    }
+  }
+  return c;
+}
+
+// the window [start, end) of product j in segment sg: its first and one-past-last bucket's starts
+__device__ __forceinline__ void nv_bounds(const NvIterArgs& a, int64_t j, int sg, int nseg, int S32,
+                                          int blo, int bhi, int& start, int& end) {
+  const int e0 = sg * NV_SEG;
+  const int len = (S32 - e0) < NV_SEG ? (S32 - e0) : NV_SEG;
+  const uint16_t* o = a.off + (j * nseg + sg) * (int64_t)NV_B;
+  start = o[blo];
+  end = (bhi + 1 < NV_B) ? o[bhi + 1] : len;
+}
+
+// kVecBatch: 16-byte key loads per lane per pass.  (Measured and not kept: loading the next
+// product's iterate and parameters before this product's scan, 4.03 vs 4.02 ms per pipelined
+// C2 epoch; preparing the next product's window and bucket starts a product ahead, 4.24 ms --
+// 80 registers leave no room for a second product's state.)
 template <int kIterWarps, int kMinBlocks, int kVecBatch>
 __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
     k_nv_iter(NvIterArgs a) {
@@ -696,6 +801,11 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
   unsigned* next = &st->pad;
   const int64_t nwarps = (int64_t)gridDim.x * kIterWarps;
   const int64_t gw = (int64_t)blockIdx.x * kIterWarps + warp;
+  ArgMin best{INFINITY, INT64_MAX};
+  const int S32 = (int)a.S;  // S < 2^31 (checked on the host)
+  const int nseg = (int)a.nseg;
+  const int qcap = min(g_nv_qcap, kCtaQueue);
+  const bool vec = (a.S & 3) == 0;  // rows start 16-byte aligned: vector key loads
   unsigned pend = 0;  // lane 0: the counter value of the product after jn
   if (lane == 0 && gw < a.d) pend = atomicAdd(next, 1u);
   int64_t jn = gw;
@@ -705,11 +815,6 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
     mun = a.mu[jn];
     sgn = a.sigma[jn];
   }
-  ArgMin best{INFINITY, INT64_MAX};
-  const int S32 = (int)a.S;  // S < 2^31 (checked on the host)
-  const int nseg = (int)a.nseg;
-  const int qcap = min(g_nv_qcap, kCtaQueue);
-  const bool vec = (a.S & 3) == 0;  // rows start 16-byte aligned: vector key loads
   for (;;) {
     // ---- (A) count certain keys, queue ambiguous draws
     for (int k = 0; k < kSlotsPerWarp; ++k) {
@@ -736,92 +841,12 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
         int start = 0, end = 0;
         const uint32_t* seg = a.keys;
         if (sg < nseg) {
-          const int e0 = sg * NV_SEG;
-          const int len = (S32 - e0) < NV_SEG ? (S32 - e0) : NV_SEG;
-          const uint16_t* o = a.off + (j * nseg + sg) * (int64_t)NV_B;
-          start = o[blo];
-          end = (bhi + 1 < NV_B) ? o[bhi + 1] : len;
-          seg = a.keys + j * a.S + e0;
+          nv_bounds(a, j, sg, nseg, S32, blo, bhi, start, end);
+          seg = a.keys + j * a.S + sg * NV_SEG;
           c += start;
         }
-        // (1) the window's ends: vec -> the 16-byte words holding start and end - 1, masked
-        //     to [start, end) (one batch); otherwise the whole window, 8 single keys per batch
-        const int hb = start & ~3, tb = (end - 1) & ~3;
-        const bool two = vec && end > start && tb > hb;  // the tail word is not the head word
-        const int hend = vec ? hb + 4 : end;             // body: [hb + 4, tb) when two
-        const int bend = two ? tb : hend;
-        for (int p0 = start, first = 1; vec ? (first != 0 && end > start) : p0 < end; p0 += 8, first = 0) {
-          uint32_t kv[8];
-          unsigned ok = 0, amb = 0;
-          if (vec) {
-            const uint4 h = *reinterpret_cast<const uint4*>(seg + hb);
-            uint4 t = h;
-            if (two) t = *reinterpret_cast<const uint4*>(seg + tb);
-            kv[0] = h.x; kv[1] = h.y; kv[2] = h.z; kv[3] = h.w;
-            kv[4] = t.x; kv[5] = t.y; kv[6] = t.z; kv[7] = t.w;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              ok |= (hb + u >= start && hb + u < end) ? 1u << u : 0u;
-              ok |= (two && tb + u < end) ? 1u << (4 + u) : 0u;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const bool v = p0 + i < end;
-              kv[i] = v ? seg[p0 + i] : 0u;
-              ok |= v ? 1u << i : 0u;
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const bool v = (ok >> i) & 1u;
-            c += (v && kv[i] < kb) ? 1 : 0;
-            amb |= (v && kv[i] - kb <= kspan) ? 1u << i : 0u;
-          }
-          while (amb) {  // ambiguous draws: rare
-            const int bit = __ffs(amb) - 1;
-            amb &= amb - 1;
-            uint32_t key = 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) key = (bit == i) ? kv[i] : key;
-            c += nv_amb_push(key, sg, slot, j, a.S, mu, sigma, x, sp, queue, &q_len, qcap);
-          }
-        }
-        // (2) the 16-byte body [hend, bend): per key one unsigned compare for "certainly
-        //     below" and one for "ambiguous" (key - kb <= kspan)
-        const int nvec = bend > hend ? (bend - hend) >> 2 : 0;
-        const uint4* vrow = reinterpret_cast<const uint4*>(seg + hend);
-        for (int v0 = 0; v0 < nvec; v0 += kVecBatch) {
-          uint4 t[kVecBatch];
-#pragma unroll
-          for (int v = 0; v < kVecBatch; ++v)
-            if (v0 + v < nvec) t[v] = vrow[v0 + v];
-          unsigned amb = 0;
-#pragma unroll
-          for (int v = 0; v < kVecBatch; ++v) {
-            if (v0 + v < nvec) {
-              const uint32_t k4[4] = {t[v].x, t[v].y, t[v].z, t[v].w};
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                c += k4[u] < kb ? 1 : 0;
-                amb |= (k4[u] - kb <= kspan) ? 1u << (4 * v + u) : 0u;
-              }
-            }
-          }
-          while (amb) {  // ambiguous draws: rare
-            const int bit = __ffs(amb) - 1;
-            amb &= amb - 1;
-            uint32_t key = 0;
-#pragma unroll
-            for (int v = 0; v < kVecBatch; ++v) {
-              key = (bit == 4 * v) ? t[v].x : key;
-              key = (bit == 4 * v + 1) ? t[v].y : key;
-              key = (bit == 4 * v + 2) ? t[v].z : key;
-              key = (bit == 4 * v + 3) ? t[v].w : key;
-            }
-            c += nv_amb_push(key, sg, slot, j, a.S, mu, sigma, x, sp, queue, &q_len, qcap);
-          }
-        }
+        c += nv_scan_window<kVecBatch>(seg, start, end, vec, kb, kspan, sg, slot, j, a.S, mu, sigma,
+                                       x, sp, queue, &q_len, qcap);
       }
 #pragma unroll
       for (int o2 = 16; o2 > 0; o2 >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o2);
@@ -955,97 +980,17 @@ __global__ void __launch_bounds__(kIterWarps * 32, 24 / kIterWarps) k_nv_iter_sm
     const uint32_t kspan = (uint32_t)((((uint64_t)th.qa) << 12) - 1 - kb);
     const int blo = (int)(w.qlo >> (NV_QBITS - 10)), bhi = (int)(w.qhi >> (NV_QBITS - 10));
     int c = 0;
-      for (int s0 = 0; s0 < nseg; s0 += 32) {
+    for (int s0 = 0; s0 < nseg; s0 += 32) {
       const int sg = s0 + lane;
       int start = 0, end = 0;
       const uint32_t* seg = a.keys;
       if (sg < nseg) {
-        const int e0 = sg * NV_SEG;
-        const int len = (S32 - e0) < NV_SEG ? (S32 - e0) : NV_SEG;
-        const uint16_t* o = a.off + (j * nseg + sg) * (int64_t)NV_B;
-        start = o[blo];
-        end = (bhi + 1 < NV_B) ? o[bhi + 1] : len;
-        seg = a.keys + j * a.S + e0;
+        nv_bounds(a, j, sg, nseg, S32, blo, bhi, start, end);
+        seg = a.keys + j * a.S + sg * NV_SEG;
         c += start;
       }
-      // (1) the window's ends: vec -> the 16-byte words holding start and end - 1, masked
-      //     to [start, end) (one batch); otherwise the whole window, 8 single keys per batch
-      const int hb = start & ~3, tb = (end - 1) & ~3;
-      const bool two = vec && end > start && tb > hb;  // the tail word is not the head word
-      const int hend = vec ? hb + 4 : end;             // body: [hb + 4, tb) when two
-      const int bend = two ? tb : hend;
-      for (int p0 = start, first = 1; vec ? (first != 0 && end > start) : p0 < end; p0 += 8, first = 0) {
-        uint32_t kv[8];
-        unsigned ok = 0, amb = 0;
-        if (vec) {
-          const uint4 h = *reinterpret_cast<const uint4*>(seg + hb);
-          uint4 t = h;
-          if (two) t = *reinterpret_cast<const uint4*>(seg + tb);
-          kv[0] = h.x; kv[1] = h.y; kv[2] = h.z; kv[3] = h.w;
-          kv[4] = t.x; kv[5] = t.y; kv[6] = t.z; kv[7] = t.w;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            ok |= (hb + u >= start && hb + u < end) ? 1u << u : 0u;
-            ok |= (two && tb + u < end) ? 1u << (4 + u) : 0u;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const bool v = p0 + i < end;
-            kv[i] = v ? seg[p0 + i] : 0u;
-            ok |= v ? 1u << i : 0u;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const bool v = (ok >> i) & 1u;
-          c += (v && kv[i] < kb) ? 1 : 0;
-          amb |= (v && kv[i] - kb <= kspan) ? 1u << i : 0u;
-        }
-        while (amb) {  // ambiguous draws: rare
-          const int bit = __ffs(amb) - 1;
-          amb &= amb - 1;
-          uint32_t key = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) key = (bit == i) ? kv[i] : key;
-          c += nv_amb_push(key, sg, 0, j, a.S, mu, sigma, x, sp, wq[warp], &wql[warp], kWarpQueue);
-        }
-      }
-      // (2) the 16-byte body [hend, bend): per key one unsigned compare for "certainly
-      //     below" and one for "ambiguous" (key - kb <= kspan)
-      const int nvec = bend > hend ? (bend - hend) >> 2 : 0;
-      const uint4* vrow = reinterpret_cast<const uint4*>(seg + hend);
-      for (int v0 = 0; v0 < nvec; v0 += kVecBatch) {
-        uint4 t[kVecBatch];
-#pragma unroll
-        for (int v = 0; v < kVecBatch; ++v)
-          if (v0 + v < nvec) t[v] = vrow[v0 + v];
-        unsigned amb = 0;
-#pragma unroll
-        for (int v = 0; v < kVecBatch; ++v) {
-          if (v0 + v < nvec) {
-            const uint32_t k4[4] = {t[v].x, t[v].y, t[v].z, t[v].w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              c += k4[u] < kb ? 1 : 0;
-              amb |= (k4[u] - kb <= kspan) ? 1u << (4 * v + u) : 0u;
-            }
-          }
-        }
-        while (amb) {  // ambiguous draws: rare
-          const int bit = __ffs(amb) - 1;
-          amb &= amb - 1;
-          uint32_t key = 0;
-#pragma unroll
-          for (int v = 0; v < kVecBatch; ++v) {
-            key = (bit == 4 * v) ? t[v].x : key;
-            key = (bit == 4 * v + 1) ? t[v].y : key;
-            key = (bit == 4 * v + 2) ? t[v].z : key;
-            key = (bit == 4 * v + 3) ? t[v].w : key;
-          }
-          c += nv_amb_push(key, sg, 0, j, a.S, mu, sigma, x, sp, wq[warp], &wql[warp], kWarpQueue);
-        }
-      }
+      c += nv_scan_window<kVecBatch>(seg, start, end, vec, kb, kspan, sg, 0, j, a.S, mu, sigma, x, sp,
+                                     wq[warp], &wql[warp], kWarpQueue);
     }
     __syncwarp();
     const int nq = min(wql[warp], kWarpQueue);
@@ -1166,15 +1111,19 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   // warp-specialised k_nv_resample_ws (3.72 vs 4.12 ms at C2).  Both are persistent grids
   // of one full wave.  The previous epoch's step kernels (high stream priority) share the
   // SMs with it: a 4-warp step block (10 K registers, 9 KB shared) fits beside the three
-  // resample CTAs (55 K registers, 3 x 57 KB); further step blocks take an SM slot whenever
+  // resample CTAs (46 K registers at the default cap, 3 x 57 KB); further step blocks take an SM slot whenever
   // the scheduler has one, which costs the resample ~0.3 ms per epoch (4,3,4 is the best
   // measured trade-off, tools/nv_iter_ab.py).
   const char* ev = getenv("SIMOPT_NV_RESAMPLE");
   if (!(ev && atoi(ev) == 1)) {
     const int64_t g = nblk < (int64_t)SIMOPT_NUM_SMS * kWsPerSm ? nblk : (int64_t)SIMOPT_NUM_SMS * kWsPerSm;
     const size_t smem = sizeof(WsSmem);
-    int regcap = 3;
-    if (const char* rc = getenv("SIMOPT_NV_WS_REGCAP")) regcap = atoi(rc) == 4 ? 4 : 3;
+    // 40 registers (regcap 4) by default: alone the resample is slower than at 48 (3.82 vs
+    // 3.70 ms at C2), but beside the previous epoch's steps -- the pipelined epoch's critical
+    // path -- it leaves them more issue slots: 3.95 vs 4.03 ms per epoch (bench 6.28k vs
+    // 6.21k FW it/s), and 0.689 vs 0.711 ms at the 8-way shard size (tools/nv_iter_ab.py)
+    int regcap = 4;
+    if (const char* rc = getenv("SIMOPT_NV_WS_REGCAP")) regcap = atoi(rc) == 3 ? 3 : 4;
     static std::mutex mu;
     static std::vector<int> ready;  // devices whose shared-memory limit is raised
     int dev = 0;
@@ -1275,7 +1224,13 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
     SIMOPT_CHECK_LAUNCH("k_nv_iter_small");
     return SIMOPT_OK;
   }
-  if (kw == 4)
+  if (kw == 4 && bps >= 12)
+    (vb == 4 ? k_nv_iter<4, 12, 4> : k_nv_iter<4, 12, 2>)<<<grid, 4 * 32, 0, s>>>(a);
+  else if (kw == 4 && bps >= 8)
+    (vb == 4 ? k_nv_iter<4, 8, 4> : k_nv_iter<4, 8, 2>)<<<grid, 4 * 32, 0, s>>>(a);
+  else if (kw == 4 && bps == 7)
+    (vb == 4 ? k_nv_iter<4, 7, 4> : k_nv_iter<4, 7, 2>)<<<grid, 4 * 32, 0, s>>>(a);
+  else if (kw == 4)
     (vb == 4 ? k_nv_iter<4, 6, 4> : k_nv_iter<4, 6, 8>)<<<grid, 4 * 32, 0, s>>>(a);
   else if (bps <= 2)
     (vb == 4 ? k_nv_iter<8, 2, 4> : k_nv_iter<8, 2, 8>)<<<grid, 8 * 32, 0, s>>>(a);

@@ -2,7 +2,7 @@
 C2 epoch: each repetition runs every configuration for `epochs` epochs in the same process,
 so box-to-box and drift effects cancel.  Prints the median pipelined epoch per config.
 
-  python tools/nv_iter_ab.py "8,3,8 4,3,4 4,3,8" [reps] [epochs]
+  python tools/nv_iter_ab.py "8,3,8 4,3,4 4,7,4/4" [reps] [epochs]   (/3: resample at 48 registers)
 env: AB_EPOCHS (overrides epochs), AB_GRAPH=1 (graph engine), AB_TIME_RESAMPLE=1 (resample
 events as bench.py records them), AB_CLOCKS=1 (bench.py's NVML sampler running beside).
 """
@@ -73,7 +73,9 @@ res = {c: [] for c in cfgs}
 run()  # warm-up
 for r in range(reps):
     for c in cfgs:
-        os.environ["SIMOPT_NV_ITER"] = c
+        it, _, rc = c.partition("/")  # "W,B,V/R": R = the resample's register cap (3: 48 registers, 4: 40, the default)
+        os.environ["SIMOPT_NV_ITER"] = it
+        os.environ["SIMOPT_NV_WS_REGCAP"] = rc or "4"
         res[c].append(run())
 for c in cfgs:
     v = res[c]

@@ -645,9 +645,17 @@ __device__ __forceinline__ double nv_update(const NvIterArgs& a, const NvStepCtx
 }
 
 // One product's window in one segment (a lane's share of a gradient step): the keys in
-// [start, end) -- vec: the 16-byte words holding start and end - 1 masked to the window,
-// then the 16-byte body between them -- certainly-below keys counted, ambiguous draws
-// queued (nv_amb_push).  Returns the count excluding `start` (the keys of lower buckets).
+// [start, end) -- bucket order, so [0, start) are the keys of lower buckets, counted by the
+// caller -- certainly-below keys counted, ambiguous draws queued (nv_amb_push).  Returns the
+// count on top of `start`.
+//  vec (16-byte aligned rows): the 16-byte words from the one holding `start` to the one
+//  holding end - 1, every key tested, no masks: the head word's keys before `start` lie in
+//  buckets below the window, i.e. below qlo < qb (certainly below: counted by the test, so
+//  taken out of `start`), and the tail word's keys from `end` on lie above qhi > qa
+//  (certainly above, never ambiguous).  Per key one compare for the count; ambiguity is one
+//  unsigned min per key and one compare per batch (key - kb <= kspan for any key), the
+//  per-key mask only formed when the batch holds an ambiguous draw.
+//  otherwise: the window itself, 8 single keys per batch.
 template <int kVecBatch>
 __device__ __forceinline__ int nv_scan_window(const uint32_t* seg, int start, int end, bool vec,
                                               uint32_t kb, uint32_t kspan, int sg, int slot,
@@ -655,71 +663,61 @@ __device__ __forceinline__ int nv_scan_window(const uint32_t* seg, int start, in
                                               double x, const NvStreamPos& sp, uint64_t* queue,
                                               int* q_len, int qcap) {
   int c = 0;
-  // (1) the window's ends: vec -> the 16-byte words holding start and end - 1, masked
-  //     to [start, end) (one batch); otherwise the whole window, 8 single keys per batch
-  const int hb = start & ~3, tb = (end - 1) & ~3;
-  const bool two = vec && end > start && tb > hb;  // the tail word is not the head word
-  const int hend = vec ? hb + 4 : end;             // body: [hb + 4, tb) when two
-  const int bend = two ? tb : hend;
-  for (int p0 = start, first = 1; vec ? (first != 0 && end > start) : p0 < end; p0 += 8, first = 0) {
-    uint32_t kv[8];
-    unsigned ok = 0, amb = 0;
-    if (vec) {
-      const uint4 h = *reinterpret_cast<const uint4*>(seg + hb);
-      uint4 t = h;
-      if (two) t = *reinterpret_cast<const uint4*>(seg + tb);
-      kv[0] = h.x; kv[1] = h.y; kv[2] = h.z; kv[3] = h.w;
-      kv[4] = t.x; kv[5] = t.y; kv[6] = t.z; kv[7] = t.w;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        ok |= (hb + u >= start && hb + u < end) ? 1u << u : 0u;
-        ok |= (two && tb + u < end) ? 1u << (4 + u) : 0u;
-      }
-    } else {
+  if (!vec) {
+    for (int p0 = start; p0 < end; p0 += 8) {
+      uint32_t kv[8];
+      unsigned amb = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const bool v = p0 + i < end;
         kv[i] = v ? seg[p0 + i] : 0u;
-        ok |= v ? 1u << i : 0u;
+        c += (v && kv[i] < kb) ? 1 : 0;
+        amb |= (v && kv[i] - kb <= kspan) ? 1u << i : 0u;
+      }
+      while (amb) {  // ambiguous draws: rare
+        const int bit = __ffs(amb) - 1;
+        amb &= amb - 1;
+        uint32_t key = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) key = (bit == i) ? kv[i] : key;
+        c += nv_amb_push(key, sg, slot, j, S, mu, sigma, x, sp, queue, q_len, qcap);
       }
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const bool v = (ok >> i) & 1u;
-      c += (v && kv[i] < kb) ? 1 : 0;
-      amb |= (v && kv[i] - kb <= kspan) ? 1u << i : 0u;
-    }
-    while (amb) {  // ambiguous draws: rare
-      const int bit = __ffs(amb) - 1;
-      amb &= amb - 1;
-      uint32_t key = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) key = (bit == i) ? kv[i] : key;
-      c += nv_amb_push(key, sg, slot, j, S, mu, sigma, x, sp, queue, q_len, qcap);
-    }
+    return c;
   }
-  // (2) the 16-byte body [hend, bend): per key one unsigned compare for "certainly
-  //     below" and one for "ambiguous" (key - kb <= kspan)
-  const int nvec = bend > hend ? (bend - hend) >> 2 : 0;
-  const uint4* vrow = reinterpret_cast<const uint4*>(seg + hend);
-  for (int v0 = 0; v0 < nvec; v0 += kVecBatch) {
+  if (end <= start) return 0;
+  const int hb = start & ~3;
+  const int nw = (((end - 1) & ~3) - hb) / 4 + 1;  // 16-byte words of the window
+  c = hb - start;
+  const uint4* vrow = reinterpret_cast<const uint4*>(seg + hb);
+  for (int v0 = 0; v0 < nw; v0 += kVecBatch) {
     uint4 t[kVecBatch];
 #pragma unroll
     for (int v = 0; v < kVecBatch; ++v)
-      if (v0 + v < nvec) t[v] = vrow[v0 + v];
-    unsigned amb = 0;
+      if (v0 + v < nw) t[v] = vrow[v0 + v];
+    uint32_t m = 0xffffffffu;  // min over the batch of key - kb (unsigned)
 #pragma unroll
     for (int v = 0; v < kVecBatch; ++v) {
-      if (v0 + v < nvec) {
+      if (v0 + v < nw) {
         const uint32_t k4[4] = {t[v].x, t[v].y, t[v].z, t[v].w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           c += k4[u] < kb ? 1 : 0;
-          amb |= (k4[u] - kb <= kspan) ? 1u << (4 * v + u) : 0u;
+          m = min(m, k4[u] - kb);
         }
       }
     }
-    while (amb) {  // ambiguous draws: rare
+    if (m > kspan) continue;  // no ambiguous draw in the batch: the common case
+    unsigned amb = 0;
+#pragma unroll
+    for (int v = 0; v < kVecBatch; ++v) {
+      if (v0 + v < nw) {
+        const uint32_t k4[4] = {t[v].x, t[v].y, t[v].z, t[v].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) amb |= (k4[u] - kb <= kspan) ? 1u << (4 * v + u) : 0u;
+      }
+    }
+    while (amb) {
       const int bit = __ffs(amb) - 1;
       amb &= amb - 1;
       uint32_t key = 0;

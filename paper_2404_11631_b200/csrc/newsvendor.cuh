@@ -106,9 +106,16 @@ struct NvWindow {
 
 __device__ __forceinline__ NvWindow nv_window(double x, double mu, double sigma) {
   NvWindow w;
-  w.t = (x - mu) / sigma;
-  // rounding slack of D = fl(mu + fl(sigma*z)) vs x and of t, in z units
-  const double eta = 8.0 * 1.1102230246251565e-16 * (fabs(mu) + fabs(x) + 10.0 * sigma) / sigma;
+  // 1/sigma from the hardware reciprocal seed and two Newton steps (a few ulps; no IEEE
+  // division: t only places the window, and its error is inside eta's slack)
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(sigma));
+  r = fma(fma(-sigma, r, 1.0), r, r);
+  r = fma(fma(-sigma, r, 1.0), r, r);
+  w.t = (x - mu) * r;
+  // rounding slack, in z units, of D = fl(mu + fl(sigma*z)) vs x (~2u (|x| + |mu|) / sigma)
+  // and of t (~4u (|x| + |mu|) / sigma), u = 2^-53, with margin
+  const double eta = 16.0 * 1.1102230246251565e-16 * (fabs(mu) + fabs(x) + 10.0 * sigma) * r;
   w.eps = NV_EPSZ + eta;
   const double a = (w.t - w.eps + NV_Z0) * NV_QSCALE - 3.0;
   const double b = (w.t + w.eps + NV_Z0) * NV_QSCALE + 3.0;

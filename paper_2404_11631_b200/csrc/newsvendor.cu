@@ -602,7 +602,6 @@ __device__ __forceinline__ NvThresh nv_thresh(const NvWindow& w) {
 //      warps instead of one partly filled pass per product);
 //  (C) one thread per product forms the gradient and its LMO value.
 // Ambiguous draws that do not fit the queue are resolved by the warp that found them.
-constexpr int kSlotsPerWarp = 4;
 constexpr int kCtaQueue = 1024;
 // usable queue entries (tests shrink it through SIMOPT_NV_QCAP to drive the overflow path)
 __device__ int g_nv_qcap = kCtaQueue;
@@ -748,7 +747,8 @@ __device__ __forceinline__ void nv_bounds(const NvIterArgs& a, int64_t j, int sg
 // product's iterate and parameters before this product's scan, 4.03 vs 4.02 ms per pipelined
 // C2 epoch; preparing the next product's window and bucket starts a product ahead, 4.24 ms --
 // 80 registers leave no room for a second product's state.)
-template <int kIterWarps, int kMinBlocks, int kVecBatch>
+// kSlotsPerWarp: products per warp per CTA round
+template <int kIterWarps, int kMinBlocks, int kVecBatch, int kSlotsPerWarp = 8>
 __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
     k_nv_iter(NvIterArgs a) {
   constexpr int kSlots = kIterWarps * kSlotsPerWarp;
@@ -1116,11 +1116,14 @@ extern "C" int simopt_nv_resample(void* stream, uint64_t seed, uint64_t sid, uin
   if (!(ev && atoi(ev) == 1)) {
     const int64_t g = nblk < (int64_t)SIMOPT_NUM_SMS * kWsPerSm ? nblk : (int64_t)SIMOPT_NUM_SMS * kWsPerSm;
     const size_t smem = sizeof(WsSmem);
-    // 40 registers (regcap 4) by default: alone the resample is slower than at 48 (3.82 vs
-    // 3.70 ms at C2), but beside the previous epoch's steps -- the pipelined epoch's critical
-    // path -- it leaves them more issue slots: 3.95 vs 4.03 ms per epoch (bench 6.28k vs
-    // 6.21k FW it/s), and 0.689 vs 0.711 ms at the 8-way shard size (tools/nv_iter_ab.py)
-    int regcap = 4;
+    // Registers: the pipelined epoch is set by whichever of the resample and the previous
+    // epoch's steps beside it ends last (tools/nv_timeline.py).  At C2 the steps' share is
+    // small enough for the 48-register resample (3.70 ms alone): resample 3.79, steps 3.80 ms
+    // beside each other (bench 6.55k vs 6.45k FW it/s at 40 registers).  On small product
+    // shards (the one-product-per-warp step kernel, d <= 12 x SMs) the steps dominate, and
+    // 40 registers leave them more issue slots: 0.689 vs 0.711 ms at the 8-way shard size.
+    const int64_t small_shard = (int64_t)4 * 3 * SIMOPT_NUM_SMS;  // as simopt_nv_iter
+    int regcap = d <= small_shard ? 4 : 3;
     if (const char* rc = getenv("SIMOPT_NV_WS_REGCAP")) regcap = atoi(rc) == 3 ? 3 : 4;
     static std::mutex mu;
     static std::vector<int> ready;  // devices whose shared-memory limit is raised
@@ -1201,9 +1204,12 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
   // V 16-byte key loads per lane per pass.  Measured on the pipelined C2 epoch (the steps
   // run beside the next epoch's resample; tools/nv_iter_ab.py, interleaved medians):
   // 4,3,4 3.88 ms; 4,3,8 3.94; 4,6,4 3.94; 8,3,4 3.95; 8,3,8 4.03; 8,2,4 4.15.  Fewer,
-  // smaller blocks take fewer issue slots from the resample.
-  int kw = 4, bps = 3, vb = 4;
-  if (const char* ev = getenv("SIMOPT_NV_ITER")) sscanf(ev, "%d,%d,%d", &kw, &bps, &vb);
+  // smaller blocks take fewer issue slots from the resample; 72 or 64 registers (more step
+  // blocks beside it) and a single block per SM were slower still.  A fourth field P sets
+  // the products per warp per CTA round: 8 (default) 3.84-3.85 ms, 16 the same, 4 3.88-3.93,
+  // 2 3.95 (fewer block barriers and fuller resolve passes per product).
+  int kw = 4, bps = 3, vb = 4, spw = 8;
+  if (const char* ev = getenv("SIMOPT_NV_ITER")) sscanf(ev, "%d,%d,%d,%d", &kw, &bps, &vb, &spw);
   const int64_t cap = a.do_grad ? (int64_t)bps * SIMOPT_NUM_SMS : 16 * SIMOPT_NUM_SMS;
   const int grid = (int)(ceil_div(a.d, kw) < cap ? ceil_div(a.d, kw) : cap);
   SIMOPT_REQUIRE(grid <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
@@ -1222,12 +1228,8 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
     SIMOPT_CHECK_LAUNCH("k_nv_iter_small");
     return SIMOPT_OK;
   }
-  if (kw == 4 && bps >= 12)
-    (vb == 4 ? k_nv_iter<4, 12, 4> : k_nv_iter<4, 12, 2>)<<<grid, 4 * 32, 0, s>>>(a);
-  else if (kw == 4 && bps >= 8)
-    (vb == 4 ? k_nv_iter<4, 8, 4> : k_nv_iter<4, 8, 2>)<<<grid, 4 * 32, 0, s>>>(a);
-  else if (kw == 4 && bps == 7)
-    (vb == 4 ? k_nv_iter<4, 7, 4> : k_nv_iter<4, 7, 2>)<<<grid, 4 * 32, 0, s>>>(a);
+  if (kw == 4 && spw != 8)
+    (spw >= 16 ? k_nv_iter<4, 6, 4, 16> : spw >= 4 ? k_nv_iter<4, 6, 4, 4> : k_nv_iter<4, 6, 4, 2>)<<<grid, 4 * 32, 0, s>>>(a);
   else if (kw == 4)
     (vb == 4 ? k_nv_iter<4, 6, 4> : k_nv_iter<4, 6, 8>)<<<grid, 4 * 32, 0, s>>>(a);
   else if (bps <= 2)

@@ -2,7 +2,7 @@
 C2 epoch: each repetition runs every configuration for `epochs` epochs in the same process,
 so box-to-box and drift effects cancel.  Prints the median pipelined epoch per config.
 
-  python tools/nv_iter_ab.py "8,3,8 4,3,4 4,7,4/4" [reps] [epochs]   (/3: resample at 48 registers)
+  python tools/nv_iter_ab.py "8,3,8 4,3,4 4,7,4/4" [reps] [epochs]   (/4: resample at 40 registers)
 env: AB_EPOCHS (overrides epochs), AB_GRAPH=1 (graph engine), AB_TIME_RESAMPLE=1 (resample
 events as bench.py records them), AB_CLOCKS=1 (bench.py's NVML sampler running beside).
 """
@@ -73,9 +73,12 @@ res = {c: [] for c in cfgs}
 run()  # warm-up
 for r in range(reps):
     for c in cfgs:
-        it, _, rc = c.partition("/")  # "W,B,V/R": R = the resample's register cap (3: 48 registers, 4: 40, the default)
+        it, _, rc = c.partition("/")  # "W,B,V[,P]/R": R = the resample's register cap (3: 48 registers, 4: 40; default by shard size)
         os.environ["SIMOPT_NV_ITER"] = it
-        os.environ["SIMOPT_NV_WS_REGCAP"] = rc or "4"
+        if rc:
+            os.environ["SIMOPT_NV_WS_REGCAP"] = rc
+        else:
+            os.environ.pop("SIMOPT_NV_WS_REGCAP", None)
         res[c].append(run())
 for c in cfgs:
     v = res[c]

@@ -1066,6 +1066,9 @@ class MvFwEngine:
         self.rings = [torch.zeros(M + 1, d, dtype=F64, device="cuda") for _ in range(2)]
         self.g, self.gq, self.s, self.dirn = empty(d), empty(d), empty(d), empty(d)
         self.gamma = empty(M)
+        # per-parity pinned staging of the epoch's step sizes: a pageable host-to-device copy
+        # synchronises the stream, i.e. would hold the host until the previous epoch ends
+        self._gamma_pin = [torch.empty(M, dtype=F64, pin_memory=True) for _ in range(2)]
         self.status = torch.zeros(M, dtype=torch.int32, device="cuda")
         self.wmin, self.wsum, self.quad, self.lin = empty(M), empty(M), empty(M), empty(M)
         self.stamps = torch.zeros(M, dtype=torch.int64, device="cuda")
@@ -1185,7 +1188,9 @@ class MvFwEngine:
             self.graphs = {}
         ws = self.rings[k % 2]
         self.status.zero_()
-        self.gamma.copy_(torch.tensor([fw_step_size(k, M, m) for m in range(M)], dtype=F64))
+        gp = self._gamma_pin[k % 2]  # its last copy (epoch k-2) ran before epoch k-1 ended
+        gp.copy_(torch.tensor([fw_step_size(k, M, m) for m in range(M)], dtype=F64))
+        self.gamma.copy_(gp, non_blocking=True)
         if (self.prob.fused and self.prob.shard is None and self.prob.dimension <= 2048
                 and os.environ.get("SIMOPT_MV_PERSISTENT", "1") != "0"):
             # the whole epoch as one cooperative launch (simopt_mv_fw_epoch)
@@ -1232,18 +1237,32 @@ def _mv_fw_run_device(prob: MeanVarProblem, config, backend, label, size, rep):
     _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[T:])))
     trace = TraceBuilder()
     n_of, events, host = [], [], {}
+    # epoch records are read back on a side stream into pinned buffers, ordered after their
+    # epoch only: a plain device-to-host copy on the main stream would also wait for the
+    # epoch enqueued after it and leave the GPU idle while the host enqueues the next one
+    rd_stream = torch.cuda.Stream()
+    pins = [torch.empty(M, dtype=a.dtype, pin_memory=True) for a in (status, wmin, wsum, quad, lin, stamps)]
+    t0_pin = torch.empty(1, dtype=torch.int64, pin_memory=True)
 
     def check_epoch(k):
         """Host validation of epoch k (its ring is intact until epoch k+2 is enqueued)."""
-        events[k].synchronize()
+        sl = slice(k * M, (k + 1) * M)
+        with torch.cuda.stream(rd_stream):
+            rd_stream.wait_event(events[k])
+            for pin, a in zip(pins, (status, wmin, wsum, quad, lin, stamps)):
+                pin.copy_(a[sl], non_blocking=True)
+            if k == 0:
+                t0_pin.copy_(stamps[T:], non_blocking=True)
+            got = torch.cuda.Event()
+            got.record(rd_stream)
+        got.synchronize()
         if prob.shard is not None and prob.fused and prob.exchange == "peer":
             from .fused import PeerReducer
             pr = PeerReducer.get(prob.shard, prob.dimension)
             if pr is not None:
                 pr.check()
-        sl = slice(k * M, (k + 1) * M)
-        st, mn, sm, qd, ln, ts = (to_host(a[sl]) for a in (status, wmin, wsum, quad, lin, stamps))
-        t0 = host.setdefault("t0", int(stamps[T].item()))
+        st, mn, sm, qd, ln, ts = (pin.numpy() for pin in pins)
+        t0 = host.setdefault("t0", int(t0_pin[0]))
         ws = eng.rings[k % 2]
         for m in range(M):
             t = k * M + m

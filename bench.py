@@ -698,6 +698,12 @@ def task_c4(args, world, shard):
                         "basis": "SURVEY 8(d) C4: 8 N_gpu d (1 + 1/M) bytes per FW iteration per GPU "
                                  "(one fused read of X per step + the amortised draw)"},
            "clocks": clk, "final_objective": float(rec.objectives[-1])}
+    try:  # the fused pass's cluster geometry on this chip (explains box-to-box spread)
+        import torch
+        from paper_2404_11631_b200.fused import MV, fused_geometry
+        out["pass_geometry"] = dict(fused_geometry(MV, d), sms=torch.cuda.get_device_properties(0).multi_processor_count)
+    except Exception as e:  # diagnostic only
+        out["pass_geometry"] = {"error": str(e)}
     del prob
     _release()
     return out

@@ -485,6 +485,11 @@ int simopt_fused_rows(void* stream, int mode, const double* x, int64_t rows, int
                       const double* v, const double* center, const double* rowaux,
                       double col_scale, int accumulate, int raw, double* t_out, double* dw_out,
                       double* col_out, double* scalar_out, const SimoptPeerReduce* peer);
+/* Launch geometry simopt_fused_rows uses for `cols` columns on the current device
+ * (diagnostic, no launch): CTAs per cluster (column bands), resident clusters (from
+ * cudaOccupancyMaxActiveClusters: how many C-CTA clusters the chip's GPCs hold at once)
+ * and the grid.  vec: 16-byte aligned even rows. */
+int simopt_fused_geometry(int mode, int64_t cols, int vec, int* cluster, int* clusters, int* grid);
 
 /* ---- NCCL communicator (csrc/comm.cu; SURVEY 8(b) "NCCL communicator handle init/teardown").
  * Replaces the reference's in-process data-parallel split (sobench/backend.py:178-204) for

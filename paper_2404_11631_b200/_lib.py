@@ -69,6 +69,7 @@ SIGNATURES = {
     "simopt_cg_step2": [_vp, _vp, _vp, _vp, _vp, _i64],
     "simopt_fused_rows": [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _d, _i32, _i32, _vp, _vp, _vp,
                           _vp, _vp],
+    "simopt_fused_geometry": [_i32, _i64, _i32, _vp, _vp, _vp],
     "simopt_peer_reduce_bytes": [_i64, _i64],
     "simopt_sample_returns_diag_rows": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _i64, _vp, _vp, _vp],
     "simopt_bernoulli_half_range": [_vp, _u64, _u64, _u64, _u64, _i64, _i64, _vp],

@@ -1258,6 +1258,20 @@ extern "C" int simopt_fused_rows(void* stream, int mode, const double* X, int64_
                 a.accumulate ? col_out : nullptr, scalar_out, peer);
 }
 
+extern "C" int simopt_fused_geometry(int mode, int64_t cols, int vec, int* cluster, int* clusters,
+                                     int* grid) {
+  SIMOPT_REQUIRE(mode == SIMOPT_FUSED_MV || mode == SIMOPT_FUSED_LR_GRAD || mode == SIMOPT_FUSED_LR_HVP,
+                 SIMOPT_E_CONFIG, "unknown fused mode %d", mode);
+  int C = 1, K = 1;
+  SIMOPT_REQUIRE(cols >= 1 && geometry(cols, &C, &K), SIMOPT_E_CONFIG, "unsupported column count %lld",
+                 (long long)cols);
+  const int g = grid_for(pick(mode, C, K, vec != 0), C, dyn_smem(mode, K));
+  if (cluster) *cluster = C;
+  if (clusters) *clusters = g / C;
+  if (grid) *grid = g;
+  return SIMOPT_OK;
+}
+
 extern "C" int simopt_fused_rows_bits(void* stream, int mode, const uint64_t* bits, int64_t rows,
                                       int64_t cols, const double* v, const double* rowaux,
                                       double col_scale, int accumulate, int raw, double* t_out,

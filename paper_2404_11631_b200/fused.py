@@ -66,6 +66,14 @@ class PeerReducer:
             raise DeviceError("peer-memory allreduce timed out (a rank never arrived)")
 
 
+def fused_geometry(mode: int, cols: int, vec: bool = True) -> dict:
+    """The pass's launch geometry on this device: CTAs per cluster, resident clusters, grid."""
+    c, n, g = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.call("simopt_fused_geometry", mode, cols, int(vec), ctypes.byref(c), ctypes.byref(n),
+              ctypes.byref(g))
+    return {"cluster": c.value, "clusters": n.value, "grid": g.value}
+
+
 def fused_rows(mode: int, x: torch.Tensor, v: torch.Tensor, *, center=None, rowaux=None,
                col_scale: float = 1.0, col_out=None, scalar_out=None, t_out=None, dw_out=None,
                accumulate: bool = True, raw: bool = False, peer: PeerReducer | None = None):

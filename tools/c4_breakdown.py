@@ -46,6 +46,8 @@ q = torch.empty(1, dtype=torch.float64, device="cuda")
 t_pass = timed(lambda: fused_rows(MV, x, w, center=mean, col_scale=1.0 / (N - 1), col_out=g,
                                   scalar_out=q))
 gb = 8 * N * d / 1e9
+from paper_2404_11631_b200.fused import fused_geometry  # noqa: E402
+print("pass geometry:", fused_geometry(MV, d))
 print(f"N={N} d={d} ({gb:.1f} GB): resample (draw + exact mean) {t_all:.1f} ms, of which the exact "
       f"column sums {t_mean:.1f} ms ({gb / t_mean:.2f} TB/s); fused pass {t_pass:.1f} ms "
       f"({gb / t_pass:.2f} TB/s); epoch estimate {t_all + 26 * t_pass:.0f} ms")

@@ -805,9 +805,32 @@ __global__ void __launch_bounds__(kNT) k_fused_nib(const uint64_t* __restrict__ 
     wts[tid] = wt;
     __syncthreads();
     if (accumulate && tid < G) {
+      // four rows per step: their four accumulators are loaded before any is stored, and
+      // a pattern repeated within the step continues from the latest earlier sum -- the
+      // same additions in the same order as one row at a time, but one shared-memory
+      // round trip per four rows instead of a load-add-store chain per row
       const int c = tid, word = c >> 4, sh = 4 * (c & 15);
       double* Ac = A + c;
-      for (int i = 0; i < (int)nrow; ++i) {
+      const int nr = (int)nrow;
+      int i = 0;
+      for (; i + 4 <= nr; i += 4) {
+        const int p0 = (int)((tb[i * WS + word] >> sh) & 15ULL);
+        const int p1 = (int)((tb[(i + 1) * WS + word] >> sh) & 15ULL);
+        const int p2 = (int)((tb[(i + 2) * WS + word] >> sh) & 15ULL);
+        const int p3 = (int)((tb[(i + 3) * WS + word] >> sh) & 15ULL);
+        const double2 wa = *reinterpret_cast<const double2*>(wts + i);
+        const double2 wb = *reinterpret_cast<const double2*>(wts + i + 2);
+        const double a0 = Ac[p0 * Gp], a1 = Ac[p1 * Gp], a2 = Ac[p2 * Gp], a3 = Ac[p3 * Gp];
+        const double s0 = a0 + wa.x;
+        const double s1 = (p1 == p0 ? s0 : a1) + wa.y;
+        const double s2 = (p2 == p1 ? s1 : (p2 == p0 ? s0 : a2)) + wb.x;
+        const double s3 = (p3 == p2 ? s2 : (p3 == p1 ? s1 : (p3 == p0 ? s0 : a3))) + wb.y;
+        Ac[p0 * Gp] = s0;  // in row order: a repeated pattern's last store holds its sum
+        Ac[p1 * Gp] = s1;
+        Ac[p2 * Gp] = s2;
+        Ac[p3 * Gp] = s3;
+      }
+      for (; i < nr; ++i) {
         const int p = (int)((tb[i * WS + word] >> sh) & 15ULL);
         Ac[p * Gp] += wts[i];
       }

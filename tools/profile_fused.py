@@ -1,7 +1,7 @@
 """Profiled fused passes (for ncu): C3 Newton-CG iteration (d=1e3, N=1e6) and a C4
 per-GPU-slice mean-variance fused FW epoch (d=2e4, N=1.25e5).
 
-  python tools/profile_fused.py [c3|c4]
+  python tools/profile_fused.py [c3|c3bits|c4]
 """
 import sys
 
@@ -17,8 +17,9 @@ from paper_2404_11631_b200.tasks import LogisticTask, MeanVarProblem  # noqa: E4
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c3"
 b = p.make_backend("cuda")
-if which == "c3":
-    task = LogisticTask(synth_classification(1000, p.RngStream(42, 0), n_rows=1_000_000))
+if which in ("c3", "c3bits"):
+    task = LogisticTask(synth_classification(1000, p.RngStream(42, 0), n_rows=1_000_000,
+                                             packed=which == "c3bits"))
     run = lambda: newton_cg(task, 1, 10, b)  # noqa: E731
 else:
     prob = MeanVarProblem(gen_meanvar_instance(20_000, p.RngStream(42, 0)), b, fused=True)

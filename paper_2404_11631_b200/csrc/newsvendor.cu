@@ -943,8 +943,12 @@ __global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks)
 // lanes (overflow resolved in place).  Same counts and LMO as k_nv_iter.
 constexpr int kWarpQueue = 64;
 
-template <int kIterWarps, int kVecBatch = 4>
-__global__ void __launch_bounds__(kIterWarps * 32, 24 / kIterWarps) k_nv_iter_small(NvIterArgs a) {
+// kMinBlocks: launch-bound blocks per SM (register cap).  The 4-warp default uses 7 (72
+// registers): two blocks then sit beside the 40-register resample the small shards use, and
+// the 8-way shard's pipelined epoch is 0.666 vs 0.677-0.688 ms at 80 registers (16-way:
+// 0.485 vs 0.488-0.496)
+template <int kIterWarps, int kVecBatch = 4, int kMinBlocks = 24 / kIterWarps>
+__global__ void __launch_bounds__(kIterWarps * 32, kMinBlocks) k_nv_iter_small(NvIterArgs a) {
   __shared__ ArgMin warp_best[kIterWarps];
   __shared__ uint64_t wq[kIterWarps][kWarpQueue];
   __shared__ int wql[kIterWarps];
@@ -1224,7 +1228,7 @@ extern "C" int simopt_nv_iter(void* stream, const NvIterArgs* args) {
     SIMOPT_REQUIRE(gs <= a.part_capacity, SIMOPT_E_CONFIG, "partials buffer too small");
     if (ws == 16) k_nv_iter_small<16><<<gs, 16 * 32, 0, s>>>(a);
     else if (ws == 8) k_nv_iter_small<8><<<gs, 8 * 32, 0, s>>>(a);
-    else k_nv_iter_small<4><<<gs, 4 * 32, 0, s>>>(a);
+    else k_nv_iter_small<4, 4, 7><<<gs, 4 * 32, 0, s>>>(a);
     SIMOPT_CHECK_LAUNCH("k_nv_iter_small");
     return SIMOPT_OK;
   }

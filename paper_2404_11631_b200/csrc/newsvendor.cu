@@ -592,9 +592,10 @@ __device__ __forceinline__ NvThresh nv_thresh(const NvWindow& w) {
 //   (2) if do_grad: g_j at the (new) x_j, LMO values g_j * (C / c_j), argmin over all
 //       products (last-block reduction), NaN flag.
 // Gradient steps run in CTA rounds:
-//  (A) each warp takes up to kSlotsPerWarp products, one at a time from a device counter
-//      (the next index and the next product's iterate and parameters are fetched while
-//      the current one is processed); lanes = the product's segments: bucket starts of the
+//  (A) each warp takes up to kSlotsPerWarp (8) products, one at a time from a device
+//      counter (the counter read for the product after the next is in flight while the
+//      current one is processed; the next product's iterate and parameters are loaded as
+//      soon as its index is known); lanes = the product's segments: bucket starts of the
 //      query window, then the window's keys in 16-byte loads (several in flight per lane),
 //      integer thresholds count the certainly-below keys and the few ambiguous draws are
 //      appended to one CTA-wide queue;

@@ -100,6 +100,10 @@ int simopt_threshold(void* stream, const double* x, double thr, int64_t n, doubl
 int simopt_dot(void* stream, const double* x, const double* y, int64_t n, int64_t chunk,
                double* out);
 int simopt_vec_sum(void* stream, const double* x, int64_t n, int64_t chunk, double* out);
+/* Deterministic dot in one CTA (fixed strided assignment, fixed xor trees; no FMA) -- not the
+ * reference's tree: the fused Newton-CG's scalars (d-vectors), where the tree's sequential
+ * chunk chain is the cost.  Meant for n up to ~10^5. */
+int simopt_dot_fast(void* stream, const double* x, const double* y, int64_t n, double* out);
 /* Two independent fixed-tree reductions in one launch: out_k = dot(x_k, y_k) (y_k != NULL)
  * or vec_sum(x_k) (y_k == NULL). */
 int simopt_tree_sums2(void* stream, const double* x0, const double* y0, int64_t n0, double* out0,

@@ -30,6 +30,7 @@ SIGNATURES = {
     "simopt_bernoulli_half": [_vp, _u64, _u64, _u64, _u64, _i64, _vp],
     "simopt_threshold": [_vp, _vp, _d, _i64, _vp],
     "simopt_dot": [_vp, _vp, _vp, _i64, _i64, _vp],
+    "simopt_dot_fast": [_vp, _vp, _vp, _i64, _vp],
     "simopt_vec_sum": [_vp, _vp, _i64, _i64, _vp],
     "simopt_tree_sums2": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64],
     "simopt_matvec": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],

@@ -465,6 +465,39 @@ extern "C" int simopt_dot(void* stream, const double* x, const double* y, int64_
   return tree_reduce(as_stream(stream), x, y, n, chunk, out);
 }
 
+namespace {
+// One CTA, fixed order: thread t sums x[i] * y[i] for i = t, t + 1024, ... (no FMA), then a
+// fixed xor tree per warp and the 32 warp sums in warp order.  Deterministic, not the
+// reference's tree: for the fused solvers' short d-vectors, where the tree's 4096-long
+// sequential chain (~10 us per dot) is the cost.
+constexpr int kDotFastThreads = 1024;
+__global__ void __launch_bounds__(kDotFastThreads) k_dot_fast(const double* __restrict__ x,
+                                                              const double* __restrict__ y,
+                                                              int64_t n, double* __restrict__ out) {
+  __shared__ double ws[kDotFastThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double s = 0.0;
+  for (int64_t i = tid; i < n; i += kDotFastThreads) s += x[i] * y[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) ws[w] = s;
+  __syncthreads();
+  if (w == 0) {
+    double t = ws[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) *out = t;
+  }
+}
+}  // namespace
+
+extern "C" int simopt_dot_fast(void* stream, const double* x, const double* y, int64_t n, double* out) {
+  SIMOPT_REQUIRE(n >= 0, SIMOPT_E_DIMENSION, "negative length");
+  k_dot_fast<<<1, kDotFastThreads, 0, as_stream(stream)>>>(x, y, n, out);
+  SIMOPT_CHECK_LAUNCH("k_dot_fast");
+  return SIMOPT_OK;
+}
+
 extern "C" int simopt_vec_sum(void* stream, const double* x, int64_t n, int64_t chunk, double* out) {
   return tree_reduce(as_stream(stream), x, nullptr, n, chunk, out);
 }

@@ -26,6 +26,8 @@ the exact fixed tree and the bit-identical trajectory.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib
@@ -178,7 +180,13 @@ def _run(task, iterations, backend, step, label, fused=False, exchange="peer", o
     stamps = torch.zeros(iterations + 1, dtype=torch.int64, device="cuda")
     lib = _lib.load()
     _lib.check(lib.simopt_timestamp(_lib.stream_ptr(), _lib.ptr(stamps[iterations:])))
-    dot = lambda x, y, out: backend.dot_device(x, y, out=out)  # noqa: E731
+    if fused and n <= 65536 and os.environ.get("SIMOPT_CG_TREE") != "1":  # one-CTA CG scalars
+        def dot(x, y, out):
+            _lib.call("simopt_dot_fast", _lib.stream_ptr(), _lib.ptr(x), _lib.ptr(y), x.numel(),
+                      _lib.ptr(out))
+            return out
+    else:
+        dot = lambda x, y, out: backend.dot_device(x, y, out=out)  # noqa: E731
     if fused:
         loss0 = empty(1)
         L.fused_gradient(w, g, loss0)

@@ -119,6 +119,39 @@ def test_dot_large(pkg):
     assert b.vec_sum(x) == orc.vec_sum(x)
 
 
+@pytest.mark.parametrize("n", [0, 1, 1000, 8192, 65536])
+def test_dot_fast(pkg, n):
+    """simopt_dot_fast: the fused CG's deterministic one-CTA dot -- its own fixed order
+    (thread-strided sums, warp xor trees), reproduced here in numpy, and within 1e-13 of
+    the exact value."""
+    import torch
+    from paper_2404_11631_b200 import _lib
+    rng = np.random.default_rng(n + 7)
+    x, y = rng.standard_normal(n), rng.standard_normal(n)
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    _lib.call("simopt_dot_fast", _lib.stream_ptr(), _lib.ptr(xd), _lib.ptr(yd), n, _lib.ptr(out))
+    got = float(out.item())
+    # restatement of the kernel's order
+    T = 1024
+    s = np.zeros(T)
+    for t in range(T):
+        acc = 0.0
+        for i in range(t, n, T):
+            acc += float(x[i] * y[i])
+        s[t] = acc
+
+    def xor_tree(v):
+        v = v.copy()
+        for o in (16, 8, 4, 2, 1):
+            v = v + v[np.arange(32) ^ o]
+        return v[0]
+    w = np.array([xor_tree(s[32 * k:32 * k + 32]) for k in range(32)])
+    assert got == xor_tree(w)
+    exact = float(np.dot(x.astype(np.longdouble), y.astype(np.longdouble))) if n else 0.0
+    assert abs(got - exact) <= 1e-13 * max(1.0, float(np.abs(x * y).sum()))
+
+
 def test_errors(pkg):
     b = pkg.make_backend("cuda")
     with pytest.raises(pkg.DimensionMismatch):

@@ -104,6 +104,11 @@ int simopt_vec_sum(void* stream, const double* x, int64_t n, int64_t chunk, doub
  * reference's tree: the fused Newton-CG's scalars (d-vectors), where the tree's sequential
  * chunk chain is the cost.  Meant for n up to ~10^5. */
 int simopt_dot_fast(void* stream, const double* x, const double* y, int64_t n, double* out);
+/* Column sums out[c] = sum_r x[r][c] of a row-major rows x cols matrix in a fixed order
+ * (64 row groups summed sequentially, then folded in group order): deterministic, not the
+ * reference's tree -- the fused mean-variance path's sample mean at small N (C1), where the
+ * tree's 4096-long chains are latency-bound. */
+int simopt_col_sums_fast(void* stream, const double* x, int64_t rows, int64_t cols, double* out);
 /* Two independent fixed-tree reductions in one launch: out_k = dot(x_k, y_k) (y_k != NULL)
  * or vec_sum(x_k) (y_k == NULL). */
 int simopt_tree_sums2(void* stream, const double* x0, const double* y0, int64_t n0, double* out0,

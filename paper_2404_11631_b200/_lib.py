@@ -31,6 +31,7 @@ SIGNATURES = {
     "simopt_threshold": [_vp, _vp, _d, _i64, _vp],
     "simopt_dot": [_vp, _vp, _vp, _i64, _i64, _vp],
     "simopt_dot_fast": [_vp, _vp, _vp, _i64, _vp],
+    "simopt_col_sums_fast": [_vp, _vp, _i64, _i64, _vp],
     "simopt_vec_sum": [_vp, _vp, _i64, _i64, _vp],
     "simopt_tree_sums2": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64],
     "simopt_matvec": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp],

@@ -498,6 +498,46 @@ extern "C" int simopt_dot_fast(void* stream, const double* x, const double* y, i
   return SIMOPT_OK;
 }
 
+namespace {
+// Column sums of a row-major rows x cols matrix in a fixed order: row group g (rows
+// [g R, (g + 1) R)) summed sequentially per column by one lane (a warp covers 32 adjacent
+// columns: 256-byte rows), then the groups' partials folded in group order.  Deterministic,
+// not the reference's 4096-chunk tree: chains of R instead of 4096 sequential additions.
+constexpr int kColGroups = 64;
+__global__ void k_col_sums_part(const double* __restrict__ x, int64_t rows, int64_t cols, int64_t R,
+                                double* __restrict__ part) {
+  const int64_t c = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+  const int64_t g = (int64_t)blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= cols || g >= kColGroups) return;
+  const int64_t r0 = g * R, r1 = r0 + R < rows ? r0 + R : rows;
+  double s = 0.0;
+  for (int64_t r = r0; r < r1; ++r) s += x[r * cols + c];
+  part[g * cols + c] = s;
+}
+__global__ void k_col_sums_fold(const double* __restrict__ part, int64_t cols, double* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double s = 0.0;
+  for (int g = 0; g < kColGroups; ++g) s += part[g * cols + c];
+  out[c] = s;
+}
+}  // namespace
+
+extern "C" int simopt_col_sums_fast(void* stream, const double* x, int64_t rows, int64_t cols,
+                                    double* out) {
+  SIMOPT_REQUIRE(rows >= 0 && cols >= 0, SIMOPT_E_DIMENSION, "negative extent");
+  if (cols == 0) return SIMOPT_OK;
+  cudaStream_t st = as_stream(stream);
+  double* part = static_cast<double*>(simopt_scratch(st, (size_t)kColGroups * cols * sizeof(double)));
+  SIMOPT_REQUIRE(part != nullptr, SIMOPT_E_CUDA, "%s", simopt_last_error());
+  const int64_t R = (rows + kColGroups - 1) / kColGroups;
+  k_col_sums_part<<<dim3((unsigned)ceil_div(cols, 32), kColGroups / 4), 128, 0, st>>>(x, rows, cols, R, part);
+  SIMOPT_CHECK_LAUNCH("k_col_sums_part");
+  k_col_sums_fold<<<(unsigned)ceil_div(cols, 256), 256, 0, st>>>(part, cols, out);
+  SIMOPT_CHECK_LAUNCH("k_col_sums_fold");
+  return SIMOPT_OK;
+}
+
 extern "C" int simopt_vec_sum(void* stream, const double* x, int64_t n, int64_t chunk, double* out) {
   return tree_reduce(as_stream(stream), x, nullptr, n, chunk, out);
 }

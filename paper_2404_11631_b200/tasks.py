@@ -201,6 +201,11 @@ class _NvDevice:
         return out.view(self.d, self.S)
 
 
+# fused mean-variance runs take the sample mean from simopt_col_sums_fast up to this many
+# samples (above it the exact tree's column sums are HBM-bound anyway: C4 7.2 TB/s)
+_FAST_MEAN_ROWS = 1 << 17
+
+
 class NewsvendorProblem:
     """Newsvendor wired for FW: sampled gradient, exact recorded objective (tasks.py:293-334)."""
 
@@ -965,7 +970,14 @@ class MeanVarProblem:
         _lib.call("simopt_sample_returns_diag", _lib.stream_ptr(), *stream.words(), n_samples, d,
                   _lib.ptr(self._mu_dev), _lib.ptr(self._sd_dev), _lib.ptr(x))
         stream.advance(2 * ((n_samples * d + 1) // 2))
-        col = self.backend.matvec_t_device(x, ones)          # build_sample_set (tasks.py:56-64)
+        if self.fused and n_samples <= _FAST_MEAN_ROWS:
+            # fused mode (trajectories within 1e-8, not the tree): the column sums in a fixed
+            # order of 64 short chains -- at C1's N the tree's 4096-long chains are latency-
+            # bound (81 vs ~10 us) and trail the next epoch's draw
+            col = empty(d)
+            _lib.call("simopt_col_sums_fast", _lib.stream_ptr(), _lib.ptr(x), n_samples, d, _lib.ptr(col))
+        else:
+            col = self.backend.matvec_t_device(x, ones)      # build_sample_set (tasks.py:56-64)
         _lib.call("simopt_scale_sub", _lib.stream_ptr(), _lib.ptr(col), 1.0 / n_samples, None, d,
                   _lib.ptr(mean))
         return MeanVarSampleSet(x, mean)

@@ -152,6 +152,26 @@ def test_dot_fast(pkg, n):
     assert abs(got - exact) <= 1e-13 * max(1.0, float(np.abs(x * y).sum()))
 
 
+@pytest.mark.parametrize("rows,cols", [(10_000, 1000), (65, 33), (1, 5), (200, 1)])
+def test_col_sums_fast(pkg, rows, cols):
+    """simopt_col_sums_fast (the fused mean-variance mean at small N): 64 row groups of
+    ceil(rows/64) summed sequentially per column, partials folded in group order."""
+    from paper_2404_11631_b200 import _lib
+    rng = np.random.default_rng(rows + cols)
+    x = rng.standard_normal((rows, cols))
+    out = torch.empty(cols, dtype=torch.float64, device="cuda")
+    _lib.call("simopt_col_sums_fast", _lib.stream_ptr(), _lib.ptr(torch.from_numpy(x).cuda()), rows, cols,
+              _lib.ptr(out))
+    R = -(-rows // 64)
+    want = np.zeros(cols)
+    for g in range(64):
+        part = np.zeros(cols)
+        for r in range(g * R, min((g + 1) * R, rows)):
+            part = part + x[r]
+        want = want + part
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
 def test_errors(pkg):
     b = pkg.make_backend("cuda")
     with pytest.raises(pkg.DimensionMismatch):

@@ -105,7 +105,7 @@ int simopt_vec_sum(void* stream, const double* x, int64_t n, int64_t chunk, doub
  * chunk chain is the cost.  Meant for n up to ~10^5. */
 int simopt_dot_fast(void* stream, const double* x, const double* y, int64_t n, double* out);
 /* Column sums out[c] = sum_r x[r][c] of a row-major rows x cols matrix in a fixed order
- * (64 row groups summed sequentially, then folded in group order): deterministic, not the
+ * (256 row groups summed sequentially, then folded in group order): deterministic, not the
  * reference's tree -- the fused mean-variance path's sample mean at small N (C1), where the
  * tree's 4096-long chains are latency-bound. */
 int simopt_col_sums_fast(void* stream, const double* x, int64_t rows, int64_t cols, double* out);

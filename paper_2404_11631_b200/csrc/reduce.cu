@@ -503,7 +503,7 @@ namespace {
 // [g R, (g + 1) R)) summed sequentially per column by one lane (a warp covers 32 adjacent
 // columns: 256-byte rows), then the groups' partials folded in group order.  Deterministic,
 // not the reference's 4096-chunk tree: chains of R instead of 4096 sequential additions.
-constexpr int kColGroups = 64;
+constexpr int kColGroups = 256;
 __global__ void k_col_sums_part(const double* __restrict__ x, int64_t rows, int64_t cols, int64_t R,
                                 double* __restrict__ part) {
   const int64_t c = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);

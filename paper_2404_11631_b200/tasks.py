@@ -972,7 +972,7 @@ class MeanVarProblem:
         stream.advance(2 * ((n_samples * d + 1) // 2))
         if self.fused and n_samples <= _FAST_MEAN_ROWS:
             # fused mode (trajectories within 1e-8, not the tree): the column sums in a fixed
-            # order of 64 short chains -- at C1's N the tree's 4096-long chains are latency-
+            # order of 256 short chains -- at C1's N the tree's 4096-long chains are latency-
             # bound (81 vs ~10 us) and trail the next epoch's draw
             col = empty(d)
             _lib.call("simopt_col_sums_fast", _lib.stream_ptr(), _lib.ptr(x), n_samples, d, _lib.ptr(col))

@@ -154,17 +154,17 @@ def test_dot_fast(pkg, n):
 
 @pytest.mark.parametrize("rows,cols", [(10_000, 1000), (65, 33), (1, 5), (200, 1)])
 def test_col_sums_fast(pkg, rows, cols):
-    """simopt_col_sums_fast (the fused mean-variance mean at small N): 64 row groups of
-    ceil(rows/64) summed sequentially per column, partials folded in group order."""
+    """simopt_col_sums_fast (the fused mean-variance mean at small N): 256 row groups of
+    ceil(rows/256) summed sequentially per column, partials folded in group order."""
     from paper_2404_11631_b200 import _lib
     rng = np.random.default_rng(rows + cols)
     x = rng.standard_normal((rows, cols))
     out = torch.empty(cols, dtype=torch.float64, device="cuda")
     _lib.call("simopt_col_sums_fast", _lib.stream_ptr(), _lib.ptr(torch.from_numpy(x).cuda()), rows, cols,
               _lib.ptr(out))
-    R = -(-rows // 64)
+    R = -(-rows // 256)
     want = np.zeros(cols)
-    for g in range(64):
+    for g in range(256):
         part = np.zeros(cols)
         for r in range(g * R, min((g + 1) * R, rows)):
             part = part + x[r]
